@@ -1,0 +1,129 @@
+/*
+ * ots.h -- C-ABI of the B200-native two-stage Householder orthogonalization
+ * (arXiv 2602.14449, Algorithm 1 and its B-inner extension).
+ *
+ * Drop-in boundary for the reference package `orthoqr` 0.1.0 (pure Python,
+ * /root/reference/pkg/src/orthoqr).  Every entry point below replaces one
+ * reference function on the hot path named by BASELINE.json's north_star;
+ * the reference interface each one replaces is cited beside it.  The Python
+ * facade `paper_2602_14449_b200` (same names/signatures as orthoqr) binds
+ * these with ctypes; INTEGRATION.md shows the binding a maintainer adds.
+ *
+ * Conventions
+ *  - All matrices are ROW-MAJOR (numpy C order, as orthoqr's as_matrix,
+ *    core.py:25-32) in DEVICE memory owned by the caller; ld = row stride in
+ *    elements, must be even and rows 16-byte aligned.
+ *  - Real f64 entry points take `double*`; complex128 entry points take
+ *    interleaved (re, im) `double*` with ld counted in complex elements.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls are
+ *    stream-ordered; the only host synchronisation is the status/diagnostic
+ *    readback at the end of a call.
+ *  - Return value: OTS_OK (0) or a negative code, one per exception class of
+ *    orthoqr/errors.py:4-65; ots_last_error() returns the message.
+ */
+#ifndef OTS_H_
+#define OTS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OTS_OK 0
+#define OTS_E_DIMENSION -1        /* DimensionError        errors.py:8  */
+#define OTS_E_NOT_HERMITIAN -2    /* NotHermitian          errors.py:12 */
+#define OTS_E_NOT_PD -3           /* NotPositiveDefinite   errors.py:16 */
+#define OTS_E_CONVERGENCE -4      /* ConvergenceError      errors.py:20 */
+#define OTS_E_SINGULAR -5         /* SingularError         errors.py:24 */
+#define OTS_E_NORM_BOUND -6       /* NormBoundError        errors.py:28 */
+#define OTS_E_SINGULAR_T -7       /* SingularTError        errors.py:32 */
+#define OTS_E_ORTHONORMALITY -8   /* OrthonormalityError   errors.py:36 */
+#define OTS_E_INTRA_FAILURE -9    /* IntraFailure          errors.py:40 */
+#define OTS_E_BREAKDOWN -10       /* BreakdownError        errors.py:52 */
+#define OTS_E_PARAMETER -12       /* ParameterError        errors.py:60 */
+#define OTS_E_VALUE -20           /* ValueError (non-finite / layout) core.py:72 */
+#define OTS_E_CUDA -30            /* CUDA runtime failure */
+#define OTS_E_UNSUPPORTED -31     /* shape outside this build's kernels */
+
+/* seed choices (reflector.py:41 CHOICES) */
+#define OTS_CHOICE_MLU 0
+#define OTS_CHOICE_QR 1
+#define OTS_CHOICE_POLAR 2
+#define OTS_CHOICE_EXPLICIT 3
+/* intra methods (twostage.py:25 INTRA_METHODS) */
+#define OTS_INTRA_HOUSEHOLDER 0
+#define OTS_INTRA_CHOLSHIFT 1
+
+typedef struct ots_ctx ots_ctx;
+
+/* One context per (device, host thread).  Owns the device workspace (grown on
+ * demand, never shrunk) and a side stream for the diagnostics. */
+int ots_ctx_create(int device, ots_ctx** out);
+void ots_ctx_destroy(ots_ctx* ctx);
+const char* ots_last_error(const ots_ctx* ctx);
+int ots_sm_count(const ots_ctx* ctx);
+int ots_version(void);
+
+/* two_stage_qr(v, a, choice, intra, p)          -- twostage.py:57-97
+ * Q (n x k), R (k x k, upper, exact zeros below), S (k0 x k) written to
+ * caller buffers.  diag_host (host, 3 doubles) <- [kappa_t, wt_inv_norm,
+ * orthonormality defect]  (ReflectorDiagnostics, reflector.py:168-171,241-247;
+ * the defect is what reflector.py:220-223 checks against orth_tol).
+ * P (k0 x k0) only for choice EXPLICIT (reflector.py:194-203), else NULL. */
+int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                      const double* V, int64_t ldv, const double* A, int64_t lda,
+                      int choice, int intra, const double* P, int64_t ldp,
+                      double orth_tol, int allow_defect,
+                      double* Q, int64_t ldq, double* R, int64_t ldr,
+                      double* S, int64_t lds, double* diag_host, void* stream);
+
+/* householder_qr(a, nonneg_diag)                 -- core.py:61-84
+ * LAPACK dgeqrf+dorgqr semantics (R diagonal signs as dlarfg); with
+ * nonneg_diag the phase fix of core.py:75-83. */
+int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,
+                           const double* A, int64_t lda, double* Q, int64_t ldq,
+                           double* R, int64_t ldr, int nonneg_diag, void* stream);
+
+/* modified_lu(z)                                  -- reflector.py:53-77
+ * LU (n x n, L strict-lower unit + U upper, packed, ld n) and p (n). */
+int ots_modified_lu_f64(ots_ctx* ctx, int64_t n, const double* Z, int64_t ldz,
+                        double* LU, double* p, void* stream);
+
+/* Per-phase device timings of the last call (CUDA events on the launching
+ * stream), enabled with ots_set_profiling(ctx, 1).  names: '\n'-separated. */
+int ots_set_profiling(ots_ctx* ctx, int enable);
+int ots_last_profile(const ots_ctx* ctx, char* names, int names_cap, float* ms, int cap);
+
+/* ---- phase-split entry points for row-sharded multi-GPU execution ------
+ * Each rank owns rows [row0, row0 + n_local) of V, A, Q (rank 0: row0 = 0,
+ * n_local >= k0 + k).  Host-side NCCL collectives run between phases
+ * (SURVEY.md §8(e)); paper_2602_14449_b200/dist.py is the orchestrator.
+ *
+ *  1  ots_dist_gram      local [V^T V | V_b^T A_b] partial  -> allreduce(sum)
+ *  2  ots_dist_seed      redundant seed / T / Z1 from the summed Gram and the
+ *                        rank-0 top rows (broadcast)
+ *  3  ots_dist_factor    X = A_b + V_b Z1, local TSQR -> rank R (KT x KT)
+ *                        -> allgather
+ *  4  ots_dist_tree      redundant top QR of the gathered R's; this rank's C
+ *  5  ots_dist_qform     local Q_, partial Y2 = -V_b^T Q_ -> allreduce(sum);
+ *                        rank 0 also the sign vector -> broadcast
+ *  6  ots_dist_finish    Z2 = T^{-1} Y2, Q = (Q_ + V_b Z2) diag(s), rank 0 top
+ */
+int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int64_t k,
+                   const double* V, int64_t ldv, const double* A, int64_t lda,
+                   double* Q, int64_t ldq, int choice, const double* P, int64_t ldp,
+                   double orth_tol, void* stream);
+int ots_dist_gram(ots_ctx* ctx, double* gram_out, int64_t* gram_count);
+int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows);
+int ots_dist_top_rows(ots_ctx* ctx, double* top_rows_out, int64_t* count);
+int ots_dist_factor(ots_ctx* ctx, double* r_local_out, int64_t* kt);
+int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank);
+int ots_dist_qform(ots_ctx* ctx, double* y2_out, int64_t* count, double* sign_out);
+int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign,
+                    double* R, int64_t ldr, double* S, int64_t lds, double* diag_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OTS_H_ */

@@ -1,0 +1,113 @@
+"""ctypes binding of the C-ABI in include/ots.h (libots.so, built in-tree by
+`make` / __graft_entry__.build()).  No CPU fallback: if the library or a CUDA
+device is missing every call raises NativeUnavailable."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+from . import errors as E
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libots.so")
+
+CHOICES = {"mlu": 0, "qr": 1, "polar": 2, "explicit": 3}
+INTRA = {"householder": 0, "cholshift": 1}
+
+_CODE_TO_EXC = {
+    -1: E.DimensionError, -2: E.NotHermitian, -3: E.NotPositiveDefinite,
+    -4: E.ConvergenceError, -5: E.SingularError, -6: E.NormBoundError,
+    -7: E.SingularTError, -8: E.OrthonormalityError, -9: E.IntraFailure,
+    -10: E.BreakdownError, -12: E.ParameterError, -20: ValueError,
+}
+
+_lib = None
+_lock = threading.Lock()
+_ctx = {}
+
+_vp, _i64, _int, _dbl = C.c_void_p, C.c_int64, C.c_int, C.c_double
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise E.NativeUnavailable(
+                        f"{LIB_PATH} not built; run `make` (or __graft_entry__.build())")
+                L = C.CDLL(LIB_PATH)
+                L.ots_ctx_create.argtypes = [_int, C.POINTER(_vp)]
+                L.ots_ctx_destroy.argtypes = [_vp]
+                L.ots_last_error.argtypes = [_vp]
+                L.ots_last_error.restype = C.c_char_p
+                L.ots_sm_count.argtypes = [_vp]
+                L.ots_version.restype = _int
+                L.ots_set_profiling.argtypes = [_vp, _int]
+                L.ots_last_profile.argtypes = [_vp, C.c_char_p, _int, C.POINTER(C.c_float), _int]
+                L.ots_two_stage_f64.argtypes = [
+                    _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64,
+                    _dbl, _int, _vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
+                L.ots_householder_qr_f64.argtypes = [
+                    _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp]
+                L.ots_modified_lu_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp]
+                L.ots_dist_begin.argtypes = [
+                    _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp,
+                    _i64, _dbl, _vp]
+                L.ots_dist_gram.argtypes = [_vp, _vp, C.POINTER(_i64)]
+                L.ots_dist_top_rows.argtypes = [_vp, _vp, C.POINTER(_i64)]
+                L.ots_dist_seed.argtypes = [_vp, _vp, _vp]
+                L.ots_dist_factor.argtypes = [_vp, _vp, C.POINTER(_i64)]
+                L.ots_dist_tree.argtypes = [_vp, _vp, _int, _int]
+                L.ots_dist_qform.argtypes = [_vp, _vp, C.POINTER(_i64), _vp]
+                L.ots_dist_finish.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i64, C.POINTER(_dbl)]
+                _lib = L
+    return _lib
+
+
+EXPORTED_SYMBOLS = [
+    "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_version",
+    "ots_two_stage_f64", "ots_householder_qr_f64", "ots_modified_lu_f64",
+    "ots_set_profiling", "ots_last_profile",
+    "ots_dist_begin", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",
+    "ots_dist_tree", "ots_dist_qform", "ots_dist_finish",
+]
+
+
+def context(device):
+    """Per-device C context (created lazily, kept for the process lifetime)."""
+    if device not in _ctx:
+        L = lib()
+        h = _vp()
+        rc = L.ots_ctx_create(int(device), C.byref(h))
+        if rc != 0:
+            msg = L.ots_last_error(h).decode() if h.value else "ots_ctx_create failed"
+            raise E.NativeUnavailable(f"CUDA context on device {device}: {msg}")
+        _ctx[device] = h
+    return _ctx[device]
+
+
+def check(rc, ctx, block=None):
+    if rc == 0:
+        return
+    msg = lib().ots_last_error(ctx).decode()
+    exc = _CODE_TO_EXC.get(rc)
+    if exc is E.IntraFailure:
+        raise E.IntraFailure(msg, block)
+    if exc is None:
+        if rc == -31:
+            raise NotImplementedError(msg)
+        raise RuntimeError(f"libots error {rc}: {msg}")
+    raise exc(msg)
+
+
+def profile(ctx):
+    """[(phase, ms)] of the last call (when profiling is enabled)."""
+    L = lib()
+    buf = C.create_string_buffer(4096)
+    ms = (C.c_float * 64)()
+    n = L.ots_last_profile(ctx, buf, 4096, ms, 64)
+    names = buf.value.decode().split("\n")
+    return [(names[i], float(ms[i])) for i in range(n)]

@@ -1,0 +1,57 @@
+// Argument structs and launchers of the streaming / chain kernels (shared by
+// tsgemm.cu, chainqr.cu and ots_api.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ots {
+
+struct TnArgs {
+  const double* P; long ldp; int pc0; int pcols;   // P columns [pc0, pc0+pcols)
+  const double* B; long ldb; int bc0; int bcols;   // B2 columns
+  long row_begin, row_end;                          // rows reduced over
+  long b_row_begin;                                 // B2 rows < this are zero
+  long p_row_begin;                                 // P rows < this are zero
+  long rows_per_cta;                                // set by the launcher
+  double* partial;                                  // [grid][PW][NTOT]
+};
+
+struct NnArgs {
+  const double* P; long ldp; int kdim;        // P rows x kdim
+  const double* Z; long ldz;                  // kdim x ncols
+  const double* B; long ldb;                  // may be null (treated as 0)
+  double* X; long ldx;
+  int ncols;
+  long row_begin, row_end;
+  const double* colscale;                     // device, ncols entries, or null
+};
+
+struct ChainGeom {
+  long nrows;            // rows of the level matrix
+  int b;                 // structured tile rows
+  int L;                 // structured tiles per chain (max)
+  long rpc;              // rows per chain = KT + L*b
+  int nchains;
+};
+
+struct FactorArgs {
+  double* D; long ldd; int ncols;
+  ChainGeom G;
+  double* U;             // per tile KT*KT, tile id = chain*(L+1) + t
+  double* Rout;          // stacked chain R's: chain*KT rows, ld KT
+};
+
+struct QformArgs {
+  double* D; long ldd; int ncols;
+  ChainGeom G;
+  const double* T;       // per tile KT*KT
+  const double* Cin;     // stacked chain C's (chain*KT rows, ld KT)
+};
+
+cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid, cudaStream_t st);
+cudaError_t launch_reduce(const double* partial, int nparts, long count, double* out, double alpha, cudaStream_t st);
+cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
+cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
+cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
+int chain_bmax(int KT);
+
+}  // namespace ots

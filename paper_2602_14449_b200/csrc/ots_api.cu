@@ -1,0 +1,780 @@
+// C-ABI of the B200 two-stage orthogonalization (include/ots.h).
+//
+// Host orchestration of Algorithm 1 (twostage.py:57-97) as a fixed sequence of
+// stream-ordered phases over row-sharded data:
+//
+//   gram    K1  G = [V^T V | V_b^T A_b]              (tsgemm_tn, DMMA)
+//   seed    K2  defect check, P, T, W_t, Z1 = T^{-T}(W^T A), S   (small.cu)
+//   diag        kappa(T), ||W T^{-1}||  -- side stream, overlaps the passes
+//   apply1  K3a X = A_b + V_b Z1  (= (H^T A)_{k0+1:n})   (tsgemm_nn)
+//   factor  K3b chain TSQR of X (+ tree levels)          (chainqr.cu)
+//   qform   K5a explicit Q_ (tree levels down to rows)   (chainqr.cu)
+//   sign        LAPACK sign recovery, R                  (small.cu)
+//   gram2   K5c Y2 = -V_b^T Q_                           (tsgemm_tn)
+//   z2          Z2 = T^{-1} Y2                           (small.cu)
+//   apply2  K5b Q_b = (Q_ + V_b Z2) diag(s)              (tsgemm_nn)
+//   qtop        Q_t = -W_t Z2 diag(s)                    (small.cu)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "small.cuh"
+#include "ots.h"
+
+#include "kernels.cuh"
+
+using namespace ots;
+
+namespace {
+
+inline int pad32(long x) { return (int)((x + 31) / 32 * 32); }
+inline int kt_for(long k) { return k <= 16 ? 16 : (k <= 32 ? 32 : 64); }
+
+__global__ void set_identity_kernel(double* D, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * n) D[i] = (i / n == i % n) ? 1.0 : 0.0;
+}
+__global__ void fill_kernel(double* D, long n, double v) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) D[i] = v;
+}
+__global__ void nonneg_fix_kernel(double* Q, long ldq, long m, int k, double* R, long ldr) {
+  // core.py:75-83 phase fix for real: column sign of R diag (0 -> +1)
+  __shared__ double ph[64];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ph[j] = (R[j * ldr + j] < 0.0) ? -1.0 : 1.0;
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+      int i = e / k, j = e - i * k;
+      double v = R[i * ldr + j] * ph[i];
+      if (i == j) v = fabs(R[i * ldr + j]);
+      R[i * ldr + j] = v;
+    }
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += (long)gridDim.x * blockDim.x) {
+    long i = e / k; int j = (int)(e - i * k);
+    Q[i * ldq + j] *= ph[j];
+  }
+}
+
+struct Level {
+  double* D; long ldd; int ncols;
+  ChainGeom G;
+  double* UT;     // per-tile U -> T
+  double* R;      // stacked chain R's (nchains * KT rows, ld KT)
+};
+
+}  // namespace
+
+struct ots_ctx {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_seed = nullptr, ev_diag = nullptr;
+  char* ws = nullptr;
+  size_t ws_size = 0;
+  int* h_status = nullptr;   // pinned
+  double* h_diag = nullptr;  // pinned
+  std::string err;
+  // profiling
+  bool profile = false;
+  std::vector<std::string> pnames;
+  std::vector<cudaEvent_t> pev;
+  std::vector<float> pms;
+  std::vector<std::string> last_names;
+  // distributed job state
+  struct Job* job = nullptr;
+};
+
+namespace {
+
+struct Arena {
+  char* base; size_t off = 0, cap;
+  Arena(char* b, size_t c) : base(b), cap(c) {}
+  template <class T>
+  T* take(size_t n) {
+    off = (off + 255) & ~(size_t)255;
+    T* p = reinterpret_cast<T*>(base + off);
+    off += n * sizeof(T);
+    return p;
+  }
+};
+
+int fail(ots_ctx* c, int code, const std::string& msg) { c->err = msg; return code; }
+
+#define CK(x)                                                                   \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess)                                                      \
+      return fail(ctx, OTS_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+void prof_mark(ots_ctx* ctx, cudaStream_t st, const char* name) {
+  if (!ctx->profile) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  ctx->pev.push_back(e);
+  ctx->pnames.push_back(name);
+}
+
+void prof_begin(ots_ctx* ctx, cudaStream_t st) {
+  for (auto e : ctx->pev) cudaEventDestroy(e);
+  ctx->pev.clear();
+  ctx->pnames.clear();
+  prof_mark(ctx, st, "start");
+}
+
+void prof_end(ots_ctx* ctx) {
+  if (!ctx->profile || ctx->pev.empty()) return;
+  cudaEventSynchronize(ctx->pev.back());
+  ctx->pms.clear();
+  ctx->last_names.clear();
+  for (size_t i = 1; i < ctx->pev.size(); ++i) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ctx->pev[i - 1], ctx->pev[i]);
+    ctx->pms.push_back(ms);
+    ctx->last_names.push_back(ctx->pnames[i]);
+  }
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// -------------------------------------------------------------------------
+// Job: one two-stage factorisation on this rank's rows.
+// -------------------------------------------------------------------------
+struct JobCfg {
+  long n_local, row0, k0, k;
+  const double* V; long ldv;
+  const double* A; long lda;
+  double* Q; long ldq;
+  int choice; const double* Pexp; long ldp;
+  double orth_tol; int allow_defect;
+  cudaStream_t st;
+  bool distributed;
+};
+
+}  // namespace
+
+struct Job {
+  JobCfg c;
+  int PW = 32, BWa = 32, KT = 16, NTOT1 = 64, ld = 32;
+  int grid_tn = 148, grid_tn2 = 148;
+  long qrow0 = 0;        // first local row of the QR block (k0 on rank 0)
+  long m = 0;            // local QR rows
+  double *partial = nullptr, *Gfull = nullptr, *Y2full = nullptr, *top = nullptr;
+  double *ident = nullptr, *svec = nullptr, *Cglob = nullptr;
+  SmallState s{};
+  std::vector<Level> lv;        // local levels (0 = data rows)
+  std::vector<Level> glv;       // global tree levels over gathered rank R's
+  double* Rall = nullptr;       // gathered R's copy (nranks*KT x KT)
+  double* Rfinal = nullptr;
+};
+
+namespace {
+
+std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, long m, int KT, int nsm) {
+  std::vector<Level> lv;
+  // level 0
+  {
+    Level L{};
+    L.D = D0; L.ldd = ldd0; L.ncols = ncols0;
+    int b = chain_bmax(KT);
+    if (b > 128 && KT == 64) b = 128;
+    long target = 2L * nsm;
+    long per = (m + target - 1) / target;
+    long Lt = per > KT ? (per - KT + b - 1) / b : 0;
+    long rpc = KT + Lt * b;
+    long nch = (m + rpc - 1) / rpc;
+    if (nch < 1) nch = 1;
+    L.G = ChainGeom{m, b, (int)Lt, rpc, (int)nch};
+    L.UT = ar.take<double>((size_t)nch * (Lt + 1) * KT * KT);
+    L.R = ar.take<double>((size_t)nch * KT * KT);
+    lv.push_back(L);
+  }
+  while (lv.back().G.nchains > 1) {
+    const Level& P = lv.back();
+    Level L{};
+    L.D = P.R; L.ldd = KT; L.ncols = KT;
+    long nrows = (long)P.G.nchains * KT;
+    int g = 4;
+    long rpc = (long)KT * g;
+    long nch = (nrows + rpc - 1) / rpc;
+    L.G = ChainGeom{nrows, KT, g - 1, rpc, (int)nch};
+    L.UT = ar.take<double>((size_t)nch * g * KT * KT);
+    L.R = ar.take<double>((size_t)nch * KT * KT);
+    lv.push_back(L);
+  }
+  return lv;
+}
+
+size_t plan_levels_bytes(long m, int KT, int nsm) {
+  // mirror of plan_levels' allocations (+ alignment slack)
+  size_t tot = 0;
+  int b = chain_bmax(KT);
+  if (b > 128 && KT == 64) b = 128;
+  long target = 2L * nsm;
+  long per = (m + target - 1) / target;
+  long Lt = per > KT ? (per - KT + b - 1) / b : 0;
+  long rpc = KT + Lt * b;
+  long nch = (m + rpc - 1) / rpc;
+  if (nch < 1) nch = 1;
+  tot += ((size_t)nch * (Lt + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + 512;
+  while (nch > 1) {
+    long nrows = nch * KT;
+    long rpc2 = (long)KT * 4;
+    long n2 = (nrows + rpc2 - 1) / rpc2;
+    tot += ((size_t)n2 * 4 * KT * KT + (size_t)n2 * KT * KT) * 8 + 512;
+    nch = n2;
+  }
+  return tot;
+}
+
+int ensure_ws(ots_ctx* ctx, size_t bytes) {
+  if (bytes <= ctx->ws_size) return OTS_OK;
+  if (ctx->ws) cudaFree(ctx->ws);
+  ctx->ws = nullptr;
+  ctx->ws_size = 0;
+  size_t b = bytes + (bytes >> 3) + (1 << 20);
+  CK(cudaMalloc(&ctx->ws, b));
+  ctx->ws_size = b;
+  return OTS_OK;
+}
+
+int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st) {
+  for (auto& L : lv) {
+    FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R};
+    CK(launch_chain_factor(fa, KT, st));
+  }
+  return OTS_OK;
+}
+
+// Q-form from the top level (whose single chain gets C = Ctop) down to level 0.
+int run_qform_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, const double* Ctop, cudaStream_t st) {
+  const double* Cin = Ctop;
+  for (int l = (int)lv.size() - 1; l >= 0; --l) {
+    Level& L = lv[l];
+    QformArgs qa{L.D, L.ldd, L.ncols, L.G, L.UT, Cin};
+    CK(launch_chain_qform(qa, KT, st));
+    Cin = L.D;  // output rows of level l are the C's of level l-1's chains
+  }
+  return OTS_OK;
+}
+
+int grid_for_tn(int PW, int BW, bool alias, bool sym, int nsm) {
+  // warps per CTA = number of 32x32 tasks; smem-limited residency.
+  int mb = PW / 32;
+  int nt = (alias ? (sym ? mb * (mb + 1) / 2 : mb * mb) : 0) + mb * (BW / 32);
+  int stage = 32 * (PW + BW) * 8;
+  int nst = std::min(4, std::max(2, (200 * 1024) / stage));
+  int smem = nst * stage;
+  int by_smem = std::max(1, (227 * 1024) / (smem + 1024));
+  int by_threads = std::max(1, 2048 / (nt * 32));
+  int per = std::min(by_smem, by_threads);
+  (void)nt;
+  return nsm * per;
+}
+
+// Build the job (workspace layout + small-state pointers).
+int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
+  j.c = c;
+  const long k0 = c.k0, k = c.k;
+  j.PW = pad32(std::max<long>(k0, 1));
+  j.BWa = k <= 32 ? 32 : 64;
+  j.KT = kt_for(k);
+  j.NTOT1 = j.PW + j.BWa;
+  j.ld = std::max(j.PW, j.KT);
+  j.qrow0 = (c.row0 == 0) ? k0 : 0;
+  j.m = c.n_local - j.qrow0;
+  j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, ctx->nsm);
+  j.grid_tn2 = grid_for_tn(j.PW, j.BWa, false, false, ctx->nsm);
+  const int ld = j.ld, KT = j.KT;
+  const int gmax = std::max(j.grid_tn, j.grid_tn2);
+  size_t bytes = 0;
+  bytes += (size_t)gmax * j.PW * j.NTOT1 * 8 + 256;
+  bytes += (size_t)j.PW * j.NTOT1 * 8 * 2 + 512;                  // Gfull, Y2full
+  bytes += (size_t)k0 * (k0 + k + 2) * 8 + 256;                    // top rows
+  bytes += (size_t)16 * ld * ld * 8 + 16 * 256;                    // small matrices
+  bytes += (size_t)8 * ld * 8 + 8 * 256;                           // vectors
+  bytes += (size_t)KT * KT * 8 * 2 + 1024;                         // ident, svec
+  bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, ctx->nsm);
+  bytes += (size_t)64 * KT * KT * 8 * 4 + 4096;                    // global tree (<=64 ranks)
+  bytes += 64;
+  int rc = ensure_ws(ctx, bytes);
+  if (rc) return rc;
+  Arena ar(ctx->ws, ctx->ws_size);
+  j.partial = ar.take<double>((size_t)gmax * j.PW * j.NTOT1);
+  j.Gfull = ar.take<double>((size_t)j.PW * j.NTOT1);
+  j.Y2full = ar.take<double>((size_t)j.PW * j.NTOT1);
+  j.top = ar.take<double>((size_t)std::max<long>(k0, 1) * (k0 + k + 2));
+  SmallState& s = j.s;
+  s = SmallState{};
+  s.k0 = (int)k0; s.k = (int)k; s.ld = ld;
+  s.choice = c.choice; s.allow_defect = c.allow_defect; s.orth_tol = c.orth_tol;
+  s.V = c.V; s.ldv = c.ldv; s.A = c.A; s.lda = c.lda;
+  s.Gfull = j.Gfull; s.ldgf = j.NTOT1; s.gf_acol = j.PW;
+  s.Pexp = c.Pexp; s.ldpe = (int)c.ldp;
+  double** mats[] = {&s.G, &s.Vt, &s.At, &s.VbA, &s.P, &s.Tf, &s.Tdense, &s.Wt,
+                     &s.Z1, &s.Z2, &s.X1, &s.X2, &s.D1, &s.D2, &s.Sd};
+  for (auto m : mats) *m = ar.take<double>((size_t)ld * ld);
+  s.pvec = ar.take<double>(ld); s.tau = ar.take<double>(ld); s.sig = ar.take<double>(ld);
+  s.sig2 = ar.take<double>(ld); s.svec = ar.take<double>(std::max(ld, KT));
+  s.piv = ar.take<int>(ld);
+  s.diag = ar.take<double>(4);
+  s.status = ar.take<int>(4);
+  j.ident = ar.take<double>((size_t)KT * KT);
+  j.svec = s.svec;
+  j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, ctx->nsm);
+  j.Rall = ar.take<double>((size_t)64 * KT * KT);
+  j.Cglob = ar.take<double>((size_t)64 * KT * KT);
+  if (ar.off > ctx->ws_size) return fail(ctx, OTS_E_CUDA, "workspace plan overflow");
+  return OTS_OK;
+}
+
+int phase_gram(ots_ctx* ctx, Job& j) {
+  const JobCfg& c = j.c;
+  TnArgs a{};
+  a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = (int)c.k0;
+  a.B = c.A; a.ldb = c.lda; a.bc0 = 0; a.bcols = (int)c.k;
+  a.row_begin = 0; a.row_end = c.n_local;
+  a.b_row_begin = j.qrow0; a.p_row_begin = 0;
+  a.partial = j.partial;
+  CK(launch_tsgemm_tn(a, j.PW, j.BWa, true, true, j.grid_tn, c.st));
+  CK(launch_reduce(j.partial, j.grid_tn, (long)j.PW * j.NTOT1, j.Gfull, 1.0, c.st));
+  return OTS_OK;
+}
+
+int phase_apply1(ots_ctx* ctx, Job& j) {
+  const JobCfg& c = j.c;
+  NnArgs a{};
+  a.P = c.V; a.ldp = c.ldv; a.kdim = (int)c.k0;
+  a.Z = j.s.Z1; a.ldz = j.ld;
+  a.B = c.A; a.ldb = c.lda;
+  a.X = c.Q; a.ldx = c.ldq;
+  a.ncols = (int)c.k;
+  a.row_begin = j.qrow0; a.row_end = c.n_local;
+  a.colscale = nullptr;
+  CK(launch_tsgemm_nn(a, j.KT, ctx->nsm, c.st));
+  return OTS_OK;
+}
+
+int phase_gram2(ots_ctx* ctx, Job& j) {
+  const JobCfg& c = j.c;
+  TnArgs a{};
+  a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = (int)c.k0;
+  a.B = c.Q; a.ldb = c.ldq; a.bc0 = 0; a.bcols = (int)c.k;
+  a.row_begin = j.qrow0; a.row_end = c.n_local;
+  a.b_row_begin = j.qrow0; a.p_row_begin = j.qrow0;
+  a.partial = j.partial;
+  CK(launch_tsgemm_tn(a, j.PW, j.BWa, false, false, j.grid_tn2, c.st));
+  CK(launch_reduce(j.partial, j.grid_tn2, (long)j.PW * j.BWa, j.Y2full, -1.0, c.st));
+  return OTS_OK;
+}
+
+__global__ void copy_y2_kernel(const double* Y2full, int ldy, double* Z2, int ld, int k0, int k) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k0 * k; e += gridDim.x * blockDim.x) {
+    int i = e / k, jj = e - i * k;
+    Z2[i * ld + jj] = Y2full[i * ldy + jj];
+  }
+}
+
+int phase_apply2(ots_ctx* ctx, Job& j) {
+  const JobCfg& c = j.c;
+  NnArgs a{};
+  a.P = c.V; a.ldp = c.ldv; a.kdim = (int)c.k0;
+  a.Z = j.s.Z2; a.ldz = j.ld;
+  a.B = c.Q; a.ldb = c.ldq;
+  a.X = c.Q; a.ldx = c.ldq;
+  a.ncols = (int)c.k;
+  a.row_begin = j.qrow0; a.row_end = c.n_local;
+  a.colscale = j.svec;
+  CK(launch_tsgemm_nn(a, j.KT, ctx->nsm, c.st));
+  return OTS_OK;
+}
+
+int read_status(ots_ctx* ctx, Job& j, double* diag_host) {
+  const JobCfg& c = j.c;
+  CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaMemcpyAsync(ctx->h_diag, j.s.diag, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  CK(cudaStreamSynchronize(c.st));
+  if (diag_host) std::memcpy(diag_host, ctx->h_diag, 3 * sizeof(double));
+  int st = ctx->h_status[0];
+  if (st != 0) {
+    char buf[256];
+    if (st == OTS_E_ORTHONORMALITY)
+      snprintf(buf, sizeof buf, "||v^* v - I||_2 = %.3e exceeds %.1e", ctx->h_diag[2], c.orth_tol);
+    else if (st == OTS_E_NOT_PD)
+      snprintf(buf, sizeof buf, "Cholesky factor of T: matrix is not positive definite");
+    else if (st == OTS_E_SINGULAR_T)
+      snprintf(buf, sizeof buf, "T is numerically singular");
+    else if (st == OTS_E_PARAMETER)
+      snprintf(buf, sizeof buf, "explicit seed p is not unitary to tolerance");
+    else
+      snprintf(buf, sizeof buf, "status %d", st);
+    return fail(ctx, st, buf);
+  }
+  return OTS_OK;
+}
+
+int validate_layout(ots_ctx* ctx, const void* p, long ld, const char* name) {
+  if (p == nullptr) return OTS_OK;
+  if ((ld & 1) || !aligned16(p))
+    return fail(ctx, OTS_E_VALUE, std::string(name) + ": rows must be 16-byte aligned (even ld)");
+  return OTS_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// exported C-ABI
+// ===========================================================================
+extern "C" {
+
+int ots_version(void) { return 1; }
+
+int ots_ctx_create(int device, ots_ctx** out) {
+  if (!out) return OTS_E_VALUE;
+  ots_ctx* c = new ots_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return OTS_E_CUDA; }
+  cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
+  cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_seed, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_diag, cudaEventDisableTiming);
+  cudaMallocHost(&c->h_status, 64);
+  cudaMallocHost(&c->h_diag, 64);
+  *out = c;
+  e = cudaGetLastError();
+  if (e != cudaSuccess) { c->err = cudaGetErrorString(e); return OTS_E_CUDA; }
+  return OTS_OK;
+}
+
+void ots_ctx_destroy(ots_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->ws) cudaFree(c->ws);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_seed) cudaEventDestroy(c->ev_seed);
+  if (c->ev_diag) cudaEventDestroy(c->ev_diag);
+  if (c->h_status) cudaFreeHost(c->h_status);
+  if (c->h_diag) cudaFreeHost(c->h_diag);
+  for (auto e : c->pev) cudaEventDestroy(e);
+  delete c->job;
+  delete c;
+}
+
+const char* ots_last_error(const ots_ctx* c) { return c ? c->err.c_str() : "null context"; }
+int ots_sm_count(const ots_ctx* c) { return c ? c->nsm : 0; }
+
+int ots_set_profiling(ots_ctx* c, int enable) { c->profile = enable != 0; return OTS_OK; }
+
+int ots_last_profile(const ots_ctx* c, char* names, int cap, float* ms, int mcap) {
+  std::string all;
+  int n = (int)c->pms.size();
+  for (int i = 0; i < n; ++i) {
+    if (i < mcap) ms[i] = c->pms[i];
+    all += c->last_names[i];
+    all += "\n";
+  }
+  if (names && cap > 0) {
+    strncpy(names, all.c_str(), cap - 1);
+    names[cap - 1] = 0;
+  }
+  return n;
+}
+
+int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const double* V, int64_t ldv,
+                      const double* A, int64_t lda, int choice, int intra, const double* P, int64_t ldp,
+                      double orth_tol, int allow_defect, double* Q, int64_t ldq, double* R, int64_t ldr,
+                      double* S, int64_t lds, double* diag_host, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0 || k0 < 0 || k < 0) return fail(ctx, OTS_E_DIMENSION, "negative dimension");
+  if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
+  if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
+  if (k0 > 128) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 128 not supported by this build");
+  if (intra != OTS_INTRA_HOUSEHOLDER) return fail(ctx, OTS_E_UNSUPPORTED, "intra method not in this build");
+  if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
+  if (choice == OTS_CHOICE_EXPLICIT && P == nullptr)
+    return fail(ctx, OTS_E_PARAMETER, "choice='explicit' requires a seed matrix p");
+  int rc;
+  if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
+  if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
+  if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
+  if (k == 0) return OTS_OK;
+  if (k0 == 0) {
+    rc = ots_householder_qr_f64(ctx, n, k, A, lda, Q, ldq, R, ldr, 0, stream);
+    if (diag_host) { diag_host[0] = 1.0; diag_host[1] = 0.0; diag_host[2] = 0.0; }
+    return rc;
+  }
+  JobCfg c{n, 0, k0, k, V, ldv, A, lda, Q, ldq, choice, P, ldp, orth_tol, allow_defect, st, false};
+  Job j;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  const int KT = j.KT;
+  prof_begin(ctx, st);
+  if ((rc = phase_gram(ctx, j))) return rc;
+  prof_mark(ctx, st, "gram");
+  j.s.Sout = S; j.s.lds_out = (int)lds;
+  CK(launch_seed(j.s, st));
+  CK(cudaEventRecord(ctx->ev_seed, st));
+  prof_mark(ctx, st, "seed");
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
+  CK(launch_diag(j.s, ctx->side));
+  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
+  if ((rc = phase_apply1(ctx, j))) return rc;
+  prof_mark(ctx, st, "apply1");
+  if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
+  prof_mark(ctx, st, "factor");
+  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
+  if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st))) return rc;
+  prof_mark(ctx, st, "qform");
+  CK(launch_sign(j.s, Q + k0 * ldq, ldq, j.lv.back().R, KT, R, (int)ldr, st));
+  if ((rc = phase_gram2(ctx, j))) return rc;
+  prof_mark(ctx, st, "gram2");
+  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
+  CK(launch_z2(j.s, st));
+  prof_mark(ctx, st, "z2");
+  if ((rc = phase_apply2(ctx, j))) return rc;
+  prof_mark(ctx, st, "apply2");
+  CK(launch_qtop(j.s, Q, ldq, st));
+  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
+  prof_mark(ctx, st, "tail");
+  rc = read_status(ctx, j, diag_host);
+  prof_end(ctx);
+  return rc;
+}
+
+int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, int64_t lda, double* Q,
+                           int64_t ldq, double* R, int64_t ldr, int nonneg_diag, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < k) return fail(ctx, OTS_E_DIMENSION, "need rows >= cols");
+  if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
+  int rc;
+  if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
+  if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
+  if (k == 0) return OTS_OK;
+  JobCfg c{m, 1 /*row0!=0: no top block*/, 0, k, nullptr, 0, A, lda, Q, ldq, OTS_CHOICE_QR, nullptr, 0,
+           1e-8, 0, st, false};
+  Job j;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  const int KT = j.KT;
+  prof_begin(ctx, st);
+  if (A != Q) CK(cudaMemcpy2DAsync(Q, ldq * 8, A, lda * 8, k * 8, m, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(j.s.status, 0, sizeof(int), st));
+  if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
+  prof_mark(ctx, st, "factor");
+  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
+  if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st))) return rc;
+  prof_mark(ctx, st, "qform");
+  CK(launch_sign(j.s, Q, ldq, j.lv.back().R, KT, R, (int)ldr, st));
+  // Q <- Q diag(s)
+  NnArgs a{};
+  a.P = nullptr; a.ldp = 0; a.kdim = 0; a.Z = nullptr; a.ldz = 0;
+  a.B = Q; a.ldb = ldq; a.X = Q; a.ldx = ldq; a.ncols = (int)k;
+  a.row_begin = 0; a.row_end = m; a.colscale = j.svec;
+  CK(launch_tsgemm_nn(a, KT, ctx->nsm, st));
+  if (nonneg_diag) nonneg_fix_kernel<<<std::min<long>(1024, (m * k + 255) / 256), 256, 0, st>>>(Q, ldq, m, (int)k, R, ldr);
+  prof_mark(ctx, st, "sign");
+  CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  prof_end(ctx);
+  CK(cudaGetLastError());
+  return OTS_OK;
+}
+
+int ots_modified_lu_f64(ots_ctx* ctx, int64_t n, const double* Z, int64_t ldz, double* LU, double* p,
+                        void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 0) return OTS_OK;
+  if (n > 512) return fail(ctx, OTS_E_UNSUPPORTED, "n > 512");
+  int rc = ensure_ws(ctx, (size_t)(n * n + 2 * n + 64) * 8);
+  if (rc) return rc;
+  double* work = reinterpret_cast<double*>(ctx->ws);
+  int* status = reinterpret_cast<int*>(work + n * n + 2 * n + 8);
+  CK(launch_mlu(Z, (int)ldz, (int)n, LU, p, work, status, st));
+  CK(cudaMemcpyAsync(ctx->h_status, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ctx->h_status[0] == OTS_E_NORM_BOUND) return fail(ctx, OTS_E_NORM_BOUND, "||z||_2 exceeds 1 beyond tolerance");
+  return OTS_OK;
+}
+
+// ----------------------------- distributed phases -------------------------
+int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int64_t k, const double* V,
+                   int64_t ldv, const double* A, int64_t lda, double* Q, int64_t ldq, int choice,
+                   const double* P, int64_t ldp, double orth_tol, void* stream) {
+  cudaSetDevice(ctx->device);
+  if (k > 64 || k0 > 128 || k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "shape not in this build");
+  if (row0 == 0 && n_local < k0 + k) return fail(ctx, OTS_E_DIMENSION, "rank 0 must own >= k0+k rows");
+  int rc;
+  if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
+  if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
+  if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
+  delete ctx->job;
+  ctx->job = new Job();
+  JobCfg c{n_local, row0, k0, k, V, ldv, A, lda, Q, ldq, choice, P, ldp, orth_tol, 0,
+           (cudaStream_t)stream, true};
+  return job_setup(ctx, *ctx->job, c);
+}
+
+int ots_dist_gram(ots_ctx* ctx, double* gram_out, int64_t* count) {
+  Job& j = *ctx->job;
+  int rc = phase_gram(ctx, j);
+  if (rc) return rc;
+  long cnt = (long)j.PW * j.NTOT1;
+  if (count) *count = cnt;
+  if (gram_out) CK(cudaMemcpyAsync(gram_out, j.Gfull, cnt * 8, cudaMemcpyDeviceToDevice, j.c.st));
+  return OTS_OK;
+}
+
+__global__ void pack_top_kernel(const double* V, long ldv, const double* A, long lda, int k0, int k,
+                                double* top, int ldt) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k0 * (k0 + k); e += gridDim.x * blockDim.x) {
+    int i = e / (k0 + k), jj = e - i * (k0 + k);
+    top[i * ldt + jj] = jj < k0 ? V[(long)i * ldv + jj] : A[(long)i * lda + (jj - k0)];
+  }
+}
+
+int ots_dist_top_rows(ots_ctx* ctx, double* top_out, int64_t* count) {
+  Job& j = *ctx->job;
+  const long k0 = j.c.k0, k = j.c.k;
+  const int ldt = (int)((k0 + k + 1) & ~1L);
+  if (count) *count = k0 * ldt;
+  if (top_out && j.c.row0 == 0)
+    pack_top_kernel<<<32, 256, 0, j.c.st>>>(j.c.V, j.c.ldv, j.c.A, j.c.lda, (int)k0, (int)k, top_out, ldt);
+  CK(cudaGetLastError());
+  return OTS_OK;
+}
+
+int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows) {
+  Job& j = *ctx->job;
+  const long k0 = j.c.k0, k = j.c.k;
+  const int ldt = (int)((k0 + k + 1) & ~1L);
+  if (gram_sum && gram_sum != j.Gfull)
+    CK(cudaMemcpyAsync(j.Gfull, gram_sum, (size_t)j.PW * j.NTOT1 * 8, cudaMemcpyDeviceToDevice, j.c.st));
+  if (top_rows) {
+    CK(cudaMemcpyAsync(j.top, top_rows, (size_t)k0 * ldt * 8, cudaMemcpyDeviceToDevice, j.c.st));
+    j.s.V = j.top; j.s.ldv = ldt; j.s.A = j.top + k0; j.s.lda = ldt;
+  }
+  j.s.Sout = j.s.Sd;  // S kept on device until finish
+  j.s.lds_out = j.ld;
+  CK(launch_seed(j.s, j.c.st));
+  CK(launch_diag(j.s, j.c.st));
+  return OTS_OK;
+}
+
+int ots_dist_factor(ots_ctx* ctx, double* r_local_out, int64_t* kt) {
+  Job& j = *ctx->job;
+  int rc = phase_apply1(ctx, j);
+  if (rc) return rc;
+  if ((rc = run_factor_levels(ctx, j.lv, j.KT, j.c.st))) return rc;
+  if (kt) *kt = j.KT;
+  if (r_local_out)
+    CK(cudaMemcpyAsync(r_local_out, j.lv.back().R, (size_t)j.KT * j.KT * 8, cudaMemcpyDeviceToDevice, j.c.st));
+  return OTS_OK;
+}
+
+int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank) {
+  Job& j = *ctx->job;
+  const int KT = j.KT;
+  cudaStream_t st = j.c.st;
+  if (nranks > 64) return fail(ctx, OTS_E_UNSUPPORTED, "more than 64 ranks");
+  CK(cudaMemcpyAsync(j.Rall, r_all, (size_t)nranks * KT * KT * 8, cudaMemcpyDeviceToDevice, st));
+  // global levels over the gathered rank R's (rows = nranks*KT)
+  char* base = reinterpret_cast<char*>(j.Cglob + (size_t)64 * KT * KT);
+  (void)base;
+  std::vector<Level> g;
+  {
+    // reuse the tail of the workspace: carve from a fresh arena after Cglob
+    size_t used = (reinterpret_cast<char*>(j.Cglob + (size_t)64 * KT * KT) - ctx->ws);
+    size_t need = plan_levels_bytes((long)nranks * KT, KT, 1) + 4096;
+    if (used + need > ctx->ws_size) return fail(ctx, OTS_E_CUDA, "workspace too small for tree");
+    Arena ar(ctx->ws + used, ctx->ws_size - used);
+    // one chain per 4 R's (same shape as the local tree levels)
+    Level L{};
+    L.D = j.Rall; L.ldd = KT; L.ncols = KT;
+    long nrows = (long)nranks * KT;
+    long rpc = (long)KT * 4;
+    L.G = ChainGeom{nrows, KT, 3, rpc, (int)((nrows + rpc - 1) / rpc)};
+    L.UT = ar.take<double>((size_t)L.G.nchains * 4 * KT * KT);
+    L.R = ar.take<double>((size_t)L.G.nchains * KT * KT);
+    g.push_back(L);
+    while (g.back().G.nchains > 1) {
+      const Level& P = g.back();
+      Level M{};
+      M.D = P.R; M.ldd = KT; M.ncols = KT;
+      long nr = (long)P.G.nchains * KT;
+      M.G = ChainGeom{nr, KT, 3, rpc, (int)((nr + rpc - 1) / rpc)};
+      M.UT = ar.take<double>((size_t)M.G.nchains * 4 * KT * KT);
+      M.R = ar.take<double>((size_t)M.G.nchains * KT * KT);
+      g.push_back(M);
+    }
+  }
+  j.glv = g;
+  int rc;
+  if ((rc = run_factor_levels(ctx, j.glv, KT, st))) return rc;
+  j.Rfinal = j.glv.back().R;
+  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
+  if ((rc = run_qform_levels(ctx, j.glv, KT, j.ident, st))) return rc;
+  // this rank's C block: rows [rank*KT, rank*KT+KT) of Rall (now output rows)
+  CK(cudaMemcpyAsync(j.Cglob, j.Rall + (size_t)rank * KT * KT, (size_t)KT * KT * 8, cudaMemcpyDeviceToDevice, st));
+  return OTS_OK;
+}
+
+int ots_dist_qform(ots_ctx* ctx, double* y2_out, int64_t* count, double* sign_out) {
+  Job& j = *ctx->job;
+  cudaStream_t st = j.c.st;
+  int rc;
+  if ((rc = run_qform_levels(ctx, j.lv, j.KT, j.Cglob, st))) return rc;
+  if (j.c.row0 == 0) {
+    CK(launch_sign(j.s, j.c.Q + j.c.k0 * j.c.ldq, j.c.ldq, j.Rfinal, j.KT, j.s.D1 /*scratch R*/, j.ld, st));
+    if (sign_out) CK(cudaMemcpyAsync(sign_out, j.svec, j.c.k * 8, cudaMemcpyDeviceToDevice, st));
+  }
+  if ((rc = phase_gram2(ctx, j))) return rc;
+  long cnt = (long)j.PW * j.BWa;
+  if (count) *count = cnt;
+  if (y2_out) CK(cudaMemcpyAsync(y2_out, j.Y2full, cnt * 8, cudaMemcpyDeviceToDevice, st));
+  return OTS_OK;
+}
+
+__global__ void rscale_kernel(const double* Rfin, int ldr, const double* s, double* R, long ldro, int k) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    int i = e / k, jj = e - i * k;
+    R[i * ldro + jj] = (jj >= i) ? s[i] * Rfin[i * ldr + jj] : 0.0;
+  }
+}
+__global__ void copy_s_kernel(const double* Sd, int ld, double* S, long lds, int k0, int k) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k0 * k; e += gridDim.x * blockDim.x) {
+    int i = e / k, jj = e - i * k;
+    S[i * lds + jj] = Sd[i * ld + jj];
+  }
+}
+
+int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign, double* R, int64_t ldr, double* S,
+                    int64_t lds, double* diag_host) {
+  Job& j = *ctx->job;
+  cudaStream_t st = j.c.st;
+  const int k0 = (int)j.c.k0, k = (int)j.c.k;
+  if (y2_sum && y2_sum != j.Y2full)
+    CK(cudaMemcpyAsync(j.Y2full, y2_sum, (size_t)j.PW * j.BWa * 8, cudaMemcpyDeviceToDevice, st));
+  if (sign && sign != j.svec) CK(cudaMemcpyAsync(j.svec, sign, (size_t)k * 8, cudaMemcpyDeviceToDevice, st));
+  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, k0, k);
+  CK(launch_z2(j.s, st));
+  int rc;
+  if ((rc = phase_apply2(ctx, j))) return rc;
+  if (j.c.row0 == 0) CK(launch_qtop(j.s, j.c.Q, j.c.ldq, st));
+  if (R) rscale_kernel<<<8, 256, 0, st>>>(j.Rfinal, j.KT, j.svec, R, ldr, k);
+  if (S) copy_s_kernel<<<8, 256, 0, st>>>(j.s.Sd, j.ld, S, lds, k0, k);
+  return read_status(ctx, j, diag_host);
+}
+
+}  // extern "C"

@@ -1,0 +1,693 @@
+// k0 x k0 / k0 x k dense work on one CTA (FP64): seed construction of the
+// generalized Householder reflector (reflector.py:174-204), the T-solvers
+// (reflector.py:80-153), the orthonormality check (core.py:43-49 via
+// reflector.py:220-223), diagnostics from k0 x k0 data only (reflector.py:
+// 241-247), LAPACK sign recovery for the intra QR
+// (SURVEY Appendix A.1), and the small tails of Algorithm 1 (twostage.py:92,96).
+//
+// All routines are block-cooperative: every thread of the CTA calls them.
+// Matrices are row-major with an explicit leading dimension and may live in
+// shared or global (L2-resident) memory (generic addressing).
+#include "common.cuh"
+#include "small.cuh"
+
+namespace ots {
+
+#define BLK_FOR(i, n) for (int i = threadIdx.x; i < (n); i += blockDim.x)
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  // red: >= 32 doubles of smem scratch
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  __syncthreads();
+  return s;
+}
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = red[0];
+  for (int i = 1; i < nw; ++i) s = fmax(s, red[i]);
+  __syncthreads();
+  return s;
+}
+
+__device__ void blk_copy(double* D, int ldd, const double* Sr, int lds, int m, int n) {
+  BLK_FOR(e, m * n) { int i = e / n, j = e - i * n; D[i * ldd + j] = Sr[(long)i * lds + j]; }
+}
+
+__device__ void blk_identity(double* D, int ldd, int n) {
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; D[i * ldd + j] = (i == j) ? 1.0 : 0.0; }
+}
+
+// C = alpha * op(A) op(B) + beta * C   (naive, block-parallel over entries)
+__device__ void blk_gemm(double* Cm, int ldc, const double* A, int lda, bool ta, const double* B,
+                         int ldb, bool tb, int m, int n, int k, double alpha, double beta) {
+  __syncthreads();
+  BLK_FOR(e, m * n) {
+    int i = e / n, j = e - i * n;
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) {
+      double av = ta ? A[l * lda + i] : A[i * lda + l];
+      double bv = tb ? B[j * ldb + l] : B[l * ldb + j];
+      s = fma(av, bv, s);
+    }
+    Cm[i * ldc + j] = alpha * s + (beta == 0.0 ? 0.0 : beta * Cm[i * ldc + j]);
+  }
+  __syncthreads();
+}
+
+// Solve op(A) X = B in place (B: n x nrhs).  A triangular (lower/upper as
+// stored); trans solves with A^T.  Substitution order as trtrs.
+__device__ void blk_trsm(const double* A, int lda, bool lower, bool trans, bool unit, double* B,
+                         int ldb, int n, int nrhs) {
+  // effective matrix E = op(A); E is lower iff (lower xor trans)
+  const bool elower = lower != trans;
+  __syncthreads();
+  for (int s = 0; s < n; ++s) {
+    const int i = elower ? s : (n - 1 - s);
+    const double dii = unit ? 1.0 : A[i * lda + i];
+    BLK_FOR(j, nrhs) B[i * ldb + j] /= dii;
+    __syncthreads();
+    // eliminate x_i from remaining rows
+    const int rem = elower ? (n - 1 - i) : i;
+    BLK_FOR(e, rem * nrhs) {
+      int rr = e / nrhs, j = e - rr * nrhs;
+      int r = elower ? (i + 1 + rr) : rr;
+      double eri = trans ? A[i * lda + r] : A[r * lda + i];
+      B[r * ldb + j] = fma(-eri, B[i * ldb + j], B[r * ldb + j]);
+    }
+    __syncthreads();
+  }
+}
+
+// dgeqr2 on an m x n block (m >= n), LAPACK dlarfg conventions; v below the
+// diagonal, R on/above, tau[n].
+__device__ void blk_geqr2(double* A, int lda, int m, int n, double* tau, double* red) {
+  for (int j = 0; j < n; ++j) {
+    double s2 = 0.0;
+    for (int r = j + 1 + (int)threadIdx.x; r < m; r += blockDim.x) { double x = A[r * lda + j]; s2 = fma(x, x, s2); }
+    s2 = block_sum(s2, red);
+    const double alpha = A[j * lda + j];
+    double beta = alpha, tj = 0.0, scal = 0.0;
+    if (s2 != 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    if (s2 != 0.0)
+      for (int r = j + 1 + (int)threadIdx.x; r < m; r += blockDim.x) A[r * lda + j] *= scal;
+    if (threadIdx.x == 0) { A[j * lda + j] = beta; tau[j] = tj; }
+    __syncthreads();
+    if (tj != 0.0) {
+      // trailing columns c > j: w = v^T A[:, c]; A[:,c] -= tau w v   (one warp per column)
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int c = j + 1 + w; c < n; c += nw) {
+        double d = 0.0;
+        for (int r = j + 1 + l; r < m; r += 32) d = fma(A[r * lda + j], A[r * lda + c], d);
+        d = warp_sum(d) + A[j * lda + c];
+        const double wc = tj * d;
+        if (l == 0) A[j * lda + c] -= wc;
+        for (int r = j + 1 + l; r < m; r += 32) A[r * lda + c] = fma(-wc, A[r * lda + j], A[r * lda + c]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// dorg2r: Q (m x n) from the reflectors stored in A (in place -> Q); W scratch n*... unused
+__device__ void blk_org2r(double* A, int lda, int m, int n, const double* tau, double* red) {
+  // Q = H_0 ... H_{n-1} [I; 0], accumulated backwards in place like dorg2r.
+  for (int j = n - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    // apply H_j to Q[j:m, j+1:n]  (columns right of j already hold Q columns)
+    if (j < n - 1 && tj != 0.0) {
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int c = j + 1 + w; c < n; c += nw) {
+        double d = 0.0;
+        for (int r = j + 1 + l; r < m; r += 32) d = fma(A[r * lda + j], A[r * lda + c], d);
+        d = warp_sum(d) + A[j * lda + c];
+        const double wc = tj * d;
+        if (l == 0) A[j * lda + c] -= wc;
+        for (int r = j + 1 + l; r < m; r += 32) A[r * lda + c] = fma(-wc, A[r * lda + j], A[r * lda + c]);
+      }
+    } else if (j < n - 1) {
+      // tau == 0: H_j = I, nothing to do for the trailing columns
+    }
+    __syncthreads();
+    // column j: Q[j:, j] = e_j - tau v ; Q[0:j, j] = 0
+    for (int r = (int)threadIdx.x; r < m; r += blockDim.x) {
+      if (r < j) A[r * lda + j] = 0.0;
+      else if (r == j) A[r * lda + j] = 1.0 - tj;
+      else A[r * lda + j] = -tj * A[r * lda + j];
+    }
+    __syncthreads();
+  }
+}
+
+// Modified LU (reflector.py:53-77 / paper Alg. 2) in place:
+// Z -> L (strict lower, unit diag implied) and U (upper), p[n].
+// signrec=true applies the LAPACK-sign-recovery variant: a pivot
+// with |z_ii| == 1 exactly keeps p_i = +sign(z_ii) and skips its elimination.
+__device__ void blk_mlu(double* Z, int ld, int n, double* p, bool signrec) {
+  for (int i = 0; i < n; ++i) {
+    __syncthreads();
+    const double zi = Z[i * ld + i];
+    bool skip = signrec && fabs(zi) == 1.0;
+    double pi;
+    if (skip) pi = (zi >= 0.0) ? 1.0 : -1.0;
+    else pi = (zi >= 0.0) ? -1.0 : 1.0;
+    const double uii = pi - zi;
+    __syncthreads();
+    if (threadIdx.x == 0) { p[i] = pi; Z[i * ld + i] = uii; }
+    if (skip) {
+      BLK_FOR(r, n - i - 1) Z[(i + 1 + r) * ld + i] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    // U row i (c > i): u = -work ; L col i: l = -work / uii
+    BLK_FOR(r, n - i - 1) {
+      int rr = i + 1 + r;
+      Z[i * ld + rr] = -Z[i * ld + rr];
+      Z[rr * ld + i] = -Z[rr * ld + i] / uii;
+    }
+    __syncthreads();
+    const int m = n - i - 1;
+    BLK_FOR(e, m * m) {
+      int a = e / m, b = e - a * m;
+      int r = i + 1 + a, c = i + 1 + b;
+      Z[r * ld + c] = fma(Z[r * ld + i], Z[i * ld + c], Z[r * ld + c]);
+    }
+  }
+  __syncthreads();
+}
+
+// Cholesky (lower, in place; upper part zeroed).  Returns false on a
+// non-positive pivot.
+__device__ bool blk_cholesky(double* A, int ld, int n, double* red) {
+  bool ok = true;
+  for (int j = 0; j < n; ++j) {
+    __syncthreads();
+    double d = A[j * ld + j];
+    if (!(d > 0.0)) { ok = false; break; }
+    const double ljj = sqrt(d);
+    __syncthreads();
+    if (threadIdx.x == 0) A[j * ld + j] = ljj;
+    BLK_FOR(r, n - j - 1) A[(j + 1 + r) * ld + j] /= ljj;
+    __syncthreads();
+    const int m = n - j - 1;
+    BLK_FOR(e, m * m) {
+      int a = e / m, b = e - a * m;
+      if (b <= a) {
+        int r = j + 1 + a, c = j + 1 + b;
+        A[r * ld + c] = fma(-A[r * ld + j], A[c * ld + j], A[r * ld + c]);
+      }
+    }
+  }
+  __syncthreads();
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; if (j > i) A[i * ld + j] = 0.0; }
+  __syncthreads();
+  return ok;
+}
+
+// LU with partial pivoting (getrf), in place; piv[i] = row swapped with i.
+// Returns false if an exactly zero pivot appears (SingularTError).
+__device__ bool blk_getrf(double* A, int ld, int n, int* piv, double* red, int* ired) {
+  bool ok = true;
+  for (int j = 0; j < n; ++j) {
+    // argmax |A[r][j]|, r >= j  (first max index, as idamax)
+    double best = -1.0; int bi = j;
+    for (int r = j + (int)threadIdx.x; r < n; r += blockDim.x) {
+      double v = fabs(A[r * ld + j]);
+      if (v > best) { best = v; bi = r; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = (blockDim.x + 31) >> 5;
+    __syncthreads();
+    if (l == 0) { red[w] = best; ired[w] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double b = red[0]; int ii = ired[0];
+      for (int q = 1; q < nw; ++q) if (red[q] > b || (red[q] == b && ired[q] < ii)) { b = red[q]; ii = ired[q]; }
+      ired[32] = ii;
+      piv[j] = ii;
+    }
+    __syncthreads();
+    const int pr = ired[32];
+    if (pr != j) BLK_FOR(c, n) { double t = A[j * ld + c]; A[j * ld + c] = A[pr * ld + c]; A[pr * ld + c] = t; }
+    __syncthreads();
+    const double d = A[j * ld + j];
+    if (d == 0.0) { ok = false; continue; }
+    BLK_FOR(r, n - j - 1) A[(j + 1 + r) * ld + j] /= d;
+    __syncthreads();
+    const int m = n - j - 1;
+    BLK_FOR(e, m * m) {
+      int a = e / m, b = e - a * m;
+      int r = j + 1 + a, c = j + 1 + b;
+      A[r * ld + c] = fma(-A[r * ld + j], A[j * ld + c], A[r * ld + c]);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  return ok;
+}
+
+// One-sided Jacobi (Hestenes) on the ROWS of W (n x n, row-major, ld):
+// rotates row pairs until mutually orthogonal.  If Jt != null the same
+// rotations are applied to the rows of Jt.  sigma[i] = ||row i|| at exit.
+// Parallel round-robin ordering: n/2 disjoint pairs per step.
+__device__ void blk_jacobi_rows(double* W, int ldw, double* Jt, int ldj, int n, double* sigma,
+                                double* red) {
+  const int ne = (n + 1) & ~1;  // even count incl. a dummy
+  const int npairs = ne / 2;
+  int gs = 1;
+  while (gs * 2 * npairs <= (int)blockDim.x && gs < 32) gs *= 2;
+  const int grp = threadIdx.x / gs, gl = threadIdx.x % gs;
+  const unsigned gmask = (gs == 32) ? 0xffffffffu : (((1u << gs) - 1u) << ((threadIdx.x & 31) & ~(gs - 1)));
+  const double tol = 4.0 * 2.220446049250313e-16 * (n > 4 ? n : 4);
+  __shared__ int rotated;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    int my_rot = 0;
+    for (int rd = 0; rd < ne - 1; ++rd) {
+      if (grp < npairs) {
+        int p, q;
+        if (grp == 0) { p = ne - 1; q = rd; }
+        else { p = (rd + grp) % (ne - 1); q = (rd - grp + (ne - 1)) % (ne - 1); }
+        if (p < n && q < n) {
+          double a = 0, b = 0, c = 0;
+          for (int e = gl; e < n; e += gs) {
+            double x = W[p * ldw + e], y = W[q * ldw + e];
+            a = fma(x, x, a); b = fma(y, y, b); c = fma(x, y, c);
+          }
+          for (int o = gs / 2; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(gmask, a, o);
+            b += __shfl_xor_sync(gmask, b, o);
+            c += __shfl_xor_sync(gmask, c, o);
+          }
+          if (c != 0.0 && fabs(c) > tol * sqrt(a) * sqrt(b)) {
+            double zeta = (b - a) / (2.0 * c);
+            double tt;
+            if (fabs(zeta) > 1e150) tt = 0.5 / zeta;
+            else tt = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+            double cs = 1.0 / sqrt(fma(tt, tt, 1.0));
+            double sn = cs * tt;
+            for (int e = gl; e < n; e += gs) {
+              double x = W[p * ldw + e], y = W[q * ldw + e];
+              W[p * ldw + e] = cs * x - sn * y;
+              W[q * ldw + e] = sn * x + cs * y;
+            }
+            if (Jt)
+              for (int e = gl; e < n; e += gs) {
+                double x = Jt[p * ldj + e], y = Jt[q * ldj + e];
+                Jt[p * ldj + e] = cs * x - sn * y;
+                Jt[q * ldj + e] = sn * x + cs * y;
+              }
+            my_rot = 1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (my_rot) rotated = 1;
+    __syncthreads();
+    int any = rotated;
+    __syncthreads();
+    if (!any) break;
+  }
+  // row norms
+  for (int i = 0; i < n; ++i) {
+    double s = 0.0;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) { double x = W[i * ldw + e]; s = fma(x, x, s); }
+    s = block_sum(s, red);
+    if (threadIdx.x == 0) sigma[i] = sqrt(s);
+  }
+  __syncthreads();
+}
+
+__device__ double blk_sigma_max(double* W, int ld, int n, double* sig, double* red) {
+  blk_jacobi_rows(W, ld, nullptr, 0, n, sig, red);
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, sig[i]);
+  return block_max(m, red);
+}
+
+// ---------------------------------------------------------------------------
+// T-solver dispatch (reflector.py:80-153).  X (n x m) overwritten.
+//   adjoint=false: T X = B ; adjoint=true: T^T X = B.
+// ---------------------------------------------------------------------------
+__device__ void t_solve(const SmallState& s, double* X, int ldx, int m, bool adjoint) {
+  const int n = s.k0;
+  const double* F = s.Tf;
+  const int ld = s.ld;
+  switch (s.choice) {
+    case CHOICE_QR:  // lower triangular T
+      blk_trsm(F, ld, true, adjoint, false, X, ldx, n, m);
+      break;
+    case CHOICE_POLAR:  // T = L L^T
+      blk_trsm(F, ld, true, false, false, X, ldx, n, m);
+      blk_trsm(F, ld, true, true, false, X, ldx, n, m);
+      break;
+    case CHOICE_MLU:
+      if (adjoint) {  // diag(p) L U x = b
+        BLK_FOR(e, n * m) { int i = e / m; X[i * ldx + (e - i * m)] *= s.pvec[i]; }
+        blk_trsm(F, ld, true, false, true, X, ldx, n, m);
+        blk_trsm(F, ld, false, false, false, X, ldx, n, m);
+      } else {        // U^T L^T diag(p) x = b
+        blk_trsm(F, ld, false, true, false, X, ldx, n, m);
+        blk_trsm(F, ld, true, true, true, X, ldx, n, m);
+        __syncthreads();
+        BLK_FOR(e, n * m) { int i = e / m; X[i * ldx + (e - i * m)] *= s.pvec[i]; }
+      }
+      break;
+    case CHOICE_EXPLICIT:  // P_piv L U = T (getrf); getrs semantics
+      if (!adjoint) {
+        for (int i = 0; i < n; ++i) {  // apply row swaps forward
+          int pr = s.piv[i];
+          __syncthreads();
+          if (pr != i) BLK_FOR(j, m) { double t = X[i * ldx + j]; X[i * ldx + j] = X[pr * ldx + j]; X[pr * ldx + j] = t; }
+        }
+        blk_trsm(F, ld, true, false, true, X, ldx, n, m);
+        blk_trsm(F, ld, false, false, false, X, ldx, n, m);
+      } else {
+        blk_trsm(F, ld, false, true, false, X, ldx, n, m);
+        blk_trsm(F, ld, true, true, true, X, ldx, n, m);
+        for (int i = n - 1; i >= 0; --i) {  // swaps backward
+          int pr = s.piv[i];
+          __syncthreads();
+          if (pr != i) BLK_FOR(j, m) { double t = X[i * ldx + j]; X[i * ldx + j] = X[pr * ldx + j]; X[pr * ldx + j] = t; }
+        }
+      }
+      break;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------------
+
+// Seed: Gram check, P/T construction, W_top, Z1 = T^{-T}(W^T A), S = P^T (H^T A)_top
+__global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
+  __shared__ double red[64];
+  __shared__ int ired[64];
+  const int n = s.k0, k = s.k, ld = s.ld;
+  if (threadIdx.x == 0) { s.status[0] = 0; }
+  // 1. symmetric Gram (lower blocks valid) and V_b^T A_b
+  BLK_FOR(e, n * n) {
+    int i = e / n, j = e - i * n;
+    double g = (j <= i) ? s.Gfull[(long)i * s.ldgf + j] : s.Gfull[(long)j * s.ldgf + i];
+    s.G[i * ld + j] = g;
+    s.X1[i * ld + j] = g - (i == j ? 1.0 : 0.0);
+  }
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.VbA[i * ld + j] = s.Gfull[(long)i * s.ldgf + s.gf_acol + j]; }
+  __syncthreads();
+  // 2. orthonormality defect (Frobenius shortcut; exact 2-norm only if needed)
+  double f = 0.0;
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; double x = s.X1[i * ld + j]; f = fma(x, x, f); }
+  f = sqrt(block_sum(f, red));
+  double defect = f;
+  if (f > s.orth_tol) defect = blk_sigma_max(s.X1, ld, n, s.sig, red);
+  if (threadIdx.x == 0) s.diag[2] = defect;
+  if (defect > s.orth_tol && !s.allow_defect) {
+    if (threadIdx.x == 0) s.status[0] = OTS_E_ORTHONORMALITY;
+    return;
+  }
+  // 3. V_t, A_t
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.Vt[i * ld + j] = s.V[(long)i * s.ldv + j]; }
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.At[i * ld + j] = s.A[(long)i * s.lda + j]; }
+  __syncthreads();
+  // 4. seed
+  int st = 0;
+  switch (s.choice) {
+    case CHOICE_QR: {
+      // nonneg-diagonal QR of V_t (core.py:61-84): P = -Q1, T = I + R1^T
+      blk_copy(s.X1, ld, s.Vt, ld, n, n);
+      __syncthreads();
+      blk_geqr2(s.X1, ld, n, n, s.tau, red);
+      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? s.X1[i * ld + j] : 0.0; }
+      __syncthreads();
+      blk_org2r(s.X1, ld, n, n, s.tau, red);  // X1 = Q1
+      BLK_FOR(i, n) { double d = s.X2[i * ld + i]; s.pvec[i] = (d < 0.0) ? -1.0 : 1.0; }
+      __syncthreads();
+      BLK_FOR(e, n * n) {
+        int i = e / n, j = e - i * n;
+        s.P[i * ld + j] = -s.X1[i * ld + j] * s.pvec[j];
+        double rji = (i >= j) ? s.X2[j * ld + i] * s.pvec[j] : 0.0;  // R1^T[i][j] = R1[j][i]
+        if (i == j) rji = fabs(s.X2[i * ld + i]);
+        double t = (i == j ? 1.0 : 0.0) + rji;
+        s.Tf[i * ld + j] = t;
+        s.Tdense[i * ld + j] = t;
+      }
+      break;
+    }
+    case CHOICE_MLU: {
+      blk_copy(s.Tf, ld, s.Vt, ld, n, n);
+      __syncthreads();
+      blk_mlu(s.Tf, ld, n, s.pvec, false);
+      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.P[i * ld + j] = (i == j) ? s.pvec[i] : 0.0; }
+      // dense T = (L U)^T diag(p):  T[i][j] = p_j * sum_l L[j][l] U[l][i]
+      BLK_FOR(e, n * n) {
+        int i = e / n, j = e - i * n;
+        double acc = 0.0;
+        int lmax = i < j ? i : j;
+        for (int l = 0; l <= lmax; ++l) {
+          double L = (l == j) ? 1.0 : s.Tf[j * ld + l];
+          acc = fma(L, s.Tf[l * ld + i], acc);
+        }
+        s.Tdense[i * ld + j] = acc * s.pvec[j];
+      }
+      break;
+    }
+    case CHOICE_POLAR: {
+      // polar V_t = U H via one-sided Jacobi SVD (core.py:108-120)
+      // rows of X1 := columns of V_t ; X2 := I (accumulates J^T)
+      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = s.Vt[j * ld + i]; }
+      blk_identity(s.X2, ld, n);
+      __syncthreads();
+      blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red);
+      // U columns u_j = X1 row j / sigma_j (null directions: v_j orthogonalised)
+      // store U^T rows in X1 (normalised)
+      BLK_FOR(e, n * n) {
+        int j = e / n, c = e - j * n;
+        double sg = s.sig[j];
+        if (sg > 0.0) s.X1[j * ld + c] /= sg;
+      }
+      __syncthreads();
+      for (int j = 0; j < n; ++j) {
+        if (s.sig[j] > 0.0) continue;
+        // u = v_j - sum_{i != j, done} (u_i . v_j) u_i, normalise
+        BLK_FOR(c, n) s.X1[j * ld + c] = s.X2[j * ld + c];
+        __syncthreads();
+        for (int pass = 0; pass < 2; ++pass)
+          for (int i = 0; i < n; ++i) {
+            if (i == j || (s.sig[i] == 0.0 && i > j)) continue;
+            double d = 0.0;
+            for (int c = threadIdx.x; c < n; c += blockDim.x) d = fma(s.X1[i * ld + c], s.X1[j * ld + c], d);
+            d = block_sum(d, red);
+            BLK_FOR(c, n) s.X1[j * ld + c] -= d * s.X1[i * ld + c];
+            __syncthreads();
+          }
+        double nn = 0.0;
+        for (int c = threadIdx.x; c < n; c += blockDim.x) nn = fma(s.X1[j * ld + c], s.X1[j * ld + c], nn);
+        nn = sqrt(block_sum(nn, red));
+        BLK_FOR(c, n) s.X1[j * ld + c] /= nn;
+        __syncthreads();
+      }
+      // Up = U V^T = sum_j u_j v_j^T ; H = V diag(sigma) V^T
+      BLK_FOR(e, n * n) {
+        int a = e / n, b = e - a * n;
+        double up = 0.0, h = 0.0;
+        for (int j = 0; j < n; ++j) {
+          up = fma(s.X1[j * ld + a], s.X2[j * ld + b], up);
+          h = fma(s.X2[j * ld + a] * s.sig[j], s.X2[j * ld + b], h);
+        }
+        s.P[a * ld + b] = -up;
+        s.Tdense[a * ld + b] = h;
+      }
+      __syncthreads();
+      BLK_FOR(e, n * n) {  // symmetrise H, T = I + H
+        int a = e / n, b = e - a * n;
+        double h = 0.5 * (s.Tdense[a * ld + b] + s.Tdense[b * ld + a]);
+        s.Tf[a * ld + b] = h + (a == b ? 1.0 : 0.0);
+      }
+      __syncthreads();
+      blk_copy(s.Tdense, ld, s.Tf, ld, n, n);
+      __syncthreads();
+      if (!blk_cholesky(s.Tf, ld, n, red)) st = OTS_E_NOT_PD;
+      break;
+    }
+    case CHOICE_EXPLICIT: {
+      blk_copy(s.P, ld, s.Pexp, s.ldpe, n, n);
+      __syncthreads();
+      // unitary check ||P^T P - I||_2 <= 1e-12 k0  (reflector.py:200-201)
+      blk_gemm(s.X1, ld, s.P, ld, true, s.P, ld, false, n, n, n, 1.0, 0.0);
+      BLK_FOR(i, n) s.X1[i * ld + i] -= 1.0;
+      __syncthreads();
+      double ff = 0.0;
+      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; double x = s.X1[i * ld + j]; ff = fma(x, x, ff); }
+      ff = sqrt(block_sum(ff, red));
+      double pd = ff;
+      const double ptol = 1e-12 * (n > 1 ? n : 1);
+      if (ff > ptol) pd = blk_sigma_max(s.X1, ld, n, s.sig, red);
+      if (pd > ptol) { st = OTS_E_PARAMETER; break; }
+      // T = I - V_t^T P, pivoted LU
+      blk_gemm(s.Tdense, ld, s.Vt, ld, true, s.P, ld, false, n, n, n, -1.0, 0.0);
+      BLK_FOR(i, n) s.Tdense[i * ld + i] += 1.0;
+      __syncthreads();
+      blk_copy(s.Tf, ld, s.Tdense, ld, n, n);
+      __syncthreads();
+      if (!blk_getrf(s.Tf, ld, n, s.piv, red, ired)) st = OTS_E_SINGULAR_T;
+      break;
+    }
+    default:
+      st = OTS_E_PARAMETER;
+  }
+  __syncthreads();
+  if (st != 0) {
+    if (threadIdx.x == 0) s.status[0] = st;
+    return;
+  }
+  // 5. W_t = fl(P - V_t)
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.Wt[i * ld + j] = s.P[i * ld + j] - s.Vt[i * ld + j]; }
+  __syncthreads();
+  // 6. Y1 = W_t^T A_t - V_b^T A_b  -> Z1 (in place)
+  blk_gemm(s.Z1, ld, s.Wt, ld, true, s.At, ld, false, n, k, n, 1.0, 0.0);
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.Z1[i * ld + j] -= s.VbA[i * ld + j]; }
+  __syncthreads();
+  // 7. Z1 = T^{-T} Y1
+  t_solve(s, s.Z1, ld, k, true);
+  // 8. AH_t = A_t - W_t Z1 ; S = P^T AH_t
+  blk_gemm(s.X1, ld, s.Wt, ld, false, s.Z1, ld, false, n, k, n, 1.0, 0.0);
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.X1[i * ld + j] = s.At[i * ld + j] - s.X1[i * ld + j]; }
+  __syncthreads();
+  blk_gemm(s.Sout, s.lds_out, s.P, ld, true, s.X1, ld, false, n, k, n, 1.0, 0.0);
+}
+
+// Diagnostics from k0 x k0 data (reflector.py:241-247):
+// kappa_2(T) and ||W T^{-1}||_2 = sqrt(lambda_max(T^{-T} W^T W T^{-1})),
+// W^T W = W_t^T W_t + (G - V_t^T V_t).
+__global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
+  __shared__ double red[64];
+  if (s.status[0] != 0) return;
+  const int n = s.k0, ld = s.ld;
+  // kappa(T)
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] = s.Tdense[i * ld + j]; }
+  __syncthreads();
+  blk_jacobi_rows(s.D1, ld, nullptr, 0, n, s.sig2, red);
+  double mx = 0.0, mn = 1e308;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { mx = fmax(mx, s.sig2[i]); mn = fmin(mn, s.sig2[i]); }
+  mx = block_max(mx, red);
+  mn = -block_max(-mn, red);
+  if (threadIdx.x == 0) s.diag[0] = (mn == 0.0) ? __longlong_as_double(0x7ff0000000000000LL) : mx / mn;
+  // W^T W
+  blk_gemm(s.D1, ld, s.Wt, ld, true, s.Wt, ld, false, n, n, n, 1.0, 0.0);
+  blk_gemm(s.D2, ld, s.Vt, ld, true, s.Vt, ld, false, n, n, n, 1.0, 0.0);
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] += s.G[i * ld + j] - s.D2[i * ld + j]; }
+  __syncthreads();
+  // X = T^{-T} (W^T W) ; M^T = T^{-T} X^T
+  t_solve(s, s.D1, ld, n, true);
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D2[i * ld + j] = s.D1[j * ld + i]; }
+  __syncthreads();
+  t_solve(s, s.D2, ld, n, true);
+  BLK_FOR(e, n * n) {  // symmetrise
+    int i = e / n, j = e - i * n;
+    s.D1[i * ld + j] = 0.5 * (s.D2[i * ld + j] + s.D2[j * ld + i]);
+  }
+  __syncthreads();
+  double lm = blk_sigma_max(s.D1, ld, n, s.sig2, red);
+  if (threadIdx.x == 0) s.diag[1] = sqrt(lm);
+}
+
+// Z2 = T^{-1} Y2
+__global__ void __launch_bounds__(SMALL_NT) z2_kernel(SmallState s) {
+  if (s.status[0] != 0) return;
+  t_solve(s, s.Z2, s.ld, s.k, false);
+}
+
+// LAPACK sign recovery on Q_ top k x k and R output
+__global__ void __launch_bounds__(SMALL_NT) sign_kernel(SmallState s, const double* Qtop, long ldq,
+                                                        const double* Rfin, int ldr, double* Rout,
+                                                        int ldro) {
+  if (s.status[0] != 0) return;
+  const int k = s.k, ld = s.ld;
+  // scratch X2: the diag kernel may run concurrently on the side stream and
+  // owns D1/D2/sig2.
+  BLK_FOR(e, k * k) { int i = e / k, j = e - i * k; s.X2[i * ld + j] = Qtop[(long)i * ldq + j]; }
+  __syncthreads();
+  blk_mlu(s.X2, ld, k, s.svec, true);
+  BLK_FOR(e, k * k) {
+    int i = e / k, j = e - i * k;
+    Rout[i * ldro + j] = (j >= i) ? s.svec[i] * Rfin[i * ldr + j] : 0.0;
+  }
+}
+
+// Q_top = -(W_t Z2) diag(svec)
+__global__ void __launch_bounds__(SMALL_NT) qtop_kernel(SmallState s, double* Q, long ldq) {
+  if (s.status[0] != 0) return;
+  const int n = s.k0, k = s.k, ld = s.ld;
+  BLK_FOR(e, n * k) {
+    int i = e / k, j = e - i * k;
+    double acc = 0.0;
+    for (int l = 0; l < n; ++l) acc = fma(s.Wt[i * ld + l], s.Z2[l * ld + j], acc);
+    Q[(long)i * ldq + j] = -acc * s.svec[j];
+  }
+}
+
+// Standalone modified LU (the `modified_lu` API, reflector.py:53-77), with
+// the ||z||_2 <= 1 + 1e-8 precondition (NormBoundError).
+__global__ void __launch_bounds__(SMALL_NT) mlu_kernel(const double* Z, int ldz, int n, double* LU,
+                                                       double* p, double* work, int* status) {
+  __shared__ double red[64];
+  blk_copy(work, n, Z, ldz, n, n);
+  __syncthreads();
+  double nrm = blk_sigma_max(work, n, n, work + n * n, red);
+  if (nrm > 1.0 + 1e-8) { if (threadIdx.x == 0) *status = OTS_E_NORM_BOUND; return; }
+  blk_copy(LU, n, Z, ldz, n, n);
+  __syncthreads();
+  blk_mlu(LU, n, n, p, false);
+  if (threadIdx.x == 0) *status = 0;
+}
+
+cudaError_t launch_seed(const SmallState& s, cudaStream_t st) {
+  seed_kernel<<<1, SMALL_NT, 0, st>>>(s);
+  return cudaGetLastError();
+}
+cudaError_t launch_diag(const SmallState& s, cudaStream_t st) {
+  diag_kernel<<<1, SMALL_NT, 0, st>>>(s);
+  return cudaGetLastError();
+}
+cudaError_t launch_z2(const SmallState& s, cudaStream_t st) {
+  z2_kernel<<<1, SMALL_NT, 0, st>>>(s);
+  return cudaGetLastError();
+}
+cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const double* Rfin, int ldr,
+                        double* Rout, int ldro, cudaStream_t st) {
+  sign_kernel<<<1, SMALL_NT, 0, st>>>(s, Qtop, ldq, Rfin, ldr, Rout, ldro);
+  return cudaGetLastError();
+}
+cudaError_t launch_qtop(const SmallState& s, double* Q, long ldq, cudaStream_t st) {
+  qtop_kernel<<<1, SMALL_NT, 0, st>>>(s, Q, ldq);
+  return cudaGetLastError();
+}
+cudaError_t launch_mlu(const double* Z, int ldz, int n, double* LU, double* p, double* work, int* status,
+                       cudaStream_t st) {
+  mlu_kernel<<<1, SMALL_NT, 0, st>>>(Z, ldz, n, LU, p, work, status);
+  return cudaGetLastError();
+}
+
+}  // namespace ots

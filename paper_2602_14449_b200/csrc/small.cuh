@@ -1,0 +1,39 @@
+// Small-matrix state shared by the single-CTA kernels of small.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ots {
+
+enum { CHOICE_MLU = 0, CHOICE_QR = 1, CHOICE_POLAR = 2, CHOICE_EXPLICIT = 3 };
+constexpr int SMALL_NT = 512;
+
+struct SmallState {
+  int k0, k, ld;             // ld = padded leading dim of every small matrix
+  int choice;
+  int allow_defect;
+  double orth_tol;
+  // inputs
+  const double* V; long ldv;   // top k0 rows are V_t
+  const double* A; long lda;   // top k0 rows are A_t
+  const double* Gfull; long ldgf; int gf_acol;  // reduced [V^T V | V_b^T A_b]
+  const double* Pexp; int ldpe;                  // explicit seed (device) or null
+  // small matrices (k0 x k0 or k0 x k, all with leading dim ld)
+  double *G, *Vt, *At, *VbA, *P, *Tf, *Tdense, *Wt, *Z1, *Z2, *X1, *X2, *D1, *D2, *Sd;
+  double *pvec, *tau, *sig, *sig2, *svec;
+  int* piv;
+  // outputs
+  double* Sout; int lds_out;   // S (k0 x k)
+  double* diag;                // [kappa_t, wt_inv_norm, defect]
+  int* status;                 // [0] = status code
+};
+
+cudaError_t launch_seed(const SmallState& s, cudaStream_t st);
+cudaError_t launch_diag(const SmallState& s, cudaStream_t st);
+cudaError_t launch_z2(const SmallState& s, cudaStream_t st);
+cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const double* Rfin, int ldr,
+                        double* Rout, int ldro, cudaStream_t st);
+cudaError_t launch_qtop(const SmallState& s, double* Q, long ldq, cudaStream_t st);
+cudaError_t launch_mlu(const double* Z, int ldz, int n, double* LU, double* p, double* work, int* status,
+                       cudaStream_t st);
+
+}  // namespace ots

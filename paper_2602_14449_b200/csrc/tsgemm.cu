@@ -1,0 +1,347 @@
+// Tall-skinny FP64 contractions on DMMA (sm_100a).
+//
+//  tsgemm_tn : C(PW x NTOT) = sum_rows  P^T [P | B]   (reduction over n rows)
+//              -- the inner-product blocks V^*V, V^*A (reflector.py:220,236)
+//                 and V^*Q_ (reflector.py:236 via twostage.py:96).
+//  tsgemm_nn : X = (B + P Z) * diag(colscale)         (row-local update)
+//              -- the reflector update  x - W (T-solve) y  (reflector.py:238)
+//                 on the n-row part, with W_bottom = -V implicit.
+//
+// Both stream row tiles HBM -> smem with multi-stage cp.async (16 B, zero
+// fill), swizzled so every m8n8k4 fragment load is conflict-minimal, and keep
+// the k0 x k accumulators in registers for the whole CTA lifetime (tn) or per
+// row tile (nn).  Cross-CTA sums go through a fixed-order reduction
+// (deterministic, run-to-run bit reproducible).
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ots {
+
+// ============================================================================
+// TN: per-CTA partial inner products
+// ============================================================================
+
+template <int PW, int BW, bool ALIAS, bool SYM>
+struct TnCfg {
+  static constexpr int MB = PW / 32;
+  static constexpr int NBV = ALIAS ? PW / 32 : 0;
+  static constexpr int NBB = BW / 32;
+  static constexpr int NVT = ALIAS ? (SYM ? MB * (MB + 1) / 2 : MB * MB) : 0;
+  static constexpr int NTASK = NVT + MB * NBB;
+  static constexpr int NT = NTASK * 32;
+  static constexpr int RT = 32;
+  static constexpr int STAGE = RT * (PW + BW);
+  static constexpr int NSTAGE_RAW = (200 * 1024) / (STAGE * 8);
+  static constexpr int NSTAGE = NSTAGE_RAW > 4 ? 4 : (NSTAGE_RAW < 2 ? 2 : NSTAGE_RAW);
+  static constexpr int SMEM = NSTAGE * STAGE * 8;
+  static constexpr int NTOT = NBV * 32 + BW;
+};
+
+template <int PW, int BW, bool ALIAS, bool SYM>
+__global__ void __launch_bounds__(TnCfg<PW, BW, ALIAS, SYM>::NT, 1)
+tsgemm_tn_kernel(TnArgs a) {
+  using C = TnCfg<PW, BW, ALIAS, SYM>;
+  extern __shared__ __align__(128) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+
+  // task decode: V-part (mi, ni<=mi or all) then B-part
+  int mi = 0, ni = 0;
+  bool fromP = false;
+  {
+    int w = warp;
+    if (w < C::NVT) {
+      fromP = true;
+      for (int m = 0; m < C::MB; ++m) {
+        int cnt = SYM ? (m + 1) : C::MB;
+        if (w < cnt) { mi = m; ni = w; break; }
+        w -= cnt;
+      }
+    } else {
+      w -= C::NVT;
+      mi = w / (C::NBB > 0 ? C::NBB : 1);
+      ni = w - mi * C::NBB;
+    }
+  }
+
+  const long r_lo = a.row_begin + (long)blockIdx.x * a.rows_per_cta;
+  long r_hi = r_lo + a.rows_per_cta;
+  if (r_hi > a.row_end) r_hi = a.row_end;
+  const int ntiles = r_hi > r_lo ? (int)((r_hi - r_lo + C::RT - 1) / C::RT) : 0;
+  const long plo = a.row_begin > a.p_row_begin ? a.row_begin : a.p_row_begin;
+  const long blo = a.row_begin > a.b_row_begin ? a.row_begin : a.b_row_begin;
+
+  auto stage_p = [&](int s) { return smem + s * C::STAGE; };
+  auto stage_b = [&](int s) { return smem + s * C::STAGE + C::RT * PW; };
+  auto issue = [&](int it) {
+    if (it < ntiles) {
+      int s = it % C::NSTAGE;
+      long r0 = r_lo + (long)it * C::RT;
+      load_tile_async(stage_p(s), PW, a.P, a.ldp, r0, C::RT, plo, r_hi, a.pc0, PW, a.pc0 + a.pcols,
+                      tid, C::NT);
+      if (BW > 0)
+        load_tile_async(stage_b(s), BW, a.B, a.ldb, r0, C::RT, blo, r_hi, a.bc0, BW, a.bc0 + a.bcols,
+                        tid, C::NT);
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < C::NSTAGE - 1; ++s) issue(s);
+
+  for (int it = 0; it < ntiles; ++it) {
+    cp_async_wait<C::NSTAGE - 2>();
+    __syncthreads();
+    issue(it + C::NSTAGE - 1);
+    const int s = it % C::NSTAGE;
+    const double* Ps = stage_p(s);
+    const double* Bs = fromP ? Ps : stage_b(s);
+    const int BWs = fromP ? PW : (BW > 0 ? BW : 32);
+    const int nb0 = fromP ? 32 * ni : 32 * ni;
+#pragma unroll
+    for (int kk = 0; kk < C::RT / 4; ++kk) {
+      const int r = 4 * kk + t;
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, nb0 + 8 * j + g, BWs)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // partial write
+  double* out = a.partial + (long)blockIdx.x * PW * C::NTOT;
+  const int ncol0 = fromP ? 32 * ni : C::NBV * 32 + 32 * ni;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int m = 32 * mi + 8 * i + g;
+      int n = ncol0 + 8 * j + 2 * t;
+      *reinterpret_cast<double2*>(out + (long)m * C::NTOT + n) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+// Fixed-order reduction of per-CTA partials: out[m][n] = sum_c partial[c][m][n]
+// (optionally scaled by alpha and added to an existing value when accumulate).
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, int nparts, long count,
+                                       double* __restrict__ out, double alpha) {
+  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int c = 0; c < nparts; ++c) s += partial[(long)c * count + i];
+  out[i] = alpha * s;
+}
+
+// ============================================================================
+// NN: X = (B + P Z) * diag(colscale) on rows [row_begin, row_end)
+// ============================================================================
+
+template <int KT>
+struct NnCfg {
+  static constexpr int WN = KT < 32 ? KT : 32;
+  static constexpr int NWN = KT / WN;
+  static constexpr int NWM = 8 / NWN;
+  static constexpr int RT = NWM * 32;
+  static constexpr int NT = 256;
+  static constexpr int KC = 32;
+  static constexpr int STAGE = RT * KC + KC * KT;
+  static constexpr int NSTAGE_RAW = (216 * 1024) / (STAGE * 8);
+  static constexpr int NSTAGE = NSTAGE_RAW > 4 ? 4 : NSTAGE_RAW;
+  static constexpr int SMEM = NSTAGE * STAGE * 8;
+};
+
+template <int KT>
+__global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
+  using C = NnCfg<KT>;
+  constexpr int WN = C::WN;
+  constexpr int NJ = WN / 8;
+  extern __shared__ __align__(128) double smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm0 = (warp / C::NWN) * 32;
+  const int wn0 = (warp % C::NWN) * WN;
+
+  const long nrows = a.row_end - a.row_begin;
+  const long ntiles_total = (nrows + C::RT - 1) / C::RT;
+  const int nchunks = (a.kdim + C::KC - 1) / C::KC;
+  // tiles owned by this CTA: blockIdx.x, +gridDim.x, ...
+  const long my_tiles = ntiles_total > blockIdx.x ? (ntiles_total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const long nit = my_tiles * nchunks;
+
+  auto tile_r0 = [&](long lt) { return a.row_begin + (blockIdx.x + lt * gridDim.x) * (long)C::RT; };
+  auto issue = [&](long it) {
+    if (it < nit) {
+      int s = (int)(it % C::NSTAGE);
+      long lt = it / nchunks;
+      int ch = (int)(it - lt * nchunks);
+      double* Ps = smem + s * C::STAGE;
+      double* Zs = Ps + C::RT * C::KC;
+      load_tile_async(Ps, C::KC, a.P, a.ldp, tile_r0(lt), C::RT, a.row_begin, a.row_end, ch * C::KC, C::KC,
+                      a.kdim, tid, C::NT);
+      // Z chunk: rows [ch*KC, ch*KC+KC) (zero beyond kdim), cols [0, KT) (zero beyond ncols)
+      load_tile_async(Zs, KT, a.Z, a.ldz, (long)ch * C::KC, C::KC, 0, a.kdim, 0, KT, a.ncols, tid, C::NT);
+    }
+    cp_async_commit();
+  };
+
+  double acc[4][NJ][2];
+  double bv[4][NJ][2];
+
+  auto epilogue_load = [&](long r0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        long r = r0 + wm0 + 8 * i + g;
+        int c = wn0 + 8 * j + 2 * t;
+        double x0 = 0.0, x1 = 0.0;
+        if (a.B != nullptr && r < a.row_end) {
+          const double* p = a.B + r * a.ldb + c;
+          if (c + 1 < a.ncols) { double2 v = *reinterpret_cast<const double2*>(p); x0 = v.x; x1 = v.y; }
+          else if (c < a.ncols) x0 = p[0];
+        }
+        bv[i][j][0] = x0; bv[i][j][1] = x1;
+      }
+  };
+  auto epilogue_store = [&](long r0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        long r = r0 + wm0 + 8 * i + g;
+        int c = wn0 + 8 * j + 2 * t;
+        if (r >= a.row_end) continue;
+        double s0 = 1.0, s1 = 1.0;
+        if (a.colscale) { if (c < a.ncols) s0 = a.colscale[c]; if (c + 1 < a.ncols) s1 = a.colscale[c + 1]; }
+        double y0 = (bv[i][j][0] + acc[i][j][0]) * s0;
+        double y1 = (bv[i][j][1] + acc[i][j][1]) * s1;
+        double* p = a.X + r * a.ldx + c;
+        if (c + 1 < a.ncols) *reinterpret_cast<double2*>(p) = make_double2(y0, y1);
+        else if (c < a.ncols) p[0] = y0;
+      }
+  };
+
+  if (nchunks == 0) {  // X = B * colscale
+    for (long lt = 0; lt < my_tiles; ++lt) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      epilogue_load(tile_r0(lt));
+      epilogue_store(tile_r0(lt));
+    }
+    return;
+  }
+
+#pragma unroll
+  for (int s = 0; s < C::NSTAGE - 1; ++s) issue(s);
+
+  for (long it = 0; it < nit; ++it) {
+    const long lt = it / nchunks;
+    const int ch = (int)(it - lt * nchunks);
+    if (ch == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+      epilogue_load(tile_r0(lt));  // in flight during the k loop
+    }
+    cp_async_wait<C::NSTAGE - 2>();
+    __syncthreads();
+    issue(it + C::NSTAGE - 1);
+    const int s = (int)(it % C::NSTAGE);
+    const double* Ps = smem + s * C::STAGE;
+    const double* Zs = Ps + C::RT * C::KC;
+#pragma unroll
+    for (int kk = 0; kk < C::KC / 4; ++kk) {
+      double af[4], bf[NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Ps[swz(wm0 + 8 * i + g, 4 * kk + t, C::KC)];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bf[j] = Zs[swz(4 * kk + t, wn0 + 8 * j + g, KT)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+    if (ch == nchunks - 1) epilogue_store(tile_r0(lt));
+  }
+  cp_async_wait<0>();
+}
+
+// ============================================================================
+// host launchers
+// ============================================================================
+template <int PW, int BW, bool ALIAS, bool SYM>
+static cudaError_t launch_tn_t(const TnArgs& a0, int grid, cudaStream_t st) {
+  using C = TnCfg<PW, BW, ALIAS, SYM>;
+  auto k = tsgemm_tn_kernel<PW, BW, ALIAS, SYM>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  TnArgs a = a0;
+  long rows = a.row_end - a.row_begin;
+  long per = (rows + grid - 1) / grid;
+  per = (per + C::RT - 1) / C::RT * C::RT;
+  if (per < C::RT) per = C::RT;
+  a.rows_per_cta = per;
+  k<<<grid, C::NT, C::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+// Dispatch on padded widths.  PW in {32,64,96,128}; BW in {0,32,64}.
+cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid,
+                             cudaStream_t st) {
+#define OTS_TN(pw, bw, al, sy)                                                   \
+  if (PW == pw && BW == bw && alias == al && sym == sy)                          \
+    return launch_tn_t<pw, bw, al, sy>(a, grid, st);
+  OTS_TN(32, 32, true, true) OTS_TN(64, 32, true, true) OTS_TN(64, 64, true, true)
+  OTS_TN(96, 32, true, true) OTS_TN(96, 64, true, true)
+  OTS_TN(128, 32, true, true) OTS_TN(128, 64, true, true)
+  OTS_TN(32, 0, true, true) OTS_TN(64, 0, true, true) OTS_TN(96, 0, true, true) OTS_TN(128, 0, true, true)
+  OTS_TN(32, 32, false, false) OTS_TN(64, 32, false, false) OTS_TN(96, 32, false, false)
+  OTS_TN(128, 32, false, false) OTS_TN(32, 64, false, false) OTS_TN(64, 64, false, false)
+  OTS_TN(96, 64, false, false) OTS_TN(128, 64, false, false)
+#undef OTS_TN
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_reduce(const double* partial, int nparts, long count, double* out, double alpha,
+                          cudaStream_t st) {
+  int bs = 256;
+  long nb = (count + bs - 1) / bs;
+  reduce_partials_kernel<<<(unsigned)nb, bs, 0, st>>>(partial, nparts, count, out, alpha);
+  return cudaGetLastError();
+}
+
+template <int KT>
+static cudaError_t launch_nn_t(const NnArgs& a, int nsm, cudaStream_t st) {
+  using C = NnCfg<KT>;
+  auto k = tsgemm_nn_kernel<KT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  long rows = a.row_end - a.row_begin;
+  if (rows <= 0) return cudaSuccess;
+  long tiles = (rows + C::RT - 1) / C::RT;
+  int grid = (int)(tiles < nsm ? tiles : nsm);
+  k<<<grid, C::NT, C::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st) {
+  if (KT == 16) return launch_nn_t<16>(a, nsm, st);
+  if (KT == 32) return launch_nn_t<32>(a, nsm, st);
+  if (KT == 64) return launch_nn_t<64>(a, nsm, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ots

@@ -1,0 +1,68 @@
+"""CPU-side checks of the drop-in boundary: the C-ABI library loads and
+exports every entry point include/ots.h declares; the facade validates
+shapes / arguments with the reference's exception classes before touching
+the device; no CPU fallback exists."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2602_14449_b200 as P
+from paper_2602_14449_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ots.h")).read()
+    return sorted(set(re.findall(r"\b(ots_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_all_declared_symbols():
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    assert set(_native.EXPORTED_SYMBOLS) <= set(syms)
+
+
+def test_version_callable_without_gpu():
+    assert _native.lib().ots_version() == 1
+
+
+def test_api_surface_names():
+    for name in ["two_stage_qr", "householder_qr", "modified_lu", "block_householder_qr",
+                 "reorthogonalized_two_stage", "TwoStageResult", "BlockQRResult",
+                 "ReflectorDiagnostics", "MLUResult", "GenHouseholder", "QRPair", "EPS",
+                 "OrthoError", "DimensionError", "OrthonormalityError", "IntraFailure",
+                 "ParameterError", "NormBoundError", "SingularTError", "NotPositiveDefinite"]:
+        assert hasattr(P, name), name
+    assert issubclass(P.OrthonormalityError, P.OrthoError)
+    assert P.IntraFailure("x", block=3).block == 3
+
+
+def test_validation_before_device():
+    # shape errors are raised by host validation (same order as twostage.py:73-80)
+    with pytest.raises(P.DimensionError):
+        P.two_stage_qr(np.ones((5, 3, 1)), np.ones((5, 2)))
+    with pytest.raises(P.DimensionError):
+        P.two_stage_qr(np.eye(6, 3), np.ones((7, 2)))
+    with pytest.raises(P.DimensionError):
+        P.two_stage_qr(np.eye(5, 3), np.ones((5, 3)))
+    with pytest.raises(P.DimensionError):
+        P.householder_qr(np.ones((2, 3)))
+    with pytest.raises(P.ParameterError):
+        P.block_householder_qr([])
+
+
+def test_no_cpu_fallback():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(P.NativeUnavailable):
+        P.two_stage_qr(np.eye(10, 3), np.ones((10, 2)))
+    with pytest.raises(P.NativeUnavailable):
+        P.householder_qr(np.ones((10, 2)))

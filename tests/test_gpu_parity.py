@@ -1,0 +1,142 @@
+"""GPU parity: the CUDA path (through the C-ABI, via the drop-in facade)
+against the reference's golden outputs and the CPU oracle on the same seeded
+inputs.  Tolerances (BASELINE.json north_star):
+  * elementwise Q, R, S within 1e-10 relative on well-conditioned inputs
+    (same LAPACK sign convention), kappa_t / wt_inv_norm within 1e-10 rel;
+  * loss of orthogonality and relative residual <= 10 n u and <= 10x the
+    oracle's own values on ill-conditioned / rank-deficient inputs.
+"""
+import numpy as np
+import pytest
+
+import paper_2602_14449_b200 as P
+from oracle import twostage_oracle as O
+from paper_2602_14449_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+def rel(x, y):
+    x, y = np.asarray(x), np.asarray(y)
+    if y.size == 0:
+        return 0.0
+    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
+
+
+def golden_cases(golden, prefix):
+    keys = sorted({k.rsplit("/", 1)[0] for k in golden.files if k.endswith("/q")})
+    return [k for k in keys if k.startswith(prefix)]
+
+
+@pytest.mark.parametrize("group", ["eq12", "eye", "real_"])
+def test_two_stage_golden(golden, group):
+    cases = golden_cases(golden, group)
+    assert cases
+    for case in cases:
+        base = case.rsplit("/", 1)[0]
+        v, a = golden[base + "/v"], golden[base + "/a"]
+        ch = str(golden[case + "/choice"])
+        p = golden[case + "/p"]
+        res = P.two_stage_qr(v, a, choice=ch, p=(p if p.size else None))
+        # Eq.(1.2): R = diag(1e-30, 1e-30) -- compare absolutely at its own scale
+        assert rel(res.q, golden[case + "/q"]) < 1e-10, case
+        assert rel(res.r, golden[case + "/r"]) < 1e-10, case
+        assert rel(res.s, golden[case + "/s"]) < 1e-10, case
+        kt = float(golden[case + "/kappa_t"])
+        wn = float(golden[case + "/wt_inv_norm"])
+        assert abs(res.diagnostics.kappa_t - kt) <= 1e-10 * kt, case
+        assert abs(res.diagnostics.wt_inv_norm - wn) <= 1e-10 * wn, case
+        assert np.all(np.tril(res.r, -1) == 0.0)
+
+
+def test_rankdef_metrics(golden):
+    for case in golden_cases(golden, "rankdef"):
+        v, a = golden["rankdef/v"], golden["rankdef/a"]
+        ch = str(golden[case + "/choice"])
+        res = P.two_stage_qr(v, a, choice=ch)
+        loss, cross, resid = O.stability(v, a, res.q, res.r, res.s)
+        n = v.shape[0]
+        assert loss <= 10 * n * U and resid <= 10 * n * U
+        assert loss <= 10 * max(float(golden[case + "/loss"]), 4 * U)
+        assert resid <= 10 * max(float(golden[case + "/resid"]), 4 * U)
+
+
+def test_householder_qr_golden(golden):
+    for nn in (0, 1):
+        qr = P.householder_qr(golden[f"hqr/nonneg{nn}/a"], nonneg_diag=bool(nn))
+        assert rel(qr.q, golden[f"hqr/nonneg{nn}/q"]) < 1e-10
+        assert rel(qr.r, golden[f"hqr/nonneg{nn}/r"]) < 1e-10
+    qr = P.householder_qr(np.array([[3.0], [4.0]]))          # SPEC.md:43 (LAPACK signs)
+    assert np.allclose(qr.q[:, 0], [-0.6, -0.8]) and np.isclose(qr.r[0, 0], -5.0)
+    qr = P.householder_qr(np.array([[3.0], [4.0]]), nonneg_diag=True)
+    assert np.allclose(qr.q[:, 0], [0.6, 0.8]) and np.isclose(qr.r[0, 0], 5.0)
+    qr = P.householder_qr(np.eye(3))
+    assert np.allclose(qr.q, np.eye(3)) and np.allclose(qr.r, np.eye(3))
+
+
+def test_modified_lu_golden(golden):
+    for tag in ("zero", "diag", "rand"):
+        m = P.modified_lu(golden[f"mlu/{tag}/z"])
+        assert np.array_equal(m.p_diag, golden[f"mlu/{tag}/p"])
+        assert rel(m.l, golden[f"mlu/{tag}/l"]) < 1e-12
+        assert rel(m.u_tri, golden[f"mlu/{tag}/u"]) < 1e-12
+    with pytest.raises(P.NormBoundError):
+        P.modified_lu(np.eye(3) * 1.5)
+
+
+def test_errors(golden):
+    with pytest.raises(P.OrthonormalityError) as ei:
+        P.two_stage_qr(golden["err/orth/v"], np.ones((60, 2)))
+    assert str(ei.value) == str(golden["err/orth/msg"])
+    with pytest.raises(P.DimensionError):
+        P.two_stage_qr(np.eye(5, 3), np.ones((5, 3)))
+    with pytest.raises(P.ParameterError):
+        P.two_stage_qr(np.eye(8, 2), np.ones((8, 2)), choice="nope")
+    with pytest.raises(ValueError):
+        a = np.ones((8, 2)); a[3, 1] = np.nan
+        P.two_stage_qr(np.eye(8, 2), a)
+
+
+def test_degenerate(golden):
+    res = P.two_stage_qr(np.zeros((50, 0)), golden["k0zero/a"])
+    assert rel(res.q, golden["k0zero/q"]) < 1e-10 and res.s.shape == (0, 3)
+    res = P.two_stage_qr(golden["kzero/v"], np.zeros((50, 0)))
+    assert res.q.shape == (50, 0) and res.s.shape == (4, 0)
+
+
+@pytest.mark.parametrize("n,k0,k", [(1 << 14, 32, 16), (1 << 16, 64, 32), (1 << 17, 128, 64),
+                                    (40000, 13, 7), (5000, 100, 50)])
+@pytest.mark.parametrize("choice", ["qr", "mlu", "polar"])
+def test_vs_oracle_random(n, k0, k, choice):
+    rng = W.make_rng(1000 + n + k0)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    a = W.normal_matrix(rng, n, k)
+    ref = O.two_stage(v, a, choice, diagnostics=(n <= 1 << 16))
+    res = P.two_stage_qr(v, a, choice=choice)
+    assert rel(res.q, ref["q"]) < 1e-10
+    assert rel(res.r, ref["r"]) < 1e-10
+    assert rel(res.s, ref["s"]) < 1e-10
+    if n <= 1 << 16:
+        assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
+        assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
+
+
+def test_config2_like_illconditioned():
+    v, a = W.config2(n=1 << 16, k0=64, k=32)
+    res = P.two_stage_qr(v, a)
+    loss, cross, resid = O.gram_stability(v, a, res.q, res.r, res.s)
+    ref = O.two_stage(v, a, "qr", diagnostics=False)
+    rl, rc, rr = O.gram_stability(v, a, ref["q"], ref["r"], ref["s"])
+    n = v.shape[0]
+    assert loss <= 10 * n * U and resid <= 10 * n * U
+    assert loss <= 10 * max(rl, 4 * U) and resid <= 10 * max(rr, 4 * U)
+
+
+def test_config3_like_rankdef():
+    v, a = W.config3(n=1 << 16, k0=128, k=64)
+    for ch in ("qr", "mlu", "polar"):
+        res = P.two_stage_qr(v, a, choice=ch)
+        loss, cross, resid = O.gram_stability(v, a, res.q, res.r, res.s)
+        n = v.shape[0]
+        assert loss <= 10 * n * U and resid <= 10 * n * U, ch
