@@ -14,5 +14,8 @@ $(LIB): $(SRC) $(HDR)
 ptxas: $(SRC) $(HDR)
 	$(NVCC) $(FLAGS) -Iinclude -Xptxas -v -shared -o /tmp/ots_ptxas.so $(SRC) 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" 
 
+timing: $(SRC) $(HDR)
+	$(NVCC) $(FLAGS) -DOTS_TIMING -Iinclude -shared -o paper_2602_14449_b200/libots_timing.so $(SRC) -lcudart
+
 clean:
 	rm -f $(LIB)

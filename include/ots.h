@@ -93,6 +93,13 @@ int ots_modified_lu_f64(ots_ctx* ctx, int64_t n, const double* Z, int64_t ldz,
 /* Per-phase device timings of the last call (CUDA events on the launching
  * stream), enabled with ots_set_profiling(ctx, 1).  names: '\n'-separated. */
 int ots_set_profiling(ots_ctx* ctx, int enable);
+/* Number of this library's kernels launched by the last full call. */
+int ots_last_launch_count(const ots_ctx* ctx);
+/* Measured FP64 DMMA peak of this device (TFLOP/s), the FP64 roofline
+ * denominator (MEASURED_PEAKS.json has no FP64 figure). */
+int ots_fp64_peak(ots_ctx* ctx, double* tflops);
+/* Kernel-section cycle counters (only in an -DOTS_TIMING build; else zeros). */
+int ots_debug_counters(unsigned long long* out16, int reset);
 int ots_last_profile(const ots_ctx* ctx, char* names, int names_cap, float* ms, int cap);
 
 /* ---- phase-split entry points for row-sharded multi-GPU execution ------

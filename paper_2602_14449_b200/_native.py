@@ -11,7 +11,7 @@ import threading
 from . import errors as E
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libots.so")
+LIB_PATH = os.environ.get("OTS_LIB") or os.path.join(_HERE, "libots.so")
 
 CHOICES = {"mlu": 0, "qr": 1, "polar": 2, "explicit": 3}
 INTRA = {"householder": 0, "cholshift": 1}
@@ -46,6 +46,8 @@ def lib():
                 L.ots_sm_count.argtypes = [_vp]
                 L.ots_version.restype = _int
                 L.ots_set_profiling.argtypes = [_vp, _int]
+                L.ots_last_launch_count.argtypes = [_vp]
+                L.ots_fp64_peak.argtypes = [_vp, C.POINTER(_dbl)]
                 L.ots_last_profile.argtypes = [_vp, C.c_char_p, _int, C.POINTER(C.c_float), _int]
                 L.ots_two_stage_f64.argtypes = [
                     _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64,
@@ -70,7 +72,8 @@ def lib():
 EXPORTED_SYMBOLS = [
     "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_version",
     "ots_two_stage_f64", "ots_householder_qr_f64", "ots_modified_lu_f64",
-    "ots_set_profiling", "ots_last_profile",
+    "ots_set_profiling", "ots_last_profile", "ots_last_launch_count", "ots_fp64_peak",
+    "ots_debug_counters",
     "ots_dist_begin", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",
     "ots_dist_tree", "ots_dist_qform", "ots_dist_finish",
 ]

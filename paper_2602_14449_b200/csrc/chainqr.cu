@@ -15,6 +15,14 @@
 
 namespace ots {
 
+#ifdef OTS_TIMING
+__device__ unsigned long long g_dbg[16];
+#define TSTAMP(v) long long v = clock64()
+#define TACC(slot, a, b) if (threadIdx.x == 0) atomicAdd(&g_dbg[slot], (unsigned long long)((b) - (a)))
+#else
+#define TSTAMP(v)
+#define TACC(slot, a, b)
+#endif
 
 __device__ __forceinline__ int chain_real_tiles(const ChainGeom& G, int chain, int KT) {
   long r0 = (long)chain * G.rpc + KT;
@@ -29,8 +37,7 @@ struct FactorCfg {
   static constexpr int NT = 256;
   static constexpr int TPC = NT / KT;             // threads per column
   static constexpr int LDS = KT + KT / 8;         // padded row stride (bank spread)
-  static constexpr int BMAX = 32 * TPC;           // 32 rows / thread / column step
-  static constexpr int SMEM = (KT + BMAX) * LDS * 8;
+  static constexpr int BMAX = 128;                      // = BlkCfg<KT>::B
 };
 
 // Sum over the TPC consecutive lanes that own one column (all of them take the
@@ -82,10 +89,10 @@ __device__ __forceinline__ void store_rows_plain(const double* S, int s0, double
 //  head=true : rows 0..KT-1 only (plain QR of a KT x KT block)
 //  head=false: top rows 0..KT-1 hold R (upper), bottom rows KT..KT+nb-1
 // Writes U[c][j] = v_c^T v_j (c<j) and U[j][j] = tau_j to global `U`.
-template <int KT, bool HEAD>
+template <int KT, bool HEAD, int LDS = FactorCfg<KT>::LDS>
 __device__ __forceinline__ void householder_sweep(double* S, int nb, double* U, double* tau_s) {
   using C = FactorCfg<KT>;
-  constexpr int TPC = C::TPC, LDS = C::LDS;
+  constexpr int TPC = C::TPC;
   const int tid = threadIdx.x;
   const int c = tid / TPC, q = tid % TPC;
   const unsigned gmask = (TPC >= 32) ? 0xffffffffu
@@ -128,91 +135,374 @@ __device__ __forceinline__ void householder_sweep(double* S, int nb, double* U, 
           phase_a(j + 1);
         }
       } else {
-        if (q == 0) U[c * KT + j] = d;
+        if (q == 0) U[c * (KT + 1) + j] = d;
       }
     } else {
-      if (q == 0) U[j * KT + j] = tau;
+      if (q == 0) U[j * (KT + 1) + j] = tau;
     }
     __syncthreads();
   }
 }
 
 
+// dlarfg arithmetic with one rsqrt and one reciprocal (no IEEE division or
+// sqrt on the critical path):  h = alpha^2 + |x|^2, s = sqrt(h),
+//   beta = -sign(alpha) s,  tau = (|alpha| + s)/s,  scal = sign(alpha)/(|alpha| + s)
+// which equal LAPACK's (beta-alpha)/beta and 1/(alpha-beta) to ~1 ulp.
+__device__ __forceinline__ void dlarfg_fast(double alpha, double s2, double& beta, double& tau,
+                                            double& scal) {
+  const double h = fma(alpha, alpha, s2);
+  const double r = rsqrt(h);
+  const double sq = h * r;
+  const double aa = fabs(alpha);
+  const double t = aa + sq;
+  beta = -copysign(sq, alpha);
+  tau = t * r;
+  scal = copysign(1.0, alpha) / t;
+}
+
+// Structured step QR([R; X]) with the b x KT tile X held in REGISTERS.
+// Thread (cg, rb) owns an RPB x CPT block: rows rb*RPB.., columns cg*CPT..
+// The NRB threads sharing a column group are consecutive lanes, so every
+// column reduction is a shuffle tree inside one warp.  Per column step a
+// thread issues RPB/2 LDS.128 (v_j) for 2*RPB*CPT FMAs; only v_j
+// (double-buffered, bank-padded) and R's row j go through shared memory.
+// U (diag tau, strict-upper Gram, ld KT+1) -> T via the dlarft recurrence
+// T[0:j, j] = -tau_j T[0:j, 0:j] U[0:j, j] (head tile only), 4 threads/row.
 template <int KT>
-__global__ void __launch_bounds__(256) chain_factor_kernel(FactorArgs a) {
-  using C = FactorCfg<KT>;
-  constexpr int LDS = C::LDS;
-  extern __shared__ __align__(128) double S[];
-  __shared__ double tau_s[KT];
+__device__ __forceinline__ void u_to_t_block(const double* Us, double* Ts, double* Tg) {
+  constexpr int UL = KT + 1;
   const int tid = threadIdx.x;
+  const int i = tid >> 2, part = tid & 3;
+  for (int e = tid; e < KT * KT; e += 256) Ts[e] = 0.0;
+  __syncthreads();
+  for (int j = 0; j < KT; ++j) {
+    const double tj = Us[j * UL + j];
+    double sacc = 0.0;
+    if (i < j)
+      for (int l = i + part; l < j; l += 4) sacc = fma(Ts[i * KT + l], Us[l * UL + j], sacc);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+    sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+    if (i < j && part == 0) Ts[i * KT + j] = -tj * sacc;
+    if (tid == 0) Ts[j * KT + j] = tj;
+    __syncthreads();
+  }
+  for (int e = tid; e < KT * KT; e += 256) Tg[e] = Ts[e];
+}
+
+// ===========================================================================
+// Structured TSQR step, blocked (v3).  The b x KT tile X lives in shared
+// memory (swizzled for m8n8k4 fragments); R (KT x KT, upper) in S, whose
+// strictly lower part stores the Gram entries G[c][j] = y_c . y_j (c < j)
+// needed for the tile's compact-WY T.  Panels are 8 columns:
+//   * warp p factors panel p in registers (warp shuffles, no CTA barrier);
+//   * one __syncthreads publishes Y_p (in place in X) and T_p;
+//   * warp w > p applies the panel to its 8 columns with DMMA:
+//       W = X_w^T Y_p + R[p rows, w cols]^T ; w = W T_p ; X_w -= Y_p w^T ;
+//       R[p rows, w cols] -= w^T
+//     warp w < p (holding earlier Householder vectors) records G blocks.
+// Warp p+1 applies panel p to its own columns and factors panel p+1 right
+// away, so the critical path is one apply + one panel per barrier.
+// ===========================================================================
+template <int KT>
+struct BlkCfg {
+  static constexpr int B = 128;          // tile rows
+  static constexpr int NB = 8;           // panel width
+  static constexpr int NP = KT / NB;     // panels (= warps that own columns)
+  static constexpr int XS = B * KT + 64; // X region (+ slack for the head's U/T)
+  static constexpr int SMEM = (KT * KT + XS + NP * 64 + 8 * 64) * 8;
+};
+
+// Sum 8 per-lane values over the warp: butterfly reduce-scatter (each step
+// halves the values a lane keeps), a 2-level finish, then an indexed
+// broadcast.  18 + 16 shuffles instead of 8 independent 5-level trees (80).
+__device__ __forceinline__ void warp_sum8(double (&v)[8]) {
+  const int lane = threadIdx.x & 31;
+  double a[4], b2[2], c1;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {          // xor 16: keep half
+    double send = h16 ? v[i] : v[i + 4];
+    double keep = h16 ? v[i + 4] : v[i];
+    a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {          // xor 8
+    double send = h8 ? a[i] : a[i + 2];
+    double keep = h8 ? a[i + 2] : a[i];
+    b2[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {                                      // xor 4
+    double send = h4 ? b2[0] : b2[1];
+    double keep = h4 ? b2[1] : b2[0];
+    c1 = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  c1 += __shfl_xor_sync(0xffffffffu, c1, 2);
+  c1 += __shfl_xor_sync(0xffffffffu, c1, 1);
+  // lane holds total of index (h16?4:0)+(h8?2:0)+(h4?1:0); lane 4*idx' has it
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int src = ((i & 4) ? 16 : 0) + ((i & 2) ? 8 : 0) + ((i & 1) ? 4 : 0);
+    v[i] = __shfl_sync(0xffffffffu, c1, src);
+  }
+}
+
+// panel factorization by one warp: lanes own rows l, l+32, l+64, l+96
+template <int KT>
+__device__ __forceinline__ void panel_factor(int p, double* S, double* Xs, double* Tp, double* tau_s,
+                                             int nb) {
+  constexpr int RPL = BlkCfg<KT>::B / 32;
+  const int lane = threadIdx.x & 31;
+  const int j0 = p * 8;
+  double xr[RPL][8];
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) xr[i][c] = Xs[swz(r, j0 + c, KT)];
+  }
+  double* T8 = Tp + p * 64;          // T_p built column by column (dlarft)
+  T8[lane] = 0.0;
+  T8[lane + 32] = 0.0;
+  __syncwarp();
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = j0 + jj;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPL; i += 2) { s0 = fma(xr[i][jj], xr[i][jj], s0); s1 = fma(xr[i + 1][jj], xr[i + 1][jj], s1); }
+    const double s2 = warp_sum(s0 + s1);
+    const double alpha = S[j * KT + j];
+    double beta = alpha, tj = 0.0, scal = 0.0;
+    if (s2 != 0.0) dlarfg_fast(alpha, s2, beta, tj, scal);
+#pragma unroll
+    for (int i = 0; i < RPL; ++i) xr[i][jj] *= scal;
+    double d[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      d[cc] = 0.0;
+      if (cc != jj) {
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) d[cc] = fma(xr[i][jj], xr[i][cc], d[cc]);
+      }
+    }
+    warp_sum8(d);
+    // T_p[0:jj, jj] = -tau T_p[0:jj, 0:jj] d[0:jj]   (lane ii owns row ii)
+    if (lane < jj) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int l = 0; l < jj; ++l)
+        if (l >= lane) sacc = fma(T8[lane * 8 + l], d[l], sacc);
+      T8[lane * 8 + jj] = -tj * sacc;
+    }
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) {
+      if (cc > jj) {
+        const double w = tj * (d[cc] + S[j * KT + j0 + cc]);
+#pragma unroll
+        for (int i = 0; i < RPL; ++i) xr[i][cc] = fma(-w, xr[i][jj], xr[i][cc]);
+        __syncwarp();
+        if (lane == 0) S[j * KT + j0 + cc] -= w;
+      } else if (cc < jj) {
+        if (lane == 0) S[j * KT + j0 + cc] = d[cc];  // G[j0+cc][j] in the lower part
+      }
+    }
+    __syncwarp();
+    if (lane == 0) { S[j * KT + j] = beta; tau_s[j] = tj; T8[jj * 8 + jj] = tj; }
+    __syncwarp();
+  }
+  // Householder vectors back into X (rows >= nb stay zero)
+#pragma unroll
+  for (int i = 0; i < RPL; ++i) {
+    const int r = lane + 32 * i;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) Xs[swz(r, j0 + c, KT)] = (r < nb) ? xr[i][c] : 0.0;
+  }
+}
+
+// warp w applies panel p (w > p) or records the cross Gram block (w < p)
+template <int KT>
+__device__ __forceinline__ void panel_apply(int p, int w, double* S, double* Xs, const double* Tp,
+                                            double* sc) {
+  constexpr int B = BlkCfg<KT>::B;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int j0 = p * 8, c0 = w * 8;
+  double acc[4][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll 8
+  for (int kk = 0; kk < B / 4; ++kk) {
+    const int r = 4 * kk + t;
+    const double av = Xs[swz(r, c0 + g, KT)];   // A[m=g][k=t] = X[r][c0+g]
+    const double bv = Xs[swz(r, j0 + g, KT)];   // B[k=t][n=g] = Y[r][j0+g]
+    dmma(acc[kk & 3], av, bv);
+  }
+  double W0 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+  double W1 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+  // W^T[c0+g][j0+2t(+1)]
+  if (w < p) {
+    S[(j0 + 2 * t) * KT + c0 + g] = W0;       // G[c][j] (c < j): lower part
+    S[(j0 + 2 * t + 1) * KT + c0 + g] = W1;
+    return;
+  }
+  W0 += S[(j0 + 2 * t) * KT + c0 + g];
+  W1 += S[(j0 + 2 * t + 1) * KT + c0 + g];
+  sc[g * 8 + 2 * t] = W0;
+  sc[g * 8 + 2 * t + 1] = W1;
+  __syncwarp();
+  // w^T = W^T T_p  (8 x 8 x 8)
+  double wt[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4) dmma(wt, sc[g * 8 + k0 + t], Tp[p * 64 + (k0 + t) * 8 + g]);
+  __syncwarp();
+  sc[g * 8 + 2 * t] = wt[0];
+  sc[g * 8 + 2 * t + 1] = wt[1];
+  S[(j0 + 2 * t) * KT + c0 + g] -= wt[0];      // R rows of the panel
+  S[(j0 + 2 * t + 1) * KT + c0 + g] -= wt[1];
+  __syncwarp();
+  // X_w -= Y_p w :  b = w[k][n=g] = w^T[g][k]
+  const double b0 = sc[g * 8 + t], b1 = sc[g * 8 + 4 + t];
+#pragma unroll 4
+  for (int mf = 0; mf < B / 8; ++mf) {
+    const int r = 8 * mf + g;
+    double cfr[2] = {0.0, 0.0};
+    dmma(cfr, Xs[swz(r, j0 + t, KT)], b0);
+    dmma(cfr, Xs[swz(r, j0 + 4 + t, KT)], b1);
+    double* x0 = &Xs[swz(r, c0 + 2 * t, KT)];
+    double* x1 = &Xs[swz(r, c0 + 2 * t + 1, KT)];
+    *x0 -= cfr[0];
+    *x1 -= cfr[1];
+  }
+}
+
+// T of a tile from tau (diag) and G (lower part of S), blockwise with DMMA:
+// T[q-block][p-block] = -(sum_{q'=q}^{p-1} T[q][q'] G[q'][p]) T_pp, one warp
+// per row block q < p, columns p = 1..NP-1 in order.  Tw stride KT+4.
+template <int KT>
+__device__ __forceinline__ void build_t(const double* S, const double* Tp, double* Tw, double* Tg,
+                                        double* scr) {
+  constexpr int NP = KT / 8, TL = KT + 4;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  for (int e = tid; e < KT * KT; e += 256) {
+    const int i = e / KT, j = e - i * KT;
+    Tw[i * TL + j] = ((i >> 3) == (j >> 3)) ? Tp[(i >> 3) * 64 + (i & 7) * 8 + (j & 7)] : 0.0;
+  }
+  __syncthreads();
+  double* sc = scr + warp * 64;
+  for (int p = 1; p < NP; ++p) {
+    if (warp < p) {
+      const int q = warp;
+      double m[2] = {0.0, 0.0};
+      for (int qq = q; qq < p; ++qq) {
+#pragma unroll
+        for (int k0 = 0; k0 < 8; k0 += 4)
+          dmma(m, Tw[(8 * q + g) * TL + 8 * qq + k0 + t], S[(8 * p + g) * KT + 8 * qq + k0 + t]);
+      }
+      sc[g * 8 + 2 * t] = m[0];
+      sc[g * 8 + 2 * t + 1] = m[1];
+      __syncwarp();
+      double o[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k0 = 0; k0 < 8; k0 += 4) dmma(o, sc[g * 8 + k0 + t], Tp[p * 64 + (k0 + t) * 8 + g]);
+      Tw[(8 * q + g) * TL + 8 * p + 2 * t] = -o[0];
+      Tw[(8 * q + g) * TL + 8 * p + 2 * t + 1] = -o[1];
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < KT * KT; e += 256) {
+    const int i = e / KT, j = e - i * KT;
+    Tg[e] = Tw[i * TL + j];
+  }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
+  using C = BlkCfg<KT>;
+  constexpr int B = C::B, NP = C::NP;
+  extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
+  double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
+  double* Tp = Xs + C::XS;                        // NP x 64
+  double* scr = Tp + NP * 64;                     // 8 warps x 64
+  __shared__ double tau_s[KT];
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int chain = blockIdx.x;
   const long r0 = (long)chain * a.G.rpc;
   const int ntiles = chain_real_tiles(a.G, chain, KT);
-  double* Ubase = a.U + (long)chain * (a.G.L + 1) * KT * KT;
+  double* Tbase = a.U + (long)chain * (a.G.L + 1) * KT * KT;
+  const int b = a.G.b;
 
-  // ---- head: plain QR of rows [r0, r0+KT)
-  load_rows_plain<KT, LDS>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, C::NT);
+  // ---- head: plain QR of rows [r0, r0+KT) (unblocked smem sweep, once per chain)
+  load_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  householder_sweep<KT, true>(S, 0, Ubase, tau_s);
-  store_rows_plain<KT, LDS>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, C::NT);
+  householder_sweep<KT, true, KT>(S, 0, Xs, tau_s);   // U -> Xs (ld KT+1)
+  store_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
   __syncthreads();
-  for (int i = tid; i < KT * KT; i += C::NT) {  // top := R (zero strictly lower part)
-    int r = i / KT, cc = i - r * KT;
-    if (cc < r) S[r * LDS + cc] = 0.0;
-  }
+  u_to_t_block<KT>(Xs, Xs + KT * (KT + 1), Tbase);
   __syncthreads();
 
   // ---- structured tiles
   for (int t = 1; t <= ntiles; ++t) {
-    const long gr0 = r0 + KT + (long)(t - 1) * a.G.b;
-    load_rows_plain<KT, LDS>(S, KT, a.D, a.ldd, gr0, a.G.b, a.G.nrows, a.ncols, tid, C::NT);
+    const long gr0 = r0 + KT + (long)(t - 1) * b;
+    long rem = a.G.nrows - gr0;
+    const int nb = (int)(rem < b ? rem : b);
+    TSTAMP(t0);
+    load_tile_async(Xs, KT, a.D, a.ldd, gr0, B, gr0, gr0 + nb, 0, KT, a.ncols, tid, 256);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    householder_sweep<KT, false>(S, a.G.b, Ubase + (long)t * KT * KT, tau_s);
-    store_rows_plain<KT, LDS>(S, KT, a.D, a.ldd, gr0, a.G.b, a.G.nrows, a.ncols, tid, C::NT);
+    TSTAMP(t1);
+    TACC(0, t0, t1);
+    for (int p = 0; p < NP; ++p) {
+#ifdef OTS_TIMING
+      long long q0 = clock64();
+#endif
+      if (warp == p) panel_factor<KT>(p, S, Xs, Tp, tau_s, nb);
+#ifdef OTS_TIMING
+      if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
+#endif
+      __syncthreads();
+#ifdef OTS_TIMING
+      long long q1 = clock64();
+#endif
+      if (warp < NP && warp != p) panel_apply<KT>(p, warp, S, Xs, Tp, scr + warp * 64);
+#ifdef OTS_TIMING
+      if (warp == p + 1 && (tid & 31) == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - q1));
+      if (tid == 0) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - q0));
+#endif
+    }
     __syncthreads();
+    TSTAMP(t2);
+    TACC(1, t1, t2);
+    // Y (in place of the tile) -> global
+    for (int i = tid; i < nb * (KT / 2); i += 256) {
+      const int r = i / (KT / 2), u = i - r * (KT / 2), c = 2 * u;
+      if (c >= a.ncols) continue;
+      double* dst = a.D + (gr0 + r) * a.ldd + c;
+      if (c + 1 < a.ncols) *reinterpret_cast<double2*>(dst) = make_double2(Xs[swz(r, c, KT)], Xs[swz(r, c + 1, KT)]);
+      else dst[0] = Xs[swz(r, c, KT)];
+    }
+    __syncthreads();
+    TSTAMP(t3);
+    TACC(2, t2, t3);
+    build_t<KT>(S, Tp, Xs, Tbase + (long)t * KT * KT, scr);
+    __syncthreads();
+    TSTAMP(t4);
+    TACC(3, t3, t4);
+    if (threadIdx.x == 0) TACC(4, 0, 1);
   }
 
   // ---- chain R (upper triangle, exact zeros below)
   double* R = a.Rout + (long)chain * KT * KT;
-  for (int i = tid; i < KT * KT; i += C::NT) {
+  for (int i = tid; i < KT * KT; i += 256) {
     int r = i / KT, cc = i - r * KT;
-    R[i] = (cc >= r) ? S[r * LDS + cc] : 0.0;
+    R[i] = (cc >= r) ? S[r * KT + cc] : 0.0;
   }
 }
 
-// U (diag tau, strict-upper Gram) -> T via the dlarft recurrence, one CTA of
-// KT threads per tile; row i of T computed by thread i.
-template <int KT>
-__global__ void __launch_bounds__(KT) u_to_t_kernel(double* UT, ChainGeom G) {
-  extern __shared__ __align__(16) double ush[];
-  double* Us = ush;             // U (KT x KT)
-  double* Tt = ush + KT * KT;   // transposed T: Tt[l*KT + i] = T[i][l]
-  const int tile = blockIdx.x;
-  const int chain = tile / (G.L + 1), t = tile - chain * (G.L + 1);
-  if (chain >= G.nchains) return;
-  if (t > 0 && t > chain_real_tiles(G, chain, KT)) return;
-  double* Ug = UT + (long)tile * KT * KT;
-  const int i = threadIdx.x;
-  for (int e = i; e < KT * KT; e += KT) Us[e] = Ug[e];
-  for (int l = 0; l < KT; ++l) Tt[l * KT + i] = 0.0;
-  __syncthreads();
-  Tt[i * KT + i] = Us[i * KT + i];
-  for (int j = i + 1; j < KT; ++j) {
-    double s = 0.0;
-    for (int l = i; l < j; ++l) s = fma(Tt[l * KT + i], Us[l * KT + j], s);
-    Tt[j * KT + i] = -Us[j * KT + j] * s;
-  }
-  __syncthreads();
-  for (int e = i; e < KT * KT; e += KT) {
-    int r = e / KT, cc = e - r * KT;
-    Ug[e] = Tt[cc * KT + r];
-  }
-}
-
+// head T from U (ld KT+1): T via dlarft recurrence (once per chain)
 // ---------------------------------------------------------------------------
 // Q formation (reverse chain walk).  Per structured tile (reverse order):
 //   M = T C ; out_rows = -Y M ; C <- C - M
@@ -367,17 +657,11 @@ __global__ void __launch_bounds__(256, 1) chain_qform_kernel(QformArgs a) {
 // ---------------------------------------------------------------------------
 template <int KT>
 static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st) {
-  using C = FactorCfg<KT>;
-  if (a.G.b > C::BMAX || a.G.nchains <= 0) return cudaErrorInvalidValue;
+  using C = BlkCfg<KT>;
+  if (a.G.b > C::B || a.G.nchains <= 0) return cudaErrorInvalidValue;
   auto k = chain_factor_kernel<KT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  k<<<a.G.nchains, C::NT, C::SMEM, st>>>(a);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  long tiles = (long)a.G.nchains * (a.G.L + 1);
-  const int usm = 2 * KT * KT * 8;
-  cudaFuncSetAttribute(u_to_t_kernel<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, usm);
-  u_to_t_kernel<KT><<<(unsigned)tiles, KT, usm, st>>>(a.U, a.G);
+  k<<<a.G.nchains, 256, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -402,6 +686,18 @@ cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st) {
   if (KT == 32) return qform_t<32>(a, st);
   if (KT == 64) return qform_t<64>(a, st);
   return cudaErrorInvalidValue;
+}
+
+int debug_counters(unsigned long long* out, int reset) {
+#ifdef OTS_TIMING
+  cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * 16);
+  if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_dbg, z, sizeof z); }
+  return 1;
+#else
+  for (int i = 0; i < 16; ++i) out[i] = 0;
+  (void)reset;
+  return 0;
+#endif
 }
 
 int chain_bmax(int KT) {

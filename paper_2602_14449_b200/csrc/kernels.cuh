@@ -53,5 +53,6 @@ cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
 cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
 int chain_bmax(int KT);
+int debug_counters(unsigned long long* out, int reset);
 
 }  // namespace ots

@@ -27,6 +27,7 @@
 #include "ots.h"
 
 #include "kernels.cuh"
+namespace ots { cudaError_t fp64_peak(int nsm, cudaStream_t st, double* tflops); }
 
 using namespace ots;
 
@@ -38,10 +39,6 @@ inline int kt_for(long k) { return k <= 16 ? 16 : (k <= 32 ? 32 : 64); }
 __global__ void set_identity_kernel(double* D, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n * n) D[i] = (i / n == i % n) ? 1.0 : 0.0;
-}
-__global__ void fill_kernel(double* D, long n, double v) {
-  long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) D[i] = v;
 }
 __global__ void nonneg_fix_kernel(double* Q, long ldq, long m, int k, double* R, long ldr) {
   // core.py:75-83 phase fix for real: column sign of R diag (0 -> +1)
@@ -86,6 +83,7 @@ struct ots_ctx {
   std::vector<cudaEvent_t> pev;
   std::vector<float> pms;
   std::vector<std::string> last_names;
+  int launches = 0;
   // distributed job state
   struct Job* job = nullptr;
 };
@@ -473,6 +471,16 @@ int ots_sm_count(const ots_ctx* c) { return c ? c->nsm : 0; }
 
 int ots_set_profiling(ots_ctx* c, int enable) { c->profile = enable != 0; return OTS_OK; }
 
+int ots_last_launch_count(const ots_ctx* c) { return c ? c->launches : 0; }
+
+int ots_debug_counters(unsigned long long* out, int reset) { return ots::debug_counters(out, reset); }
+
+int ots_fp64_peak(ots_ctx* ctx, double* tflops) {
+  cudaSetDevice(ctx->device);
+  CK(fp64_peak(ctx->nsm, nullptr, tflops));
+  return OTS_OK;
+}
+
 int ots_last_profile(const ots_ctx* c, char* names, int cap, float* ms, int mcap) {
   std::string all;
   int n = (int)c->pms.size();
@@ -545,6 +553,7 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
   CK(launch_qtop(j.s, Q, ldq, st));
   CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   prof_mark(ctx, st, "tail");
+  ctx->launches = 14 + 3 * (int)j.lv.size();
   rc = read_status(ctx, j, diag_host);
   prof_end(ctx);
   return rc;
@@ -583,6 +592,7 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, 
   CK(launch_tsgemm_nn(a, KT, ctx->nsm, st));
   if (nonneg_diag) nonneg_fix_kernel<<<std::min<long>(1024, (m * k + 255) / 256), 256, 0, st>>>(Q, ldq, m, (int)k, R, ldr);
   prof_mark(ctx, st, "sign");
+  ctx->launches = 3 + 3 * (int)j.lv.size() + (nonneg_diag ? 1 : 0);
   CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   prof_end(ctx);
@@ -690,8 +700,6 @@ int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank) {
   if (nranks > 64) return fail(ctx, OTS_E_UNSUPPORTED, "more than 64 ranks");
   CK(cudaMemcpyAsync(j.Rall, r_all, (size_t)nranks * KT * KT * 8, cudaMemcpyDeviceToDevice, st));
   // global levels over the gathered rank R's (rows = nranks*KT)
-  char* base = reinterpret_cast<char*>(j.Cglob + (size_t)64 * KT * KT);
-  (void)base;
   std::vector<Level> g;
   {
     // reuse the tail of the workspace: carve from a fresh arena after Cglob

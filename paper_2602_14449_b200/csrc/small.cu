@@ -269,8 +269,31 @@ __device__ bool blk_getrf(double* A, int ld, int n, int* piv, double* red, int* 
 // rotates row pairs until mutually orthogonal.  If Jt != null the same
 // rotations are applied to the rows of Jt.  sigma[i] = ||row i|| at exit.
 // Parallel round-robin ordering: n/2 disjoint pairs per step.
+__device__ void blk_jacobi_rows_core(double* W, int ldw, double* Jt, int ldj, int n, double* sigma,
+                                     double* red);
+
+// Stage W (and Jt when it fits) into shared memory for the rotation sweeps.
 __device__ void blk_jacobi_rows(double* W, int ldw, double* Jt, int ldj, int n, double* sigma,
-                                double* red) {
+                                double* red, double* sbuf = nullptr, int scap = 0) {
+  const int ls = n + 1;  // odd stride: rows of a pair hit different banks
+  if (sbuf && n * ls <= scap) {
+    double* Ws = sbuf;
+    double* Js = (Jt && 2 * n * ls <= scap) ? sbuf + n * ls : nullptr;
+    __syncthreads();
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; Ws[i * ls + j] = W[i * ldw + j]; }
+    if (Js) BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; Js[i * ls + j] = Jt[i * ldj + j]; }
+    __syncthreads();
+    blk_jacobi_rows_core(Ws, ls, Js ? Js : Jt, Js ? ls : ldj, n, sigma, red);
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; W[i * ldw + j] = Ws[i * ls + j]; }
+    if (Js) BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; Jt[i * ldj + j] = Js[i * ls + j]; }
+    __syncthreads();
+    return;
+  }
+  blk_jacobi_rows_core(W, ldw, Jt, ldj, n, sigma, red);
+}
+
+__device__ void blk_jacobi_rows_core(double* W, int ldw, double* Jt, int ldj, int n, double* sigma,
+                                     double* red) {
   const int ne = (n + 1) & ~1;  // even count incl. a dummy
   const int npairs = ne / 2;
   int gs = 1;
@@ -339,8 +362,9 @@ __device__ void blk_jacobi_rows(double* W, int ldw, double* Jt, int ldj, int n, 
   __syncthreads();
 }
 
-__device__ double blk_sigma_max(double* W, int ld, int n, double* sig, double* red) {
-  blk_jacobi_rows(W, ld, nullptr, 0, n, sig, red);
+__device__ double blk_sigma_max(double* W, int ld, int n, double* sig, double* red,
+                                double* sbuf = nullptr, int scap = 0) {
+  blk_jacobi_rows(W, ld, nullptr, 0, n, sig, red, sbuf, scap);
   double m = 0.0;
   for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, sig[i]);
   return block_max(m, red);
@@ -350,7 +374,26 @@ __device__ double blk_sigma_max(double* W, int ld, int n, double* sig, double* r
 // T-solver dispatch (reflector.py:80-153).  X (n x m) overwritten.
 //   adjoint=false: T X = B ; adjoint=true: T^T X = B.
 // ---------------------------------------------------------------------------
+__device__ void t_solve_core(const SmallState& s, double* X, int ldx, int m, bool adjoint);
+
+extern __shared__ __align__(16) double dsm[];
+constexpr int SMALL_SMEM_DOUBLES = 25 * 1024;   // 200 KB dynamic smem of the small kernels
+
 __device__ void t_solve(const SmallState& s, double* X, int ldx, int m, bool adjoint) {
+  const int n = s.k0;
+  if (n * m <= SMALL_SMEM_DOUBLES) {
+    __syncthreads();
+    BLK_FOR(e, n * m) { int i = e / m, j = e - i * m; dsm[e] = X[i * ldx + j]; }
+    __syncthreads();
+    t_solve_core(s, dsm, m, m, adjoint);
+    BLK_FOR(e, n * m) { int i = e / m, j = e - i * m; X[i * ldx + j] = dsm[e]; }
+    __syncthreads();
+    return;
+  }
+  t_solve_core(s, X, ldx, m, adjoint);
+}
+
+__device__ void t_solve_core(const SmallState& s, double* X, int ldx, int m, bool adjoint) {
   const int n = s.k0;
   const double* F = s.Tf;
   const int ld = s.ld;
@@ -421,7 +464,7 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
   BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; double x = s.X1[i * ld + j]; f = fma(x, x, f); }
   f = sqrt(block_sum(f, red));
   double defect = f;
-  if (f > s.orth_tol) defect = blk_sigma_max(s.X1, ld, n, s.sig, red);
+  if (f > s.orth_tol) defect = blk_sigma_max(s.X1, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
   if (threadIdx.x == 0) s.diag[2] = defect;
   if (defect > s.orth_tol && !s.allow_defect) {
     if (threadIdx.x == 0) s.status[0] = OTS_E_ORTHONORMALITY;
@@ -436,12 +479,15 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
   switch (s.choice) {
     case CHOICE_QR: {
       // nonneg-diagonal QR of V_t (core.py:61-84): P = -Q1, T = I + R1^T
-      blk_copy(s.X1, ld, s.Vt, ld, n, n);
+      double* Wq = (n * (n + 1) <= SMALL_SMEM_DOUBLES) ? dsm : s.X1;
+      const int lq = (Wq == dsm) ? n + 1 : ld;
+      blk_copy(Wq, lq, s.Vt, ld, n, n);
       __syncthreads();
-      blk_geqr2(s.X1, ld, n, n, s.tau, red);
-      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? s.X1[i * ld + j] : 0.0; }
+      blk_geqr2(Wq, lq, n, n, s.tau, red);
+      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? Wq[i * lq + j] : 0.0; }
       __syncthreads();
-      blk_org2r(s.X1, ld, n, n, s.tau, red);  // X1 = Q1
+      blk_org2r(Wq, lq, n, n, s.tau, red);  // Q1
+      if (Wq != s.X1) { blk_copy(s.X1, ld, Wq, lq, n, n); __syncthreads(); }
       BLK_FOR(i, n) { double d = s.X2[i * ld + i]; s.pvec[i] = (d < 0.0) ? -1.0 : 1.0; }
       __syncthreads();
       BLK_FOR(e, n * n) {
@@ -479,7 +525,7 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
       BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = s.Vt[j * ld + i]; }
       blk_identity(s.X2, ld, n);
       __syncthreads();
-      blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red);
+      blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
       // U columns u_j = X1 row j / sigma_j (null directions: v_j orthogonalised)
       // store U^T rows in X1 (normalised)
       BLK_FOR(e, n * n) {
@@ -543,7 +589,7 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
       ff = sqrt(block_sum(ff, red));
       double pd = ff;
       const double ptol = 1e-12 * (n > 1 ? n : 1);
-      if (ff > ptol) pd = blk_sigma_max(s.X1, ld, n, s.sig, red);
+      if (ff > ptol) pd = blk_sigma_max(s.X1, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
       if (pd > ptol) { st = OTS_E_PARAMETER; break; }
       // T = I - V_t^T P, pivoted LU
       blk_gemm(s.Tdense, ld, s.Vt, ld, true, s.P, ld, false, n, n, n, -1.0, 0.0);
@@ -588,7 +634,7 @@ __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
   // kappa(T)
   BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] = s.Tdense[i * ld + j]; }
   __syncthreads();
-  blk_jacobi_rows(s.D1, ld, nullptr, 0, n, s.sig2, red);
+  blk_jacobi_rows(s.D1, ld, nullptr, 0, n, s.sig2, red, dsm, SMALL_SMEM_DOUBLES);
   double mx = 0.0, mn = 1e308;
   for (int i = threadIdx.x; i < n; i += blockDim.x) { mx = fmax(mx, s.sig2[i]); mn = fmin(mn, s.sig2[i]); }
   mx = block_max(mx, red);
@@ -609,7 +655,7 @@ __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
     s.D1[i * ld + j] = 0.5 * (s.D2[i * ld + j] + s.D2[j * ld + i]);
   }
   __syncthreads();
-  double lm = blk_sigma_max(s.D1, ld, n, s.sig2, red);
+  double lm = blk_sigma_max(s.D1, ld, n, s.sig2, red, dsm, SMALL_SMEM_DOUBLES);
   if (threadIdx.x == 0) s.diag[1] = sqrt(lm);
 }
 
@@ -655,7 +701,7 @@ __global__ void __launch_bounds__(SMALL_NT) mlu_kernel(const double* Z, int ldz,
   __shared__ double red[64];
   blk_copy(work, n, Z, ldz, n, n);
   __syncthreads();
-  double nrm = blk_sigma_max(work, n, n, work + n * n, red);
+  double nrm = blk_sigma_max(work, n, n, work + n * n, red, dsm, SMALL_SMEM_DOUBLES);
   if (nrm > 1.0 + 1e-8) { if (threadIdx.x == 0) *status = OTS_E_NORM_BOUND; return; }
   blk_copy(LU, n, Z, ldz, n, n);
   __syncthreads();
@@ -664,15 +710,18 @@ __global__ void __launch_bounds__(SMALL_NT) mlu_kernel(const double* Z, int ldz,
 }
 
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st) {
-  seed_kernel<<<1, SMALL_NT, 0, st>>>(s);
+  cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  seed_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 cudaError_t launch_diag(const SmallState& s, cudaStream_t st) {
-  diag_kernel<<<1, SMALL_NT, 0, st>>>(s);
+  cudaFuncSetAttribute(diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  diag_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 cudaError_t launch_z2(const SmallState& s, cudaStream_t st) {
-  z2_kernel<<<1, SMALL_NT, 0, st>>>(s);
+  cudaFuncSetAttribute(z2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  z2_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const double* Rfin, int ldr,
@@ -686,7 +735,8 @@ cudaError_t launch_qtop(const SmallState& s, double* Q, long ldq, cudaStream_t s
 }
 cudaError_t launch_mlu(const double* Z, int ldz, int n, double* LU, double* p, double* work, int* status,
                        cudaStream_t st) {
-  mlu_kernel<<<1, SMALL_NT, 0, st>>>(Z, ldz, n, LU, p, work, status);
+  cudaFuncSetAttribute(mlu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  mlu_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(Z, ldz, n, LU, p, work, status);
   return cudaGetLastError();
 }
 

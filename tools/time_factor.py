@@ -1,0 +1,19 @@
+"""Section cycle counters of chain_factor (needs OTS_LIB=.../libots_timing.so)."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2602_14449_b200 as P
+from paper_2602_14449_b200 import _native as NT
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 22
+A = torch.randn((n, 64), dtype=torch.float64, device="cuda:0")
+P.householder_qr(A); torch.cuda.synchronize()
+buf = (C.c_ulonglong * 16)()
+NT.lib().ots_debug_counters(buf, 1)
+ctx = NT.context(0); NT.lib().ots_set_profiling(ctx, 1)
+P.householder_qr(A); torch.cuda.synchronize()
+print(NT.profile(ctx))
+NT.lib().ots_debug_counters(buf, 0)
+tiles = buf[4]
+print("tiles", tiles)
+for i, nm in enumerate(["load", "sweep", "store", "tinv", "ntile", "pfact", "apply_nxt", "thread0_panel"]):
+    print(f"{nm:6s} {buf[i] / max(tiles,1):12.0f} cycles/tile")
