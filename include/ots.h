@@ -121,12 +121,14 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
                    const double* V, int64_t ldv, const double* A, int64_t lda,
                    double* Q, int64_t ldq, int choice, const double* P, int64_t ldp,
                    double orth_tol, void* stream);
-int ots_dist_gram(ots_ctx* ctx, double* gram_out, int64_t* gram_count);
+/* element counts of the exchanged device buffers: [gram, top rows, KT, y2] */
+int ots_dist_sizes(ots_ctx* ctx, int64_t* out4);
+int ots_dist_gram(ots_ctx* ctx, double* gram_out);
+int ots_dist_top_rows(ots_ctx* ctx, double* top_rows_out);   /* rank 0 writes */
 int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows);
-int ots_dist_top_rows(ots_ctx* ctx, double* top_rows_out, int64_t* count);
-int ots_dist_factor(ots_ctx* ctx, double* r_local_out, int64_t* kt);
+int ots_dist_factor(ots_ctx* ctx, double* r_local_out);      /* KT x KT */
 int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank);
-int ots_dist_qform(ots_ctx* ctx, double* y2_out, int64_t* count, double* sign_out);
+int ots_dist_qform(ots_ctx* ctx, double* y2_out, double* sign_out);  /* sign: rank 0 */
 int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign,
                     double* R, int64_t ldr, double* S, int64_t lds, double* diag_host);
 

@@ -54,16 +54,18 @@ def lib():
                     _dbl, _int, _vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
                 L.ots_householder_qr_f64.argtypes = [
                     _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp]
+                L.ots_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), _int]
                 L.ots_modified_lu_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp]
                 L.ots_dist_begin.argtypes = [
                     _vp, _i64, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp,
                     _i64, _dbl, _vp]
-                L.ots_dist_gram.argtypes = [_vp, _vp, C.POINTER(_i64)]
-                L.ots_dist_top_rows.argtypes = [_vp, _vp, C.POINTER(_i64)]
+                L.ots_dist_sizes.argtypes = [_vp, C.POINTER(_i64)]
+                L.ots_dist_gram.argtypes = [_vp, _vp]
+                L.ots_dist_top_rows.argtypes = [_vp, _vp]
                 L.ots_dist_seed.argtypes = [_vp, _vp, _vp]
-                L.ots_dist_factor.argtypes = [_vp, _vp, C.POINTER(_i64)]
+                L.ots_dist_factor.argtypes = [_vp, _vp]
                 L.ots_dist_tree.argtypes = [_vp, _vp, _int, _int]
-                L.ots_dist_qform.argtypes = [_vp, _vp, C.POINTER(_i64), _vp]
+                L.ots_dist_qform.argtypes = [_vp, _vp, _vp]
                 L.ots_dist_finish.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i64, C.POINTER(_dbl)]
                 _lib = L
     return _lib
@@ -74,7 +76,7 @@ EXPORTED_SYMBOLS = [
     "ots_two_stage_f64", "ots_householder_qr_f64", "ots_modified_lu_f64",
     "ots_set_profiling", "ots_last_profile", "ots_last_launch_count", "ots_fp64_peak",
     "ots_debug_counters",
-    "ots_dist_begin", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",
+    "ots_dist_begin", "ots_dist_sizes", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",
     "ots_dist_tree", "ots_dist_qform", "ots_dist_finish",
 ]
 
@@ -90,6 +92,16 @@ def context(device):
             raise E.NativeUnavailable(f"CUDA context on device {device}: {msg}")
         _ctx[device] = h
     return _ctx[device]
+
+
+def new_context(device):
+    """A fresh, uncached C context (e.g. one per simulated rank)."""
+    L = lib()
+    h = _vp()
+    rc = L.ots_ctx_create(int(device), C.byref(h))
+    if rc != 0:
+        raise E.NativeUnavailable(f"CUDA context on device {device}")
+    return h
 
 
 def check(rc, ctx, block=None):

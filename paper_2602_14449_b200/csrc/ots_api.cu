@@ -409,6 +409,8 @@ int read_status(ots_ctx* ctx, Job& j, double* diag_host) {
       snprintf(buf, sizeof buf, "Cholesky factor of T: matrix is not positive definite");
     else if (st == OTS_E_SINGULAR_T)
       snprintf(buf, sizeof buf, "T is numerically singular");
+    else if (st == OTS_E_VALUE)
+      snprintf(buf, sizeof buf, "input contains non-finite entries");
     else if (st == OTS_E_PARAMETER)
       snprintf(buf, sizeof buf, "explicit seed p is not unitary to tolerance");
     else
@@ -636,12 +638,21 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
   return job_setup(ctx, *ctx->job, c);
 }
 
-int ots_dist_gram(ots_ctx* ctx, double* gram_out, int64_t* count) {
+int ots_dist_sizes(ots_ctx* ctx, int64_t* out4) {
+  if (!ctx->job) return fail(ctx, OTS_E_VALUE, "ots_dist_begin not called");
+  Job& j = *ctx->job;
+  out4[0] = (int64_t)j.PW * j.NTOT1;                          // gram partial
+  out4[1] = j.c.k0 * ((j.c.k0 + j.c.k + 1) & ~1L);            // packed top rows
+  out4[2] = j.KT;                                              // R block is KT x KT
+  out4[3] = (int64_t)j.PW * j.BWa;                             // Y2 partial
+  return OTS_OK;
+}
+
+int ots_dist_gram(ots_ctx* ctx, double* gram_out) {
   Job& j = *ctx->job;
   int rc = phase_gram(ctx, j);
   if (rc) return rc;
   long cnt = (long)j.PW * j.NTOT1;
-  if (count) *count = cnt;
   if (gram_out) CK(cudaMemcpyAsync(gram_out, j.Gfull, cnt * 8, cudaMemcpyDeviceToDevice, j.c.st));
   return OTS_OK;
 }
@@ -654,11 +665,10 @@ __global__ void pack_top_kernel(const double* V, long ldv, const double* A, long
   }
 }
 
-int ots_dist_top_rows(ots_ctx* ctx, double* top_out, int64_t* count) {
+int ots_dist_top_rows(ots_ctx* ctx, double* top_out) {
   Job& j = *ctx->job;
   const long k0 = j.c.k0, k = j.c.k;
   const int ldt = (int)((k0 + k + 1) & ~1L);
-  if (count) *count = k0 * ldt;
   if (top_out && j.c.row0 == 0)
     pack_top_kernel<<<32, 256, 0, j.c.st>>>(j.c.V, j.c.ldv, j.c.A, j.c.lda, (int)k0, (int)k, top_out, ldt);
   CK(cudaGetLastError());
@@ -682,12 +692,11 @@ int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows) 
   return OTS_OK;
 }
 
-int ots_dist_factor(ots_ctx* ctx, double* r_local_out, int64_t* kt) {
+int ots_dist_factor(ots_ctx* ctx, double* r_local_out) {
   Job& j = *ctx->job;
   int rc = phase_apply1(ctx, j);
   if (rc) return rc;
   if ((rc = run_factor_levels(ctx, j.lv, j.KT, j.c.st))) return rc;
-  if (kt) *kt = j.KT;
   if (r_local_out)
     CK(cudaMemcpyAsync(r_local_out, j.lv.back().R, (size_t)j.KT * j.KT * 8, cudaMemcpyDeviceToDevice, j.c.st));
   return OTS_OK;
@@ -738,7 +747,7 @@ int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank) {
   return OTS_OK;
 }
 
-int ots_dist_qform(ots_ctx* ctx, double* y2_out, int64_t* count, double* sign_out) {
+int ots_dist_qform(ots_ctx* ctx, double* y2_out, double* sign_out) {
   Job& j = *ctx->job;
   cudaStream_t st = j.c.st;
   int rc;
@@ -749,7 +758,6 @@ int ots_dist_qform(ots_ctx* ctx, double* y2_out, int64_t* count, double* sign_ou
   }
   if ((rc = phase_gram2(ctx, j))) return rc;
   long cnt = (long)j.PW * j.BWa;
-  if (count) *count = cnt;
   if (y2_out) CK(cudaMemcpyAsync(y2_out, j.Y2full, cnt * 8, cudaMemcpyDeviceToDevice, st));
   return OTS_OK;
 }

@@ -470,6 +470,21 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
     if (threadIdx.x == 0) s.status[0] = OTS_E_ORTHONORMALITY;
     return;
   }
+  // Non-finite V or A (core.py:72-73, reached by the reference at the intra
+  // QR): any NaN/Inf entry poisons the Gram block [V^T V | V_b^T A_b] or the
+  // top rows A_t, so checking those k0 x (k0+k) values covers the n-row data.
+  {
+    int bad = 0;
+    BLK_FOR(e, n * n) { if (!isfinite(s.G[(e / n) * ld + (e % n)])) bad = 1; }
+    BLK_FOR(e, n * k) {
+      const int i = e / k, j = e - i * k;
+      if (!isfinite(s.VbA[i * ld + j]) || !isfinite(s.A[(long)i * s.lda + j])) bad = 1;
+    }
+    if (__syncthreads_or(bad)) {
+      if (threadIdx.x == 0) s.status[0] = OTS_E_VALUE;
+      return;
+    }
+  }
   // 3. V_t, A_t
   BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.Vt[i * ld + j] = s.V[(long)i * s.ldv + j]; }
   BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.At[i * ld + j] = s.A[(long)i * s.lda + j]; }

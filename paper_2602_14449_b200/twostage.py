@@ -16,7 +16,7 @@ import numpy as np
 from . import _device as D
 from . import errors as E
 from ._native import CHOICES, INTRA, check, lib
-from .core import all_finite, as_matrix, householder_qr, is_complex
+from .core import as_matrix, householder_qr, is_complex
 from .reflector import ReflectorDiagnostics
 
 INTRA_METHODS = ("householder", "cholshift")   # twostage.py:25
@@ -87,7 +87,6 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
                                f"('mlu', 'qr', 'polar', 'explicit')")
     if intra not in INTRA:
         raise E.ParameterError(f"unknown intra method {intra!r}; expected {INTRA_METHODS}")
-    finite = all_finite(v) and all_finite(a)
     dev = D.pick_device(v, a)
     ctx = D.ctx(dev)
     V = D.to_device(v, dev)
@@ -108,11 +107,7 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         ctx, n, k0, k, V.ptr, V.ld, A.ptr, A.ld, CHOICES[choice], INTRA[intra],
         P.ptr if P is not None else None, P.ld if P is not None else 0,
         1e-8, 0, Q.ptr, Q.ld, R.ptr, R.ld, S.ptr, S.ld, diag, D.stream_ptr(dev))
-    if rc == -8 or rc == -12:
-        check(rc, ctx)
-    if not finite:
-        raise ValueError("input contains non-finite entries")
-    check(rc, ctx)
+    check(rc, ctx)   # OrthonormalityError before the non-finite ValueError (device-side order)
     return TwoStageResult(Q.view() if was_torch else Q.numpy(),
                           R.view() if was_torch else R.numpy(),
                           S.view() if was_torch else S.numpy(),
