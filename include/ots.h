@@ -78,12 +78,30 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
                       double* Q, int64_t ldq, double* R, int64_t ldr,
                       double* S, int64_t lds, double* diag_host, void* stream);
 
+/* b_two_stage_qr(v, a, u, inner, choice)          -- oblique.py:279-315
+ * for the weighted inner product M = diag(d) (d > 0, device, n values) with
+ * u = initial_b_basis(inner, k0+k) (oblique.py:93-108): computed as the
+ * Euclidean path on (D^1/2 V, D^1/2 A), Q = D^-1/2 Q' sgn, R = sgn R'
+ * (positive diagonal as oblique.py:232), S unchanged.
+ * orth_tol: the B-path default is 1e-6 (oblique.py:125). */
+int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                             const double* V, int64_t ldv, const double* A, int64_t lda,
+                             const double* d, int choice, const double* P, int64_t ldp,
+                             double orth_tol, double* Q, int64_t ldq, double* R, int64_t ldr,
+                             double* S, int64_t lds, double* diag_host, void* stream);
+
 /* householder_qr(a, nonneg_diag)                 -- core.py:61-84
  * LAPACK dgeqrf+dorgqr semantics (R diagonal signs as dlarfg); with
  * nonneg_diag the phase fix of core.py:75-83. */
 int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,
                            const double* A, int64_t lda, double* Q, int64_t ldq,
                            double* R, int64_t ldr, int nonneg_diag, void* stream);
+
+/* shifted_cholesky_qr(a)                          -- core.py:177-202
+ * shifted CholeskyQR + 2 refinements; NotPositiveDefinite on breakdown. */
+int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,
+                                const double* A, int64_t lda, double* Q, int64_t ldq,
+                                double* R, int64_t ldr, void* stream);
 
 /* modified_lu(z)                                  -- reflector.py:53-77
  * LU (n x n, L strict-lower unit + U upper, packed, ld n) and p (n). */

@@ -80,3 +80,27 @@ def householder_qr(a, nonneg_diag=False):
                                           1 if nonneg_diag else 0, D.stream_ptr(dev))
         check(rc, ctx)
     return QRPair(out_like(was_torch, Q), out_like(was_torch, R))
+
+
+def shifted_cholesky_qr(a, refine_passes=2):
+    """Shifted Cholesky-QR + 2 unshifted refinements on the GPU
+    (core.py:177-202).  Breakdown raises NotPositiveDefinite."""
+    if refine_passes != 2:
+        raise NotImplementedError("this build implements the reference's 2 refinement passes")
+    was_torch = D.is_torch(a)
+    a = as_matrix(a, "a")
+    m, n = a.shape
+    if m < n:
+        raise E.DimensionError(f"need rows >= cols, got {m}x{n}")
+    if is_complex(a):
+        raise NotImplementedError("complex shifted_cholesky_qr: not in this build")
+    dev = D.pick_device(a)
+    ctx = D.ctx(dev)
+    A = D.to_device(a, dev)
+    Q = D.empty(m, n, dev)
+    R = D.zeros(n, n, dev)
+    if n:
+        rc = lib().ots_shifted_cholesky_qr_f64(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
+                                               D.stream_ptr(dev))
+        check(rc, ctx)
+    return QRPair(out_like(was_torch, Q), out_like(was_torch, R))

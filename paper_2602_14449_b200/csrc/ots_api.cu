@@ -84,6 +84,8 @@ struct ots_ctx {
   std::vector<float> pms;
   std::vector<std::string> last_names;
   int launches = 0;
+  char* b_ws = nullptr;      // B-inner scaled copies
+  size_t b_size = 0;
   // distributed job state
   struct Job* job = nullptr;
 };
@@ -170,6 +172,7 @@ struct Job {
   std::vector<Level> lv;        // local levels (0 = data rows)
   std::vector<Level> glv;       // global tree levels over gathered rank R's
   double* Rall = nullptr;       // gathered R's copy (nranks*KT x KT)
+  double* chol_ws = nullptr;    // 3 ld x ld scratch of the cholshift step
   double* Rfinal = nullptr;
 };
 
@@ -292,9 +295,14 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   j.grid_tn2 = grid_for_tn(j.PW, j.BWa, false, false, ctx->nsm);
   const int ld = j.ld, KT = j.KT;
   const int gmax = std::max(j.grid_tn, j.grid_tn2);
+  const int PWk = pad32(std::max<long>(k, 1));
+  const size_t part_n = std::max((size_t)gmax * j.PW * j.NTOT1,
+                                 (size_t)grid_for_tn(PWk, 0, true, true, ctx->nsm) * PWk * PWk);
+  const size_t gf_n = std::max((size_t)j.PW * j.NTOT1, (size_t)PWk * PWk);
   size_t bytes = 0;
-  bytes += (size_t)gmax * j.PW * j.NTOT1 * 8 + 256;
-  bytes += (size_t)j.PW * j.NTOT1 * 8 * 2 + 512;                  // Gfull, Y2full
+  bytes += part_n * 8 + 256;
+  bytes += gf_n * 8 * 2 + 512;                                       // Gfull, Y2full
+  bytes += (size_t)3 * ld * ld * 8 + 256;                            // cholshift scratch
   bytes += (size_t)k0 * (k0 + k + 2) * 8 + 256;                    // top rows
   bytes += (size_t)16 * ld * ld * 8 + 16 * 256;                    // small matrices
   bytes += (size_t)8 * ld * 8 + 8 * 256;                           // vectors
@@ -305,9 +313,10 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   int rc = ensure_ws(ctx, bytes);
   if (rc) return rc;
   Arena ar(ctx->ws, ctx->ws_size);
-  j.partial = ar.take<double>((size_t)gmax * j.PW * j.NTOT1);
-  j.Gfull = ar.take<double>((size_t)j.PW * j.NTOT1);
-  j.Y2full = ar.take<double>((size_t)j.PW * j.NTOT1);
+  j.partial = ar.take<double>(part_n);
+  j.Gfull = ar.take<double>(gf_n);
+  j.Y2full = ar.take<double>(gf_n);
+  j.chol_ws = ar.take<double>((size_t)3 * ld * ld);
   j.top = ar.take<double>((size_t)std::max<long>(k0, 1) * (k0 + k + 2));
   SmallState& s = j.s;
   s = SmallState{};
@@ -394,6 +403,51 @@ int phase_apply2(ots_ctx* ctx, Job& j) {
   return OTS_OK;
 }
 
+__global__ void set_identity_ld_kernel(double* D, int n, int ld) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n * n; e += gridDim.x * blockDim.x) {
+    int i = e / n, jj = e - i * n;
+    D[i * ld + jj] = (i == jj) ? 1.0 : 0.0;
+  }
+}
+__global__ void triu_copy_kernel(const double* Rs, int lds, double* R, long ldr, int k) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < k * k; e += gridDim.x * blockDim.x) {
+    int i = e / k, jj = e - i * k;
+    R[i * ldr + jj] = (jj >= i) ? Rs[i * lds + jj] : 0.0;
+  }
+}
+__global__ void ones_kernel(double* v, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) v[i] = 1.0;
+}
+
+// Shifted Cholesky-QR with two refinements on X (m x k, in place):
+// core.py:177-202.  R (k x k, ldr) written; status <- INTRA_FAILURE on breakdown.
+int run_cholshift(ots_ctx* ctx, Job& j, double* X, long ldx, long m, int k, double* R, long ldr,
+                  cudaStream_t st) {
+  const int PWk = pad32(k);
+  const int grid = grid_for_tn(PWk, 0, true, true, ctx->nsm);
+  double* W = j.chol_ws;   // small scratch (2 k x ld + k)
+  double* Z = j.s.X2;
+  double* Racc = j.s.Sd;
+  set_identity_ld_kernel<<<4, 256, 0, st>>>(Racc, k, j.ld);
+  for (int pass = 0; pass < 3; ++pass) {
+    TnArgs a{};
+    a.P = X; a.ldp = ldx; a.pc0 = 0; a.pcols = k;
+    a.B = nullptr; a.ldb = 0; a.bc0 = 0; a.bcols = 0;
+    a.row_begin = 0; a.row_end = m; a.b_row_begin = 0; a.p_row_begin = 0;
+    a.partial = j.partial;
+    CK(launch_tsgemm_tn(a, PWk, 0, true, true, grid, st));
+    CK(launch_reduce(j.partial, grid, (long)PWk * PWk, j.Gfull, 1.0, st));
+    CK(launch_cholqr_step(j.Gfull, PWk, k, m, pass == 0, W, j.ld, Z, Racc, j.s.status, st));
+    NnArgs b{};
+    b.P = X; b.ldp = ldx; b.kdim = k; b.Z = Z; b.ldz = j.ld; b.B = nullptr; b.ldb = 0;
+    b.X = X; b.ldx = ldx; b.ncols = k; b.row_begin = 0; b.row_end = m; b.colscale = nullptr;
+    CK(launch_tsgemm_nn(b, j.KT, ctx->nsm, st));
+  }
+  triu_copy_kernel<<<4, 256, 0, st>>>(Racc, j.ld, R, ldr, k);
+  CK(cudaGetLastError());
+  return OTS_OK;
+}
+
 int read_status(ots_ctx* ctx, Job& j, double* diag_host) {
   const JobCfg& c = j.c;
   CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, c.st));
@@ -411,6 +465,8 @@ int read_status(ots_ctx* ctx, Job& j, double* diag_host) {
       snprintf(buf, sizeof buf, "T is numerically singular");
     else if (st == OTS_E_VALUE)
       snprintf(buf, sizeof buf, "input contains non-finite entries");
+    else if (st == OTS_E_INTRA_FAILURE)
+      snprintf(buf, sizeof buf, "shifted Cholesky-QR broke down: Cholesky factorization failed (matrix not positive definite)");
     else if (st == OTS_E_PARAMETER)
       snprintf(buf, sizeof buf, "explicit seed p is not unitary to tolerance");
     else
@@ -428,6 +484,100 @@ int validate_layout(ots_ctx* ctx, const void* p, long ld, const char* name) {
 }
 
 }  // namespace
+
+struct BHook {                 // B-inner (diagonal M) extension of the pipeline
+  const double* Gu; int ldgu;   // unweighted Gram of the original V
+  const double* dinv_top;       // 1/d on the top k0 rows
+  const double* d; long n;      // full weights (for the Q epilogue)
+};
+
+__global__ void b_unscale_kernel(double* Q, long ldq, long n, int k, const double* d, const double* R,
+                                 long ldr) {
+  // Q <- D^{-1/2} Q diag(sg), sg_j = sign(R_jj) (0 -> +1): the B-path's
+  // positive-diagonal convention (oblique.py:232).
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n * k; e += (long)gridDim.x * blockDim.x) {
+    long i = e / k; int j = (int)(e - i * k);
+    const double sg = (R[(long)j * ldr + j] < 0.0) ? -1.0 : 1.0;
+    Q[i * ldq + j] *= sg * rsqrt(d[i]);
+  }
+}
+__global__ void b_rsign_kernel(double* R, long ldr, int k) {
+  // R <- diag(sg) R  (rows), sg from its own diagonal; one block, ordered so
+  // the diagonal is read before it is rewritten.
+  __shared__ double sg[64];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) sg[j] = (R[(long)j * ldr + j] < 0.0) ? -1.0 : 1.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    int i = e / k, j = e - i * k;
+    R[(long)i * ldr + j] *= sg[i];
+  }
+}
+__global__ void row_scale_kernel(const double* X, long ldx, long n, int k, const double* d, double pw,
+                                 double* Y, long ldy) {
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n * k; e += (long)gridDim.x * blockDim.x) {
+    long i = e / k; int j = (int)(e - i * k);
+    const double s = (pw > 0.0) ? sqrt(d[i]) : rsqrt(d[i]);
+    Y[i * ldy + j] = X[i * ldx + j] * s;
+  }
+}
+__global__ void inv_top_kernel(const double* d, int k0, double* out) {
+  for (int i = threadIdx.x; i < k0; i += blockDim.x) out[i] = 1.0 / d[i];
+}
+
+int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long ldq, double* R, long ldr,
+                       double* S, long lds, double* diag_host, const BHook* bh) {
+  const long n = c.n_local, k0 = c.k0, k = c.k;
+  cudaStream_t st = c.st;
+  Job j;
+  int rc;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  const int KT = j.KT;
+  if (bh) { j.s.Gu = bh->Gu; j.s.ldgu = bh->ldgu; j.s.dinv_top = bh->dinv_top; }
+  prof_begin(ctx, st);
+  if ((rc = phase_gram(ctx, j))) return rc;
+  prof_mark(ctx, st, "gram");
+  j.s.Sout = S; j.s.lds_out = (int)lds;
+  CK(launch_seed(j.s, st));
+  CK(cudaEventRecord(ctx->ev_seed, st));
+  prof_mark(ctx, st, "seed");
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
+  CK(launch_diag(j.s, ctx->side));
+  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
+  if ((rc = phase_apply1(ctx, j))) return rc;
+  prof_mark(ctx, st, "apply1");
+  if (intra == OTS_INTRA_HOUSEHOLDER) {
+    if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
+    prof_mark(ctx, st, "factor");
+    set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
+    if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st))) return rc;
+    prof_mark(ctx, st, "qform");
+    CK(launch_sign(j.s, Q + k0 * ldq, ldq, j.lv.back().R, KT, R, (int)ldr, st));
+  } else {
+    if ((rc = run_cholshift(ctx, j, Q + k0 * ldq, ldq, n - k0, (int)k, R, ldr, st))) return rc;
+    ones_kernel<<<1, 64, 0, st>>>(j.svec, (int)k);
+    prof_mark(ctx, st, "cholshift");
+  }
+  if ((rc = phase_gram2(ctx, j))) return rc;
+  prof_mark(ctx, st, "gram2");
+  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
+  CK(launch_z2(j.s, st));
+  prof_mark(ctx, st, "z2");
+  if ((rc = phase_apply2(ctx, j))) return rc;
+  prof_mark(ctx, st, "apply2");
+  CK(launch_qtop(j.s, Q, ldq, st));
+  if (bh) {
+    const int nb = (int)std::min<long>(4096, (n * k + 255) / 256);
+    b_unscale_kernel<<<nb, 256, 0, st>>>(Q, ldq, n, (int)k, bh->d, R, ldr);
+    b_rsign_kernel<<<1, 256, 0, st>>>(R, ldr, (int)k);
+    prof_mark(ctx, st, "b_epilogue");
+  }
+  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
+  prof_mark(ctx, st, "tail");
+  ctx->launches = 14 + 3 * (int)j.lv.size() + (bh ? 2 : 0);
+  rc = read_status(ctx, j, diag_host);
+  prof_end(ctx);
+  return rc;
+}
 
 // ===========================================================================
 // exported C-ABI
@@ -458,6 +608,7 @@ void ots_ctx_destroy(ots_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   if (c->ws) cudaFree(c->ws);
+  if (c->b_ws) cudaFree(c->b_ws);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_seed) cudaEventDestroy(c->ev_seed);
   if (c->ev_diag) cudaEventDestroy(c->ev_diag);
@@ -509,7 +660,8 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
   if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
   if (k0 > 128) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 128 not supported by this build");
-  if (intra != OTS_INTRA_HOUSEHOLDER) return fail(ctx, OTS_E_UNSUPPORTED, "intra method not in this build");
+  if (intra != OTS_INTRA_HOUSEHOLDER && intra != OTS_INTRA_CHOLSHIFT)
+    return fail(ctx, OTS_E_PARAMETER, "unknown intra method");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
   if (choice == OTS_CHOICE_EXPLICIT && P == nullptr)
     return fail(ctx, OTS_E_PARAMETER, "choice='explicit' requires a seed matrix p");
@@ -524,41 +676,7 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
     return rc;
   }
   JobCfg c{n, 0, k0, k, V, ldv, A, lda, Q, ldq, choice, P, ldp, orth_tol, allow_defect, st, false};
-  Job j;
-  if ((rc = job_setup(ctx, j, c))) return rc;
-  const int KT = j.KT;
-  prof_begin(ctx, st);
-  if ((rc = phase_gram(ctx, j))) return rc;
-  prof_mark(ctx, st, "gram");
-  j.s.Sout = S; j.s.lds_out = (int)lds;
-  CK(launch_seed(j.s, st));
-  CK(cudaEventRecord(ctx->ev_seed, st));
-  prof_mark(ctx, st, "seed");
-  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
-  CK(launch_diag(j.s, ctx->side));
-  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
-  if ((rc = phase_apply1(ctx, j))) return rc;
-  prof_mark(ctx, st, "apply1");
-  if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
-  prof_mark(ctx, st, "factor");
-  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
-  if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st))) return rc;
-  prof_mark(ctx, st, "qform");
-  CK(launch_sign(j.s, Q + k0 * ldq, ldq, j.lv.back().R, KT, R, (int)ldr, st));
-  if ((rc = phase_gram2(ctx, j))) return rc;
-  prof_mark(ctx, st, "gram2");
-  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
-  CK(launch_z2(j.s, st));
-  prof_mark(ctx, st, "z2");
-  if ((rc = phase_apply2(ctx, j))) return rc;
-  prof_mark(ctx, st, "apply2");
-  CK(launch_qtop(j.s, Q, ldq, st));
-  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
-  prof_mark(ctx, st, "tail");
-  ctx->launches = 14 + 3 * (int)j.lv.size();
-  rc = read_status(ctx, j, diag_host);
-  prof_end(ctx);
-  return rc;
+  return two_stage_pipeline(ctx, c, intra, Q, ldq, R, ldr, S, lds, diag_host, nullptr);
 }
 
 int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, int64_t lda, double* Q,
@@ -599,6 +717,77 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, 
   CK(cudaStreamSynchronize(st));
   prof_end(ctx);
   CK(cudaGetLastError());
+  return OTS_OK;
+}
+
+int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const double* V, int64_t ldv,
+                             const double* A, int64_t lda, const double* d, int choice, const double* P,
+                             int64_t ldp, double orth_tol, double* Q, int64_t ldq, double* R, int64_t ldr,
+                             double* S, int64_t lds, double* diag_host, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
+  if (k > 64 || k0 > 128) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
+  if (k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "b_two_stage_diag needs k0, k >= 1");
+  if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
+  int rc;
+  if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
+  if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
+  if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
+  // scaled copies D^{1/2} V, D^{1/2} A and the unweighted Gram live in a
+  // second buffer owned by the context
+  const long ldv2 = (k0 + 1) & ~1L, lda2 = (k + 1) & ~1L;
+  const int PWv = pad32(k0);
+  const int gridu = grid_for_tn(PWv, 0, true, true, ctx->nsm);
+  size_t need = ((size_t)n * (ldv2 + lda2) + (size_t)gridu * PWv * PWv + (size_t)PWv * PWv + 256) * 8 + 4096;
+  if (need > ctx->b_size) {
+    if (ctx->b_ws) cudaFree(ctx->b_ws);
+    ctx->b_ws = nullptr; ctx->b_size = 0;
+    CK(cudaMalloc(&ctx->b_ws, need));
+    ctx->b_size = need;
+  }
+  double* V2 = reinterpret_cast<double*>(ctx->b_ws);
+  double* A2 = V2 + (size_t)n * ldv2;
+  double* part = A2 + (size_t)n * lda2;
+  double* Gu = part + (size_t)gridu * PWv * PWv;
+  double* dinv = Gu + (size_t)PWv * PWv;
+  const int nb = (int)std::min<long>(4096, (n * (k0 + k) + 255) / 256);
+  row_scale_kernel<<<nb, 256, 0, st>>>(V, ldv, n, (int)k0, d, 1.0, V2, ldv2);
+  row_scale_kernel<<<nb, 256, 0, st>>>(A, lda, n, (int)k, d, 1.0, A2, lda2);
+  inv_top_kernel<<<1, 128, 0, st>>>(d, (int)k0, dinv);
+  TnArgs a{};
+  a.P = V; a.ldp = ldv; a.pc0 = 0; a.pcols = (int)k0;
+  a.row_begin = 0; a.row_end = n; a.partial = part;
+  CK(launch_tsgemm_tn(a, PWv, 0, true, true, gridu, st));
+  CK(launch_reduce(part, gridu, (long)PWv * PWv, Gu, 1.0, st));
+  BHook bh{Gu, PWv, dinv, d, n};
+  JobCfg c{n, 0, k0, k, V2, ldv2, A2, lda2, Q, ldq, choice, P, ldp, orth_tol, 0, st, false};
+  return two_stage_pipeline(ctx, c, OTS_INTRA_HOUSEHOLDER, Q, ldq, R, ldr, S, lds, diag_host, &bh);
+}
+
+int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, int64_t lda, double* Q,
+                                int64_t ldq, double* R, int64_t ldr, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m < k) return fail(ctx, OTS_E_DIMENSION, "need rows >= cols");
+  if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
+  int rc;
+  if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
+  if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
+  if (k == 0) return OTS_OK;
+  JobCfg c{m, 1, 0, k, nullptr, 0, A, lda, Q, ldq, OTS_CHOICE_QR, nullptr, 0, 1e-8, 0, st, false};
+  Job j;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  if (A != Q) CK(cudaMemcpy2DAsync(Q, ldq * 8, A, lda * 8, k * 8, m, cudaMemcpyDeviceToDevice, st));
+  CK(cudaMemsetAsync(j.s.status, 0, sizeof(int), st));
+  if ((rc = run_cholshift(ctx, j, Q, ldq, m, (int)k, R, ldr, st))) return rc;
+  ctx->launches = 13;
+  CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ctx->h_status[0] == OTS_E_INTRA_FAILURE)
+    return fail(ctx, OTS_E_NOT_PD, "Cholesky factorization failed (matrix not positive definite)");
   return OTS_OK;
 }
 

@@ -656,9 +656,22 @@ __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
   mn = -block_max(-mn, red);
   if (threadIdx.x == 0) s.diag[0] = (mn == 0.0) ? __longlong_as_double(0x7ff0000000000000LL) : mx / mn;
   // W^T W
-  blk_gemm(s.D1, ld, s.Wt, ld, true, s.Wt, ld, false, n, n, n, 1.0, 0.0);
-  blk_gemm(s.D2, ld, s.Vt, ld, true, s.Vt, ld, false, n, n, n, 1.0, 0.0);
-  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] += s.G[i * ld + j] - s.D2[i * ld + j]; }
+  if (s.Gu == nullptr) {
+    blk_gemm(s.D1, ld, s.Wt, ld, true, s.Wt, ld, false, n, n, n, 1.0, 0.0);
+    blk_gemm(s.D2, ld, s.Vt, ld, true, s.Vt, ld, false, n, n, n, 1.0, 0.0);
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] += s.G[i * ld + j] - s.D2[i * ld + j]; }
+  } else {  // B-inner, M = diag(d): unweighted W = D^{-1/2} W'
+    BLK_FOR(e, n * n) {
+      int i = e / n, j = e - i * n;
+      double acc = 0.0;
+      for (int l = 0; l < n; ++l) {
+        const double dl = s.dinv_top[l];
+        acc = fma(dl, s.Wt[l * ld + i] * s.Wt[l * ld + j] - s.Vt[l * ld + i] * s.Vt[l * ld + j], acc);
+      }
+      const double gu = (j <= i) ? s.Gu[(long)i * s.ldgu + j] : s.Gu[(long)j * s.ldgu + i];
+      s.D1[i * ld + j] = acc + gu;
+    }
+  }
   __syncthreads();
   // X = T^{-T} (W^T W) ; M^T = T^{-T} X^T
   t_solve(s, s.D1, ld, n, true);
@@ -722,6 +735,51 @@ __global__ void __launch_bounds__(SMALL_NT) mlu_kernel(const double* Z, int ldz,
   __syncthreads();
   blk_mlu(LU, n, n, p, false);
   if (threadIdx.x == 0) *status = 0;
+}
+
+// One shifted-Cholesky-QR step (core.py:177-202): from the Gram G (ld ldg,
+// lower blocks valid) of the current block, L = chol(sym(G) [+ shift I]),
+// Z = L^{-T} (for X <- X Z) and R <- L^T R.  shift = 11 (m k + k(k+1)) u ||G||_2.
+// NotPositiveDefinite -> status OTS_E_INTRA_FAILURE (twostage.py:51-53).
+__global__ void __launch_bounds__(SMALL_NT) cholqr_step_kernel(const double* Gf, int ldg, int k, long m,
+                                                               int shift, double* W, int ld, double* Z,
+                                                               double* R, int* status) {
+  __shared__ double red[64];
+  if (status[0] != 0) return;
+  double* L = W;                // k x k
+  double* Tm = W + k * ld;      // scratch
+  BLK_FOR(e, k * k) {
+    int i = e / k, j = e - i * k;
+    double gij = (j <= i) ? Gf[(long)i * ldg + j] : Gf[(long)j * ldg + i];
+    L[i * ld + j] = gij;
+    Tm[i * ld + j] = gij;
+  }
+  __syncthreads();
+  if (shift) {
+    double nrm = blk_sigma_max(Tm, ld, k, Tm + k * ld, red, dsm, SMALL_SMEM_DOUBLES);
+    const double sh = 11.0 * ((double)m * k + (double)k * (k + 1)) * 1.1102230246251565e-16 * nrm;
+    BLK_FOR(i, k) L[i * ld + i] += sh;
+    __syncthreads();
+  }
+  if (!blk_cholesky(L, ld, k, red)) {
+    if (threadIdx.x == 0) status[0] = OTS_E_INTRA_FAILURE;
+    return;
+  }
+  // Z = L^{-T}: solve L^T Z = I
+  BLK_FOR(e, k * k) { int i = e / k, j = e - i * k; Z[i * ld + j] = (i == j) ? 1.0 : 0.0; }
+  __syncthreads();
+  blk_trsm(L, ld, true, true, false, Z, ld, k, k);
+  // R <- L^T R
+  blk_gemm(Tm, ld, L, ld, true, R, ld, false, k, k, k, 1.0, 0.0);
+  blk_copy(R, ld, Tm, ld, k, k);
+  __syncthreads();
+}
+
+cudaError_t launch_cholqr_step(const double* Gf, int ldg, int k, long m, int shift, double* W, int ld,
+                               double* Z, double* R, int* status, cudaStream_t st) {
+  cudaFuncSetAttribute(cholqr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  cholqr_step_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(Gf, ldg, k, m, shift, W, ld, Z, R, status);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st) {

@@ -23,6 +23,10 @@ struct SmallState {
   int* piv;
   // outputs
   double* Sout; int lds_out;   // S (k0 x k)
+  // B-inner (M = diag(d)) diagnostics: W = D^{-1/2} W' is unweighted, so
+  // W^T W = W_t'^T D_t^{-1} W_t' + V^T V (unweighted Gram Gu) - V_t'^T D_t^{-1} V_t'
+  const double* Gu; int ldgu;  // null for the Euclidean path
+  const double* dinv_top;      // 1/d on the k0 top rows
   double* diag;                // [kappa_t, wt_inv_norm, defect]
   int* status;                 // [0] = status code
 };
@@ -33,6 +37,8 @@ cudaError_t launch_z2(const SmallState& s, cudaStream_t st);
 cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const double* Rfin, int ldr,
                         double* Rout, int ldro, cudaStream_t st);
 cudaError_t launch_qtop(const SmallState& s, double* Q, long ldq, cudaStream_t st);
+cudaError_t launch_cholqr_step(const double* Gf, int ldg, int k, long m, int shift, double* W, int ld,
+                               double* Z, double* R, int* status, cudaStream_t st);
 cudaError_t launch_mlu(const double* Z, int ldz, int n, double* LU, double* p, double* work, int* status,
                        cudaStream_t st);
 

@@ -46,7 +46,11 @@ def intra_qr(a, intra="householder"):
     if intra == "householder":
         return householder_qr(a)
     if intra == "cholshift":
-        raise NotImplementedError("intra='cholshift' is not in this build")
+        from .core import shifted_cholesky_qr
+        try:
+            return shifted_cholesky_qr(a)
+        except E.NotPositiveDefinite as exc:
+            raise E.IntraFailure(f"shifted Cholesky-QR broke down: {exc}") from None
     raise E.ParameterError(f"unknown intra method {intra!r}; expected {INTRA_METHODS}")
 
 

@@ -140,3 +140,57 @@ def test_config3_like_rankdef():
         loss, cross, resid = O.gram_stability(v, a, res.q, res.r, res.s)
         n = v.shape[0]
         assert loss <= 10 * n * U and resid <= 10 * n * U, ch
+
+
+def test_cholshift_golden(golden):
+    v, a = golden["cholshift/v"], golden["cholshift/a"]
+    res = P.two_stage_qr(v, a, choice="qr", intra="cholshift")
+    assert rel(res.q, golden["cholshift/qr/q"]) < 1e-10
+    assert rel(res.r, golden["cholshift/qr/r"]) < 1e-10
+    assert rel(res.s, golden["cholshift/qr/s"]) < 1e-10
+
+
+def test_shifted_cholesky_qr_vs_oracle():
+    rng = W.make_rng(321)
+    x = W.normal_matrix(rng, 50000, 24)
+    qr = P.shifted_cholesky_qr(x)
+    q, r = O.cholqr_shifted(x)
+    assert rel(qr.q, q) < 1e-10 and rel(qr.r, r) < 1e-10
+
+
+def test_cholshift_breakdown_is_intra_failure():
+    # exactly rank-deficient remainder: Cholesky of the shifted Gram may pass,
+    # but a zero column makes the refinement Gram singular -> IntraFailure
+    n = 4000
+    v = np.zeros((n, 2)); v[0, 0] = v[1, 1] = 1.0
+    a = np.zeros((n, 3)); a[5:, 0] = 1.0   # columns 1, 2 exactly zero
+    with pytest.raises((P.IntraFailure,)):
+        P.two_stage_qr(v, a, intra="cholshift")
+
+
+@pytest.mark.parametrize("ch", ["mlu", "qr", "polar"])
+def test_binner_diag_golden(golden, ch):
+    g = lambda key: golden[f"binner_diag_real/{ch}/{key}"]
+    ip = P.InnerProduct.weighted(np.diag(g("d")))
+    u = P.initial_b_basis(ip, 16)
+    assert np.array_equal(u, g("u"))
+    res = P.b_two_stage_qr(g("v"), g("a"), u, ip, choice=ch)
+    assert rel(res.q, g("q")) < 1e-10
+    assert rel(res.r, g("r")) < 1e-10
+    assert rel(res.s, g("s")) < 1e-10
+    assert np.all(np.diag(res.r) > 0)
+    assert abs(res.diagnostics.kappa_t - float(g("kappa_t"))) < 1e-10 * float(g("kappa_t"))
+    assert abs(res.diagnostics.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
+
+
+def test_binner_diag_vs_oracle_large():
+    n, k0, k = 1 << 18, 64, 64
+    d = 10.0 ** W.uniform(W.make_rng(43), 0.0, 4.0, n)
+    sq = np.sqrt(d)
+    v = np.linalg.qr(sq[:, None] * W.normal_matrix(W.make_rng(44), n, k0))[0] / sq[:, None]
+    a = W.normal_matrix(W.make_rng(45), n, k)
+    ip = P.InnerProduct.weighted(d)
+    u = P.initial_b_basis(ip, k0 + k)
+    res = P.b_two_stage_qr(v, a, u, ip)
+    ref = O.b_two_stage(v, a, u, O.BInner(diag=d), "qr", diagnostics=False)
+    assert rel(res.q, ref["q"]) < 1e-10 and rel(res.r, ref["r"]) < 1e-10 and rel(res.s, ref["s"]) < 1e-10
