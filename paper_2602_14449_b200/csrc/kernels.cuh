@@ -49,6 +49,8 @@ struct QformArgs {
 
 cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid, cudaStream_t st);
 cudaError_t launch_reduce(const double* partial, int nparts, long count, double* out, double alpha, cudaStream_t st);
+cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, int cols, int ldp, double* out,
+                                  long ldo, double alpha, cudaStream_t st);
 cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
 cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);

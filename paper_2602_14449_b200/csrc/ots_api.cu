@@ -296,8 +296,13 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   const int ld = j.ld, KT = j.KT;
   const int gmax = std::max(j.grid_tn, j.grid_tn2);
   const int PWk = pad32(std::max<long>(k, 1));
-  const size_t part_n = std::max((size_t)gmax * j.PW * j.NTOT1,
-                                 (size_t)grid_for_tn(PWk, 0, true, true, ctx->nsm) * PWk * PWk);
+  size_t part_n = std::max((size_t)gmax * j.PW * j.NTOT1,
+                           (size_t)grid_for_tn(PWk, 0, true, true, ctx->nsm) * PWk * PWk);
+  if (k0 > 128) {
+    part_n = std::max(part_n, (size_t)grid_for_tn(128, 0, true, true, ctx->nsm) * 128 * 128);
+    part_n = std::max(part_n, (size_t)grid_for_tn(128, 128, false, false, ctx->nsm) * 128 * 128);
+    part_n = std::max(part_n, (size_t)grid_for_tn(128, j.BWa, false, false, ctx->nsm) * 128 * j.BWa);
+  }
   const size_t gf_n = std::max((size_t)j.PW * j.NTOT1, (size_t)PWk * PWk);
   size_t bytes = 0;
   bytes += part_n * 8 + 256;
@@ -342,16 +347,57 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   return OTS_OK;
 }
 
+// K1: Gfull = [V^T V | V_b^T A_b] (PW x NTOT1).  k0 <= 128: one launch.  Larger
+// k0: 128-column blocks of V -- diagonal blocks (alias, symmetric), lower
+// off-diagonal blocks V_a^T V_b, and V_a^T A_b -- each reduced in place.
 int phase_gram(ots_ctx* ctx, Job& j) {
   const JobCfg& c = j.c;
-  TnArgs a{};
-  a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = (int)c.k0;
-  a.B = c.A; a.ldb = c.lda; a.bc0 = 0; a.bcols = (int)c.k;
-  a.row_begin = 0; a.row_end = c.n_local;
-  a.b_row_begin = j.qrow0; a.p_row_begin = 0;
-  a.partial = j.partial;
-  CK(launch_tsgemm_tn(a, j.PW, j.BWa, true, true, j.grid_tn, c.st));
-  CK(launch_reduce(j.partial, j.grid_tn, (long)j.PW * j.NTOT1, j.Gfull, 1.0, c.st));
+  const int k0 = (int)c.k0, k = (int)c.k;
+  if (k0 <= 128) {
+    TnArgs a{};
+    a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = k0;
+    a.B = c.A; a.ldb = c.lda; a.bc0 = 0; a.bcols = k;
+    a.row_begin = 0; a.row_end = c.n_local;
+    a.b_row_begin = j.qrow0; a.p_row_begin = 0;
+    a.partial = j.partial;
+    CK(launch_tsgemm_tn(a, j.PW, j.BWa, true, true, j.grid_tn, c.st));
+    CK(launch_reduce(j.partial, j.grid_tn, (long)j.PW * j.NTOT1, j.Gfull, 1.0, c.st));
+    return OTS_OK;
+  }
+  const int nbk = (k0 + 127) / 128;
+  for (int ab = 0; ab < nbk; ++ab) {
+    const int a0 = 128 * ab, aw = std::min(128, k0 - a0), PWa = pad32(aw);
+    for (int bb = 0; bb <= ab; ++bb) {
+      const int b0 = 128 * bb, bw = std::min(128, k0 - b0), PWb = pad32(bw);
+      TnArgs a{};
+      a.P = c.V; a.ldp = c.ldv; a.pc0 = a0; a.pcols = aw;
+      a.row_begin = 0; a.row_end = c.n_local; a.b_row_begin = 0; a.p_row_begin = 0;
+      a.partial = j.partial;
+      int grid, ldp;
+      if (ab == bb) {
+        a.B = nullptr; a.ldb = 0; a.bc0 = 0; a.bcols = 0;
+        grid = grid_for_tn(PWa, 0, true, true, ctx->nsm);
+        ldp = PWa;
+        CK(launch_tsgemm_tn(a, PWa, 0, true, true, grid, c.st));
+      } else {
+        a.B = c.V; a.ldb = c.ldv; a.bc0 = b0; a.bcols = bw;
+        grid = grid_for_tn(PWa, PWb, false, false, ctx->nsm);
+        ldp = PWb;
+        CK(launch_tsgemm_tn(a, PWa, PWb, false, false, grid, c.st));
+      }
+      CK(launch_reduce_strided(j.partial, grid, aw, bw, ldp, j.Gfull + (long)a0 * j.NTOT1 + b0, j.NTOT1, 1.0,
+                               c.st));
+    }
+    TnArgs a{};
+    a.P = c.V; a.ldp = c.ldv; a.pc0 = a0; a.pcols = aw;
+    a.B = c.A; a.ldb = c.lda; a.bc0 = 0; a.bcols = k;
+    a.row_begin = 0; a.row_end = c.n_local; a.b_row_begin = j.qrow0; a.p_row_begin = 0;
+    a.partial = j.partial;
+    const int grid = grid_for_tn(PWa, j.BWa, false, false, ctx->nsm);
+    CK(launch_tsgemm_tn(a, PWa, j.BWa, false, false, grid, c.st));
+    CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Gfull + (long)a0 * j.NTOT1 + j.PW, j.NTOT1, 1.0,
+                             c.st));
+  }
   return OTS_OK;
 }
 
@@ -371,14 +417,20 @@ int phase_apply1(ots_ctx* ctx, Job& j) {
 
 int phase_gram2(ots_ctx* ctx, Job& j) {
   const JobCfg& c = j.c;
-  TnArgs a{};
-  a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = (int)c.k0;
-  a.B = c.Q; a.ldb = c.ldq; a.bc0 = 0; a.bcols = (int)c.k;
-  a.row_begin = j.qrow0; a.row_end = c.n_local;
-  a.b_row_begin = j.qrow0; a.p_row_begin = j.qrow0;
-  a.partial = j.partial;
-  CK(launch_tsgemm_tn(a, j.PW, j.BWa, false, false, j.grid_tn2, c.st));
-  CK(launch_reduce(j.partial, j.grid_tn2, (long)j.PW * j.BWa, j.Y2full, -1.0, c.st));
+  const int k0 = (int)c.k0, k = (int)c.k;
+  const int nbk = (k0 + 127) / 128;
+  for (int ab = 0; ab < nbk; ++ab) {
+    const int a0 = 128 * ab, aw = std::min(128, k0 - a0), PWa = pad32(aw);
+    TnArgs a{};
+    a.P = c.V; a.ldp = c.ldv; a.pc0 = a0; a.pcols = aw;
+    a.B = c.Q; a.ldb = c.ldq; a.bc0 = 0; a.bcols = k;
+    a.row_begin = j.qrow0; a.row_end = c.n_local;
+    a.b_row_begin = j.qrow0; a.p_row_begin = j.qrow0;
+    a.partial = j.partial;
+    const int grid = (nbk == 1) ? j.grid_tn2 : grid_for_tn(PWa, j.BWa, false, false, ctx->nsm);
+    CK(launch_tsgemm_tn(a, PWa, j.BWa, false, false, grid, c.st));
+    CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Y2full + (long)a0 * j.BWa, j.BWa, -1.0, c.st));
+  }
   return OTS_OK;
 }
 
@@ -659,7 +711,7 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
   if (n < 0 || k0 < 0 || k < 0) return fail(ctx, OTS_E_DIMENSION, "negative dimension");
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
   if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
-  if (k0 > 128) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 128 not supported by this build");
+  if (k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 512 not supported by this build");
   if (intra != OTS_INTRA_HOUSEHOLDER && intra != OTS_INTRA_CHOLSHIFT)
     return fail(ctx, OTS_E_PARAMETER, "unknown intra method");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
@@ -728,7 +780,7 @@ int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, con
   cudaSetDevice(ctx->device);
   cudaStream_t st = (cudaStream_t)stream;
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
-  if (k > 64 || k0 > 128) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
+  if (k > 64 || k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
   if (k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "b_two_stage_diag needs k0, k >= 1");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
   int rc;
@@ -814,7 +866,7 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
                    int64_t ldv, const double* A, int64_t lda, double* Q, int64_t ldq, int choice,
                    const double* P, int64_t ldp, double orth_tol, void* stream) {
   cudaSetDevice(ctx->device);
-  if (k > 64 || k0 > 128 || k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "shape not in this build");
+  if (k > 64 || k0 > 512 || k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "shape not in this build");
   if (row0 == 0 && n_local < k0 + k) return fail(ctx, OTS_E_DIMENSION, "rank 0 must own >= k0+k rows");
   int rc;
   if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;

@@ -312,8 +312,32 @@ cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool s
   OTS_TN(32, 32, false, false) OTS_TN(64, 32, false, false) OTS_TN(96, 32, false, false)
   OTS_TN(128, 32, false, false) OTS_TN(32, 64, false, false) OTS_TN(64, 64, false, false)
   OTS_TN(96, 64, false, false) OTS_TN(128, 64, false, false)
+  OTS_TN(128, 128, false, false) OTS_TN(128, 96, false, false) OTS_TN(96, 96, false, false)
+  OTS_TN(64, 128, false, false) OTS_TN(96, 128, false, false) OTS_TN(32, 128, false, false)
 #undef OTS_TN
   return cudaErrorInvalidValue;
+}
+
+// out[(m0+i)*ldo + n0 + j] = alpha * sum_c partial[c][i][j]   (i < rows, j < cols of a rows x ldp block)
+__global__ void reduce_partials_strided_kernel(const double* __restrict__ partial, int nparts, int rows,
+                                               int cols, int ldp, int prow, double* __restrict__ out,
+                                               long ldo, double alpha) {
+  long e = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (long)rows * cols) return;
+  const int i = (int)(e / cols), j = (int)(e - (long)i * cols);
+  const long stride = (long)prow * ldp;   // per-CTA partial = padded rows x ldp
+  double s = 0.0;
+  for (int c = 0; c < nparts; ++c) s += partial[c * stride + (long)i * ldp + j];
+  out[(long)i * ldo + j] = alpha * s;
+}
+
+cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, int cols, int ldp, double* out,
+                                  long ldo, double alpha, cudaStream_t st) {
+  long count = (long)rows * cols;
+  const int prow = (rows + 31) / 32 * 32;
+  reduce_partials_strided_kernel<<<(unsigned)((count + 255) / 256), 256, 0, st>>>(partial, nparts, rows, cols,
+                                                                                  ldp, prow, out, ldo, alpha);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_reduce(const double* partial, int nparts, long count, double* out, double alpha,

@@ -194,3 +194,48 @@ def test_binner_diag_vs_oracle_large():
     res = P.b_two_stage_qr(v, a, u, ip)
     ref = O.b_two_stage(v, a, u, O.BInner(diag=d), "qr", diagnostics=False)
     assert rel(res.q, ref["q"]) < 1e-10 and rel(res.r, ref["r"]) < 1e-10 and rel(res.s, ref["s"]) < 1e-10
+
+
+@pytest.mark.parametrize("k0,k,choice", [(200, 48, "qr"), (384, 64, "qr"), (256, 64, "mlu"),
+                                         (160, 32, "polar")])
+def test_large_k0_vs_oracle(k0, k, choice):
+    n = 1 << 15
+    rng = W.make_rng(900 + k0)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    a = W.normal_matrix(rng, n, k)
+    ref = O.two_stage(v, a, choice, diagnostics=True)
+    res = P.two_stage_qr(v, a, choice=choice)
+    assert rel(res.q, ref["q"]) < 1e-10
+    assert rel(res.r, ref["r"]) < 1e-10
+    assert rel(res.s, ref["s"]) < 1e-10
+    assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
+    assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
+
+
+def test_block_krylov_sweep_small():
+    """configs[4] shape at small n: k0 = 0, 64, ..., 512 with A <- L Q_prev."""
+    import torch
+    n, k, steps = 1 << 14, 64, 8
+    a0 = W.normal_matrix(W.make_rng(5), n, k)
+
+    def lap(q):
+        out = 2.0 * q
+        out[1:] -= q[:-1]
+        out[:-1] -= q[1:]
+        return out
+
+    blocks_gpu = [a0]
+    qs = [P.two_stage_qr(np.zeros((n, 0)), a0).q]
+    ref_qs = [O.two_stage(np.zeros((n, 0)), a0)["q"]]
+    for i in range(steps):
+        vq = np.hstack(qs)
+        ai = lap(qs[-1])
+        res = P.two_stage_qr(vq, ai)
+        qs.append(res.q)
+        vr = np.hstack(ref_qs)
+        rr = O.two_stage(vr, lap(ref_qs[-1]), diagnostics=False)
+        ref_qs.append(rr["q"])
+    Qg = np.hstack(qs)
+    loss = np.abs(np.linalg.eigvalsh(Qg.T @ Qg) - 1).max()
+    assert loss <= 10 * n * U
+    assert rel(Qg, np.hstack(ref_qs)) < 1e-8
