@@ -108,6 +108,27 @@ int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,
 int ots_modified_lu_f64(ots_ctx* ctx, int64_t n, const double* Z, int64_t ldz,
                         double* LU, double* p, void* stream);
 
+/* Generalized Householder reflector H = I - W T^{-1} W^*, W = [P;0] - V
+ * (GenHouseholder, reflector.py:156-165).  The object keeps a pointer to V
+ * (caller keeps V alive) and the k0 x k0 seed state on the device. */
+typedef struct ots_refl ots_refl;
+/* build_reflector(v, choice, p, orth_tol, allow_defect) -- reflector.py:207-228 */
+int ots_build_reflector_f64(ots_ctx* ctx, int64_t n, int64_t k0, const double* V, int64_t ldv,
+                            int choice, const double* P, int64_t ldp, double orth_tol,
+                            int allow_defect, ots_refl** out, double* defect_host, void* stream);
+void ots_reflector_destroy(ots_refl* r);
+/* apply_reflector(h, x, adjoint)                   -- reflector.py:231-238 (m <= 64) */
+int ots_apply_reflector_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, const double* X, int64_t ldx,
+                            double* Y, int64_t ldy, int adjoint, void* stream);
+/* reflector_diagnostics(h) -> [kappa_t, wt_inv_norm] -- reflector.py:241-247 */
+int ots_reflector_diagnostics_f64(ots_ctx* ctx, const ots_refl* r, double* diag_host, void* stream);
+/* t_solver.solve(b, adjoint) on a device k0 x m block  -- reflector.py:80-153 */
+int ots_reflector_tsolve_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, double* B, int64_t ldb,
+                             int adjoint, void* stream);
+/* which = 0: seed P; which = 1: dense T (t_solver.reconstruct()) */
+int ots_reflector_get_f64(ots_ctx* ctx, const ots_refl* r, int which, double* out, int64_t ldo,
+                          void* stream);
+
 /* Per-phase device timings of the last call (CUDA events on the launching
  * stream), enabled with ots_set_profiling(ctx, 1).  names: '\n'-separated. */
 int ots_set_profiling(ots_ctx* ctx, int enable);

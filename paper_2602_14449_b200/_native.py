@@ -55,6 +55,14 @@ def lib():
                 L.ots_b_two_stage_diag_f64.argtypes = [
                     _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _int, _vp, _i64, _dbl,
                     _vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
+                L.ots_build_reflector_f64.argtypes = [
+                    _vp, _i64, _i64, _vp, _i64, _int, _vp, _i64, _dbl, _int, C.POINTER(_vp),
+                    C.POINTER(_dbl), _vp]
+                L.ots_reflector_destroy.argtypes = [_vp]
+                L.ots_apply_reflector_f64.argtypes = [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp]
+                L.ots_reflector_diagnostics_f64.argtypes = [_vp, _vp, C.POINTER(_dbl), _vp]
+                L.ots_reflector_tsolve_f64.argtypes = [_vp, _vp, _i64, _vp, _i64, _int, _vp]
+                L.ots_reflector_get_f64.argtypes = [_vp, _vp, _int, _vp, _i64, _vp]
                 L.ots_householder_qr_f64.argtypes = [
                     _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp]
                 L.ots_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), _int]
@@ -80,6 +88,8 @@ EXPORTED_SYMBOLS = [
     "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_version",
     "ots_two_stage_f64", "ots_householder_qr_f64", "ots_modified_lu_f64",
     "ots_shifted_cholesky_qr_f64", "ots_b_two_stage_diag_f64",
+    "ots_build_reflector_f64", "ots_reflector_destroy", "ots_apply_reflector_f64",
+    "ots_reflector_diagnostics_f64", "ots_reflector_tsolve_f64", "ots_reflector_get_f64",
     "ots_set_profiling", "ots_last_profile", "ots_last_launch_count", "ots_fp64_peak",
     "ots_debug_counters",
     "ots_dist_begin", "ots_dist_sizes", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",

@@ -415,7 +415,11 @@ int phase_apply1(ots_ctx* ctx, Job& j) {
   return OTS_OK;
 }
 
-int phase_gram2(ots_ctx* ctx, Job& j) {
+int phase_vtb(ots_ctx* ctx, Job& j, const double* Bm, long ldb, double alpha);
+int phase_gram2(ots_ctx* ctx, Job& j) { return phase_vtb(ctx, j, j.c.Q, j.c.ldq, -1.0); }
+
+// Y2full (k0 x k, ld BWa) = alpha * V_b^T B_b over this rank's QR rows
+int phase_vtb(ots_ctx* ctx, Job& j, const double* Bm, long ldb, double alpha) {
   const JobCfg& c = j.c;
   const int k0 = (int)c.k0, k = (int)c.k;
   const int nbk = (k0 + 127) / 128;
@@ -423,13 +427,13 @@ int phase_gram2(ots_ctx* ctx, Job& j) {
     const int a0 = 128 * ab, aw = std::min(128, k0 - a0), PWa = pad32(aw);
     TnArgs a{};
     a.P = c.V; a.ldp = c.ldv; a.pc0 = a0; a.pcols = aw;
-    a.B = c.Q; a.ldb = c.ldq; a.bc0 = 0; a.bcols = k;
+    a.B = Bm; a.ldb = ldb; a.bc0 = 0; a.bcols = k;
     a.row_begin = j.qrow0; a.row_end = c.n_local;
     a.b_row_begin = j.qrow0; a.p_row_begin = j.qrow0;
     a.partial = j.partial;
     const int grid = (nbk == 1) ? j.grid_tn2 : grid_for_tn(PWa, j.BWa, false, false, ctx->nsm);
     CK(launch_tsgemm_tn(a, PWa, j.BWa, false, false, grid, c.st));
-    CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Y2full + (long)a0 * j.BWa, j.BWa, -1.0, c.st));
+    CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Y2full + (long)a0 * j.BWa, j.BWa, alpha, c.st));
   }
   return OTS_OK;
 }
@@ -729,6 +733,151 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
   }
   JobCfg c{n, 0, k0, k, V, ldv, A, lda, Q, ldq, choice, P, ldp, orth_tol, allow_defect, st, false};
   return two_stage_pipeline(ctx, c, intra, Q, ldq, R, ldr, S, lds, diag_host, nullptr);
+}
+
+}  // extern "C"
+
+// ----------------------------- reflector objects ---------------------------
+struct ots_refl {
+  int device = 0;
+  long n = 0, k0 = 0, ldv = 0;
+  const double* V = nullptr;
+  int choice = 1, ld = 32;
+  double* buf = nullptr;       // persistent small state
+  SmallState s{};
+  double defect = 0.0;
+};
+
+namespace {
+// copy the reflector-defining small matrices of a job into the object
+void refl_capture(ots_refl* r, const Job& j, cudaStream_t st) {
+  const size_t m2 = (size_t)j.ld * j.ld;
+  double** dst[] = {&r->s.G, &r->s.Vt, &r->s.P, &r->s.Tf, &r->s.Tdense, &r->s.Wt};
+  const double* src[] = {j.s.G, j.s.Vt, j.s.P, j.s.Tf, j.s.Tdense, j.s.Wt};
+  for (int i = 0; i < 6; ++i) {
+    *dst[i] = r->buf + i * m2;
+    cudaMemcpyAsync(*dst[i], src[i], m2 * 8, cudaMemcpyDeviceToDevice, st);
+  }
+  r->s.pvec = r->buf + 6 * m2;
+  cudaMemcpyAsync(r->s.pvec, j.s.pvec, j.ld * 8, cudaMemcpyDeviceToDevice, st);
+  r->s.piv = reinterpret_cast<int*>(r->buf + 6 * m2 + j.ld);
+  cudaMemcpyAsync(r->s.piv, j.s.piv, j.ld * sizeof(int), cudaMemcpyDeviceToDevice, st);
+}
+// point a job's small state at the reflector's matrices
+void refl_attach(const ots_refl* r, Job& j) {
+  j.s.G = r->s.G; j.s.Vt = r->s.Vt; j.s.P = r->s.P; j.s.Tf = r->s.Tf; j.s.Tdense = r->s.Tdense;
+  j.s.Wt = r->s.Wt; j.s.pvec = r->s.pvec; j.s.piv = r->s.piv; j.s.choice = r->choice;
+}
+}  // namespace
+
+extern "C" {
+
+/* build_reflector(v, choice, p, orth_tol, allow_defect)  -- reflector.py:207-228 */
+int ots_build_reflector_f64(ots_ctx* ctx, int64_t n, int64_t k0, const double* V, int64_t ldv, int choice,
+                            const double* P, int64_t ldp, double orth_tol, int allow_defect, ots_refl** out,
+                            double* defect_host, void* stream) {
+  if (!ctx || !out) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k0 > n) return fail(ctx, OTS_E_DIMENSION, "v must be tall");
+  if (k0 == 0) return fail(ctx, OTS_E_DIMENSION, "v must have at least one column");
+  if (k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 512 not supported by this build");
+  if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
+  int rc;
+  if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
+  // a one-column job on A = V gives the Gram, the defect check and the seed
+  JobCfg c{n, 0, k0, 1, V, ldv, V, ldv, nullptr, 0, choice, P, ldp, orth_tol, allow_defect, st, false};
+  Job j;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  if ((rc = phase_gram(ctx, j))) return rc;
+  j.s.Sout = j.s.Sd; j.s.lds_out = j.ld;
+  CK(launch_seed(j.s, st));
+  ots_refl* r = new ots_refl();
+  r->device = ctx->device; r->n = n; r->k0 = k0; r->ldv = ldv; r->V = V; r->choice = choice; r->ld = j.ld;
+  r->s = j.s;
+  CK(cudaMalloc(&r->buf, ((size_t)6 * j.ld * j.ld + 2 * j.ld + 64) * 8));
+  refl_capture(r, j, st);
+  double diag[3];
+  rc = read_status(ctx, j, diag);
+  r->defect = diag[2];
+  if (defect_host) *defect_host = diag[2];
+  if (rc) { cudaFree(r->buf); delete r; return rc; }
+  *out = r;
+  return OTS_OK;
+}
+
+void ots_reflector_destroy(ots_refl* r) {
+  if (!r) return;
+  cudaSetDevice(r->device);
+  cudaFree(r->buf);
+  delete r;
+}
+
+/* apply_reflector(h, x, adjoint)                   -- reflector.py:231-238
+ * Y (n x m) = X - W T^{-(*)} (W^T X); Y may alias X. m <= 64 per call. */
+int ots_apply_reflector_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, const double* X, int64_t ldx,
+                            double* Y, int64_t ldy, int adjoint, void* stream) {
+  if (!ctx || !r) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (m == 0) return OTS_OK;
+  if (m > 64) return fail(ctx, OTS_E_UNSUPPORTED, "apply_reflector: at most 64 columns per call");
+  int rc;
+  if ((rc = validate_layout(ctx, X, ldx, "X"))) return rc;
+  if ((rc = validate_layout(ctx, Y, ldy, "Y"))) return rc;
+  JobCfg c{r->n, 0, r->k0, m, r->V, r->ldv, X, ldx, Y, ldy, r->choice, nullptr, 0, 1.0, 1, st, false};
+  Job j;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  refl_attach(r, j);
+  CK(cudaMemsetAsync(j.s.status, 0, sizeof(int), st));
+  if ((rc = phase_vtb(ctx, j, X, ldx, 1.0))) return rc;        // V_b^T X_b
+  j.s.Gfull = j.Y2full; j.s.ldgf = j.BWa;
+  j.s.Sout = j.s.D2; j.s.lds_out = j.ld;                       // out_t staged (Y may alias X)
+  CK(launch_refl_apply(j.s, adjoint, st));
+  if ((rc = phase_apply1(ctx, j))) return rc;                  // Y_b = X_b + V_b Z
+  CK(cudaMemcpy2DAsync(Y, ldy * 8, j.s.D2, j.ld * 8, m * 8, r->k0, cudaMemcpyDeviceToDevice, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->launches = 5;
+  return OTS_OK;
+}
+
+/* reflector_diagnostics(h) -> [kappa_t, wt_inv_norm]  -- reflector.py:241-247 */
+int ots_reflector_diagnostics_f64(ots_ctx* ctx, const ots_refl* r, double* diag_host, void* stream) {
+  if (!ctx || !r) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  cudaStream_t st = (cudaStream_t)stream;
+  JobCfg c{r->n, 0, r->k0, 1, r->V, r->ldv, r->V, r->ldv, nullptr, 0, r->choice, nullptr, 0, 1.0, 1, st, false};
+  Job j;
+  int rc;
+  if ((rc = job_setup(ctx, j, c))) return rc;
+  refl_attach(r, j);
+  CK(cudaMemsetAsync(j.s.status, 0, sizeof(int), st));
+  CK(launch_diag(j.s, st));
+  double d3[3];
+  rc = read_status(ctx, j, d3);
+  if (diag_host) { diag_host[0] = d3[0]; diag_host[1] = d3[1]; }
+  return rc;
+}
+
+/* t_solver.solve(b, adjoint) (reflector.py:80-153): B (k0 x m, device) in place.
+ * t_solver.reconstruct() / seed p: ots_reflector_get (which 0 = P, 1 = T). */
+int ots_reflector_tsolve_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, double* B, int64_t ldb, int adjoint,
+                             void* stream) {
+  if (!ctx || !r) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  SmallState s = r->s;
+  CK(launch_tsolve(s, B, (int)ldb, (int)m, adjoint, (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return OTS_OK;
+}
+
+int ots_reflector_get_f64(ots_ctx* ctx, const ots_refl* r, int which, double* out, int64_t ldo, void* stream) {
+  if (!ctx || !r) return OTS_E_VALUE;
+  const double* src = which == 0 ? r->s.P : r->s.Tdense;
+  CK(cudaMemcpy2DAsync(out, ldo * 8, src, r->ld * 8, r->k0 * 8, r->k0, cudaMemcpyDeviceToDevice,
+                       (cudaStream_t)stream));
+  CK(cudaStreamSynchronize((cudaStream_t)stream));
+  return OTS_OK;
 }
 
 int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, int64_t lda, double* Q,

@@ -687,6 +687,26 @@ __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
   if (threadIdx.x == 0) s.diag[1] = sqrt(lm);
 }
 
+// apply_reflector (reflector.py:231-238) small part: Y = W_t^T X_t - V_b^T X_b
+// (VbX from the reduced Gram block at Gfull/ldgf), Z = T^{-(*)} Y into Z1,
+// top rows out_t = X_t - W_t Z into Sout (ld lds_out).  X_t = s.A (lda).
+__global__ void __launch_bounds__(SMALL_NT) refl_apply_kernel(SmallState s, int adjoint) {
+  const int n = s.k0, k = s.k, ld = s.ld;
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.At[i * ld + j] = s.A[(long)i * s.lda + j]; }
+  __syncthreads();
+  blk_gemm(s.Z1, ld, s.Wt, ld, true, s.At, ld, false, n, k, n, 1.0, 0.0);
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.Z1[i * ld + j] -= s.Gfull[(long)i * s.ldgf + j]; }
+  __syncthreads();
+  t_solve(s, s.Z1, ld, k, adjoint != 0);
+  blk_gemm(s.X1, ld, s.Wt, ld, false, s.Z1, ld, false, n, k, n, 1.0, 0.0);
+  BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.Sout[(long)i * s.lds_out + j] = s.At[i * ld + j] - s.X1[i * ld + j]; }
+}
+
+// T-solver entry (reflector.py:80-153): B (k0 x m, ld ldb) <- T^{-(*)} B
+__global__ void __launch_bounds__(SMALL_NT) tsolve_kernel(SmallState s, double* B, int ldb, int m, int adjoint) {
+  t_solve(s, B, ldb, m, adjoint != 0);
+}
+
 // Z2 = T^{-1} Y2
 __global__ void __launch_bounds__(SMALL_NT) z2_kernel(SmallState s) {
   if (s.status[0] != 0) return;
@@ -792,6 +812,17 @@ cudaError_t launch_diag(const SmallState& s, cudaStream_t st) {
   diag_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
+cudaError_t launch_refl_apply(const SmallState& s, int adjoint, cudaStream_t st) {
+  cudaFuncSetAttribute(refl_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  refl_apply_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s, adjoint);
+  return cudaGetLastError();
+}
+cudaError_t launch_tsolve(const SmallState& s, double* B, int ldb, int m, int adjoint, cudaStream_t st) {
+  cudaFuncSetAttribute(tsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  tsolve_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s, B, ldb, m, adjoint);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_z2(const SmallState& s, cudaStream_t st) {
   cudaFuncSetAttribute(z2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
   z2_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);

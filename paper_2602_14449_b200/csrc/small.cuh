@@ -34,6 +34,8 @@ struct SmallState {
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st);
 cudaError_t launch_diag(const SmallState& s, cudaStream_t st);
 cudaError_t launch_z2(const SmallState& s, cudaStream_t st);
+cudaError_t launch_refl_apply(const SmallState& s, int adjoint, cudaStream_t st);
+cudaError_t launch_tsolve(const SmallState& s, double* B, int ldb, int m, int adjoint, cudaStream_t st);
 cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const double* Rfin, int ldr,
                         double* Rout, int ldro, cudaStream_t st);
 cudaError_t launch_qtop(const SmallState& s, double* Q, long ldq, cudaStream_t st);

@@ -35,15 +35,141 @@ class ReflectorDiagnostics:
     wt_inv_norm: float
 
 
-@dataclass
+class _DeviceTSolver:
+    """T-solver of a device reflector (reflector.py:80-153): solve(b, adjoint)
+    and reconstruct() run on the GPU."""
+
+    kinds = {"mlu": "mlu", "qr": "tri", "polar": "chol", "explicit": "lu"}
+
+    def __init__(self, handle, choice, k0, dev, like_torch):
+        self._h, self.kind, self.k0, self._dev, self._torch = handle, self.kinds[choice], k0, dev, like_torch
+
+    def solve(self, b, adjoint=False):
+        was_torch = D.is_torch(b)
+        bb = as_matrix(b if (was_torch or np.ndim(b) == 2) else np.asarray(b)[:, None], "b")
+        vec = (not was_torch) and np.ndim(b) == 1
+        B = D.to_device(bb, self._dev)
+        out = D.empty(B.rows, B.cols, self._dev)
+        out.buf[:, :B.cols].copy_(B.view())
+        ctx = D.ctx(self._dev)
+        check(lib().ots_reflector_tsolve_f64(ctx, self._h.ptr, B.cols, out.ptr, out.ld, int(bool(adjoint)),
+                                             D.stream_ptr(self._dev)), ctx)
+        res = out.view() if was_torch else out.numpy()
+        return res[:, 0] if vec else res
+
+    def reconstruct(self):
+        return self._h.get(1, self._torch)
+
+
+class _Handle:
+    def __init__(self, ptr, dev):
+        import weakref
+        self.ptr = ptr
+        self.dev = dev
+        self._fin = weakref.finalize(self, lib().ots_reflector_destroy, ptr)
+
+    def get(self, which, as_torch):
+        import ctypes as C
+        t = D.torch()
+        ctx = D.ctx(self.dev)
+        k0 = self.k0
+        out = D.empty(k0, k0, self.dev)
+        check(lib().ots_reflector_get_f64(ctx, self.ptr, which, out.ptr, out.ld, D.stream_ptr(self.dev)), ctx)
+        return out.view().clone() if as_torch else out.numpy()
+
+
 class GenHouseholder:
-    """reflector.py:156-165 (record shape kept for drop-in callers)."""
-    w: object
-    t_solver: object
-    p: object
-    choice: str
-    n: int
-    k0: int
+    """reflector.py:156-165.  Device-backed: `w` is materialised lazily
+    (W = -V with the top k0 rows replaced by fl(P - V_t)), `p` and
+    `t_solver` read the seed state from the device."""
+
+    def __init__(self, handle, V, choice, n, k0, like_torch):
+        self._h, self._V, self.choice, self.n, self.k0 = handle, V, choice, n, k0
+        self._torch = like_torch
+        handle.k0 = k0
+        self.t_solver = _DeviceTSolver(handle, choice, k0, handle.dev, like_torch)
+        self._w = None
+
+    @property
+    def p(self):
+        return self._h.get(0, self._torch)
+
+    @property
+    def w(self):
+        if self._w is None:
+            t = D.torch()
+            V = self._V.view()
+            w = -V.clone()
+            p = t.as_tensor(self.p, device=V.device) if not self._torch else self.p
+            w[:self.k0] = p - V[:self.k0]
+            self._w = w if self._torch else w.cpu().numpy()
+        return self._w
+
+
+def build_reflector(v, choice="qr", p=None, orth_tol=1e-8, allow_defect=False):
+    """reflector.py:207-228 on the GPU (defect check, seed, W_top)."""
+    import ctypes as C
+    was_torch = D.is_torch(v)
+    v = as_matrix(v, "v")
+    n, k0 = v.shape
+    if k0 > n:
+        raise E.DimensionError(f"v must be tall, got {tuple(v.shape)}")
+    if k0 == 0:
+        raise E.DimensionError("v must have at least one column")
+    if is_complex(v):
+        raise NotImplementedError("complex build_reflector: not in this build")
+    if choice not in CHOICES:
+        raise E.ParameterError(f"unknown choice {choice!r}; expected one of {CHOICES}")
+    dev = D.pick_device(v)
+    ctx = D.ctx(dev)
+    V = D.to_device(v, dev)
+    P = None
+    if choice == "explicit":
+        if p is None:
+            raise E.ParameterError("choice='explicit' requires a seed matrix p")
+        p = as_matrix(p, "p")
+        if tuple(p.shape) != (k0, k0):
+            raise E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}")
+        P = D.to_device(p, dev)
+    h = C.c_void_p()
+    defect = C.c_double()
+    from ._native import CHOICES as _CH
+    rc = lib().ots_build_reflector_f64(ctx, n, k0, V.ptr, V.ld, _CH[choice],
+                                       P.ptr if P is not None else None, P.ld if P is not None else 0,
+                                       orth_tol, int(bool(allow_defect)), C.byref(h), C.byref(defect),
+                                       D.stream_ptr(dev))
+    check(rc, ctx)
+    return GenHouseholder(_Handle(h, dev), V, choice, n, k0, was_torch)
+
+
+def apply_reflector(h, x, adjoint=False):
+    """reflector.py:231-238: x - W T^{-(*)} (W^* x), on the GPU."""
+    was_torch = D.is_torch(x)
+    x = as_matrix(x, "x")
+    if x.shape[0] != h.n:
+        raise E.DimensionError(f"x has {x.shape[0]} rows, reflector expects {h.n}")
+    dev = h._h.dev
+    ctx = D.ctx(dev)
+    X = D.to_device(x, dev)
+    m = X.cols
+    Y = D.empty(h.n, m, dev)
+    for c0 in range(0, m, 64):
+        c1 = min(m, c0 + 64)
+        Xc = D.to_device(X.view()[:, c0:c1], dev)
+        Yc = D.empty(h.n, c1 - c0, dev)
+        check(lib().ots_apply_reflector_f64(ctx, h._h.ptr, c1 - c0, Xc.ptr, Xc.ld, Yc.ptr, Yc.ld,
+                                            int(bool(adjoint)), D.stream_ptr(dev)), ctx)
+        Y.buf[:, c0:c1].copy_(Yc.view())
+    return Y.view() if was_torch else Y.numpy()
+
+
+def reflector_diagnostics(h):
+    """reflector.py:241-247 from k0 x k0 device data."""
+    import ctypes as C
+    ctx = D.ctx(h._h.dev)
+    d = (C.c_double * 2)()
+    check(lib().ots_reflector_diagnostics_f64(ctx, h._h.ptr, d, D.stream_ptr(h._h.dev)), ctx)
+    return ReflectorDiagnostics(float(d[0]), float(d[1]))
 
 
 def modified_lu(z):

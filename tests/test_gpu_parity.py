@@ -239,3 +239,37 @@ def test_block_krylov_sweep_small():
     loss = np.abs(np.linalg.eigvalsh(Qg.T @ Qg) - 1).max()
     assert loss <= 10 * n * U
     assert rel(Qg, np.hstack(ref_qs)) < 1e-8
+
+
+@pytest.mark.parametrize("ch", ["mlu", "qr", "polar"])
+def test_reflector_api_golden(golden, ch):
+    v = golden[f"refl/{ch}/v"]
+    h = P.build_reflector(v, ch)
+    assert rel(h.p, golden[f"refl/{ch}/p"]) < 1e-12
+    assert rel(h.w[:10], golden[f"refl/{ch}/wtop"]) < 1e-12
+    assert rel(h.t_solver.reconstruct(), golden[f"refl/{ch}/t"]) < 1e-12
+    d = P.reflector_diagnostics(h)
+    assert abs(d.kappa_t - float(golden[f"refl/{ch}/kappa_t"])) < 1e-10 * d.kappa_t
+    assert abs(d.wt_inv_norm - float(golden[f"refl/{ch}/wt_inv_norm"])) < 1e-10 * d.wt_inv_norm
+
+
+@pytest.mark.parametrize("ch", ["qr", "mlu", "polar"])
+def test_apply_reflector_vs_oracle(ch):
+    rng = W.make_rng(55)
+    n, k0, m = 20000, 48, 80
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    x = W.normal_matrix(rng, n, m)
+    h = P.build_reflector(v, ch)
+    ho = O.Reflector(v, ch)
+    for adj in (False, True):
+        assert rel(P.apply_reflector(h, x, adjoint=adj), ho.apply(x, adjoint=adj)) < 1e-10
+    # v = [I;0], qr seed -> H = diag(-I, I)
+    e = np.zeros((10, 3)); e[:3] = np.eye(3)
+    he = P.build_reflector(e, "qr")
+    assert np.allclose(P.apply_reflector(he, np.eye(10)[:, :1]), -np.eye(10)[:, :1])
+    assert np.allclose(P.apply_reflector(he, np.eye(10)[:, 3:4]), np.eye(10)[:, 3:4])
+    # t_solver.solve round trip
+    b = W.normal_matrix(rng, k0, 5)
+    tt = h.t_solver.reconstruct()
+    assert rel(tt @ h.t_solver.solve(b), b) < 1e-12
+    assert rel(tt.T @ h.t_solver.solve(b, adjoint=True), b) < 1e-12
