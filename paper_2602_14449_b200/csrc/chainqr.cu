@@ -533,11 +533,11 @@ template <int KT>
 struct QformCfg {
   static constexpr int NT = 256;
   static constexpr int BMAX = FactorCfg<KT>::BMAX;
-  static constexpr int SMEM = (3 * KT * KT + BMAX * KT) * 8;
+  static constexpr int YH = 64;                              // Y rows per half-step
+  static constexpr int SMEM = (2 * KT * KT + YH * KT) * 8;   // C, T|M, Y half
 };
 
-// out(KT x KT, swizzled smem) = op(A) * B   [8 warps; warp w < KT/8 -> m-frag w]
-template <int KT, bool TA, bool UPPER_A>
+template <int KT, bool TA, bool UPPER_A, bool TB = false>
 __device__ __forceinline__ void kt_gemm(const double* A, const double* B, double (&acc)[KT / 8][2]) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
 #pragma unroll
@@ -548,7 +548,8 @@ __device__ __forceinline__ void kt_gemm(const double* A, const double* B, double
   for (int kk = kk0; kk < KT / 4; ++kk) {
     double av = TA ? A[swz(4 * kk + t, 8 * warp + g, KT)] : A[swz(8 * warp + g, 4 * kk + t, KT)];
 #pragma unroll
-    for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, B[swz(4 * kk + t, 8 * j + g, KT)]);
+    for (int j = 0; j < KT / 8; ++j)
+      dmma(acc[j], av, TB ? B[swz(8 * j + g, 4 * kk + t, KT)] : B[swz(4 * kk + t, 8 * j + g, KT)]);
   }
 }
 
@@ -564,101 +565,120 @@ __device__ __forceinline__ void kt_store(double* O, const double (&acc)[KT / 8][
 }
 
 
+// Tall product out = -Y M over rows [y0, y0+nr) of a tile half in smem
+// (YH x KT), warp tiles 16 x WN, written to global rows grow0.. (< rhi).
 template <int KT>
-__global__ void __launch_bounds__(256, 1) chain_qform_kernel(QformArgs a) {
+__device__ __forceinline__ void qform_half(const double* Ys, const double* Ms, double* D, long ldd, int ncols,
+                                           long grow0, long rhi) {
+  constexpr int YH = QformCfg<KT>::YH;
+  constexpr int WN = KT < 32 ? KT : 32;
+  constexpr int NJ = WN / 8;
+  constexpr int NWN = KT / WN;
+  constexpr int NWT = (YH / 16) * NWN;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  for (int wt = warp; wt < NWT; wt += 8) {
+    const int wm0 = (wt / NWN) * 16, wn0 = (wt % NWN) * WN;
+    double o[2][NJ][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) o[i][j][0] = o[i][j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < KT / 4; ++kk) {
+      double af[2], bf[NJ];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) af[i] = Ys[swz(wm0 + 8 * i + g, 4 * kk + t4, KT)];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) bf[j] = Ms[swz(4 * kk + t4, wn0 + 8 * j + g, KT)];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma(o[i][j], af[i], bf[j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const long r = grow0 + wm0 + 8 * i + g;
+        const int cc = wn0 + 8 * j + 2 * t4;
+        if (r >= rhi) continue;
+        double* p = D + r * ldd + cc;
+        if (cc + 1 < ncols) *reinterpret_cast<double2*>(p) = make_double2(-o[i][j][0], -o[i][j][1]);
+        else if (cc < ncols) p[0] = -o[i][j][0];
+      }
+  }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(256, 2) chain_qform_kernel(QformArgs a) {
   using C = QformCfg<KT>;
+  constexpr int YH = C::YH;
   extern __shared__ __align__(128) double sm[];
   double* Cs = sm;
-  double* Ms = Cs + KT * KT;
-  double* Ts = Ms + KT * KT;
-  double* Ys = Ts + KT * KT;
+  double* Ts = Cs + KT * KT;    // T, then M = T C in place
+  double* Ys = Ts + KT * KT;    // YH rows of Y
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int chain = blockIdx.x;
   const long r0 = (long)chain * a.G.rpc;
   const int ntiles = chain_real_tiles(a.G, chain, KT);
   const double* Tbase = a.T + (long)chain * (a.G.L + 1) * KT * KT;
 
-  // C (chain) -> smem (swizzled)
   load_tile_async(Cs, KT, a.Cin + (long)chain * KT * KT, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
   cp_async_commit();
 
-  constexpr int WN = KT < 32 ? KT : 32;
-  constexpr int NJ = WN / 8;
-  constexpr int NWN = KT / WN;
-
   for (int tt = ntiles; tt >= 1; --tt) {
     const long gr0 = r0 + KT + (long)(tt - 1) * a.G.b;
+    const long rhi = gr0 + a.G.b < a.G.nrows ? gr0 + a.G.b : a.G.nrows;   // this tile only
     load_tile_async(Ts, KT, Tbase + (long)tt * KT * KT, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
-    const long rhi = gr0 + a.G.b < a.G.nrows ? gr0 + a.G.b : a.G.nrows;  // this tile only
-    const int brows = (a.G.b + 31) / 32 * 32;
-    load_tile_async(Ys, KT, a.D, a.ldd, gr0, brows, gr0, rhi, 0, KT, a.ncols, tid, C::NT);
+    load_tile_async(Ys, KT, a.D, a.ldd, gr0, YH, gr0, rhi, 0, KT, a.ncols, tid, C::NT);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
     double acc[KT / 8][2];
     kt_gemm<KT, false, true>(Ts, Cs, acc);  // M = T C
-    kt_store<KT>(Ms, acc);
     __syncthreads();
-    for (int e = tid; e < KT * KT; e += C::NT) {  // C <- C - M (same swizzle positions)
-      Cs[e] -= Ms[e];
-    }
-    // out rows = -Y M  (b x KT): warp tiles 32 x WN
-    const int nwt = (brows / 32) * NWN;
-    for (int wt = warp; wt < nwt; wt += 8) {
-      const int wm0 = (wt / NWN) * 32, wn0 = (wt % NWN) * WN;
-      double o[4][NJ][2];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) o[i][j][0] = o[i][j][1] = 0.0;
-#pragma unroll 2
-      for (int kk = 0; kk < KT / 4; ++kk) {
-        double af[4], bf[NJ];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Ys[swz(wm0 + 8 * i + g, 4 * kk + t4, KT)];
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) bf[j] = Ms[swz(4 * kk + t4, wn0 + 8 * j + g, KT)];
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < NJ; ++j) dmma(o[i][j], af[i], bf[j]);
+    kt_store<KT>(Ts, acc);                  // M over T
+    __syncthreads();
+    for (int e = tid; e < KT * KT; e += C::NT) Cs[e] -= Ts[e];   // C <- C - M (same swizzle)
+    for (int h = 0; h * YH < a.G.b; ++h) {
+      const long y0 = gr0 + (long)h * YH;
+      if (y0 >= rhi) break;
+      if (h > 0) {
+        __syncthreads();
+        load_tile_async(Ys, KT, a.D, a.ldd, y0, YH, y0, rhi, 0, KT, a.ncols, tid, C::NT);
+        cp_async_commit();
+        cp_async_wait<0>();
+        __syncthreads();
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          long r = gr0 + wm0 + 8 * i + g;
-          int cc = wn0 + 8 * j + 2 * t4;
-          if (r >= rhi) continue;
-          double* p = a.D + r * a.ldd + cc;
-          if (cc + 1 < a.ncols) *reinterpret_cast<double2*>(p) = make_double2(-o[i][j][0], -o[i][j][1]);
-          else if (cc < a.ncols) p[0] = -o[i][j][0];
-        }
+      qform_half<KT>(Ys, Ts, a.D, a.ldd, a.ncols, y0, rhi);
     }
     __syncthreads();
   }
 
-  // ---- head
+  // ---- head (Yt unit lower, from the stored head block): rows [r0, r0+KT)
+  double* Yt = Ys;   // KT <= YH rows
   load_tile_async(Ts, KT, Tbase, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
-  load_tile_async(Ys, KT, a.D, a.ldd, r0, KT, r0, (r0 + KT < a.G.nrows ? r0 + KT : a.G.nrows), 0, KT,
+  load_tile_async(Yt, KT, a.D, a.ldd, r0, KT, r0, (r0 + KT < a.G.nrows ? r0 + KT : a.G.nrows), 0, KT,
                   a.ncols, tid, C::NT);
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
   for (int e = tid; e < KT * KT; e += C::NT) {  // Yt: unit lower
     int r = e / KT, cc = e - r * KT;
-    if (cc >= r) Ys[swz(r, cc, KT)] = (cc == r) ? 1.0 : 0.0;
+    if (cc >= r) Yt[swz(r, cc, KT)] = (cc == r) ? 1.0 : 0.0;
   }
   __syncthreads();
+  // out = C - Yt T Yt^T C = C - Yt M,  M = (T Yt^T) C  (all in smem)
   double acc[KT / 8][2];
-  kt_gemm<KT, true, false>(Ys, Cs, acc);  // W1 = Yt^T C
-  kt_store<KT>(Ms, acc);
+  kt_gemm<KT, false, true, true>(Ts, Yt, acc);   // N = T Yt^T
   __syncthreads();
-  kt_gemm<KT, false, true>(Ts, Ms, acc);  // M = T W1
+  kt_store<KT>(Ts, acc);
   __syncthreads();
-  kt_store<KT>(Ms, acc);
+  kt_gemm<KT, false, false>(Ts, Cs, acc);        // M = N C
   __syncthreads();
-  kt_gemm<KT, false, false>(Ys, Ms, acc);  // Yt M
+  kt_store<KT>(Ts, acc);
+  __syncthreads();
+  kt_gemm<KT, false, false>(Yt, Ts, acc);        // Yt M
   if (warp < KT / 8) {
 #pragma unroll
     for (int j = 0; j < KT / 8; ++j) {

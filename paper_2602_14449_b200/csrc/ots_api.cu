@@ -270,7 +270,8 @@ int grid_for_tn(int PW, int BW, bool alias, bool sym, int nsm) {
   // warps per CTA = number of 32x32 tasks; smem-limited residency.
   int mb = PW / 32;
   int nt = (alias ? (sym ? mb * (mb + 1) / 2 : mb * mb) : 0) + mb * (BW / 32);
-  int stage = 32 * (PW + BW) * 8;
+  const int RT = 32;                                   // mirrors TnCfg
+  int stage = RT * (PW + BW) * 8;
   int nst = std::min(4, std::max(2, (200 * 1024) / stage));
   int smem = nst * stage;
   int by_smem = std::max(1, (227 * 1024) / (smem + 1024));

@@ -157,13 +157,12 @@ struct NnCfg {
   static constexpr int NT = 256;
   static constexpr int KC = 32;
   static constexpr int STAGE = RT * KC + KC * KT;
-  static constexpr int NSTAGE_RAW = (216 * 1024) / (STAGE * 8);
-  static constexpr int NSTAGE = NSTAGE_RAW > 4 ? 4 : NSTAGE_RAW;
+  static constexpr int NSTAGE = 2;                    // 2 CTAs / SM share the SM
   static constexpr int SMEM = NSTAGE * STAGE * 8;
 };
 
 template <int KT>
-__global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
+__global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
   using C = NnCfg<KT>;
   constexpr int WN = C::WN;
   constexpr int NJ = WN / 8;
@@ -176,7 +175,6 @@ __global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
   const long nrows = a.row_end - a.row_begin;
   const long ntiles_total = (nrows + C::RT - 1) / C::RT;
   const int nchunks = (a.kdim + C::KC - 1) / C::KC;
-  // tiles owned by this CTA: blockIdx.x, +gridDim.x, ...
   const long my_tiles = ntiles_total > blockIdx.x ? (ntiles_total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   const long nit = my_tiles * nchunks;
 
@@ -190,16 +188,15 @@ __global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
       double* Zs = Ps + C::RT * C::KC;
       load_tile_async(Ps, C::KC, a.P, a.ldp, tile_r0(lt), C::RT, a.row_begin, a.row_end, ch * C::KC, C::KC,
                       a.kdim, tid, C::NT);
-      // Z chunk: rows [ch*KC, ch*KC+KC) (zero beyond kdim), cols [0, KT) (zero beyond ncols)
       load_tile_async(Zs, KT, a.Z, a.ldz, (long)ch * C::KC, C::KC, 0, a.kdim, 0, KT, a.ncols, tid, C::NT);
     }
     cp_async_commit();
   };
 
   double acc[4][NJ][2];
-  double bv[4][NJ][2];
 
-  auto epilogue_load = [&](long r0) {
+  // accumulators start from B (so the epilogue is a plain store)
+  auto acc_from_b = [&](long r0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -209,10 +206,10 @@ __global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
         double x0 = 0.0, x1 = 0.0;
         if (a.B != nullptr && r < a.row_end) {
           const double* p = a.B + r * a.ldb + c;
-          if (c + 1 < a.ncols) { double2 v = *reinterpret_cast<const double2*>(p); x0 = v.x; x1 = v.y; }
+          if (c + 1 < a.ncols) { double2 v = __ldcs(reinterpret_cast<const double2*>(p)); x0 = v.x; x1 = v.y; }
           else if (c < a.ncols) x0 = p[0];
         }
-        bv[i][j][0] = x0; bv[i][j][1] = x1;
+        acc[i][j][0] = x0; acc[i][j][1] = x1;
       }
   };
   auto epilogue_store = [&](long r0) {
@@ -225,21 +222,17 @@ __global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
         if (r >= a.row_end) continue;
         double s0 = 1.0, s1 = 1.0;
         if (a.colscale) { if (c < a.ncols) s0 = a.colscale[c]; if (c + 1 < a.ncols) s1 = a.colscale[c + 1]; }
-        double y0 = (bv[i][j][0] + acc[i][j][0]) * s0;
-        double y1 = (bv[i][j][1] + acc[i][j][1]) * s1;
+        double y0 = acc[i][j][0] * s0;
+        double y1 = acc[i][j][1] * s1;
         double* p = a.X + r * a.ldx + c;
-        if (c + 1 < a.ncols) *reinterpret_cast<double2*>(p) = make_double2(y0, y1);
+        if (c + 1 < a.ncols) __stcs(reinterpret_cast<double2*>(p), make_double2(y0, y1));
         else if (c < a.ncols) p[0] = y0;
       }
   };
 
   if (nchunks == 0) {  // X = B * colscale
     for (long lt = 0; lt < my_tiles; ++lt) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      epilogue_load(tile_r0(lt));
+      acc_from_b(tile_r0(lt));
       epilogue_store(tile_r0(lt));
     }
     return;
@@ -251,13 +244,7 @@ __global__ void __launch_bounds__(256, 1) tsgemm_nn_kernel(NnArgs a) {
   for (long it = 0; it < nit; ++it) {
     const long lt = it / nchunks;
     const int ch = (int)(it - lt * nchunks);
-    if (ch == 0) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      epilogue_load(tile_r0(lt));  // in flight during the k loop
-    }
+    if (ch == 0) acc_from_b(tile_r0(lt));
     cp_async_wait<C::NSTAGE - 2>();
     __syncthreads();
     issue(it + C::NSTAGE - 1);
@@ -356,7 +343,7 @@ static cudaError_t launch_nn_t(const NnArgs& a, int nsm, cudaStream_t st) {
   long rows = a.row_end - a.row_begin;
   if (rows <= 0) return cudaSuccess;
   long tiles = (rows + C::RT - 1) / C::RT;
-  int grid = (int)(tiles < nsm ? tiles : nsm);
+  int grid = (int)(tiles < 2L * nsm ? tiles : 2L * nsm);
   k<<<grid, C::NT, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
