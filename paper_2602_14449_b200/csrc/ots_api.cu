@@ -270,6 +270,7 @@ int grid_for_tn(int PW, int BW, bool alias, bool sym, int nsm) {
   // warps per CTA = number of 32x32 tasks; smem-limited residency.
   int mb = PW / 32;
   int nt = (alias ? (sym ? mb * (mb + 1) / 2 : mb * mb) : 0) + mb * (BW / 32);
+  if (nt % 4 == 2 && nt > 4) nt += 2;   // mirrors TnCfg::NSPLIT
   const int RT = 32;                                   // mirrors TnCfg
   int stage = RT * (PW + BW) * 8;
   int nst = std::min(4, std::max(2, (200 * 1024) / stage));

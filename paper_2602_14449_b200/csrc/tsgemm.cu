@@ -27,7 +27,11 @@ struct TnCfg {
   static constexpr int NBV = ALIAS ? PW / 32 : 0;
   static constexpr int NBB = BW / 32;
   static constexpr int NVT = ALIAS ? (SYM ? MB * (MB + 1) / 2 : MB * MB) : 0;
-  static constexpr int NTASK = NVT + MB * NBB;
+  static constexpr int NFULL = NVT + MB * NBB;
+  // Balance DMMA work over the 4 SM sub-partitions (warp w -> SMSP w % 4):
+  // when NFULL = 2 mod 4, split the last two 32x32 tasks into 32x16 halves.
+  static constexpr int NSPLIT = (NFULL % 4 == 2 && NFULL > 4) ? 2 : 0;
+  static constexpr int NTASK = NFULL + NSPLIT;      // warps
   static constexpr int NT = NTASK * 32;
   static constexpr int RT = 32;
   static constexpr int STAGE = RT * (PW + BW);
@@ -45,11 +49,18 @@ tsgemm_tn_kernel(TnArgs a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
 
-  // task decode: V-part (mi, ni<=mi or all) then B-part
-  int mi = 0, ni = 0;
-  bool fromP = false;
+  // task decode: V-part (mi, ni<=mi or all) then B-part; the last NSPLIT
+  // full tasks become 2*NSPLIT half tasks (n-range of 16 columns each)
+  int mi = 0, ni = 0, nhalf = 0;
+  bool fromP = false, half = false;
   {
     int w = warp;
+    if (C::NSPLIT && w >= C::NFULL - C::NSPLIT) {
+      const int hw = w - (C::NFULL - C::NSPLIT);     // 0 .. 2*NSPLIT-1
+      w = C::NFULL - C::NSPLIT + hw / 2;
+      half = true;
+      nhalf = hw & 1;
+    }
     if (w < C::NVT) {
       fromP = true;
       for (int m = 0; m < C::MB; ++m) {
@@ -104,29 +115,48 @@ tsgemm_tn_kernel(TnArgs a) {
     const double* Bs = fromP ? Ps : stage_b(s);
     const int BWs = fromP ? PW : (BW > 0 ? BW : 32);
     const int nb0 = fromP ? 32 * ni : 32 * ni;
+    if (!half) {
 #pragma unroll
-    for (int kk = 0; kk < C::RT / 4; ++kk) {
-      const int r = 4 * kk + t;
-      double af[4], bf[4];
+      for (int kk = 0; kk < C::RT / 4; ++kk) {
+        const int r = 4 * kk + t;
+        double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, nb0 + 8 * j + g, BWs)];
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, nb0 + 8 * j + g, BWs)];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+        for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+          for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+    } else {
+      const int nbh = nb0 + 16 * nhalf;
+#pragma unroll
+      for (int kk = 0; kk < C::RT / 4; ++kk) {
+        const int r = 4 * kk + t;
+        double af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = Bs[swz(r, nbh + 8 * j + g, BWs)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
     }
   }
   cp_async_wait<0>();
 
   // partial write
   double* out = a.partial + (long)blockIdx.x * PW * C::NTOT;
-  const int ncol0 = fromP ? 32 * ni : C::NBV * 32 + 32 * ni;
+  const int ncol0 = (fromP ? 32 * ni : C::NBV * 32 + 32 * ni) + (half ? 16 * nhalf : 0);
+  const int nj = half ? 2 : 4;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
+      if (j >= nj) continue;
       int m = 32 * mi + 8 * i + g;
       int n = ncol0 + 8 * j + 2 * t;
       *reinterpret_cast<double2*>(out + (long)m * C::NTOT + n) = make_double2(acc[i][j][0], acc[i][j][1]);
