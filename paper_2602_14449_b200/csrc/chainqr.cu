@@ -729,9 +729,11 @@ cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+void debug_counters_small(unsigned long long* out, int reset);
 int debug_counters(unsigned long long* out, int reset) {
 #ifdef OTS_TIMING
   cudaMemcpyFromSymbol(out, g_dbg, sizeof(unsigned long long) * 16);
+  debug_counters_small(out, reset);
   if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_dbg, z, sizeof z); }
   return 1;
 #else

@@ -311,8 +311,8 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   bytes += gf_n * 8 * 2 + 512;                                       // Gfull, Y2full
   bytes += (size_t)3 * ld * ld * 8 + 256;                            // cholshift scratch
   bytes += (size_t)k0 * (k0 + k + 2) * 8 + 256;                    // top rows
-  bytes += (size_t)16 * ld * ld * 8 + 16 * 256;                    // small matrices
-  bytes += (size_t)8 * ld * 8 + 8 * 256;                           // vectors
+  bytes += (size_t)22 * ld * ld * 8 + 22 * 256;                    // small matrices + diag scratch
+  bytes += (size_t)8 * ld * 8 + 10 * 256;                          // vectors, dlam, dcount
   bytes += (size_t)KT * KT * 8 * 2 + 1024;                         // ident, svec
   bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, ctx->nsm);
   bytes += (size_t)64 * KT * KT * 8 * 4 + 4096;                    // global tree (<=64 ranks)
@@ -335,6 +335,9 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   double** mats[] = {&s.G, &s.Vt, &s.At, &s.VbA, &s.P, &s.Tf, &s.Tdense, &s.Wt,
                      &s.Z1, &s.Z2, &s.X1, &s.X2, &s.D1, &s.D2, &s.Sd};
   for (auto m : mats) *m = ar.take<double>((size_t)ld * ld);
+  for (auto& m : s.dg) m = ar.take<double>((size_t)ld * ld);
+  s.dlam = ar.take<double>(4);
+  s.dcount = ar.take<int>(4);
   s.pvec = ar.take<double>(ld); s.tau = ar.take<double>(ld); s.sig = ar.take<double>(ld);
   s.sig2 = ar.take<double>(ld); s.svec = ar.take<double>(std::max(ld, KT));
   s.piv = ar.take<int>(ld);

@@ -13,6 +13,13 @@
 
 namespace ots {
 
+#ifdef OTS_TIMING
+__device__ unsigned long long g_dbg_small[16];
+#define SMARK(slot, t0) if (threadIdx.x == 0) { long long _t = clock64(); atomicAdd(&g_dbg_small[slot], (unsigned long long)(_t - t0)); t0 = _t; }
+#else
+#define SMARK(slot, t0)
+#endif
+
 #define BLK_FOR(i, n) for (int i = threadIdx.x; i < (n); i += blockDim.x)
 
 __device__ __forceinline__ double block_sum(double v, double* red) {
@@ -48,45 +55,137 @@ __device__ void blk_identity(double* D, int ldd, int n) {
   BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; D[i * ldd + j] = (i == j) ? 1.0 : 0.0; }
 }
 
-// C = alpha * op(A) op(B) + beta * C   (naive, block-parallel over entries)
+// C = alpha * op(A) op(B) + beta * C.  Register-tiled: a warp owns 4-row x
+// 128-column strips of C, lane l the columns l + 32c (coalesced B rows,
+// broadcast A entries).  Summation order per entry is p = 0..k-1 (fma), as
+// in a plain dot product.  C must not alias A or B.
 __device__ void blk_gemm(double* Cm, int ldc, const double* A, int lda, bool ta, const double* B,
                          int ldb, bool tb, int m, int n, int k, double alpha, double beta) {
   __syncthreads();
-  BLK_FOR(e, m * n) {
-    int i = e / n, j = e - i * n;
-    double s = 0.0;
-    for (int l = 0; l < k; ++l) {
-      double av = ta ? A[l * lda + i] : A[i * lda + l];
-      double bv = tb ? B[j * ldb + l] : B[l * ldb + j];
-      s = fma(av, bv, s);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int rs = (m + 3) >> 2, cs = (n + 127) >> 7;
+  for (int t = w; t < rs * cs; t += nw) {
+    const int i0 = (t / cs) * 4, j0 = (t % cs) * 128;
+    int jj[4];
+    bool jv[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { jj[c] = j0 + l + 32 * c; jv[c] = jj[c] < n; }
+    bool iv[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) iv[r] = i0 + r < m;
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+    for (int p0 = 0; p0 < k; p0 += 4) {  // 4-deep batches keep loads in flight
+      double a[4][4], b[4][4];
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp) {
+        const int p = p0 + pp;
+        const bool pv = p < k;
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+          a[pp][r] = (pv && iv[r]) ? (ta ? A[p * lda + i0 + r] : A[(i0 + r) * lda + p]) : 0.0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          b[pp][c] = (pv && jv[c]) ? (tb ? B[jj[c] * ldb + p] : B[p * ldb + jj[c]]) : 0.0;
+      }
+#pragma unroll
+      for (int pp = 0; pp < 4; ++pp)
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[pp][r], b[pp][c], acc[r][c]);
     }
-    Cm[i * ldc + j] = alpha * s + (beta == 0.0 ? 0.0 : beta * Cm[i * ldc + j]);
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (iv[r] && jv[c]) {
+          double* cp = Cm + (i0 + r) * ldc + jj[c];
+          *cp = alpha * acc[r][c] + (beta == 0.0 ? 0.0 : beta * *cp);
+        }
   }
   __syncthreads();
 }
 
 // Solve op(A) X = B in place (B: n x nrhs).  A triangular (lower/upper as
 // stored); trans solves with A^T.  Substitution order as trtrs.
+// Register-resident substitution: a group of G lanes (same warp) owns one
+// right-hand side at a time, lane gl holding rows gl + G q (q < RPT) in
+// registers; x_i is broadcast by its owner with a width-G shuffle.  The
+// arithmetic per entry (x_i = b_i / a_ii, b_r -= e_ri x_i in order of i) is
+// that of the plain column sweep.
+template <int RPT, bool TRANS, bool ELOWER>
+__device__ __noinline__ void trsm_reg(const double* A, int lda, bool unit, double* B, int ldb, int n,
+                                      int nrhs, int G) {
+  constexpr bool trans = TRANS, elower = ELOWER;
+  const int gl = threadIdx.x % G, grp = threadIdx.x / G, ngrp = blockDim.x / G;
+  const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const int nq = (n + G - 1) / G;
+  for (int j = grp; j < nrhs; j += ngrp) {
+    double b[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) { const int r = gl + G * q; b[q] = (r < n) ? B[r * ldb + j] : 0.0; }
+    for (int s = 0; s < nq * G; ++s) {
+      const int q = elower ? (s / G) : (nq - 1 - s / G);
+      const int g = elower ? (s % G) : (G - 1 - s % G);
+      const int i = g + G * q;
+      if (i >= n) continue;
+      double bq = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < RPT; ++qq) if (qq == q) bq = b[qq];
+      const double dii = unit ? 1.0 : A[i * lda + i];
+      const double x = __shfl_sync(mask, bq, g, G) / dii;
+#pragma unroll
+      for (int q2 = 0; q2 < RPT; ++q2) {
+        const int r = gl + G * q2;
+        if (r == i) b[q2] = x;
+        else if (elower ? (r > i && r < n) : (r < i))
+          b[q2] = fma(-(trans ? A[i * lda + r] : A[r * lda + i]), x, b[q2]);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) { const int r = gl + G * q; if (r < n) B[r * ldb + j] = b[q]; }
+  }
+}
+
 __device__ void blk_trsm(const double* A, int lda, bool lower, bool trans, bool unit, double* B,
                          int ldb, int n, int nrhs) {
   // effective matrix E = op(A); E is lower iff (lower xor trans)
   const bool elower = lower != trans;
   __syncthreads();
-  for (int s = 0; s < n; ++s) {
-    const int i = elower ? s : (n - 1 - s);
-    const double dii = unit ? 1.0 : A[i * lda + i];
-    BLK_FOR(j, nrhs) B[i * ldb + j] /= dii;
-    __syncthreads();
-    // eliminate x_i from remaining rows
-    const int rem = elower ? (n - 1 - i) : i;
-    BLK_FOR(e, rem * nrhs) {
-      int rr = e / nrhs, j = e - rr * nrhs;
-      int r = elower ? (i + 1 + rr) : rr;
-      double eri = trans ? A[i * lda + r] : A[r * lda + i];
-      B[r * ldb + j] = fma(-eri, B[i * ldb + j], B[r * ldb + j]);
+  if (n <= 0 || nrhs <= 0) return;
+  int G = 1;
+  while (G < 32 && G * 2 * nrhs <= (int)blockDim.x) G *= 2;
+  while (G < 32 && (n + G - 1) / G > 16) G *= 2;
+  const int rpt = (n + G - 1) / G;
+#define OTS_TRSM(R)                                                                   \
+  if (trans) { if (elower) trsm_reg<R, true, true>(A, lda, unit, B, ldb, n, nrhs, G);   \
+               else trsm_reg<R, true, false>(A, lda, unit, B, ldb, n, nrhs, G); }       \
+  else { if (elower) trsm_reg<R, false, true>(A, lda, unit, B, ldb, n, nrhs, G);        \
+         else trsm_reg<R, false, false>(A, lda, unit, B, ldb, n, nrhs, G); }
+  if (rpt <= 8) { OTS_TRSM(8) }
+  else if (rpt <= 16) { OTS_TRSM(16) }
+#undef OTS_TRSM
+  else {
+    for (int s = 0; s < n; ++s) {  // n > 512: plain column sweep
+      const int i = elower ? s : (n - 1 - s);
+      const double dii = unit ? 1.0 : A[i * lda + i];
+      BLK_FOR(j, nrhs) B[i * ldb + j] /= dii;
+      __syncthreads();
+      const int rem = elower ? (n - 1 - i) : i;
+      BLK_FOR(e, rem * nrhs) {
+        int rr = e / nrhs, j = e - rr * nrhs;
+        int r = elower ? (i + 1 + rr) : rr;
+        double eri = trans ? A[i * lda + r] : A[r * lda + i];
+        B[r * ldb + j] = fma(-eri, B[i * ldb + j], B[r * ldb + j]);
+      }
+      __syncthreads();
     }
-    __syncthreads();
   }
+  __syncthreads();
 }
 
 // dgeqr2 on an m x n block (m >= n), LAPACK dlarfg conventions; v below the
@@ -370,33 +469,132 @@ __device__ double blk_sigma_max(double* W, int ld, int n, double* sig, double* r
   return block_max(m, red);
 }
 
+// Largest eigenvalue of a symmetric n x n matrix S (overwritten): Householder
+// tridiagonalisation (dsytd2, lower) followed by parallel multisection on the
+// Sturm count of the tridiagonal (dstebz-style, one shift per thread).
+// vec: >= 4 n doubles of scratch (shared memory preferred).
+__device__ double blk_sym_lmax(double* S, int lds, int n, double* vec, double* red) {
+  double* v = vec;           // Householder vector
+  double* pw = vec + n;      // p, then w
+  double* d = vec + 2 * n;   // diagonal
+  double* e = vec + 3 * n;   // off-diagonal
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  for (int j = 0; j + 2 < n; ++j) {
+    const int m = n - j - 1;
+    const double* x = S + (j + 1) * lds + j;  // column j below the diagonal, stride lds
+    double s2 = 0.0;
+    for (int r = 1 + (int)threadIdx.x; r < m; r += blockDim.x) { double t = x[r * lds]; s2 = fma(t, t, s2); }
+    s2 = block_sum(s2, red);
+    const double alpha = x[0];
+    if (threadIdx.x == 0) d[j] = S[j * lds + j];
+    if (s2 == 0.0) {
+      if (threadIdx.x == 0) e[j] = alpha;
+      __syncthreads();
+      continue;
+    }
+    const double beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+    const double tau = (beta - alpha) / beta;
+    const double scal = 1.0 / (alpha - beta);
+    for (int r = threadIdx.x; r < m; r += blockDim.x) v[r] = (r == 0) ? 1.0 : x[r * lds] * scal;
+    if (threadIdx.x == 0) e[j] = beta;
+    __syncthreads();
+    // p = tau S22 v  (one warp per row)
+    double* S22 = S + (j + 1) * lds + (j + 1);
+    double pv = 0.0;
+    for (int r = w; r < m; r += nw) {
+      double acc = 0.0;
+      for (int c = l; c < m; c += 32) acc = fma(S22[r * lds + c], v[c], acc);
+      acc = warp_sum(acc) * tau;
+      if (l == 0) pw[r] = acc;
+      pv = fma(acc, v[r], pv);
+    }
+    if (l != 0) pv = 0.0;
+    pv = block_sum(pv, red);
+    const double K = -0.5 * tau * pv;
+    for (int r = threadIdx.x; r < m; r += blockDim.x) pw[r] = fma(K, v[r], pw[r]);
+    __syncthreads();
+    // S22 -= v w^T + w v^T
+    for (int r = w; r < m; r += nw) {
+      const double vr = v[r], wr = pw[r];
+      for (int c = l; c < m; c += 32) S22[r * lds + c] -= vr * pw[c] + wr * v[c];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    if (n >= 2) { d[n - 2] = S[(n - 2) * lds + n - 2]; e[n - 2] = S[(n - 1) * lds + n - 2]; }
+    d[n - 1] = S[(n - 1) * lds + n - 1];
+  }
+  __syncthreads();
+  // Gershgorin upper bound; max diagonal is a lower bound of lambda_max
+  double lo = -1.7976931348623157e308, hi = lo, e2max = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double el = (i > 0) ? fabs(e[i - 1]) : 0.0, er = (i + 1 < n) ? fabs(e[i]) : 0.0;
+    lo = fmax(lo, d[i]);
+    hi = fmax(hi, d[i] + el + er);
+    e2max = fmax(e2max, er * er);
+  }
+  lo = block_max(lo, red);
+  hi = block_max(hi, red);
+  e2max = block_max(e2max, red);
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, e2max);
+  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) pw[i] = e[i] * e[i];
+  __syncthreads();
+  const int NT = blockDim.x;
+  __shared__ int first_full;
+  for (int it = 0; it < 64; ++it) {
+    if (!(hi - lo > 2.2e-16 * fmax(fabs(lo), fabs(hi)) + pivmin)) break;
+    // x_t = lo + (hi - lo) (t + 1) / (NT + 1); count of eigenvalues < x_t
+    const double xt = lo + (hi - lo) * (double)(threadIdx.x + 1) / (double)(NT + 1);
+    int cnt = 0;
+    double q = d[0] - xt;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += (q < 0.0);
+    for (int i = 1; i < n; ++i) {
+      q = (d[i] - xt) - pw[i - 1] / q;
+      if (fabs(q) < pivmin) q = -pivmin;
+      cnt += (q < 0.0);
+    }
+    if (threadIdx.x == 0) first_full = NT;
+    __syncthreads();
+    if (cnt >= n) atomicMin(&first_full, (int)threadIdx.x);
+    __syncthreads();
+    const int t = first_full;
+    const double nlo = (t == 0) ? lo : lo + (hi - lo) * (double)t / (double)(NT + 1);
+    const double nhi = (t == NT) ? hi : lo + (hi - lo) * (double)(t + 1) / (double)(NT + 1);
+    lo = nlo; hi = nhi;
+    __syncthreads();
+  }
+  return 0.5 * (lo + hi);
+}
+
 // ---------------------------------------------------------------------------
 // T-solver dispatch (reflector.py:80-153).  X (n x m) overwritten.
 //   adjoint=false: T X = B ; adjoint=true: T^T X = B.
 // ---------------------------------------------------------------------------
-__device__ void t_solve_core(const SmallState& s, double* X, int ldx, int m, bool adjoint);
+__device__ void t_solve_core(const SmallState& s, const double* F, int ld, double* X, int ldx, int m,
+                             bool adjoint);
 
 extern __shared__ __align__(16) double dsm[];
 constexpr int SMALL_SMEM_DOUBLES = 25 * 1024;   // 200 KB dynamic smem of the small kernels
 
 __device__ void t_solve(const SmallState& s, double* X, int ldx, int m, bool adjoint) {
+  // the right-hand sides live in registers inside blk_trsm; stage the factor
   const int n = s.k0;
-  if (n * m <= SMALL_SMEM_DOUBLES) {
+  if (n * (n + 1) <= SMALL_SMEM_DOUBLES) {
     __syncthreads();
-    BLK_FOR(e, n * m) { int i = e / m, j = e - i * m; dsm[e] = X[i * ldx + j]; }
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; dsm[i * (n + 1) + j] = s.Tf[i * s.ld + j]; }
     __syncthreads();
-    t_solve_core(s, dsm, m, m, adjoint);
-    BLK_FOR(e, n * m) { int i = e / m, j = e - i * m; X[i * ldx + j] = dsm[e]; }
+    t_solve_core(s, dsm, n + 1, X, ldx, m, adjoint);
     __syncthreads();
     return;
   }
-  t_solve_core(s, X, ldx, m, adjoint);
+  t_solve_core(s, s.Tf, s.ld, X, ldx, m, adjoint);
 }
 
-__device__ void t_solve_core(const SmallState& s, double* X, int ldx, int m, bool adjoint) {
+__device__ void t_solve_core(const SmallState& s, const double* F, int ld, double* X, int ldx, int m,
+                             bool adjoint) {
   const int n = s.k0;
-  const double* F = s.Tf;
-  const int ld = s.ld;
   switch (s.choice) {
     case CHOICE_QR:  // lower triangular T
       blk_trsm(F, ld, true, adjoint, false, X, ldx, n, m);
@@ -642,49 +840,81 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
 // Diagnostics from k0 x k0 data (reflector.py:241-247):
 // kappa_2(T) and ||W T^{-1}||_2 = sqrt(lambda_max(T^{-T} W^T W T^{-1})),
 // W^T W = W_t^T W_t + (G - V_t^T V_t).
+// Diagnostics from k0 x k0 data only: kappa(T) = sigma_max(T)
+// sigma_max(T^-1) and ||W T^-1||_2 = sqrt(lambda_max(T^-T W^T W T^-1)), as the
+// largest eigenvalues of three symmetric matrices, one per CTA (grid 3); the
+// last CTA to finish combines them.
 __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
   __shared__ double red[64];
+  __shared__ double vec[4 * 512];
+  __shared__ int last;
   if (s.status[0] != 0) return;
   const int n = s.k0, ld = s.ld;
-  // kappa(T)
-  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] = s.Tdense[i * ld + j]; }
-  __syncthreads();
-  blk_jacobi_rows(s.D1, ld, nullptr, 0, n, s.sig2, red, dsm, SMALL_SMEM_DOUBLES);
-  double mx = 0.0, mn = 1e308;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) { mx = fmax(mx, s.sig2[i]); mn = fmin(mn, s.sig2[i]); }
-  mx = block_max(mx, red);
-  mn = -block_max(-mn, red);
-  if (threadIdx.x == 0) s.diag[0] = (mn == 0.0) ? __longlong_as_double(0x7ff0000000000000LL) : mx / mn;
-  // W^T W
-  if (s.Gu == nullptr) {
-    blk_gemm(s.D1, ld, s.Wt, ld, true, s.Wt, ld, false, n, n, n, 1.0, 0.0);
-    blk_gemm(s.D2, ld, s.Vt, ld, true, s.Vt, ld, false, n, n, n, 1.0, 0.0);
-    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D1[i * ld + j] += s.G[i * ld + j] - s.D2[i * ld + j]; }
-  } else {  // B-inner, M = diag(d): unweighted W = D^{-1/2} W'
-    BLK_FOR(e, n * n) {
-      int i = e / n, j = e - i * n;
-      double acc = 0.0;
-      for (int l = 0; l < n; ++l) {
-        const double dl = s.dinv_top[l];
-        acc = fma(dl, s.Wt[l * ld + i] * s.Wt[l * ld + j] - s.Vt[l * ld + i] * s.Vt[l * ld + j], acc);
+  long long tm0 = clock64();
+  const bool fit = n * (n + 1) <= SMALL_SMEM_DOUBLES;
+  const int lss = fit ? n + 1 : ld;
+  double lam;
+  if (blockIdx.x == 0) {  // T^T T
+    double* S = fit ? dsm : s.dg[0];
+    blk_gemm(S, lss, s.Tdense, ld, true, s.Tdense, ld, false, n, n, n, 1.0, 0.0);
+    lam = blk_sym_lmax(S, lss, n, vec, red);
+    SMARK(10, tm0);
+  } else if (blockIdx.x == 1) {  // T^-T T^-1
+    double* E = s.dg[1];
+    blk_identity(E, ld, n);
+    t_solve(s, E, ld, n, false);
+    double* S = fit ? dsm : s.dg[2];
+    blk_gemm(S, lss, E, ld, true, E, ld, false, n, n, n, 1.0, 0.0);
+    lam = blk_sym_lmax(S, lss, n, vec, red);
+    SMARK(11, tm0);
+  } else {  // M = T^-T (W^T W) T^-1
+    double *E = s.dg[3], *WW = s.dg[4], *H = s.dg[5];
+    blk_identity(E, ld, n);
+    t_solve(s, E, ld, n, false);
+    SMARK(12, tm0);
+    if (s.Gu == nullptr) {
+      blk_gemm(WW, ld, s.Wt, ld, true, s.Wt, ld, false, n, n, n, 1.0, 0.0);
+      blk_gemm(WW, ld, s.Vt, ld, true, s.Vt, ld, false, n, n, n, -1.0, 1.0);
+      BLK_FOR(e2, n * n) { int i = e2 / n, j = e2 - i * n; WW[i * ld + j] += s.G[i * ld + j]; }
+    } else {  // B-inner, M = diag(d): unweighted W = D^{-1/2} W'
+      BLK_FOR(e2, n * n) { int i = e2 / n, j = e2 - i * n; H[i * ld + j] = s.dinv_top[i] * s.Wt[i * ld + j]; }
+      blk_gemm(WW, ld, s.Wt, ld, true, H, ld, false, n, n, n, 1.0, 0.0);
+      BLK_FOR(e2, n * n) { int i = e2 / n, j = e2 - i * n; H[i * ld + j] = s.dinv_top[i] * s.Vt[i * ld + j]; }
+      blk_gemm(WW, ld, s.Vt, ld, true, H, ld, false, n, n, n, -1.0, 1.0);
+      BLK_FOR(e2, n * n) {
+        int i = e2 / n, j = e2 - i * n;
+        WW[i * ld + j] += (j <= i) ? s.Gu[(long)i * s.ldgu + j] : s.Gu[(long)j * s.ldgu + i];
       }
-      const double gu = (j <= i) ? s.Gu[(long)i * s.ldgu + j] : s.Gu[(long)j * s.ldgu + i];
-      s.D1[i * ld + j] = acc + gu;
     }
+    blk_gemm(H, ld, WW, ld, false, E, ld, false, n, n, n, 1.0, 0.0);
+    double* S = fit ? dsm : WW;
+    blk_gemm(S, lss, E, ld, true, H, ld, false, n, n, n, 1.0, 0.0);
+    BLK_FOR(e2, n * n) {  // symmetrise
+      int i = e2 / n, j = e2 - i * n;
+      if (j < i) {
+        const double h = 0.5 * (S[i * lss + j] + S[j * lss + i]);
+        S[i * lss + j] = h;
+        S[j * lss + i] = h;
+      }
+    }
+    SMARK(13, tm0);
+    lam = blk_sym_lmax(S, lss, n, vec, red);
+    SMARK(14, tm0);
+  }
+  if (threadIdx.x == 0) {
+    s.dlam[blockIdx.x] = lam;
+    __threadfence();
+    last = (atomicAdd(s.dcount, 1) == (int)gridDim.x - 1);
   }
   __syncthreads();
-  // X = T^{-T} (W^T W) ; M^T = T^{-T} X^T
-  t_solve(s, s.D1, ld, n, true);
-  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.D2[i * ld + j] = s.D1[j * ld + i]; }
-  __syncthreads();
-  t_solve(s, s.D2, ld, n, true);
-  BLK_FOR(e, n * n) {  // symmetrise
-    int i = e / n, j = e - i * n;
-    s.D1[i * ld + j] = 0.5 * (s.D2[i * ld + j] + s.D2[j * ld + i]);
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    const volatile double* L = s.dlam;
+    const double l0 = L[0], l1 = L[1], l2 = L[2];
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    s.diag[0] = (l1 < inf) ? sqrt(fmax(l0, 0.0)) * sqrt(fmax(l1, 0.0)) : inf;
+    s.diag[1] = sqrt(fmax(l2, 0.0));
   }
-  __syncthreads();
-  double lm = blk_sigma_max(s.D1, ld, n, s.sig2, red, dsm, SMALL_SMEM_DOUBLES);
-  if (threadIdx.x == 0) s.diag[1] = sqrt(lm);
 }
 
 // apply_reflector (reflector.py:231-238) small part: Y = W_t^T X_t - V_b^T X_b
@@ -809,7 +1039,8 @@ cudaError_t launch_seed(const SmallState& s, cudaStream_t st) {
 }
 cudaError_t launch_diag(const SmallState& s, cudaStream_t st) {
   cudaFuncSetAttribute(diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
-  diag_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
+  cudaMemsetAsync(s.dcount, 0, sizeof(int), st);
+  diag_kernel<<<3, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 cudaError_t launch_refl_apply(const SmallState& s, int adjoint, cudaStream_t st) {
@@ -842,6 +1073,17 @@ cudaError_t launch_mlu(const double* Z, int ldz, int n, double* LU, double* p, d
   cudaFuncSetAttribute(mlu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
   mlu_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(Z, ldz, n, LU, p, work, status);
   return cudaGetLastError();
+}
+
+void debug_counters_small(unsigned long long* out, int reset) {
+#ifdef OTS_TIMING
+  unsigned long long tmp[16];
+  cudaMemcpyFromSymbol(tmp, g_dbg_small, sizeof tmp);
+  for (int i = 10; i < 16; ++i) out[i] += tmp[i];
+  if (reset) { unsigned long long z[16] = {0}; cudaMemcpyToSymbol(g_dbg_small, z, sizeof z); }
+#else
+  (void)out; (void)reset;
+#endif
 }
 
 }  // namespace ots

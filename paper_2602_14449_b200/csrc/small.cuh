@@ -27,6 +27,9 @@ struct SmallState {
   // W^T W = W_t'^T D_t^{-1} W_t' + V^T V (unweighted Gram Gu) - V_t'^T D_t^{-1} V_t'
   const double* Gu; int ldgu;  // null for the Euclidean path
   const double* dinv_top;      // 1/d on the k0 top rows
+  double* dg[6];               // diagnostics scratch (k0 x k0 each, ld)
+  double* dlam;                // [3] per-CTA eigenvalues of the diagnostics kernel
+  int* dcount;                 // CTA completion counter of the diagnostics kernel
   double* diag;                // [kappa_t, wt_inv_norm, defect]
   int* status;                 // [0] = status code
 };
