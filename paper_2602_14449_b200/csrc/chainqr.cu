@@ -196,27 +196,59 @@ __device__ __forceinline__ void u_to_t_block(const double* Us, double* Ts, doubl
 }
 
 // ===========================================================================
-// Structured TSQR step, blocked (v3).  The b x KT tile X lives in shared
-// memory (swizzled for m8n8k4 fragments); R (KT x KT, upper) in S, whose
-// strictly lower part stores the Gram entries G[c][j] = y_c . y_j (c < j)
-// needed for the tile's compact-WY T.  Panels are 8 columns:
-//   * warp p factors panel p in registers (warp shuffles, no CTA barrier);
-//   * one __syncthreads publishes Y_p (in place in X) and T_p;
-//   * warp w > p applies the panel to its 8 columns with DMMA:
-//       W = X_w^T Y_p + R[p rows, w cols]^T ; w = W T_p ; X_w -= Y_p w^T ;
-//       R[p rows, w cols] -= w^T
-//     warp w < p (holding earlier Householder vectors) records G blocks.
-// Warp p+1 applies panel p to its own columns and factors panel p+1 right
-// away, so the critical path is one apply + one panel per barrier.
+// Structured TSQR step, blocked, register-resident (v5).  The 128 x KT tile
+// lives in REGISTERS: warp w (< KT/8) owns columns 8w..8w+7, lane (g, t)
+// (g = lane>>2, t = lane&3) holds x[f][h] = X[8f + 2t + h][8w + g] -- the
+// C-fragment layout of m8n8k4 with X^T as the output.  R (KT x KT, upper) is
+// in shared memory S, whose strictly lower part stores the Gram entries
+// G[c][j] = y_c . y_j (c < j) for the tile's compact-WY T.  Per 8-column panel:
+//   * warp p factors its panel: column norms and dots are 4-lane reductions
+//     (a column's 128 rows sit in one lane quad), v is broadcast with 32
+//     independent shuffles; Y_p goes to a double-buffered smem slot and T_p
+//     (8 x 8, dlarft) to smem;
+//   * one __syncthreads;
+//   * warp w > p:  W^T = X_w^T Y_p + R[p rows, w cols]^T  (A from registers,
+//     B = Y_p from smem), w^T = W^T T_p, R -= w, X_w^T -= w^T Y_p^T with the
+//     register tile as the DMMA accumulator;  warp w < p records G blocks.
+// Shared-memory traffic per DMMA is one 8-byte load per lane.
 // ===========================================================================
 template <int KT>
 struct BlkCfg {
   static constexpr int B = 128;          // tile rows
   static constexpr int NB = 8;           // panel width
   static constexpr int NP = KT / NB;     // panels (= warps that own columns)
-  static constexpr int XS = B * KT + 64; // X region (+ slack for the head's U/T)
+  static constexpr int YS = 12;          // Y slot row stride: 2 wavefronts per 32-lane access
+  static constexpr int YSLOT = B * YS;
+  static constexpr int XS0 = (2 * KT * KT + KT > 2 * YSLOT) ? 2 * KT * KT + KT : 2 * YSLOT;
+  static constexpr int XS = (XS0 > KT * (KT + 4) ? XS0 : KT * (KT + 4)) + 64;  // head U|T, Y slots, Tw
   static constexpr int SMEM = (KT * KT + XS + NP * 64 + 8 * 64) * 8;
 };
+
+__device__ __forceinline__ void tile_regs_load(double (&x)[16][2], const double* D, long ldd, long gr0,
+                                               int nb, int col, int ncols) {
+  const int t = threadIdx.x & 3;
+  const bool cv = col < ncols;
+#pragma unroll
+  for (int f = 0; f < 16; ++f)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * f + 2 * t + h;
+      x[f][h] = (cv && r < nb) ? D[(gr0 + r) * ldd + col] : 0.0;
+    }
+}
+
+__device__ __forceinline__ void tile_regs_store(const double (&x)[16][2], double* D, long ldd, long gr0,
+                                                int nb, int col, int ncols) {
+  const int t = threadIdx.x & 3;
+  if (col >= ncols) return;
+#pragma unroll
+  for (int f = 0; f < 16; ++f)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = 8 * f + 2 * t + h;
+      if (r < nb) D[(gr0 + r) * ldd + col] = x[f][h];
+    }
+}
 
 // Sum 8 per-lane values over the warp: butterfly reduce-scatter (each step
 // halves the values a lane keeps), a 2-level finish, then an indexed
@@ -252,147 +284,227 @@ __device__ __forceinline__ void warp_sum8(double (&v)[8]) {
   }
 }
 
-// panel factorization by one warp: lanes own rows l, l+32, l+64, l+96
-template <int KT>
-__device__ __forceinline__ void panel_factor(int p, double* S, double* Xs, double* Tp, double* tau_s,
-                                             int nb) {
-  constexpr int RPL = BlkCfg<KT>::B / 32;
+// dlarfg without branches (one basic block): MUFU rsqrt/rcp seeds with two
+// Newton steps each; s2 == 0 gives tau = 0, beta = alpha, scal = 0.
+__device__ __forceinline__ void dlarfg_nb(double alpha, double s2, double& beta, double& tau,
+                                          double& scal) {
+  const double h = fma(alpha, alpha, s2);
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(h));
+  r = r * fma(-0.5 * h * r, r, 1.5);
+  r = r * fma(-0.5 * h * r, r, 1.5);
+  const double sq = h * r;
+  const double t = fabs(alpha) + sq;
+  double rt;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(rt) : "d"(t));
+  rt = rt * fma(-t, rt, 2.0);
+  rt = rt * fma(-t, rt, 2.0);
+  const bool z = (s2 == 0.0);
+  beta = z ? alpha : -copysign(sq, alpha);
+  tau = z ? 0.0 : t * r;
+  scal = z ? 0.0 : copysign(rt, alpha);
+}
+
+// One sweep over the 8 columns of a panel in the lane-per-row layout (lane
+// owns rows l, l+32, l+64, l+96).  EXACT=false takes every column norm after
+// the first from the downdate |x - w v|^2 = N - 2 w (x.v) + w^2 |v|^2 and is
+// branch-free, so ptxas schedules the 8 steps as one block and overlaps the
+// off-critical work (other dots, updates, T) with the reflector chain;
+// returns true when a downdate cancelled more than half of N (then the caller
+// replays the panel with EXACT=true, which reduces every norm).
+template <int KT, bool EXACT>
+__device__ __forceinline__ bool panel_core(int p, double (&xr)[4][8], double* S, double* T8,
+                                           double* tau_s) {
   const int lane = threadIdx.x & 31;
   const int j0 = p * 8;
-  double xr[RPL][8];
+  const int lr = lane < 8 ? lane : 7;
+  double s2n = 0.0;
+  bool bad = false;
+  double trow[8];       // lane ii < 8: row ii of T_p
 #pragma unroll
-  for (int i = 0; i < RPL; ++i) {
-    const int r = lane + 32 * i;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) xr[i][c] = Xs[swz(r, j0 + c, KT)];
-  }
-  double* T8 = Tp + p * 64;          // T_p built column by column (dlarft)
-  T8[lane] = 0.0;
-  T8[lane + 32] = 0.0;
-  __syncwarp();
-  double s2n = -1.0;   // next column's norm^2 when known from the downdate
+  for (int l = 0; l < 8; ++l) trow[l] = 0.0;
 #pragma unroll
   for (int jj = 0; jj < 8; ++jj) {
     const int j = j0 + jj;
+    double rrow[8];
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc) rrow[cc] = (cc >= jj) ? S[j * KT + j0 + cc] : 0.0;
     double s2 = s2n;
-    if (!(s2 >= 0.0)) {   // exact reduction (first column, or cancellation)
+    if (EXACT || jj == 0) {
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-      for (int i = 0; i < RPL; i += 2) { s0 = fma(xr[i][jj], xr[i][jj], s0); s1 = fma(xr[i + 1][jj], xr[i + 1][jj], s1); }
+      for (int i = 0; i < 4; i += 2) { s0 = fma(xr[i][jj], xr[i][jj], s0); s1 = fma(xr[i + 1][jj], xr[i + 1][jj], s1); }
       s2 = warp_sum(s0 + s1);
     }
-    const double alpha = S[j * KT + j];
-    double beta = alpha, tj = 0.0, scal = 0.0;
-    if (s2 != 0.0) dlarfg_fast(alpha, s2, beta, tj, scal);
+    double beta, tj, scal;
+    dlarfg_nb(rrow[jj], s2, beta, tj, scal);
 #pragma unroll
-    for (int i = 0; i < RPL; ++i) xr[i][jj] *= scal;
+    for (int i = 0; i < 4; ++i) xr[i][jj] *= scal;
     double d[8];
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) {
       d[cc] = 0.0;
       if (cc != jj) {
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) d[cc] = fma(xr[i][jj], xr[i][cc], d[cc]);
+        for (int i = 0; i < 4; ++i) d[cc] = fma(xr[i][jj], xr[i][cc], d[cc]);
       } else if (jj + 1 < 8) {   // slot jj carries |x_{jj+1}|^2 (pre-update)
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) d[cc] = fma(xr[i][jj + 1], xr[i][jj + 1], d[cc]);
+        for (int i = 0; i < 4; ++i) d[cc] = fma(xr[i][jj + 1], xr[i][jj + 1], d[cc]);
       }
     }
     warp_sum8(d);
     if (jj + 1 < 8) {
-      // |x - w v|^2 = N - 2 w (x.v) + w^2 |v|^2, exact algebra; accept when at
-      // most half of N cancels (relative error stays ~u), else recompute.
       const double N = d[jj];
       const double vv = s2 * scal * scal;
-      const double w = tj * (d[jj + 1] + S[j * KT + j + 1]);
+      const double w = tj * (d[jj + 1] + rrow[jj + 1]);
       const double nn = fma(w * w, vv, fma(-2.0 * w, d[jj + 1], N));
-      s2n = (N > 0.0 && nn >= 0.5 * N) ? nn : -1.0;
+      bad = bad || !(nn >= 0.5 * N);
+      s2n = fmax(nn, 0.0);
     }
-    // T_p[0:jj, jj] = -tau T_p[0:jj, 0:jj] d[0:jj]   (lane ii owns row ii)
-    if (lane < jj) {
-      double sacc = 0.0;
-#pragma unroll
-      for (int l = 0; l < jj; ++l)
-        if (l >= lane) sacc = fma(T8[lane * 8 + l], d[l], sacc);
-      T8[lane * 8 + jj] = -tj * sacc;
-    }
+    double mine = 0.0;
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) {
       if (cc > jj) {
-        const double w = tj * (d[cc] + S[j * KT + j0 + cc]);
+        const double w = tj * (d[cc] + rrow[cc]);
 #pragma unroll
-        for (int i = 0; i < RPL; ++i) xr[i][cc] = fma(-w, xr[i][jj], xr[i][cc]);
-        __syncwarp();
-        if (lane == 0) S[j * KT + j0 + cc] -= w;
+        for (int i = 0; i < 4; ++i) xr[i][cc] = fma(-w, xr[i][jj], xr[i][cc]);
+        mine = (lane == cc) ? rrow[cc] - w : mine;
       } else if (cc < jj) {
-        if (lane == 0) S[j * KT + j0 + cc] = d[cc];  // G[j0+cc][j] in the lower part
+        mine = (lane == cc) ? d[cc] : mine;      // G[j0+cc][j] in the lower part
+      } else {
+        mine = (lane == cc) ? beta : mine;
       }
     }
-    __syncwarp();
-    if (lane == 0) { S[j * KT + j] = beta; tau_s[j] = tj; T8[jj * 8 + jj] = tj; }
-    __syncwarp();
-  }
-  // Householder vectors back into X (rows >= nb stay zero)
+    if (lane < 8) S[j * KT + j0 + lane] = mine;
+    // T_p[ii][jj] = -tau sum_{l=ii}^{jj-1} T_p[ii][l] G[l][jj]  (lane ii < 8)
+    double sacc = 0.0;
 #pragma unroll
-  for (int i = 0; i < RPL; ++i) {
-    const int r = lane + 32 * i;
-#pragma unroll
-    for (int c = 0; c < 8; ++c) Xs[swz(r, j0 + c, KT)] = (r < nb) ? xr[i][c] : 0.0;
+    for (int l = 0; l < jj; ++l) sacc = fma((l >= lr) ? trow[l] : 0.0, d[l], sacc);
+    trow[jj] = (lr == jj) ? tj : ((lr < jj) ? -tj * sacc : 0.0);
+    if (lane == jj) tau_s[j] = tj;
   }
+  if (lane < 8) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) T8[lane * 8 + l] = trow[l];
+  }
+  return bad;
 }
 
-// warp w applies panel p (w > p) or records the cross Gram block (w < p)
+// Panel factorization by the owning warp.  The panel is transposed through
+// its Y slot into the lane-per-row layout so that v stays lane-local and the
+// 7 dot products of a step are one reduce-scatter over the warp; the
+// Householder vectors go back to the slot (published Y_p) and to the quad
+// layout of the registers.
 template <int KT>
-__device__ __forceinline__ void panel_apply(int p, int w, double* S, double* Xs, const double* Tp,
-                                            double* sc) {
-  constexpr int B = BlkCfg<KT>::B;
+__device__ __forceinline__ void panel_factor(int p, double (&x)[16][2], double* S, double* Ys,
+                                             double* Tp, double* tau_s, double* save) {
+  constexpr int YS = BlkCfg<KT>::YS;
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int j0 = p * 8;
+#ifdef OTS_TIMING
+  long long pq = clock64();
+#define PMARK(slot) { long long _t = clock64(); if (lane == 0) atomicAdd(&g_dbg[slot], (unsigned long long)(_t - pq)); pq = _t; }
+#else
+#define PMARK(slot)
+#endif
+#pragma unroll
+  for (int f = 0; f < 16; ++f)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) Ys[(8 * f + 2 * t + h) * YS + g] = x[f][h];
+  // R rows of the panel (8 x 8 block) for a replay
+  save[lane] = S[(j0 + (lane >> 3)) * KT + j0 + (lane & 7)];
+  save[lane + 32] = S[(j0 + 4 + (lane >> 3)) * KT + j0 + (lane & 7)];
+  __syncwarp();
+  double xr[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) {
+      const double2 u = *reinterpret_cast<const double2*>(Ys + (lane + 32 * i) * YS + c);
+      xr[i][c] = u.x;
+      xr[i][c + 1] = u.y;
+    }
+  PMARK(8);
+  double* T8 = Tp + p * 64;
+  const bool bad = panel_core<KT, false>(p, xr, S, T8, tau_s);
+  PMARK(9);
+  if (__any_sync(0xffffffffu, bad)) {   // rare: replay with exact norms
+    __syncwarp();
+    S[(j0 + (lane >> 3)) * KT + j0 + (lane & 7)] = save[lane];
+    S[(j0 + 4 + (lane >> 3)) * KT + j0 + (lane & 7)] = save[lane + 32];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int c = 0; c < 8; c += 2) {
+        const double2 u = *reinterpret_cast<const double2*>(Ys + (lane + 32 * i) * YS + c);
+        xr[i][c] = u.x;
+        xr[i][c + 1] = u.y;
+      }
+    __syncwarp();
+    panel_core<KT, true>(p, xr, S, T8, tau_s);
+  }
+  __syncwarp();
+  // Y_p -> slot (published) -> quad-layout registers
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; c += 2)
+      *reinterpret_cast<double2*>(Ys + (lane + 32 * i) * YS + c) = make_double2(xr[i][c], xr[i][c + 1]);
+  __syncwarp();
+#pragma unroll
+  for (int f = 0; f < 16; ++f)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) x[f][h] = Ys[(8 * f + 2 * t + h) * YS + g];
+  PMARK(12);
+#undef PMARK
+}
+
+// warp w applies panel p to its register columns (w > p) or records the
+// Gram block G[w cols][p cols] (w < p)
+template <int KT>
+__device__ __forceinline__ void panel_apply(int p, int w, double (&x)[16][2], double* S, const double* Ys,
+                                            const double* Tp) {
+  constexpr int YS = BlkCfg<KT>::YS;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int j0 = p * 8, c0 = w * 8;
   double acc[4][2];
 #pragma unroll
   for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
-#pragma unroll 8
-  for (int kk = 0; kk < B / 4; ++kk) {
-    const int r = 4 * kk + t;
-    const double av = Xs[swz(r, c0 + g, KT)];   // A[m=g][k=t] = X[r][c0+g]
-    const double bv = Xs[swz(r, j0 + g, KT)];   // B[k=t][n=g] = Y[r][j0+g]
-    dmma(acc[kk & 3], av, bv);
+  // k index kk <-> tile row 8(kk>>1) + 2t + (kk&1): A = own registers
+#pragma unroll
+  for (int kk = 0; kk < 32; ++kk) {
+    const int r = 8 * (kk >> 1) + 2 * t + (kk & 1);
+    dmma(acc[kk & 3], x[kk >> 1][kk & 1], Ys[r * YS + g]);
   }
   double W0 = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
   double W1 = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
-  // W^T[c0+g][j0+2t(+1)]
-  if (w < p) {
-    S[(j0 + 2 * t) * KT + c0 + g] = W0;       // G[c][j] (c < j): lower part
-    S[(j0 + 2 * t + 1) * KT + c0 + g] = W1;
-    return;
-  }
-  W0 += S[(j0 + 2 * t) * KT + c0 + g];
-  W1 += S[(j0 + 2 * t + 1) * KT + c0 + g];
-  sc[g * 8 + 2 * t] = W0;
-  sc[g * 8 + 2 * t + 1] = W1;
-  __syncwarp();
-  // w^T = W^T T_p  (8 x 8 x 8)
-  double wt[2] = {0.0, 0.0};
+  // W^T[c0+g][j0+2t+h]
+  double* r0p = S + (j0 + 2 * t) * KT + c0 + g;
+  double* r1p = r0p + KT;
+  if (w < p) { *r0p = W0; *r1p = W1; return; }
+  W0 += *r0p;
+  W1 += *r1p;
+  // A operand W^T[g][k] for k = t and k = t+4 (lane quad holds k = 2t, 2t+1)
+  auto regather = [&](double e0, double e1, double& lo, double& hi) {
+    const int sl = 4 * g + (t >> 1), sh = sl + 2;
+    const double l0 = __shfl_sync(0xffffffffu, e0, sl), l1 = __shfl_sync(0xffffffffu, e1, sl);
+    const double h0 = __shfl_sync(0xffffffffu, e0, sh), h1 = __shfl_sync(0xffffffffu, e1, sh);
+    lo = (t & 1) ? l1 : l0;
+    hi = (t & 1) ? h1 : h0;
+  };
+  double alo, ahi;
+  regather(W0, W1, alo, ahi);
+  double o[2] = {0.0, 0.0};          // w^T[c0+g][j0+2t+h] = (W^T T_p)
+  dmma(o, alo, Tp[p * 64 + t * 8 + g]);
+  dmma(o, ahi, Tp[p * 64 + (t + 4) * 8 + g]);
+  *r0p -= o[0];
+  *r1p -= o[1];
+  regather(-o[0], -o[1], alo, ahi);
+  // X^T[c0+g][8f + n] -= sum_k w^T[g][k] Y[8f + n][j0 + k]
 #pragma unroll
-  for (int k0 = 0; k0 < 8; k0 += 4) dmma(wt, sc[g * 8 + k0 + t], Tp[p * 64 + (k0 + t) * 8 + g]);
-  __syncwarp();
-  sc[g * 8 + 2 * t] = wt[0];
-  sc[g * 8 + 2 * t + 1] = wt[1];
-  S[(j0 + 2 * t) * KT + c0 + g] -= wt[0];      // R rows of the panel
-  S[(j0 + 2 * t + 1) * KT + c0 + g] -= wt[1];
-  __syncwarp();
-  // X_w -= Y_p w :  b = w[k][n=g] = w^T[g][k]
-  const double b0 = sc[g * 8 + t], b1 = sc[g * 8 + 4 + t];
-#pragma unroll 4
-  for (int mf = 0; mf < B / 8; ++mf) {
-    const int r = 8 * mf + g;
-    double cfr[2] = {0.0, 0.0};
-    dmma(cfr, Xs[swz(r, j0 + t, KT)], b0);
-    dmma(cfr, Xs[swz(r, j0 + 4 + t, KT)], b1);
-    double* x0 = &Xs[swz(r, c0 + 2 * t, KT)];
-    double* x1 = &Xs[swz(r, c0 + 2 * t + 1, KT)];
-    *x0 -= cfr[0];
-    *x1 -= cfr[1];
+  for (int f = 0; f < 16; ++f) {
+    dmma(x[f], alo, Ys[(8 * f + g) * YS + t]);
+    dmma(x[f], ahi, Ys[(8 * f + g) * YS + 4 + t]);
   }
 }
 
@@ -440,7 +552,7 @@ __device__ __forceinline__ void build_t(const double* S, const double* Tp, doubl
 template <int KT>
 __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   using C = BlkCfg<KT>;
-  constexpr int B = C::B, NP = C::NP;
+  constexpr int NP = C::NP;
   extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
   double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
   double* Tp = Xs + C::XS;                        // NP x 64
@@ -464,23 +576,26 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   u_to_t_block<KT>(Xs, Xs + KT * (KT + 1), Tbase);
   __syncthreads();
 
-  // ---- structured tiles
+  // ---- structured tiles (register-resident, see BlkCfg)
+  const bool owner = warp < NP;
+  const int mycol = 8 * warp + ((tid & 31) >> 2);
+  double* Ys = Xs;                                  // 2 panel slots of Y
+  double x[16][2];
+  if (owner && ntiles > 0) {
+    const long g0 = r0 + KT;
+    const long rem0 = a.G.nrows - g0;
+    tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
+  }
   for (int t = 1; t <= ntiles; ++t) {
     const long gr0 = r0 + KT + (long)(t - 1) * b;
-    long rem = a.G.nrows - gr0;
+    const long rem = a.G.nrows - gr0;
     const int nb = (int)(rem < b ? rem : b);
-    TSTAMP(t0);
-    load_tile_async(Xs, KT, a.D, a.ldd, gr0, B, gr0, gr0 + nb, 0, KT, a.ncols, tid, 256);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
     TSTAMP(t1);
-    TACC(0, t0, t1);
     for (int p = 0; p < NP; ++p) {
 #ifdef OTS_TIMING
       long long q0 = clock64();
 #endif
-      if (warp == p) panel_factor<KT>(p, S, Xs, Tp, tau_s, nb);
+      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p & 1) * C::YSLOT, Tp, tau_s, scr + warp * 64);
 #ifdef OTS_TIMING
       if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
 #endif
@@ -488,7 +603,7 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
 #ifdef OTS_TIMING
       long long q1 = clock64();
 #endif
-      if (warp < NP && warp != p) panel_apply<KT>(p, warp, S, Xs, Tp, scr + warp * 64);
+      if (owner && warp != p) panel_apply<KT>(p, warp, x, S, Ys + (p & 1) * C::YSLOT, Tp);
 #ifdef OTS_TIMING
       if (warp == p + 1 && (tid & 31) == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - q1));
       if (tid == 0) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - q0));
@@ -497,15 +612,15 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     __syncthreads();
     TSTAMP(t2);
     TACC(1, t1, t2);
-    // Y (in place of the tile) -> global
-    for (int i = tid; i < nb * (KT / 2); i += 256) {
-      const int r = i / (KT / 2), u = i - r * (KT / 2), c = 2 * u;
-      if (c >= a.ncols) continue;
-      double* dst = a.D + (gr0 + r) * a.ldd + c;
-      if (c + 1 < a.ncols) *reinterpret_cast<double2*>(dst) = make_double2(Xs[swz(r, c, KT)], Xs[swz(r, c + 1, KT)]);
-      else dst[0] = Xs[swz(r, c, KT)];
+    // Y (in place of the tile) -> global; next tile -> registers
+    if (owner) {
+      tile_regs_store(x, a.D, a.ldd, gr0, nb, mycol, a.ncols);
+      if (t < ntiles) {
+        const long g1 = gr0 + b;
+        const long rem1 = a.G.nrows - g1;
+        tile_regs_load(x, a.D, a.ldd, g1, (int)(rem1 < b ? rem1 : b), mycol, a.ncols);
+      }
     }
-    __syncthreads();
     TSTAMP(t3);
     TACC(2, t2, t3);
     build_t<KT>(S, Tp, Xs, Tbase + (long)t * KT * KT, scr);

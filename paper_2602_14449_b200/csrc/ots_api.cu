@@ -21,6 +21,7 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "small.cuh"
@@ -178,6 +179,17 @@ struct Job {
 
 namespace {
 
+// level-0 chains per SM (2 = the two CTAs an SM holds); OTS_CHAINS_PER_SM
+// overrides it for experiments
+long chains_per_sm() {
+  static long v = [] {
+    const char* e = getenv("OTS_CHAINS_PER_SM");
+    long x = e ? atol(e) : 2;
+    return x >= 1 ? x : 2;
+  }();
+  return v;
+}
+
 std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, long m, int KT, int nsm) {
   std::vector<Level> lv;
   // level 0
@@ -186,7 +198,7 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     L.D = D0; L.ldd = ldd0; L.ncols = ncols0;
     int b = chain_bmax(KT);
     if (b > 128 && KT == 64) b = 128;
-    long target = 2L * nsm;
+    long target = chains_per_sm() * nsm;
     long per = (m + target - 1) / target;
     long Lt = per > KT ? (per - KT + b - 1) / b : 0;
     long rpc = KT + Lt * b;
@@ -218,7 +230,7 @@ size_t plan_levels_bytes(long m, int KT, int nsm) {
   size_t tot = 0;
   int b = chain_bmax(KT);
   if (b > 128 && KT == 64) b = 128;
-  long target = 2L * nsm;
+  long target = chains_per_sm() * nsm;
   long per = (m + target - 1) / target;
   long Lt = per > KT ? (per - KT + b - 1) / b : 0;
   long rpc = KT + Lt * b;

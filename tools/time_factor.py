@@ -15,5 +15,5 @@ print(NT.profile(ctx))
 NT.lib().ots_debug_counters(buf, 0)
 tiles = buf[4]
 print("tiles", tiles)
-for i, nm in enumerate(["load", "sweep", "store", "tinv", "ntile", "pfact", "apply_nxt", "thread0_panel", "pf_load", "pf_loop"]):
+for i, nm in enumerate(["load", "sweep", "store", "tinv", "ntile", "pfact", "apply_nxt", "thread0_panel", "pf_load", "pf_dlarfg", "pf_dots", "pf_update", "pf_store"]):
     print(f"{nm:6s} {buf[i] / max(tiles,1):12.0f} cycles/tile")
