@@ -3,7 +3,7 @@ NVCC ?= nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 FLAGS := -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr $(ARCH)
 SRC := $(wildcard paper_2602_14449_b200/csrc/*.cu)
-HDR := $(wildcard paper_2602_14449_b200/csrc/*.cuh) include/ots.h
+HDR := $(wildcard paper_2602_14449_b200/csrc/*.cuh) $(wildcard paper_2602_14449_b200/csrc/*.inc) include/ots.h
 LIB := paper_2602_14449_b200/libots.so
 
 all: $(LIB)

@@ -97,6 +97,25 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,
                            const double* A, int64_t lda, double* Q, int64_t ldq,
                            double* R, int64_t ldr, int nonneg_diag, void* stream);
 
+/* complex128 variants (configs[3] of BASELINE.json).  Complex arrays are
+ * interleaved (re, im) double pairs, row-major, leading dimensions in complex
+ * elements, 16-byte aligned.
+ *
+ * two_stage_qr(v, a, choice, intra="householder", p) -- twostage.py:57-97
+ * on c128 data (zgeqrf/zungqr semantics for the intra QR, LAPACK zlarfg
+ * signs: R real diagonal).  k <= 64, k0 <= 256. */
+int ots_two_stage_c128(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                       const void* V, int64_t ldv, const void* A, int64_t lda,
+                       int choice, int intra, const void* P, int64_t ldp,
+                       double orth_tol, int allow_defect,
+                       void* Q, int64_t ldq, void* R, int64_t ldr,
+                       void* S, int64_t lds, double* diag_host, void* stream);
+
+/* householder_qr(a, nonneg_diag)                  -- core.py:61-84, c128 */
+int ots_householder_qr_c128(ots_ctx* ctx, int64_t m, int64_t k,
+                            const void* A, int64_t lda, void* Q, int64_t ldq,
+                            void* R, int64_t ldr, int nonneg_diag, void* stream);
+
 /* shifted_cholesky_qr(a)                          -- core.py:177-202
  * shifted CholeskyQR + 2 refinements; NotPositiveDefinite on breakdown. */
 int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,

@@ -89,6 +89,37 @@ def to_device(x, device):
     return d
 
 
+def cempty(rows, cols, device):
+    """complex128 row-major device matrix (ld in complex elements)."""
+    t = torch()
+    return DMat(t.empty((max(rows, 1), max(cols, 1)), dtype=t.complex128, device=f"cuda:{device}"), cols)
+
+
+def czeros(rows, cols, device):
+    t = torch()
+    return DMat(t.zeros((max(rows, 1), max(cols, 1)), dtype=t.complex128, device=f"cuda:{device}"), cols)
+
+
+def cto_device(x, device):
+    """numpy (or torch) matrix -> complex128 DMat on `device` (zero-copy for a
+    row-major CUDA complex128 tensor)."""
+    t = torch()
+    if is_torch(x):
+        if x.dtype != t.complex128:
+            x = x.to(t.complex128)
+        if x.is_cuda and x.device.index == device and x.dim() == 2 and x.stride(1) == 1 \
+                and x.data_ptr() % 16 == 0 and x.stride(0) >= x.shape[1]:
+            return DMat(x, x.shape[1], ld=x.stride(0))
+        src = x
+    else:
+        src = t.from_numpy(np.ascontiguousarray(x, dtype=np.complex128))
+    rows, cols = src.shape
+    d = cempty(rows, cols, device)
+    if rows and cols:
+        d.buf[:rows, :cols].copy_(src, non_blocking=False)
+    return d
+
+
 def stream_ptr(device):
     return C.c_void_p(torch().cuda.current_stream(device).cuda_stream)
 

@@ -68,10 +68,17 @@ def householder_qr(a, nonneg_diag=False):
         raise E.DimensionError(f"need rows >= cols, got {m}x{n}")
     if not all_finite(a):
         raise ValueError("input contains non-finite entries")
-    if is_complex(a):
-        raise NotImplementedError("complex householder_qr: not in this build")
     dev = D.pick_device(a)
     ctx = D.ctx(dev)
+    if is_complex(a):
+        A = D.cto_device(a, dev)
+        Q = D.cempty(m, n, dev)
+        R = D.czeros(n, n, dev)
+        if n:
+            rc = lib().ots_householder_qr_c128(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
+                                               1 if nonneg_diag else 0, D.stream_ptr(dev))
+            check(rc, ctx)
+        return QRPair(out_like(was_torch, Q), out_like(was_torch, R))
     A = D.to_device(a, dev)
     Q = D.empty(m, n, dev)
     R = D.zeros(n, n, dev)

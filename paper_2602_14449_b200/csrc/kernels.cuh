@@ -54,6 +54,13 @@ cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, i
 cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
 cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
+// complex128 TSQR (zchain.cu): same argument records, pointers to interleaved
+// (re, im) data, leading dimensions in complex units
+using ZFactorArgs = FactorArgs;
+using ZQformArgs = QformArgs;
+cudaError_t launch_zchain_factor(const ZFactorArgs& a, int KT, cudaStream_t st);
+cudaError_t launch_zchain_qform(const ZQformArgs& a, int KT, cudaStream_t st);
+int zchain_bmax();
 int chain_bmax(int KT);
 int debug_counters(unsigned long long* out, int reset);
 

@@ -41,21 +41,51 @@ __global__ void set_identity_kernel(double* D, int n) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n * n) D[i] = (i / n == i % n) ? 1.0 : 0.0;
 }
-__global__ void nonneg_fix_kernel(double* Q, long ldq, long m, int k, double* R, long ldr) {
-  // core.py:75-83 phase fix for real: column sign of R diag (0 -> +1)
+// core.py:75-83 phase fix for real: Q columns times sign(R_jj) (0 -> +1),
+// then (second launch, one block) R rows likewise with |R_jj| on the diagonal
+// -- two launches so no block reads a diagonal another block already rewrote.
+__global__ void nonneg_q_kernel(double* Q, long ldq, long m, int k, const double* R, long ldr) {
   __shared__ double ph[64];
   for (int j = threadIdx.x; j < k; j += blockDim.x) ph[j] = (R[j * ldr + j] < 0.0) ? -1.0 : 1.0;
   __syncthreads();
-  if (blockIdx.x == 0)
-    for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
-      int i = e / k, j = e - i * k;
-      double v = R[i * ldr + j] * ph[i];
-      if (i == j) v = fabs(R[i * ldr + j]);
-      R[i * ldr + j] = v;
-    }
   for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += (long)gridDim.x * blockDim.x) {
     long i = e / k; int j = (int)(e - i * k);
     Q[i * ldq + j] *= ph[j];
+  }
+}
+__global__ void nonneg_r_kernel(int k, double* R, long ldr) {
+  __shared__ double ph[64];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ph[j] = (R[j * ldr + j] < 0.0) ? -1.0 : 1.0;
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    int i = e / k, j = e - i * k;
+    R[i * ldr + j] = (i == j) ? fabs(R[i * ldr + j]) : R[i * ldr + j] * ph[i];
+  }
+}
+// complex: ph_j = R_jj / |R_jj| (1 for 0); Q <- Q diag(ph), R <- diag(conj ph) R
+__device__ __forceinline__ double2 zphase(double2 d) {
+  const double mg = hypot(d.x, d.y);
+  return (mg != 0.0) ? make_double2(d.x / mg, d.y / mg) : make_double2(1.0, 0.0);
+}
+__global__ void zc_nonneg_q_kernel(double2* Q, long ldq, long m, int k, const double2* R, long ldr) {
+  __shared__ double2 ph[64];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ph[j] = zphase(R[j * ldr + j]);
+  __syncthreads();
+  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < m * k; e += (long)gridDim.x * blockDim.x) {
+    long i = e / k; int j = (int)(e - i * k);
+    const double2 q = Q[i * ldq + j], p = ph[j];
+    Q[i * ldq + j] = make_double2(q.x * p.x - q.y * p.y, q.x * p.y + q.y * p.x);
+  }
+}
+__global__ void zc_nonneg_r_kernel(int k, double2* R, long ldr) {
+  __shared__ double2 ph[64];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) ph[j] = zphase(R[j * ldr + j]);
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
+    int i = e / k, j = e - i * k;
+    const double2 r = R[i * ldr + j], p = ph[i];
+    R[i * ldr + j] = (i == j) ? make_double2(hypot(r.x, r.y), 0.0)
+                              : make_double2(r.x * p.x + r.y * p.y, r.y * p.x - r.x * p.y);
   }
 }
 
@@ -928,7 +958,10 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, 
   a.B = Q; a.ldb = ldq; a.X = Q; a.ldx = ldq; a.ncols = (int)k;
   a.row_begin = 0; a.row_end = m; a.colscale = j.svec;
   CK(launch_tsgemm_nn(a, KT, ctx->nsm, st));
-  if (nonneg_diag) nonneg_fix_kernel<<<std::min<long>(1024, (m * k + 255) / 256), 256, 0, st>>>(Q, ldq, m, (int)k, R, ldr);
+  if (nonneg_diag) {
+    nonneg_q_kernel<<<std::min<long>(1024, (m * k + 255) / 256), 256, 0, st>>>(Q, ldq, m, (int)k, R, ldr);
+    nonneg_r_kernel<<<1, 256, 0, st>>>((int)k, R, ldr);
+  }
   prof_mark(ctx, st, "sign");
   ctx->launches = 3 + 3 * (int)j.lv.size() + (nonneg_diag ? 1 : 0);
   CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1201,3 +1234,5 @@ int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign, doub
 }
 
 }  // extern "C"
+
+#include "zpath.inc"

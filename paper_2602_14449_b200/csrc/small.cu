@@ -643,6 +643,68 @@ __device__ void t_solve_core(const SmallState& s, const double* F, int ld, doubl
 // ---------------------------------------------------------------------------
 
 // Seed: Gram check, P/T construction, W_top, Z1 = T^{-T}(W^T A), S = P^T (H^T A)_top
+// polar V_t = U H via one-sided Jacobi SVD (core.py:108-120):
+// P = -U, Tdense = T = I + H, Tf = chol(T).  Returns a status code.
+__device__ int seed_polar(const SmallState& s, double* red) {
+  const int n = s.k0, ld = s.ld;
+  int st = 0;
+  // rows of X1 := columns of V_t ; X2 := I (accumulates J^T)
+  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = s.Vt[j * ld + i]; }
+  blk_identity(s.X2, ld, n);
+  __syncthreads();
+  blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
+  // U columns u_j = X1 row j / sigma_j (null directions: v_j orthogonalised)
+  // store U^T rows in X1 (normalised)
+  BLK_FOR(e, n * n) {
+    int j = e / n, c = e - j * n;
+    double sg = s.sig[j];
+    if (sg > 0.0) s.X1[j * ld + c] /= sg;
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (s.sig[j] > 0.0) continue;
+    // u = v_j - sum_{i != j, done} (u_i . v_j) u_i, normalise
+    BLK_FOR(c, n) s.X1[j * ld + c] = s.X2[j * ld + c];
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass)
+      for (int i = 0; i < n; ++i) {
+        if (i == j || (s.sig[i] == 0.0 && i > j)) continue;
+        double d = 0.0;
+        for (int c = threadIdx.x; c < n; c += blockDim.x) d = fma(s.X1[i * ld + c], s.X1[j * ld + c], d);
+        d = block_sum(d, red);
+        BLK_FOR(c, n) s.X1[j * ld + c] -= d * s.X1[i * ld + c];
+        __syncthreads();
+      }
+    double nn = 0.0;
+    for (int c = threadIdx.x; c < n; c += blockDim.x) nn = fma(s.X1[j * ld + c], s.X1[j * ld + c], nn);
+    nn = sqrt(block_sum(nn, red));
+    BLK_FOR(c, n) s.X1[j * ld + c] /= nn;
+    __syncthreads();
+  }
+  // Up = U V^T = sum_j u_j v_j^T ; H = V diag(sigma) V^T
+  BLK_FOR(e, n * n) {
+    int a = e / n, b = e - a * n;
+    double up = 0.0, h = 0.0;
+    for (int j = 0; j < n; ++j) {
+      up = fma(s.X1[j * ld + a], s.X2[j * ld + b], up);
+      h = fma(s.X2[j * ld + a] * s.sig[j], s.X2[j * ld + b], h);
+    }
+    s.P[a * ld + b] = -up;
+    s.Tdense[a * ld + b] = h;
+  }
+  __syncthreads();
+  BLK_FOR(e, n * n) {  // symmetrise H, T = I + H
+    int a = e / n, b = e - a * n;
+    double h = 0.5 * (s.Tdense[a * ld + b] + s.Tdense[b * ld + a]);
+    s.Tf[a * ld + b] = h + (a == b ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  blk_copy(s.Tdense, ld, s.Tf, ld, n, n);
+  __syncthreads();
+  if (!blk_cholesky(s.Tf, ld, n, red)) st = OTS_E_NOT_PD;
+  return st;
+}
+
 __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
   __shared__ double red[64];
   __shared__ int ired[64];
@@ -732,64 +794,9 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
       }
       break;
     }
-    case CHOICE_POLAR: {
-      // polar V_t = U H via one-sided Jacobi SVD (core.py:108-120)
-      // rows of X1 := columns of V_t ; X2 := I (accumulates J^T)
-      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = s.Vt[j * ld + i]; }
-      blk_identity(s.X2, ld, n);
-      __syncthreads();
-      blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
-      // U columns u_j = X1 row j / sigma_j (null directions: v_j orthogonalised)
-      // store U^T rows in X1 (normalised)
-      BLK_FOR(e, n * n) {
-        int j = e / n, c = e - j * n;
-        double sg = s.sig[j];
-        if (sg > 0.0) s.X1[j * ld + c] /= sg;
-      }
-      __syncthreads();
-      for (int j = 0; j < n; ++j) {
-        if (s.sig[j] > 0.0) continue;
-        // u = v_j - sum_{i != j, done} (u_i . v_j) u_i, normalise
-        BLK_FOR(c, n) s.X1[j * ld + c] = s.X2[j * ld + c];
-        __syncthreads();
-        for (int pass = 0; pass < 2; ++pass)
-          for (int i = 0; i < n; ++i) {
-            if (i == j || (s.sig[i] == 0.0 && i > j)) continue;
-            double d = 0.0;
-            for (int c = threadIdx.x; c < n; c += blockDim.x) d = fma(s.X1[i * ld + c], s.X1[j * ld + c], d);
-            d = block_sum(d, red);
-            BLK_FOR(c, n) s.X1[j * ld + c] -= d * s.X1[i * ld + c];
-            __syncthreads();
-          }
-        double nn = 0.0;
-        for (int c = threadIdx.x; c < n; c += blockDim.x) nn = fma(s.X1[j * ld + c], s.X1[j * ld + c], nn);
-        nn = sqrt(block_sum(nn, red));
-        BLK_FOR(c, n) s.X1[j * ld + c] /= nn;
-        __syncthreads();
-      }
-      // Up = U V^T = sum_j u_j v_j^T ; H = V diag(sigma) V^T
-      BLK_FOR(e, n * n) {
-        int a = e / n, b = e - a * n;
-        double up = 0.0, h = 0.0;
-        for (int j = 0; j < n; ++j) {
-          up = fma(s.X1[j * ld + a], s.X2[j * ld + b], up);
-          h = fma(s.X2[j * ld + a] * s.sig[j], s.X2[j * ld + b], h);
-        }
-        s.P[a * ld + b] = -up;
-        s.Tdense[a * ld + b] = h;
-      }
-      __syncthreads();
-      BLK_FOR(e, n * n) {  // symmetrise H, T = I + H
-        int a = e / n, b = e - a * n;
-        double h = 0.5 * (s.Tdense[a * ld + b] + s.Tdense[b * ld + a]);
-        s.Tf[a * ld + b] = h + (a == b ? 1.0 : 0.0);
-      }
-      __syncthreads();
-      blk_copy(s.Tdense, ld, s.Tf, ld, n, n);
-      __syncthreads();
-      if (!blk_cholesky(s.Tf, ld, n, red)) st = OTS_E_NOT_PD;
+    case CHOICE_POLAR:
+      st = seed_polar(s, red);
       break;
-    }
     case CHOICE_EXPLICIT: {
       blk_copy(s.P, ld, s.Pexp, s.ldpe, n, n);
       __syncthreads();
@@ -1085,5 +1092,7 @@ void debug_counters_small(unsigned long long* out, int reset) {
   (void)out; (void)reset;
 #endif
 }
+
+#include "zsmall.inc"
 
 }  // namespace ots

@@ -34,7 +34,31 @@ struct SmallState {
   int* status;                 // [0] = status code
 };
 
+// complex128 k0 x k0 state (zsmall.inc).  Complex matrices are interleaved
+// double2 arrays (ld in complex units); `r` is the stacked real embedding
+// (k0' = 2 k0, choice EXPLICIT = pivoted LU of phi(T)) used for the T-solves
+// and the diagnostics kernel.
+struct ZState {
+  int k0, k, ldc;
+  int choice, allow_defect;
+  double orth_tol;
+  const double2* V; long ldv;       // top k0 rows of V, A (device)
+  const double2* A; long lda;
+  const double* Gr; long ldgr;      // real Gram of the interleaved V view (lower valid)
+  const double* VbAr; long ldvba;   // real V_b'^T A_b' (2k0 x 2k)
+  const double2* Pexp; int ldpe;
+  double2 *G, *Vt, *At, *VbA, *P, *T, *Wt, *Z1, *Z2, *W1, *W2, *tau;
+  double *Z1x, *Z2x; int ldzx;      // interleaved real expansions (2k0 x 2k)
+  double *svec, *svec2;             // sign recovery (k), per real column (2k)
+  double2* Sout; int lds_out;
+  SmallState r;
+};
+
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st);
+cudaError_t launch_zseed(const ZState& z, cudaStream_t st);
+cudaError_t launch_zz2(const ZState& z, const double* Y2r, long ldy, void* Qtop, long ldq, cudaStream_t st);
+cudaError_t launch_zsign(const ZState& z, const void* Qtop, long ldq, const void* Rfin, int ldr, void* Rout,
+                         long ldro, cudaStream_t st);
 cudaError_t launch_diag(const SmallState& s, cudaStream_t st);
 cudaError_t launch_z2(const SmallState& s, cudaStream_t st);
 cudaError_t launch_refl_apply(const SmallState& s, int adjoint, cudaStream_t st);

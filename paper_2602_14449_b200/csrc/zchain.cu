@@ -1,0 +1,372 @@
+// complex128 intra-block Householder QR (zgeqrf + zungqr semantics behind
+// `householder_qr`, core.py:61-84, for complex input; twostage.py:93).
+//
+// Same flat-chain TSQR structure as the real path (chainqr.cu): a chain owns
+// rows [c*RPC, (c+1)*RPC), a KT-row head is factored by a plain Householder
+// QR, then L structured tiles QR([R; tile]) with reflectors v_j = [e_j; y_j];
+// a tree over the chain R's; Q formed in reverse.  Reflectors follow zlarfg
+// (beta real, tau complex) and are applied as H^H = I - conj(tau) v v^H, so
+// Q = H_1 H_2 ... = I - V T V^H with the zlarft forward T.  Arithmetic is
+// FP64 on CUDA cores (no complex tensor-core MMA exists); this path serves
+// the complex configuration (BASELINE configs[3]), not the headline.
+//
+// Data: interleaved (re, im) row-major, leading dimensions in complex units.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace ots {
+
+namespace {
+
+typedef double2 cplx;
+__device__ __forceinline__ cplx cmk(double r, double i) { return make_double2(r, i); }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cmk(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return cmk(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return cmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }
+// a * b + c
+__device__ __forceinline__ cplx cfma(cplx a, cplx b, cplx c) {
+  return cmk(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+// conj(a) * b + c
+__device__ __forceinline__ cplx cfmac(cplx a, cplx b, cplx c) {
+  return cmk(fma(a.x, b.x, fma(a.y, b.y, c.x)), fma(a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+__device__ __forceinline__ cplx conjc(cplx a) { return cmk(a.x, -a.y); }
+__device__ __forceinline__ cplx cneg(cplx a) { return cmk(-a.x, -a.y); }
+__device__ __forceinline__ cplx crecip(cplx b) {
+  const double d = b.x * b.x + b.y * b.y;
+  return cmk(b.x / d, -b.y / d);
+}
+__device__ __forceinline__ cplx cshfl_xor(unsigned mask, cplx v, int o) {
+  return cmk(__shfl_xor_sync(mask, v.x, o), __shfl_xor_sync(mask, v.y, o));
+}
+
+template <int KT>
+struct ZCfg {
+  static constexpr int NT = 256;
+  static constexpr int B = 64;            // structured tile rows (BMAX)
+  static constexpr int TPC = NT / KT;     // threads per column
+  static constexpr int LDS = KT + 1;      // smem row stride (complex units)
+  static constexpr int ROWS = KT + B;     // R rows + tile rows
+  static constexpr int UL = KT + 1;
+  static constexpr int SMEM = (ROWS * LDS + KT * UL + KT) * 16;
+};
+
+template <int TPC>
+__device__ __forceinline__ double gsum(double v, unsigned mask) {
+#pragma unroll
+  for (int o = TPC / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+template <int TPC>
+__device__ __forceinline__ cplx gsumc(cplx v, unsigned mask) {
+#pragma unroll
+  for (int o = TPC / 2; o > 0; o >>= 1) v = cadd(v, cshfl_xor(mask, v, o));
+  return v;
+}
+
+// rows [s0, s0+nr) of the smem block <- global rows [gr0, gr0+nr) (zero
+// beyond nrows / ncols)
+template <int KT>
+__device__ void zload_rows(cplx* A, int s0, const cplx* D, long ldd, long gr0, int nr, long nrows, int ncols) {
+  constexpr int LDS = ZCfg<KT>::LDS;
+  for (int e = threadIdx.x; e < nr * KT; e += blockDim.x) {
+    const int r = e / KT, c = e - r * KT;
+    const long gr = gr0 + r;
+    A[(s0 + r) * LDS + c] = (gr < nrows && c < ncols) ? D[gr * ldd + c] : cmk(0.0, 0.0);
+  }
+}
+template <int KT>
+__device__ void zstore_rows(const cplx* A, int s0, cplx* D, long ldd, long gr0, int nr, long nrows, int ncols) {
+  constexpr int LDS = ZCfg<KT>::LDS;
+  for (int e = threadIdx.x; e < nr * KT; e += blockDim.x) {
+    const int r = e / KT, c = e - r * KT;
+    const long gr = gr0 + r;
+    if (gr < nrows && c < ncols) D[gr * ldd + c] = A[(s0 + r) * LDS + c];
+  }
+}
+
+// One Householder sweep over the KT columns of the smem block A.
+//  HEAD : plain QR of rows 0..KT-1 (reflector j spans rows j..KT-1)
+//  !HEAD: rows 0..KT-1 hold R (upper, zero below), rows KT..KT+nb-1 the
+//         tile; reflector j = [e_j; y_j] spans row j and the tile rows.
+// U[c][j] = v_c^H v_j (c < j), U[j][j] = tau_j.
+template <int KT, bool HEAD>
+__device__ void zsweep(cplx* A, int nb, cplx* U, cplx* tau_s) {
+  using C = ZCfg<KT>;
+  constexpr int TPC = C::TPC, LDS = C::LDS, UL = C::UL;
+  const int tid = threadIdx.x;
+  const int c = tid / TPC, q = tid % TPC;
+  const unsigned gmask = (TPC >= 32) ? 0xffffffffu : (((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1)));
+  auto rbeg = [&](int j) { return HEAD ? (j + 1 + q) : (KT + q); };
+  const int rend = HEAD ? KT : (KT + nb);
+
+  auto phase_a = [&](int j) {   // owners of column j: zlarfg
+    double s2 = 0.0;
+    for (int r = rbeg(j); r < rend; r += TPC) { const cplx x = A[r * LDS + j]; s2 = fma(x.x, x.x, fma(x.y, x.y, s2)); }
+    s2 = gsum<TPC>(s2, gmask);
+    const cplx alpha = A[j * LDS + j];
+    cplx tau = cmk(0.0, 0.0);
+    cplx beta = alpha;
+    if (s2 != 0.0 || alpha.y != 0.0) {
+      const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
+      tau = cmk((bt - alpha.x) / bt, -alpha.y / bt);
+      const cplx scal = crecip(csub(alpha, cmk(bt, 0.0)));
+      for (int r = rbeg(j); r < rend; r += TPC) A[r * LDS + j] = cmul(A[r * LDS + j], scal);
+      beta = cmk(bt, 0.0);
+    }
+    if (q == 0) { A[j * LDS + j] = beta; tau_s[j] = tau; }
+  };
+
+  if (c == 0) phase_a(0);
+  __syncthreads();
+  for (int j = 0; j < KT; ++j) {
+    const cplx tj = tau_s[j];
+    if (c != j) {
+      // d = sum over reflector rows of conj(v_r) a_c  (v_j = 1 at row j)
+      cplx d = cmk(0.0, 0.0);
+      for (int r = rbeg(j); r < rend; r += TPC) d = cfmac(A[r * LDS + j], A[r * LDS + c], d);
+      d = gsumc<TPC>(d, gmask);
+      if (c > j) {
+        d = cadd(d, A[j * LDS + c]);
+        const cplx w = cmul(conjc(tj), d);           // conj(tau) v^H a
+        for (int r = rbeg(j); r < rend; r += TPC) A[r * LDS + c] = csub(A[r * LDS + c], cmul(w, A[r * LDS + j]));
+        if (q == 0) A[j * LDS + c] = csub(A[j * LDS + c], w);
+        if (c == j + 1) {
+          __syncwarp(gmask);
+          phase_a(j + 1);
+        }
+      } else {
+        // d = v_j^H v_c over the tile rows; the head adds v_c[j] * 1
+        // (v_c[j] = A[j][c]).  U[c][j] = v_c^H v_j = conj(d).
+        if (HEAD) d = cadd(d, A[j * LDS + c]);
+        if (q == 0) U[c * UL + j] = conjc(d);
+      }
+    } else {
+      if (q == 0) U[j * UL + j] = tj;
+    }
+    __syncthreads();
+  }
+}
+
+// T (zlarft forward, columnwise) from U; T -> global Tg (KT x KT, row-major)
+template <int KT>
+__device__ void zu_to_t(cplx* U, cplx* Tg) {
+  constexpr int UL = ZCfg<KT>::UL;
+  // in place in U: column j of T over rows i < j uses T[i][l] (l < j, already
+  // final in U's upper part; U[i][i] = tau_i = T[i][i]) and U[l][j] (column j
+  // still holds Gram entries); the new column is written after a barrier.
+  for (int j = 1; j < KT; ++j) {
+    const cplx tj = U[j * UL + j];
+    cplx val = cmk(0.0, 0.0);
+    const int i = threadIdx.x;
+    if (i < j) {
+      cplx s = cmk(0.0, 0.0);
+      for (int l = i; l < j; ++l) s = cfma(U[i * UL + l], U[l * UL + j], s);
+      val = cneg(cmul(tj, s));
+    }
+    __syncthreads();
+    if (i < j) U[i * UL + j] = val;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int i = e / KT, j = e - i * KT;
+    Tg[e] = (j >= i) ? U[i * UL + j] : cmk(0.0, 0.0);
+  }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(256, 1) zchain_factor_kernel(ZFactorArgs a) {
+  using C = ZCfg<KT>;
+  constexpr int LDS = C::LDS, UL = C::UL;
+  extern __shared__ __align__(16) unsigned char zsm_raw[];
+  cplx* A = reinterpret_cast<cplx*>(zsm_raw);
+  cplx* U = A + C::ROWS * LDS;
+  cplx* tau_s = U + KT * UL;
+  const cplx* D0 = reinterpret_cast<const cplx*>(a.D);
+  cplx* D = reinterpret_cast<cplx*>(a.D);
+  const int chain = blockIdx.x;
+  const long r0 = (long)chain * a.G.rpc;
+  const int b = a.G.b;
+  long rem0 = a.G.nrows - (r0 + KT);
+  int ntiles = 0;
+  if (rem0 > 0) { long t = (rem0 + b - 1) / b; ntiles = (int)(t < a.G.L ? t : a.G.L); }
+  cplx* Tbase = reinterpret_cast<cplx*>(a.U) + (long)chain * (a.G.L + 1) * KT * KT;
+
+  // head
+  zload_rows<KT>(A, 0, D0, a.ldd, r0, KT, a.G.nrows, a.ncols);
+  __syncthreads();
+  zsweep<KT, true>(A, 0, U, tau_s);
+  zstore_rows<KT>(A, 0, D, a.ldd, r0, KT, a.G.nrows, a.ncols);
+  __syncthreads();
+  zu_to_t<KT>(U, Tbase);
+  // R region: zero the strictly lower part (the head's vectors are stored)
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int i = e / KT, j = e - i * KT;
+    if (j < i) A[i * LDS + j] = cmk(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int t = 1; t <= ntiles; ++t) {
+    const long gr0 = r0 + KT + (long)(t - 1) * b;
+    const long rem = a.G.nrows - gr0;
+    const int nb = (int)(rem < b ? rem : b);
+    zload_rows<KT>(A, KT, D0, a.ldd, gr0, C::B, gr0 + nb, a.ncols);
+    __syncthreads();
+    zsweep<KT, false>(A, nb, U, tau_s);
+    zstore_rows<KT>(A, KT, D, a.ldd, gr0, nb, a.G.nrows, a.ncols);
+    __syncthreads();
+    zu_to_t<KT>(U, Tbase + (long)t * KT * KT);
+    __syncthreads();
+  }
+  cplx* R = reinterpret_cast<cplx*>(a.Rout) + (long)chain * KT * KT;
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int i = e / KT, j = e - i * KT;
+    R[e] = (j >= i) ? A[i * LDS + j] : cmk(0.0, 0.0);
+  }
+}
+
+// M = T C  (T upper triangular, global; C smem)  into smem M
+template <int KT>
+__device__ void z_tc(const cplx* T, const cplx* Cs, cplx* Ms) {
+  constexpr int LDS = ZCfg<KT>::LDS;
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int i = e / KT, j = e - i * KT;
+    cplx s = cmk(0.0, 0.0);
+    for (int l = i; l < KT; ++l) s = cfma(T[i * KT + l], Cs[l * LDS + j], s);
+    Ms[i * LDS + j] = s;
+  }
+}
+
+// Reverse chain walk: per structured tile (reverse)  M = T C, out = -Y M,
+// C <- C - M;  head: W1 = Yh^H C, M = Th W1, out = C - Yh M.
+template <int KT>
+__global__ void __launch_bounds__(256, 1) zchain_qform_kernel(ZQformArgs a) {
+  using C = ZCfg<KT>;
+  constexpr int LDS = C::LDS;
+  extern __shared__ __align__(16) unsigned char zsm_raw[];
+  cplx* Cs = reinterpret_cast<cplx*>(zsm_raw);
+  cplx* Ms = Cs + KT * LDS;
+  cplx* Ys = Ms + KT * LDS;      // 32-row chunk
+  cplx* D = reinterpret_cast<cplx*>(a.D);
+  const int chain = blockIdx.x;
+  const long r0 = (long)chain * a.G.rpc;
+  const int b = a.G.b;
+  long rem0 = a.G.nrows - (r0 + KT);
+  int ntiles = 0;
+  if (rem0 > 0) { long t = (rem0 + b - 1) / b; ntiles = (int)(t < a.G.L ? t : a.G.L); }
+  const cplx* Tbase = reinterpret_cast<const cplx*>(a.T) + (long)chain * (a.G.L + 1) * KT * KT;
+  const cplx* Cin = reinterpret_cast<const cplx*>(a.Cin) + (long)chain * KT * KT;
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int i = e / KT, j = e - i * KT;
+    Cs[i * LDS + j] = Cin[e];
+  }
+  __syncthreads();
+  for (int t = ntiles; t >= 1; --t) {
+    const long gr0 = r0 + KT + (long)(t - 1) * b;
+    const long rem = a.G.nrows - gr0;
+    const int nb = (int)(rem < b ? rem : b);
+    z_tc<KT>(Tbase + (long)t * KT * KT, Cs, Ms);
+    __syncthreads();
+    for (int c0 = 0; c0 < nb; c0 += 32) {
+      const int nr = (nb - c0 < 32) ? nb - c0 : 32;
+      for (int e = threadIdx.x; e < nr * KT; e += blockDim.x) {
+        const int r = e / KT, c = e - r * KT;
+        Ys[r * LDS + c] = (c < a.ncols) ? D[(gr0 + c0 + r) * a.ldd + c] : cmk(0.0, 0.0);
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < nr * KT; e += blockDim.x) {
+        const int r = e / KT, c = e - r * KT;
+        cplx s = cmk(0.0, 0.0);
+        for (int l = 0; l < KT; ++l) s = cfma(Ys[r * LDS + l], Ms[l * LDS + c], s);
+        if (c < a.ncols) D[(gr0 + c0 + r) * a.ldd + c] = cneg(s);
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+      const int i = e / KT, j = e - i * KT;
+      Cs[i * LDS + j] = csub(Cs[i * LDS + j], Ms[i * LDS + j]);
+    }
+    __syncthreads();
+  }
+  // head rows [r0, r0+KT): Yh unit lower (strictly lower part of the stored head)
+  const int hn = (int)((a.G.nrows - r0) < KT ? (a.G.nrows - r0) : KT);
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int r = e / KT, c = e - r * KT;
+    cplx y = cmk(0.0, 0.0);
+    if (c < r && r < hn && c < a.ncols) y = D[(r0 + r) * a.ldd + c];
+    if (c == r) y = cmk(1.0, 0.0);
+    Ys[r * LDS + c] = y;   // Ys holds KT rows here (C::QSMEM sized for it below)
+  }
+  __syncthreads();
+  // W1 = Yh^H C -> Ms
+  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+    const int i = e / KT, j = e - i * KT;
+    cplx s = cmk(0.0, 0.0);
+    for (int r = i; r < KT; ++r) s = cfmac(Ys[r * LDS + i], Cs[r * LDS + j], s);
+    Ms[i * LDS + j] = s;
+  }
+  __syncthreads();
+  // M = Th W1 -> reuse: out = C - Yh (Th W1); compute N = Th W1 into registers per entry then store into Ms
+  {
+    const cplx* Th = Tbase;
+    cplx vals[KT * KT / 256 + 1];
+    int cnt = 0;
+    for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+      const int i = e / KT, j = e - i * KT;
+      cplx s = cmk(0.0, 0.0);
+      for (int l = i; l < KT; ++l) s = cfma(Th[i * KT + l], Ms[l * LDS + j], s);
+      vals[cnt++] = s;
+    }
+    __syncthreads();
+    cnt = 0;
+    for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+      const int i = e / KT, j = e - i * KT;
+      Ms[i * LDS + j] = vals[cnt++];
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < hn * KT; e += blockDim.x) {
+    const int r = e / KT, c = e - r * KT;
+    cplx s = Cs[r * LDS + c];
+    for (int l = 0; l <= r; ++l) s = csub(s, cmul(Ys[r * LDS + l], Ms[l * LDS + c]));
+    if (c < a.ncols) D[(r0 + r) * a.ldd + c] = s;
+  }
+}
+
+template <int KT>
+cudaError_t zfactor_t(const ZFactorArgs& a, cudaStream_t st) {
+  using C = ZCfg<KT>;
+  if (a.G.b > C::B || a.G.nchains <= 0) return cudaErrorInvalidValue;
+  auto k = zchain_factor_kernel<KT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  k<<<a.G.nchains, 256, C::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+template <int KT>
+cudaError_t zqform_t(const ZQformArgs& a, cudaStream_t st) {
+  using C = ZCfg<KT>;
+  constexpr int SM = (2 * KT * C::LDS + (KT > 32 ? KT : 32) * C::LDS) * 16;
+  auto k = zchain_qform_kernel<KT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+  k<<<a.G.nchains, 256, SM, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+int zchain_bmax() { return ZCfg<64>::B; }
+
+cudaError_t launch_zchain_factor(const ZFactorArgs& a, int KT, cudaStream_t st) {
+  if (KT == 16) return zfactor_t<16>(a, st);
+  if (KT == 32) return zfactor_t<32>(a, st);
+  if (KT == 64) return zfactor_t<64>(a, st);
+  return cudaErrorInvalidValue;
+}
+cudaError_t launch_zchain_qform(const ZQformArgs& a, int KT, cudaStream_t st) {
+  if (KT == 16) return zqform_t<16>(a, st);
+  if (KT == 32) return zqform_t<32>(a, st);
+  if (KT == 64) return zqform_t<64>(a, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace ots

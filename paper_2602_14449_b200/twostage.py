@@ -55,10 +55,11 @@ def intra_qr(a, intra="householder"):
 
 
 def _zeros_like(was_torch, shape, ref=None):
+    cplx = ref is not None and is_complex(ref)
     if was_torch:
         t = D.torch()
-        return t.zeros(shape, dtype=t.float64, device=ref.device)
-    return np.zeros(shape)
+        return t.zeros(shape, dtype=t.complex128 if cplx else t.float64, device=ref.device)
+    return np.zeros(shape, dtype=np.complex128 if cplx else np.float64)
 
 
 def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
@@ -77,15 +78,15 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         raise E.DimensionError(f"v has {n} rows but a has {a.shape[0]}")
     if k0 + k > n:
         raise E.DimensionError(f"need k0 + k <= n, got {k0}+{k} > {n}")
-    if is_complex(v) or is_complex(a):
-        raise NotImplementedError("complex two_stage_qr: not in this build")
+    cplx = is_complex(v) or is_complex(a)
     if k0 == 0:
         qr = intra_qr(a, intra)
         return TwoStageResult(qr.q, qr.r, _zeros_like(was_torch, (0, k), a),
                               ReflectorDiagnostics(1.0, 0.0))
     if k == 0:
-        return TwoStageResult(_zeros_like(was_torch, (n, 0), a), _zeros_like(was_torch, (0, 0), a),
-                              _zeros_like(was_torch, (k0, 0), a), ReflectorDiagnostics(1.0, 0.0))
+        ref = v if is_complex(v) else a
+        return TwoStageResult(_zeros_like(was_torch, (n, 0), ref), _zeros_like(was_torch, (0, 0), ref),
+                              _zeros_like(was_torch, (k0, 0), ref), ReflectorDiagnostics(1.0, 0.0))
     if choice not in CHOICES:
         raise E.ParameterError(f"unknown choice {choice!r}; expected one of "
                                f"('mlu', 'qr', 'polar', 'explicit')")
@@ -93,8 +94,11 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         raise E.ParameterError(f"unknown intra method {intra!r}; expected {INTRA_METHODS}")
     dev = D.pick_device(v, a)
     ctx = D.ctx(dev)
-    V = D.to_device(v, dev)
-    A = D.to_device(a, dev)
+    if cplx and intra != "householder":
+        raise NotImplementedError("complex intra='cholshift': not in this build")
+    todev = D.cto_device if cplx else D.to_device
+    V = todev(v, dev)
+    A = todev(a, dev)
     P = None
     if choice == "explicit":
         if p is None:
@@ -102,12 +106,18 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         p = as_matrix(p, "p")
         if tuple(p.shape) != (k0, k0):
             raise E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}")
-        P = D.to_device(p, dev)
-    Q = D.empty(n, k, dev)
-    R = D.zeros(k, k, dev)
-    S = D.empty(k0, k, dev)
+        P = todev(p, dev)
+    if cplx:
+        Q = D.cempty(n, k, dev)
+        R = D.czeros(k, k, dev)
+        S = D.cempty(k0, k, dev)
+    else:
+        Q = D.empty(n, k, dev)
+        R = D.zeros(k, k, dev)
+        S = D.empty(k0, k, dev)
     diag = (C.c_double * 3)()
-    rc = lib().ots_two_stage_f64(
+    fn = lib().ots_two_stage_c128 if cplx else lib().ots_two_stage_f64
+    rc = fn(
         ctx, n, k0, k, V.ptr, V.ld, A.ptr, A.ld, CHOICES[choice], INTRA[intra],
         P.ptr if P is not None else None, P.ld if P is not None else 0,
         1e-8, 0, Q.ptr, Q.ld, R.ptr, R.ld, S.ptr, S.ld, diag, D.stream_ptr(dev))

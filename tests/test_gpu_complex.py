@@ -1,0 +1,106 @@
+"""GPU parity for complex128 (BASELINE configs[3]): two_stage_qr and
+householder_qr on c128 data through the C-ABI (ots_two_stage_c128 /
+ots_householder_qr_c128) against the reference's golden outputs and the CPU
+oracle.  Tolerances as in test_gpu_parity.py (north_star)."""
+import numpy as np
+import pytest
+
+import paper_2602_14449_b200 as P
+from oracle import twostage_oracle as O
+
+pytestmark = pytest.mark.gpu
+U = 2.0 ** -53
+
+
+def rel(x, y):
+    x, y = np.asarray(x), np.asarray(y)
+    if y.size == 0:
+        return 0.0
+    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
+
+
+def golden_cases(golden, prefix):
+    keys = sorted({k.rsplit("/", 1)[0] for k in golden.files if k.endswith("/q")})
+    return [k for k in keys if k.startswith(prefix)]
+
+
+def cgauss(rng, n, m):
+    return (rng.standard_normal((n, m)) + 1j * rng.standard_normal((n, m))) / np.sqrt(2.0)
+
+
+def test_complex_two_stage_golden(golden):
+    cases = golden_cases(golden, "cplx_")
+    assert cases
+    for case in cases:
+        base = case.rsplit("/", 1)[0]
+        v, a = golden[base + "/v"], golden[base + "/a"]
+        ch = str(golden[case + "/choice"])
+        p = golden[case + "/p"]
+        res = P.two_stage_qr(v, a, choice=ch, p=(p if p.size else None))
+        assert np.iscomplexobj(res.q) and np.iscomplexobj(res.r)
+        assert rel(res.q, golden[case + "/q"]) < 1e-10, case
+        assert rel(res.r, golden[case + "/r"]) < 1e-10, case
+        assert rel(res.s, golden[case + "/s"]) < 1e-10, case
+        kt = float(golden[case + "/kappa_t"])
+        wn = float(golden[case + "/wt_inv_norm"])
+        assert abs(res.diagnostics.kappa_t - kt) <= 1e-10 * kt, case
+        assert abs(res.diagnostics.wt_inv_norm - wn) <= 1e-10 * wn, case
+        assert np.all(np.tril(res.r, -1) == 0.0)
+        assert np.all(np.diag(res.r).imag == 0.0)
+
+
+@pytest.mark.parametrize("choice", ["qr", "mlu", "polar", "explicit"])
+def test_complex_two_stage_oracle(choice):
+    rng = np.random.default_rng(7)
+    n, k0, k = 6000, 32, 24
+    v, _ = np.linalg.qr(cgauss(rng, n, k0))
+    a = cgauss(rng, n, k)
+    p = None
+    if choice == "explicit":
+        p, _ = np.linalg.qr(cgauss(rng, k0, k0))
+    ref = O.two_stage(v, a, choice, p=p)
+    res = P.two_stage_qr(v, a, choice=choice, p=p)
+    assert rel(res.q, ref["q"]) < 1e-10
+    assert rel(res.r, ref["r"]) < 1e-10
+    assert rel(res.s, ref["s"]) < 1e-10
+    assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
+    assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (7, 3), (130, 64), (4099, 17), (20000, 64), (300000, 32)])
+def test_complex_householder_qr(shape):
+    rng = np.random.default_rng(shape[0] + shape[1])
+    a = cgauss(rng, *shape)
+    q0, r0 = np.linalg.qr(a)
+    res = P.householder_qr(a)
+    assert rel(res.r, r0) < 1e-10
+    assert rel(res.q, q0) < 1e-10
+    nn = P.householder_qr(a, nonneg_diag=True)
+    d = np.diag(nn.r)
+    assert np.all(d.imag == 0.0) and np.all(d.real >= 0.0)
+    assert rel(nn.q @ nn.r, a) < 1e-13
+
+
+def test_complex_config4_like_torch():
+    """configs[3] shape class on the device (n = 2^20, k0 = k = 64) with
+    torch CUDA inputs; size-independent properties (loss, cross, residual)."""
+    import torch
+    g = torch.Generator(device="cuda:0")
+    g.manual_seed(3)
+    n, k0, k = 1 << 20, 64, 64
+    re = torch.randn((n, k0), generator=g, dtype=torch.float64, device="cuda:0")
+    im = torch.randn((n, k0), generator=g, dtype=torch.float64, device="cuda:0")
+    v0 = torch.complex(re, im) / np.sqrt(2.0)
+    vq = P.householder_qr(v0).q
+    a = torch.complex(torch.randn((n, k), generator=g, dtype=torch.float64, device="cuda:0"),
+                      torch.randn((n, k), generator=g, dtype=torch.float64, device="cuda:0")) / np.sqrt(2.0)
+    for ch in ("qr", "mlu", "polar"):
+        res = P.two_stage_qr(vq, a, choice=ch)
+        Qf = torch.cat([vq, res.q], dim=1)
+        G = Qf.conj().T @ Qf
+        loss = torch.linalg.matrix_norm(G - torch.eye(k0 + k, dtype=G.dtype, device=G.device), ord=2).item()
+        resid = (torch.linalg.matrix_norm(a - vq @ res.s - res.q @ res.r) /
+                 torch.linalg.matrix_norm(a)).item()
+        assert loss <= 10 * n * U, (ch, loss)
+        assert resid <= 10 * n * U, (ch, resid)
+        assert torch.all(torch.diagonal(res.r).imag == 0)
