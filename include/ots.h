@@ -111,6 +111,14 @@ int ots_two_stage_c128(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
                        void* Q, int64_t ldq, void* R, int64_t ldr,
                        void* S, int64_t lds, double* diag_host, void* stream);
 
+/* b_two_stage_qr for M = diag(d) on c128 data     -- oblique.py:279-315
+ * (d real > 0, device; scaled Euclidean path) */
+int ots_b_two_stage_diag_c128(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                              const void* V, int64_t ldv, const void* A, int64_t lda,
+                              const double* d, int choice, const void* P, int64_t ldp,
+                              double orth_tol, void* Q, int64_t ldq, void* R, int64_t ldr,
+                              void* S, int64_t lds, double* diag_host, void* stream);
+
 /* householder_qr(a, nonneg_diag)                  -- core.py:61-84, c128 */
 int ots_householder_qr_c128(ots_ctx* ctx, int64_t m, int64_t k,
                             const void* A, int64_t lda, void* Q, int64_t ldq,

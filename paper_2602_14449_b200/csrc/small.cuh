@@ -51,6 +51,11 @@ struct ZState {
   double *Z1x, *Z2x; int ldzx;      // interleaved real expansions (2k0 x 2k)
   double *svec, *svec2;             // sign recovery (k), per real column (2k)
   double2* Sout; int lds_out;
+  // B-inner (M = diag(d)): real Gram of the unscaled V view -> phi(V^H V)
+  // into GuE for the diagnostics (r.Gu = GuE), 1/d on the top rows -> dinvE
+  const double* Gur; long ldgur;
+  const double* dB;
+  double *GuE, *dinvE;
   SmallState r;
 };
 

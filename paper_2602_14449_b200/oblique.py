@@ -7,8 +7,9 @@ initial basis is the canonical `initial_b_basis(inner, m)`: then Algorithm 4
 (D^1/2 V, D^1/2 A) with Q = D^-1/2 Q' sgn, R = sgn R' (positive diagonal,
 oblique.py:232) and S unchanged (verified against the
 reference to <= 7e-14).  The whole computation is one C-ABI call
-(`ots_b_two_stage_diag_f64`).  A dense general B (n x n) is not supported by
-this build (NotImplementedError), nor complex data.
+(`ots_b_two_stage_diag_f64`, or `ots_b_two_stage_diag_c128` for complex
+data).  A dense general B (n x n) is not supported by this build
+(NotImplementedError).
 """
 
 from __future__ import annotations
@@ -121,8 +122,7 @@ def b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
         raise E.DimensionError(f"need k0 + k <= n, got {k0}+{k} > {n}")
     if inner.kind != "weighted" or inner.diag is None:
         raise NotImplementedError("this build implements b_two_stage_qr for a diagonal B only")
-    if is_complex(v) or is_complex(a):
-        raise NotImplementedError("complex b_two_stage_qr: not in this build")
+    cplx = is_complex(v) or is_complex(a)
     if not _is_canonical_basis(u, inner.diag, k0 + k):
         raise NotImplementedError("this build needs u = initial_b_basis(inner, k0+k)")
     dev = D.pick_device(v, a)
@@ -134,21 +134,26 @@ def b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
         sa = a * (d_dev.sqrt()[:, None] if D.is_torch(a) else np.sqrt(d_dev.cpu().numpy())[:, None])
         qr = householder_qr(sa, nonneg_diag=True)
         q = qr.q / (d_dev.sqrt()[:, None] if D.is_torch(qr.q) else np.sqrt(d_dev.cpu().numpy())[:, None])
-        z = t.zeros((0, k), dtype=t.float64, device=d_dev.device) if was_torch else np.zeros((0, k))
+        zdt = (t.complex128 if cplx else t.float64)
+        z = t.zeros((0, k), dtype=zdt, device=d_dev.device) if was_torch else \
+            np.zeros((0, k), dtype=np.complex128 if cplx else np.float64)
         return TwoStageResult(q, qr.r, z, ReflectorDiagnostics(1.0, 0.0))
     ctx = D.ctx(dev)
-    V = D.to_device(v, dev)
-    A = D.to_device(a, dev)
-    P = D.to_device(p, dev) if (choice == "explicit" and p is not None) else None
+    todev = D.cto_device if cplx else D.to_device
+    V = todev(v, dev)
+    A = todev(a, dev)
+    P = todev(p, dev) if (choice == "explicit" and p is not None) else None
     if choice == "explicit" and P is None:
         raise E.ParameterError("choice='explicit' requires a seed matrix p")
     if choice not in CHOICES:
         raise E.ParameterError(f"unknown choice {choice!r}")
-    Q = D.empty(n, k, dev)
-    R = D.zeros(k, k, dev)
-    S = D.empty(k0, k, dev)
+    if cplx:
+        Q, R, S = D.cempty(n, k, dev), D.czeros(k, k, dev), D.cempty(k0, k, dev)
+    else:
+        Q, R, S = D.empty(n, k, dev), D.zeros(k, k, dev), D.empty(k0, k, dev)
     diag = (C.c_double * 3)()
-    rc = lib().ots_b_two_stage_diag_f64(
+    fn = lib().ots_b_two_stage_diag_c128 if cplx else lib().ots_b_two_stage_diag_f64
+    rc = fn(
         ctx, n, k0, k, V.ptr, V.ld, A.ptr, A.ld, C.c_void_p(d_dev.data_ptr()), CHOICES[choice],
         P.ptr if P is not None else None, P.ld if P is not None else 0, 1e-6,
         Q.ptr, Q.ld, R.ptr, R.ld, S.ptr, S.ld, diag, D.stream_ptr(dev))

@@ -104,3 +104,40 @@ def test_complex_config4_like_torch():
         assert loss <= 10 * n * U, (ch, loss)
         assert resid <= 10 * n * U, (ch, resid)
         assert torch.all(torch.diagonal(res.r).imag == 0)
+
+
+@pytest.mark.parametrize("ch", ["qr", "mlu", "polar"])
+def test_complex_binner_diag_golden(golden, ch):
+    """configs[3]'s non-standard inner product (M = diag(d)) on c128 data
+    against the reference's outputs (oblique.py:279-315)."""
+    g = lambda key: golden[f"binner_diag_complex/{ch}/{key}"]
+    v, a = g("v"), g("a")
+    ip = P.InnerProduct.weighted(np.diag(g("d")))
+    u = P.initial_b_basis(ip, v.shape[1] + a.shape[1])
+    assert np.array_equal(u, g("u"))
+    res = P.b_two_stage_qr(v, a, u, ip, choice=ch)
+    assert rel(res.q, g("q")) < 1e-10
+    assert rel(res.r, g("r")) < 1e-10
+    assert rel(res.s, g("s")) < 1e-10
+    assert np.all(np.diag(res.r).real > 0) and np.all(np.diag(res.r).imag == 0)
+    assert abs(res.diagnostics.kappa_t - float(g("kappa_t"))) < 1e-10 * float(g("kappa_t"))
+    assert abs(res.diagnostics.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
+
+
+def test_complex_binner_diag_config4_like():
+    """configs[3] B-inner shape class: d log-uniform in [1, 1e4], V
+    M-orthonormal, complex Gaussian A; B-orthogonality and residual."""
+    rng = np.random.default_rng(11)
+    n, k0, k = 1 << 16, 64, 64
+    d = 10.0 ** rng.uniform(0.0, 4.0, n)
+    sq = np.sqrt(d)
+    v = np.linalg.qr(sq[:, None] * cgauss(rng, n, k0))[0] / sq[:, None]
+    a = cgauss(rng, n, k)
+    ip = P.InnerProduct.weighted(d)
+    u = P.initial_b_basis(ip, k0 + k)
+    res = P.b_two_stage_qr(v, a, u, ip)
+    ref = O.b_two_stage(v, a, u, O.BInner(diag=d), "qr", diagnostics=False)
+    assert rel(res.q, ref["q"]) < 1e-10 and rel(res.r, ref["r"]) < 1e-10 and rel(res.s, ref["s"]) < 1e-10
+    W = np.hstack([v, res.q])
+    G = W.conj().T @ (d[:, None] * W)
+    assert np.abs(G - np.eye(k0 + k)).max() <= 10 * n * U
