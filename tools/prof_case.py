@@ -15,11 +15,18 @@ ap.add_argument("--k0", type=int, default=128)
 ap.add_argument("--k", type=int, default=64)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--choice", default="qr")
+ap.add_argument("--vgen", default="ots", help="ots | torch (cuSOLVER QR) | eye ([I; 0]); the last two keep our kernels out of the setup")
 a = ap.parse_args()
 g = torch.Generator(device="cuda:0")
 g.manual_seed(1)
 G = torch.randn((a.n, a.k0), generator=g, dtype=torch.float64, device="cuda:0")
-V = P.block_householder_qr([G[:, i:i + 64].contiguous() for i in range(0, a.k0, 64)]).q.contiguous()
+if a.vgen == "eye":      # exactly orthonormal [I; 0] (no setup kernels)
+    V = torch.zeros((a.n, a.k0), dtype=torch.float64, device="cuda:0")
+    V[:a.k0].copy_(torch.eye(a.k0, dtype=torch.float64))
+elif a.vgen == "torch":
+    V = torch.linalg.qr(G)[0].contiguous()
+else:
+    V = P.block_householder_qr([G[:, i:i + 64].contiguous() for i in range(0, a.k0, 64)]).q.contiguous()
 A = torch.randn((a.n, a.k), generator=g, dtype=torch.float64, device="cuda:0")
 ctx = NT.context(0)
 NT.lib().ots_set_profiling(ctx, 1)
