@@ -22,7 +22,7 @@ struct NnArgs {
   double* X; long ldx;
   int ncols;
   long row_begin, row_end;
-  const double* colscale;                     // device, ncols entries, or null
+  const double* colscale;                     // device, ncols entries of +-1, or null
 };
 
 struct ChainGeom {

@@ -224,6 +224,16 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
   };
 
   double acc[4][NJ][2];
+  // this thread's output columns with a negative colscale (bit 2j+h)
+  unsigned negmask = 0;
+  if (a.colscale) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int c = wn0 + 8 * j + 2 * t;
+      if (c < a.ncols && a.colscale[c] < 0.0) negmask |= 1u << (2 * j);
+      if (c + 1 < a.ncols && a.colscale[c + 1] < 0.0) negmask |= 1u << (2 * j + 1);
+    }
+  }
 
   // accumulators start from B (so the epilogue is a plain store)
   auto acc_from_b = [&](long r0) {
@@ -250,10 +260,15 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
         long r = r0 + wm0 + 8 * i + g;
         int c = wn0 + 8 * j + 2 * t;
         if (r >= a.row_end) continue;
-        double s0 = 1.0, s1 = 1.0;
-        if (a.colscale) { if (c < a.ncols) s0 = a.colscale[c]; if (c + 1 < a.ncols) s1 = a.colscale[c + 1]; }
-        double y0 = acc[i][j][0] * s0;
-        double y1 = acc[i][j][1] * s1;
+        // colscale entries are +-1 (LAPACK sign recovery): flip the sign bit
+        // with integer ops instead of DMULs competing with DMMA for the FP64 pipe
+        double y0 = acc[i][j][0], y1 = acc[i][j][1];
+        if (negmask) {
+          const unsigned long long f0 = ((negmask >> (2 * j)) & 1u) ? 0x8000000000000000ull : 0ull;
+          const unsigned long long f1 = ((negmask >> (2 * j + 1)) & 1u) ? 0x8000000000000000ull : 0ull;
+          y0 = __longlong_as_double(__double_as_longlong(y0) ^ f0);
+          y1 = __longlong_as_double(__double_as_longlong(y1) ^ f1);
+        }
         double* p = a.X + r * a.ldx + c;
         if (c + 1 < a.ncols) __stcs(reinterpret_cast<double2*>(p), make_double2(y0, y1));
         else if (c < a.ncols) p[0] = y0;
