@@ -828,12 +828,225 @@ cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
+// ---------------------------------------------------------------------------
+// Q formation, pipelined (v2): one 512-thread CTA per SM walks its chains;
+// C, T, M = T C and a double-buffered whole Y tile live in shared memory
+// (224 KB at KT = 64), so T and Y of tile t-1 stream in (cp.async) while tile
+// t's out = -Y M runs on all 16 warps.
+// ---------------------------------------------------------------------------
+template <int KT>
+struct Qform2Cfg {
+  static constexpr int NT = 512;
+  static constexpr int NW = NT / 32;
+  static constexpr int B = BlkCfg<KT>::B;             // tile rows (>= any level's b)
+  static constexpr int SMEM = (3 * KT * KT + 2 * B * KT) * 8;
+};
+
+// Ms = -(T C) (KT x KT) with T upper triangular; 16 warps: 8-row blocks x
+// column splits.
+template <int KT>
+__device__ __forceinline__ void q2_tc(const double* Ts, const double* Cs, double* Ms) {
+  constexpr int RB = KT / 8;              // row blocks
+  constexpr int CB = KT / 8;              // 8-column blocks
+  constexpr int CS = (16 / RB < CB) ? 16 / RB : CB;   // column splits per row block
+  constexpr int CW = KT / CS;             // columns per warp (>= 8)
+  constexpr int NJ = CW / 8;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  if (warp >= RB * CS) return;
+  const int rb = warp / CS, c0 = (warp % CS) * CW;
+  double acc[NJ][2];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 2 * rb; kk < KT / 4; ++kk) {
+    const double av = Ts[swz(8 * rb + g, 4 * kk + t, KT)];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) dmma(acc[j], av, Cs[swz(4 * kk + t, c0 + 8 * j + g, KT)]);
+  }
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {   // store -M: the tall product then needs no negation
+    Ms[swz(8 * rb + g, c0 + 8 * j + 2 * t, KT)] = -acc[j][0];
+    Ms[swz(8 * rb + g, c0 + 8 * j + 2 * t + 1, KT)] = -acc[j][1];
+  }
+}
+
+// out rows [y0, rhi) = Y Ms (Ms = -M); Y tile (B x KT) in smem; 16 warps as 4 row
+// bands of 32 x 4 column quarters of KT/4.
+template <int KT>
+__device__ __forceinline__ void q2_ym(const double* Ys, const double* Ms, double* D, long ldd, int ncols, long y0,
+                                      long rhi) {
+  constexpr int B = Qform2Cfg<KT>::B;
+  constexpr int WN = KT / 4;              // 16 / 8 / 4
+  constexpr int NJ = WN >= 8 ? WN / 8 : 1;
+  constexpr int NBANDS = B / 32;          // 4
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int band = warp / 4, wn0 = (warp % 4) * WN;
+  if (band >= NBANDS || WN < 8) {
+    if (WN >= 8) return;
+  }
+  if (WN < 8) {   // KT = 16: 4 warps per band would split 8-col fragments; use 2
+    if ((warp % 4) >= 2) return;
+  }
+  constexpr int NJJ = WN >= 8 ? NJ : 1;
+  const int c0 = WN >= 8 ? wn0 : (warp % 4) * 8;
+  const int wm0 = band * 32;
+  if (y0 + wm0 >= rhi) return;
+  double o[4][NJJ][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJJ; ++j) o[i][j][0] = o[i][j][1] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < KT / 4; ++kk) {
+    double af[4], bf[NJJ];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) af[i] = Ys[swz(wm0 + 8 * i + g, 4 * kk + t, KT)];
+#pragma unroll
+    for (int j = 0; j < NJJ; ++j) bf[j] = Ms[swz(4 * kk + t, c0 + 8 * j + g, KT)];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < NJJ; ++j) dmma(o[i][j], af[i], bf[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJJ; ++j) {
+      const long r = y0 + wm0 + 8 * i + g;
+      const int cc = c0 + 8 * j + 2 * t;
+      if (r >= rhi) continue;
+      double* p = D + r * ldd + cc;
+      if (cc + 1 < ncols) __stcs(reinterpret_cast<double2*>(p), make_double2(o[i][j][0], o[i][j][1]));
+      else if (cc < ncols) p[0] = o[i][j][0];
+    }
+}
+
+template <int KT>
+__global__ void __launch_bounds__(512, 1) chain_qform2_kernel(QformArgs a) {
+  using C = Qform2Cfg<KT>;
+  constexpr int B = C::B;
+  extern __shared__ __align__(128) double sm[];
+  double* Cs = sm;
+  double* Ts = Cs + KT * KT;
+  double* Ms = Ts + KT * KT;
+  double* Yb = Ms + KT * KT;          // 2 x (B x KT)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  for (int chain = blockIdx.x; chain < a.G.nchains; chain += gridDim.x) {
+    const long r0 = (long)chain * a.G.rpc;
+    const int ntiles = chain_real_tiles(a.G, chain, KT);
+    const double* Tbase = a.T + (long)chain * (a.G.L + 1) * KT * KT;
+    auto tile_rows = [&](int tt, long& gr0, long& rhi) {
+      gr0 = r0 + KT + (long)(tt - 1) * a.G.b;
+      rhi = gr0 + a.G.b < a.G.nrows ? gr0 + a.G.b : a.G.nrows;
+    };
+    auto issue_tile = [&](int tt, int buf) {   // T_tt and Y_tt (tt >= 1) or head (tt == 0)
+      load_tile_async(Ts, KT, Tbase + (long)tt * KT * KT, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
+      if (tt >= 1) {
+        long gr0, rhi;
+        tile_rows(tt, gr0, rhi);
+        load_tile_async(Yb + buf * B * KT, KT, a.D, a.ldd, gr0, B, gr0, rhi, 0, KT, a.ncols, tid, C::NT);
+      } else {
+        const long hhi = r0 + KT < a.G.nrows ? r0 + KT : a.G.nrows;
+        load_tile_async(Yb + buf * B * KT, KT, a.D, a.ldd, r0, KT, r0, hhi, 0, KT, a.ncols, tid, C::NT);
+      }
+    };
+    __syncthreads();   // previous chain done with all buffers
+    load_tile_async(Cs, KT, a.Cin + (long)chain * KT * KT, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
+    issue_tile(ntiles, 0);
+    cp_async_commit();
+    int buf = 0;
+    for (int tt = ntiles; tt >= 1; --tt) {
+      cp_async_wait<0>();
+      __syncthreads();
+      q2_tc<KT>(Ts, Cs, Ms);                         // M = T C
+      __syncthreads();
+      issue_tile(tt - 1, buf ^ 1);                   // T, Y of the next (lower) tile
+      cp_async_commit();
+      for (int e = tid; e < KT * KT; e += C::NT) Cs[e] += Ms[e];   // C <- C - M (Ms = -M)
+      long gr0, rhi;
+      tile_rows(tt, gr0, rhi);
+      q2_ym<KT>(Yb + buf * B * KT, Ms, a.D, a.ldd, a.ncols, gr0, rhi);
+      buf ^= 1;
+    }
+    // ---- head: out = C - Yt (T Yt^T) C  (Yt unit lower)
+    cp_async_wait<0>();
+    __syncthreads();
+    double* Yt = Yb + buf * B * KT;
+    for (int e = tid; e < KT * KT; e += C::NT) {
+      const int r = e / KT, cc = e - r * KT;
+      if (cc >= r) Yt[swz(r, cc, KT)] = (cc == r) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    // N = T Yt^T -> Ms (first 8 warps, row blocks), then M = N C -> Ts
+    if (warp < KT / 8) {
+      double acc[KT / 8][2];
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+      for (int kk = 2 * warp; kk < KT / 4; ++kk) {
+        const double av = Ts[swz(8 * warp + g, 4 * kk + t4, KT)];
+#pragma unroll
+        for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Yt[swz(8 * j + g, 4 * kk + t4, KT)]);
+      }
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) {
+        Ms[swz(8 * warp + g, 8 * j + 2 * t4, KT)] = acc[j][0];
+        Ms[swz(8 * warp + g, 8 * j + 2 * t4 + 1, KT)] = acc[j][1];
+      }
+    }
+    __syncthreads();
+    if (warp < KT / 8) {
+      double acc[KT / 8][2];
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < KT / 4; ++kk) {
+        const double av = Ms[swz(8 * warp + g, 4 * kk + t4, KT)];
+#pragma unroll
+        for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Cs[swz(4 * kk + t4, 8 * j + g, KT)]);
+      }
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) {
+        Ts[swz(8 * warp + g, 8 * j + 2 * t4, KT)] = acc[j][0];
+        Ts[swz(8 * warp + g, 8 * j + 2 * t4 + 1, KT)] = acc[j][1];
+      }
+    }
+    __syncthreads();
+    if (warp < KT / 8) {
+      double acc[KT / 8][2];
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+      for (int kk = 0; kk < KT / 4; ++kk) {
+        const double av = Yt[swz(8 * warp + g, 4 * kk + t4, KT)];
+#pragma unroll
+        for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Ts[swz(4 * kk + t4, 8 * j + g, KT)]);
+      }
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) {
+        const int r = 8 * warp + g, cc = 8 * j + 2 * t4;
+        const long gr = r0 + r;
+        if (gr >= a.G.nrows) continue;
+        const double y0 = Cs[swz(r, cc, KT)] - acc[j][0];
+        const double y1 = Cs[swz(r, cc + 1, KT)] - acc[j][1];
+        double* p = a.D + gr * a.ldd + cc;
+        if (cc + 1 < a.ncols) *reinterpret_cast<double2*>(p) = make_double2(y0, y1);
+        else if (cc < a.ncols) p[0] = y0;
+      }
+    }
+  }
+}
+
 template <int KT>
 static cudaError_t qform_t(const QformArgs& a, cudaStream_t st) {
-  using C = QformCfg<KT>;
-  auto k = chain_qform_kernel<KT>;
+  using C = Qform2Cfg<KT>;
+  auto k = chain_qform2_kernel<KT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  k<<<a.G.nchains, C::NT, C::SMEM, st>>>(a);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.G.nchains < nsm ? a.G.nchains : nsm;
+  k<<<grid, C::NT, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 
