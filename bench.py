@@ -119,8 +119,9 @@ class ClockSampler:
 
     def start(self):
         try:
+            ids = [] if self.device is None else [f"--id={self.device}"]
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                ["nvidia-smi", *ids, f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
@@ -200,14 +201,16 @@ def run_gpu(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    # OTS_BENCH_SHARE_DEVICE=1: every rank on cuda:0 with gloo collectives --
+    # a plumbing check of the N>1 leg on a one-GPU box, never a measurement
+    share = os.environ.get("OTS_BENCH_SHARE_DEVICE") == "1"
+    torch.cuda.set_device(0 if share else local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group("gloo" if share else "nccl")
     n, k0, k = args.n, args.k0, args.k
 
     if world > 1:
-        from paper_2602_14449_b200 import dist as PD
-        return PD.bench_sharded(args, n, k0, k, rank, world, local)
+        return run_sharded(args, n, k0, k, rank, world, 0 if share else local)
 
     ctx = NT.context(local)
     L = NT.lib()
@@ -362,13 +365,52 @@ def run_gpu(args):
     return 0
 
 
+def run_sharded(args, n, k0, k, rank, world, local):
+    """N > 1: rows of the headline problem split across ranks (strong scaling,
+    NCCL for the SURVEY 8(e) collectives); rank 0 prints the line."""
+    import torch.distributed as dist
+    from paper_2602_14449_b200 import dist as PD
+    m = PD.bench_sharded(args, n, k0, k, rank, world, local)
+    if rank == 0:
+        F = f_alg(n, k0, k)
+        ms = m["ms"]
+        val = F / (ms * 1e-3) / 1e9
+        t_roof = F / (world * 37.0e12)
+        line = {
+            "metric": "fp64 two-stage orthogonalization GFLOP/s", "value": round(val, 2), "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "headline two_stage_qr(V, A) choice=qr intra=householder, row-sharded",
+                       "n": n, "k0": k0, "k": k,
+                       "parallelism": f"row-sharded x{world} (NCCL allreduce/allgather/broadcast of the "
+                                      f"k0x(k0+k), KTxKT, k0xk blocks)",
+                       "l2": "inputs >> L2 on every rank (no flush needed)"},
+            "roofline": {"bound": "tensor", "kernel": "whole step", "achieved": round(F / (ms * 1e-3) / 1e12, 3),
+                         "peak": round(world * 37.0, 1), "unit": "TFLOP/s",
+                         "frac": round(t_roof / (ms * 1e-3), 4), "traffic": None,
+                         "peak_source": "N x FP64 DMMA peak measured at N=1 (profiles/r01_fp64_peak.json)"},
+            "cpu_baseline": None,
+            "e2e": {"value": round(F / (m["e2e_ms"] * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+                    "ms_per_step": round(m["e2e_ms"], 2), "h2d_bytes_per_step": m["h2d"],
+                    "d2h_bytes_per_step": m["d2h"], "steps": m["e2e_steps"],
+                    "api": "dist.run_phases per rank with pinned host shards (serial copy in / call / copy out)"},
+            "gpu_launches": m["launches"],
+            "clocks": m["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_HEAD)
+    ap.add_argument("--n", "--rows", dest="n", type=int, default=N_HEAD)
     ap.add_argument("--k0", type=int, default=K0_HEAD)
     ap.add_argument("--k", type=int, default=K_HEAD)
     ap.add_argument("--no-cpu", action="store_true")

@@ -1230,6 +1230,13 @@ int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign, doub
   if (j.c.row0 == 0) CK(launch_qtop(j.s, j.c.Q, j.c.ldq, st));
   if (R) rscale_kernel<<<8, 256, 0, st>>>(j.Rfinal, j.KT, j.svec, R, ldr, k);
   if (S) copy_s_kernel<<<8, 256, 0, st>>>(j.s.Sd, j.ld, S, lds, k0, k);
+  {  // kernels this rank launched for the call (ots_last_launch_count)
+    const int nb = (k0 + 127) / 128;
+    const int gram = (k0 <= 128) ? 2 : nb * (nb + 1) + 2 * nb;
+    const bool top = j.c.row0 == 0;
+    ctx->launches = gram + (top ? 1 : 0) + 2 + 1 + 2 * (int)j.lv.size() + 2 * (int)j.glv.size() + 1 +
+                    (top ? 1 : 0) + 2 * nb + 3 + (top ? 1 : 0) + (R ? 1 : 0) + (S ? 1 : 0);
+  }
   return read_status(ctx, j, diag_host);
 }
 

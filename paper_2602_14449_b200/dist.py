@@ -32,7 +32,8 @@ from ._native import CHOICES, check, lib
 # communicators
 # ---------------------------------------------------------------------------
 class TorchComm:
-    """torch.distributed process group (NCCL for device tensors, gloo for CPU)."""
+    """torch.distributed process group (NCCL for device tensors; with the gloo
+    backend device tensors are staged through host memory)."""
 
     def __init__(self, group=None):
         import torch.distributed as dist
@@ -40,20 +41,32 @@ class TorchComm:
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.host = dist.get_backend(group) == "gloo"
+
+    def _stage(self, t):
+        return t.cpu() if (self.host and t.is_cuda) else t
 
     def allreduce_sum(self, t):
-        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        h = self._stage(t)
+        self.dist.all_reduce(h, op=self.dist.ReduceOp.SUM, group=self.group)
+        if h is not t:
+            t.copy_(h)
         return t
 
     def broadcast(self, t, src=0):
-        self.dist.broadcast(t, src=src, group=self.group)
+        h = self._stage(t)
+        self.dist.broadcast(h, src=src, group=self.group)
+        if h is not t:
+            t.copy_(h)
         return t
 
     def allgather_cat(self, t):
         import torch
-        out = [torch.empty_like(t) for _ in range(self.world)]
-        self.dist.all_gather(out, t, group=self.group)
-        return torch.cat(out, dim=0)
+        h = self._stage(t)
+        out = [torch.empty_like(h) for _ in range(self.world)]
+        self.dist.all_gather(out, h, group=self.group)
+        cat = torch.cat(out, dim=0)
+        return cat.to(t.device) if h is not t else cat
 
 
 class LocalComm:
@@ -211,10 +224,10 @@ def two_stage_qr_sharded(v_local, a_local, row0, choice="qr", p=None, group=None
 
 
 def bench_sharded(args, n, k0, k, rank, world, local):  # pragma: no cover - GPU box only
-    """bench.py N>1 leg: strong scaling, n rows split across ranks."""
-    import json
-    import time
-
+    """bench.py N>1 leg: rows of the headline problem split across ranks
+    (strong scaling).  Device time of K steps (CUDA events, barrier +
+    synchronize on both sides, max over ranks) and an end-to-end variant with
+    each rank's shard copied in from pinned host memory and Q copied out."""
     import torch
     import torch.distributed as dist
 
@@ -223,44 +236,69 @@ def bench_sharded(args, n, k0, k, rank, world, local):  # pragma: no cover - GPU
     base = n // world
     n_local = base + (n - base * world if rank == world - 1 else 0)
     row0 = rank * base
-    g = torch.Generator(device=f"cuda:{local}")
+    dev = torch.cuda.current_device()
+    g = torch.Generator(device=f"cuda:{dev}")
     g.manual_seed(1234 + rank)
-    G = torch.randn((n_local, k0), generator=g, dtype=torch.float64, device=f"cuda:{local}")
+    G = torch.randn((n_local, k0), generator=g, dtype=torch.float64, device=f"cuda:{dev}")
     Qr = P.block_householder_qr([G[:, i:i + 64].contiguous() for i in range(0, k0, 64)]).q
     V = (Qr / (world ** 0.5)).contiguous()     # V^T V = sum_r Q_r^T Q_r / world = I
-    A = torch.randn((n_local, k), generator=g, dtype=torch.float64, device=f"cuda:{local}")
+    A = torch.randn((n_local, k), generator=g, dtype=torch.float64, device=f"cuda:{dev}")
     del G, Qr
-    be = NativePhases(local)
-    Vd, Ad = D.to_device(V, local), D.to_device(A, local)
-    Qd, Rd, Sd = D.empty(n_local, k, local), D.zeros(k, k, local), D.empty(k0, k, local)
+    be = NativePhases(dev)
+    Vd, Ad = D.to_device(V, dev), D.to_device(A, dev)
+    Qd, Rd, Sd = D.empty(n_local, k, dev), D.zeros(k, k, dev), D.empty(k0, k, dev)
+    stream = torch.cuda.current_stream(dev)
 
-    def step():
-        run_phases(be, comm, n_local, row0, k0, k, Vd, Ad, Qd, Rd, Sd)
+    def step(Vx=Vd, Ax=Ad):
+        run_phases(be, comm, n_local, row0, k0, k, Vx, Ax, Qd, Rd, Sd)
+
+    def timed(fn, steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = torch.tensor([e0.elapsed_time(e1) / steps], device=f"cuda:{dev}")
+        red = comm._stage(ms)
+        dist.all_reduce(red, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        return float(red.item())
 
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
-        step()
-    e1.record()
-    torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=f"cuda:{local}")
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    dist.barrier()
+    launches = int(be.L.ots_last_launch_count(be.ctx))
+    clk = None
     if rank == 0:
-        from bench import f_alg
-        F = f_alg(n, k0, k)
-        val = F / (ms.item() * 1e-3) / 1e9
-        print(json.dumps({
-            "metric": "fp64 two-stage orthogonalization GFLOP/s", "value": round(val, 2),
-            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms.item(), 3), "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "headline two_stage_qr row-sharded", "n": n, "k0": k0, "k": k,
-                       "parallelism": f"row-sharded x{world} (NCCL allreduce/allgather/bcast)"},
-            "gpu_launches": None, "time": time.time()}), flush=True)
-    dist.destroy_process_group()
-    return 0
+        from bench import ClockSampler
+        clk = ClockSampler(None)
+        clk.start()
+    ms = timed(step, args.steps)
+    clocks = clk.stop() if clk is not None else None
+
+    # e2e: this rank's V, A shard in from pinned host memory, Q shard (and R, S
+    # on every rank) out, every step
+    Vh, Ah = V.cpu().pin_memory(), A.cpu().pin_memory()
+    Qh = torch.empty((n_local, k), dtype=torch.float64).pin_memory()
+    Rh = torch.empty((k, k), dtype=torch.float64).pin_memory()
+    Sh = torch.empty((k0, k), dtype=torch.float64).pin_memory()
+
+    def e2e_step():
+        Vd.buf[:, :k0].copy_(Vh, non_blocking=True)
+        Ad.buf[:, :k].copy_(Ah, non_blocking=True)
+        step()
+        Qh.copy_(Qd.view(), non_blocking=True)
+        Rh.copy_(Rd.view(), non_blocking=True)
+        Sh.copy_(Sd.view(), non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 3))
+    e2e_ms = timed(e2e_step, e2e_steps)
+    h2d = n_local * (k0 + k) * 8
+    d2h = (n_local * k + k * k + k0 * k) * 8
+    tot = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device=f"cuda:{dev}")
+    comm.allreduce_sum(tot)
+    out = dict(ms=ms, e2e_ms=e2e_ms, launches=launches, clocks=clocks, h2d=int(tot[0].item()),
+               d2h=int(tot[1].item()), e2e_steps=e2e_steps)
+    return out
