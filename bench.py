@@ -227,7 +227,8 @@ def run_gpu(args):
     for _ in range(args.warmup):
         res = P.two_stage_qr(V, A)
     torch.cuda.synchronize()
-    loss, resid = gram_check(V, A, res)
+    rep = P.compute_metrics(V, A, res, augmented=True)   # GPU metrics judge (metrics.py)
+    loss, resid = rep.loss_orth, rep.rel_residual
     del res
 
     # timed region: K steps, inputs (24 GiB) >> L2 (126 MB), no flush needed

@@ -124,6 +124,17 @@ int ots_householder_qr_c128(ots_ctx* ctx, int64_t m, int64_t k,
                             const void* A, int64_t lda, void* Q, int64_t ldq,
                             void* R, int64_t ldr, int nonneg_diag, void* stream);
 
+/* compute_metrics(v, a, result, augmented) / orthogonality_loss(q, v)
+ *                                                  -- metrics.py:25-73
+ * Gram-based on the device: out3 (host) = {loss_orth,
+ * cross_orth, rel_residual}.  V may be null (k0 = 0), A null (no residual);
+ * E: n x k device scratch for a - v s - q r.  1 <= k <= 64, k0 <= 512. */
+int ots_stability_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                      const double* V, int64_t ldv, const double* A, int64_t lda,
+                      const double* Q, int64_t ldq, const double* R, int64_t ldr,
+                      const double* S, int64_t lds, int augmented,
+                      double* E, int64_t lde, double* out3, void* stream);
+
 /* shifted_cholesky_qr(a)                          -- core.py:177-202
  * shifted CholeskyQR + 2 refinements; NotPositiveDefinite on breakdown. */
 int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,

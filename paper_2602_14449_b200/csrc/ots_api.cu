@@ -1243,3 +1243,4 @@ int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign, doub
 }  // extern "C"
 
 #include "zpath.inc"
+#include "metrics.inc"

@@ -473,7 +473,7 @@ __device__ double blk_sigma_max(double* W, int ld, int n, double* sig, double* r
 // tridiagonalisation (dsytd2, lower) followed by parallel multisection on the
 // Sturm count of the tridiagonal (dstebz-style, one shift per thread).
 // vec: >= 4 n doubles of scratch (shared memory preferred).
-__device__ double blk_sym_lmax(double* S, int lds, int n, double* vec, double* red) {
+__device__ void blk_tridiag(double* S, int lds, int n, double* vec, double* red) {
   double* v = vec;           // Householder vector
   double* pw = vec + n;      // p, then w
   double* d = vec + 2 * n;   // diagonal
@@ -526,46 +526,84 @@ __device__ double blk_sym_lmax(double* S, int lds, int n, double* vec, double* r
     d[n - 1] = S[(n - 1) * lds + n - 1];
   }
   __syncthreads();
-  // Gershgorin upper bound; max diagonal is a lower bound of lambda_max
-  double lo = -1.7976931348623157e308, hi = lo, e2max = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double el = (i > 0) ? fabs(e[i - 1]) : 0.0, er = (i + 1 < n) ? fabs(e[i]) : 0.0;
-    lo = fmax(lo, d[i]);
-    hi = fmax(hi, d[i] + el + er);
-    e2max = fmax(e2max, er * er);
-  }
-  lo = block_max(lo, red);
-  hi = block_max(hi, red);
-  e2max = block_max(e2max, red);
-  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, e2max);
-  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) pw[i] = e[i] * e[i];
+}
+
+// kth smallest eigenvalue (0-based) of the symmetric tridiagonal (d, e) left
+// by blk_tridiag, in [lo, hi]: 512-way multisection on the Sturm count
+// (count(x) = #eigenvalues < x), dstebz-style pivmin guard.  Uses vec+n for e^2.
+__device__ double blk_sturm_kth(double* vec, int n, int kth, double lo, double hi, double pivmin) {
+  double* e2 = vec + n;
+  const double* d = vec + 2 * n;
+  const double* e = vec + 3 * n;
+  __syncthreads();
+  for (int i = threadIdx.x; i + 1 < n; i += blockDim.x) e2[i] = e[i] * e[i];
   __syncthreads();
   const int NT = blockDim.x;
-  __shared__ int first_full;
+  __shared__ int first_hit;
   for (int it = 0; it < 64; ++it) {
     if (!(hi - lo > 2.2e-16 * fmax(fabs(lo), fabs(hi)) + pivmin)) break;
-    // x_t = lo + (hi - lo) (t + 1) / (NT + 1); count of eigenvalues < x_t
     const double xt = lo + (hi - lo) * (double)(threadIdx.x + 1) / (double)(NT + 1);
     int cnt = 0;
     double q = d[0] - xt;
     if (fabs(q) < pivmin) q = -pivmin;
     cnt += (q < 0.0);
     for (int i = 1; i < n; ++i) {
-      q = (d[i] - xt) - pw[i - 1] / q;
+      q = (d[i] - xt) - e2[i - 1] / q;
       if (fabs(q) < pivmin) q = -pivmin;
       cnt += (q < 0.0);
     }
-    if (threadIdx.x == 0) first_full = NT;
+    if (threadIdx.x == 0) first_hit = NT;
     __syncthreads();
-    if (cnt >= n) atomicMin(&first_full, (int)threadIdx.x);
+    if (cnt >= kth + 1) atomicMin(&first_hit, (int)threadIdx.x);
     __syncthreads();
-    const int t = first_full;
+    const int t = first_hit;
     const double nlo = (t == 0) ? lo : lo + (hi - lo) * (double)t / (double)(NT + 1);
     const double nhi = (t == NT) ? hi : lo + (hi - lo) * (double)(t + 1) / (double)(NT + 1);
     lo = nlo; hi = nhi;
     __syncthreads();
   }
   return 0.5 * (lo + hi);
+}
+
+// Gershgorin bounds of the tridiagonal and the pivmin guard
+__device__ void blk_tridiag_bounds(const double* vec, int n, double* red, double& glo, double& ghi,
+                                   double& dmax, double& pivmin) {
+  const double* d = vec + 2 * n;
+  const double* e = vec + 3 * n;
+  double lo = 1.7976931348623157e308, hi = -lo, dm = -lo, e2max = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double el = (i > 0) ? fabs(e[i - 1]) : 0.0, er = (i + 1 < n) ? fabs(e[i]) : 0.0;
+    lo = fmin(lo, d[i] - el - er);
+    hi = fmax(hi, d[i] + el + er);
+    dm = fmax(dm, d[i]);
+    e2max = fmax(e2max, er * er);
+  }
+  glo = -block_max(-lo, red);
+  ghi = block_max(hi, red);
+  dmax = block_max(dm, red);
+  e2max = block_max(e2max, red);
+  pivmin = 2.2250738585072014e-308 * fmax(1.0, e2max);
+}
+
+// Largest eigenvalue of a symmetric n x n matrix S (overwritten): Householder
+// tridiagonalisation (dsytd2, lower) followed by parallel multisection on the
+// Sturm count of the tridiagonal (dstebz-style, one shift per thread).
+// vec: >= 4 n doubles of scratch (shared memory preferred).
+__device__ double blk_sym_lmax(double* S, int lds, int n, double* vec, double* red) {
+  blk_tridiag(S, lds, n, vec, red);
+  double glo, ghi, dmax, pivmin;
+  blk_tridiag_bounds(vec, n, red, glo, ghi, dmax, pivmin);
+  return blk_sturm_kth(vec, n, n - 1, dmax, ghi, pivmin);   // lambda_max >= max diagonal
+}
+
+// (lambda_min, lambda_max) of a symmetric S (overwritten)
+__device__ void blk_sym_extremes(double* S, int lds, int n, double* vec, double* red, double& lmin,
+                                 double& lmax) {
+  blk_tridiag(S, lds, n, vec, red);
+  double glo, ghi, dmax, pivmin;
+  blk_tridiag_bounds(vec, n, red, glo, ghi, dmax, pivmin);
+  lmax = blk_sturm_kth(vec, n, n - 1, dmax, ghi, pivmin);
+  lmin = blk_sturm_kth(vec, n, 0, glo, ghi, pivmin);
 }
 
 // ---------------------------------------------------------------------------
@@ -1091,6 +1129,69 @@ void debug_counters_small(unsigned long long* out, int reset) {
 #else
   (void)out; (void)reset;
 #endif
+}
+
+// Stability metrics from Gram blocks (metrics.py:25-73 restated for the GPU,
+// SURVEY 8(f)): loss = max |lambda(G) - 1| over the Gram of q (or of [v, q]),
+// cross = ||v^* q||_F, residual = sqrt(lambda_max(E^T E) / lambda_max(A^T A))
+// with E = a - v s - q r formed explicitly.  Symmetric inputs: lower valid.
+__global__ void __launch_bounds__(SMALL_NT) stability_kernel(const double* Gvv, long ldvv, const double* Gvq,
+                                                             long ldvq, const double* Gqq, long ldqq,
+                                                             const double* Gee, long ldee, const double* Gaa,
+                                                             long ldaa, int k0, int k, int augmented,
+                                                             double* work, double* out3) {
+  __shared__ double red[64];
+  const int m = augmented ? k0 + k : k;
+  double* M = work;                 // m x m
+  double* vec = work + (long)m * m; // 4 m
+  auto lowsym = [](const double* G, long ld, int i, int j) { return (j <= i) ? G[i * ld + j] : G[j * ld + i]; };
+  BLK_FOR(e, m * m) {
+    const int i = e / m, j = e - i * m;
+    double x;
+    if (!augmented) x = lowsym(Gqq, ldqq, i, j);
+    else if (i < k0 && j < k0) x = lowsym(Gvv, ldvv, i, j);
+    else if (i < k0) x = Gvq[(long)i * ldvq + (j - k0)];
+    else if (j < k0) x = Gvq[(long)j * ldvq + (i - k0)];
+    else x = lowsym(Gqq, ldqq, i - k0, j - k0);
+    M[e] = x - (i == j ? 1.0 : 0.0);
+  }
+  double cr = 0.0;
+  if (Gvq) BLK_FOR(e, k0 * k) { const double x = Gvq[(long)(e / k) * ldvq + (e % k)]; cr = fma(x, x, cr); }
+  cr = block_sum(cr, red);
+  __syncthreads();
+  double lmin = 0.0, lmax = 0.0;
+  if (m > 0) blk_sym_extremes(M, m, m, vec, red, lmin, lmax);
+  const double loss = fmax(fabs(lmax), fabs(lmin));
+  double resid = 0.0;
+  if (Gee) {
+    BLK_FOR(e, k * k) { const int i = e / k, j = e - i * k; M[e] = lowsym(Gee, ldee, i, j); }
+    __syncthreads();
+    const double le = blk_sym_lmax(M, k, k, vec, red);
+    BLK_FOR(e, k * k) { const int i = e / k, j = e - i * k; M[e] = lowsym(Gaa, ldaa, i, j); }
+    __syncthreads();
+    const double la = blk_sym_lmax(M, k, k, vec, red);
+    resid = (la > 0.0) ? sqrt(fmax(le, 0.0) / la) : 0.0;
+  }
+  if (threadIdx.x == 0) { out3[0] = loss; out3[1] = sqrt(cr); out3[2] = resid; }
+}
+
+cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, long ldvq, const double* Gqq,
+                             long ldqq, const double* Gee, long ldee, const double* Gaa, long ldaa, int k0, int k,
+                             int augmented, double* work, double* out3, cudaStream_t st) {
+  stability_kernel<<<1, SMALL_NT, 0, st>>>(Gvv, ldvv, Gvq, ldvq, Gqq, ldqq, Gee, ldee, Gaa, ldaa, k0, k,
+                                           augmented, work, out3);
+  return cudaGetLastError();
+}
+
+__global__ void neg_copy_kernel(const double* X, long ldx, int r, int c, double* Y, long ldy) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < r * c; e += gridDim.x * blockDim.x) {
+    const int i = e / c, j = e - i * c;
+    Y[i * ldy + j] = -X[i * ldx + j];
+  }
+}
+cudaError_t launch_neg_copy(const double* X, long ldx, int r, int c, double* Y, long ldy, cudaStream_t st) {
+  neg_copy_kernel<<<32, 256, 0, st>>>(X, ldx, r, c, Y, ldy);
+  return cudaGetLastError();
 }
 
 #include "zsmall.inc"

@@ -60,6 +60,10 @@ struct ZState {
 };
 
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st);
+cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, long ldvq, const double* Gqq,
+                             long ldqq, const double* Gee, long ldee, const double* Gaa, long ldaa, int k0, int k,
+                             int augmented, double* work, double* out3, cudaStream_t st);
+cudaError_t launch_neg_copy(const double* X, long ldx, int r, int c, double* Y, long ldy, cudaStream_t st);
 cudaError_t launch_zseed(const ZState& z, cudaStream_t st);
 cudaError_t launch_zz2(const ZState& z, const double* Y2r, long ldy, void* Qtop, long ldq, cudaStream_t st);
 cudaError_t launch_zsign(const ZState& z, const void* Qtop, long ldq, const void* Rfin, int ldr, void* Rout,

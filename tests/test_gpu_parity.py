@@ -295,3 +295,26 @@ def test_stream_front_end_matches_calls():
     assert len(got) == 3
     for (q, r_, s), ref in zip(got, refs):
         assert rel(q, ref.q) < 1e-13 and rel(r_, ref.r) < 1e-13 and rel(s, ref.s) < 1e-13
+
+
+@pytest.mark.parametrize("case", ["small", "augmented", "illcond"])
+def test_gpu_metrics_vs_oracle(case):
+    """metrics.py (compute_metrics / orthogonality_loss) on the GPU against the
+    oracle's SVD-based values (loss and cross absolute to 1e-13, residual to 1e-3
+    relative or 1e-16 absolute)."""
+    rng = np.random.default_rng(9)
+    n, k0, k = 20000, 48, 24
+    v = np.linalg.qr(rng.standard_normal((n, k0)))[0]
+    a = rng.standard_normal((n, k))
+    if case == "illcond":
+        a[:, 1] = a[:, 0] + 1e-9 * a[:, 1]
+    res = P.two_stage_qr(v, a)
+    loss, cross, resid = O.stability(v, a, res.q, res.r, res.s)
+    rep = P.compute_metrics(v, a, res, augmented=(case != "small"))
+    if case == "small":
+        loss = float(np.max(np.abs(np.linalg.svd(res.q, compute_uv=False) ** 2 - 1)))
+    assert abs(rep.loss_orth - loss) < 1e-13
+    assert abs(rep.cross_orth - cross) < 1e-13
+    assert abs(rep.rel_residual - resid) <= max(1e-3 * resid, 1e-16)
+    assert rep.kappa_t == res.diagnostics.kappa_t
+    assert abs(P.orthogonality_loss(res.q, v=v) - O.stability(v, a, res.q, res.r, res.s)[0]) < 1e-13
