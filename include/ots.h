@@ -119,6 +119,16 @@ int ots_b_two_stage_diag_c128(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
                               double orth_tol, void* Q, int64_t ldq, void* R, int64_t ldr,
                               void* S, int64_t lds, double* diag_host, void* stream);
 
+/* shifted_cholesky_qr(a)                          -- core.py:177-202, c128 */
+int ots_shifted_cholesky_qr_c128(ots_ctx* ctx, int64_t m, int64_t k,
+                                 const void* A, int64_t lda, void* Q, int64_t ldq,
+                                 void* R, int64_t ldr, void* stream);
+
+/* modified_lu(z)                                  -- reflector.py:53-77, c128
+ * LU packed complex (ld n), p real (n). */
+int ots_modified_lu_c128(ots_ctx* ctx, int64_t n, const void* Z, int64_t ldz,
+                         void* LU, double* p, void* stream);
+
 /* householder_qr(a, nonneg_diag)                  -- core.py:61-84, c128 */
 int ots_householder_qr_c128(ots_ctx* ctx, int64_t m, int64_t k,
                             const void* A, int64_t lda, void* Q, int64_t ldq,

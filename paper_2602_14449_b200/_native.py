@@ -68,6 +68,8 @@ def lib():
                 L.ots_two_stage_c128.argtypes = L.ots_two_stage_f64.argtypes
                 L.ots_householder_qr_c128.argtypes = L.ots_householder_qr_f64.argtypes
                 L.ots_b_two_stage_diag_c128.argtypes = L.ots_b_two_stage_diag_f64.argtypes
+                L.ots_shifted_cholesky_qr_c128.argtypes = L.ots_shifted_cholesky_qr_f64.argtypes
+                L.ots_modified_lu_c128.argtypes = L.ots_modified_lu_f64.argtypes
                 L.ots_stability_f64.argtypes = [
                     _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int,
                     _vp, _i64, C.POINTER(_dbl), _vp]
@@ -94,6 +96,7 @@ EXPORTED_SYMBOLS = [
     "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_version",
     "ots_two_stage_f64", "ots_householder_qr_f64", "ots_modified_lu_f64",
     "ots_two_stage_c128", "ots_householder_qr_c128", "ots_b_two_stage_diag_c128", "ots_stability_f64",
+    "ots_shifted_cholesky_qr_c128", "ots_modified_lu_c128",
     "ots_shifted_cholesky_qr_f64", "ots_b_two_stage_diag_f64",
     "ots_build_reflector_f64", "ots_reflector_destroy", "ots_apply_reflector_f64",
     "ots_reflector_diagnostics_f64", "ots_reflector_tsolve_f64", "ots_reflector_get_f64",

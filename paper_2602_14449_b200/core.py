@@ -99,10 +99,17 @@ def shifted_cholesky_qr(a, refine_passes=2):
     m, n = a.shape
     if m < n:
         raise E.DimensionError(f"need rows >= cols, got {m}x{n}")
-    if is_complex(a):
-        raise NotImplementedError("complex shifted_cholesky_qr: not in this build")
     dev = D.pick_device(a)
     ctx = D.ctx(dev)
+    if is_complex(a):
+        A = D.cto_device(a, dev)
+        Q = D.cempty(m, n, dev)
+        R = D.czeros(n, n, dev)
+        if n:
+            rc = lib().ots_shifted_cholesky_qr_c128(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
+                                                    D.stream_ptr(dev))
+            check(rc, ctx)
+        return QRPair(out_like(was_torch, Q), out_like(was_torch, R))
     A = D.to_device(a, dev)
     Q = D.empty(m, n, dev)
     R = D.zeros(n, n, dev)

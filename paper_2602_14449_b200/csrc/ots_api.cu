@@ -117,6 +117,8 @@ struct ots_ctx {
   int launches = 0;
   char* b_ws = nullptr;      // B-inner scaled copies
   size_t b_size = 0;
+  char* z_ws = nullptr;      // complex cholshift ping-pong buffer
+  size_t z_size = 0;
   // distributed job state
   struct Job* job = nullptr;
 };
@@ -712,6 +714,7 @@ void ots_ctx_destroy(ots_ctx* c) {
   cudaSetDevice(c->device);
   if (c->ws) cudaFree(c->ws);
   if (c->b_ws) cudaFree(c->b_ws);
+  if (c->z_ws) cudaFree(c->z_ws);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_seed) cudaEventDestroy(c->ev_seed);
   if (c->ev_diag) cudaEventDestroy(c->ev_diag);
@@ -733,6 +736,7 @@ int ots_debug_counters(unsigned long long* out, int reset) { return ots::debug_c
 
 int ots_fp64_peak(ots_ctx* ctx, double* tflops) {
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   CK(fp64_peak(ctx->nsm, nullptr, tflops));
   return OTS_OK;
 }
@@ -758,6 +762,7 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
                       double* S, int64_t lds, double* diag_host, void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 0 || k0 < 0 || k < 0) return fail(ctx, OTS_E_DIMENSION, "negative dimension");
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
@@ -825,6 +830,7 @@ int ots_build_reflector_f64(ots_ctx* ctx, int64_t n, int64_t k0, const double* V
                             double* defect_host, void* stream) {
   if (!ctx || !out) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (k0 > n) return fail(ctx, OTS_E_DIMENSION, "v must be tall");
   if (k0 == 0) return fail(ctx, OTS_E_DIMENSION, "v must have at least one column");
@@ -866,6 +872,7 @@ int ots_apply_reflector_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, const do
                             double* Y, int64_t ldy, int adjoint, void* stream) {
   if (!ctx || !r) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (m == 0) return OTS_OK;
   if (m > 64) return fail(ctx, OTS_E_UNSUPPORTED, "apply_reflector: at most 64 columns per call");
@@ -892,6 +899,7 @@ int ots_apply_reflector_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, const do
 int ots_reflector_diagnostics_f64(ots_ctx* ctx, const ots_refl* r, double* diag_host, void* stream) {
   if (!ctx || !r) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   JobCfg c{r->n, 0, r->k0, 1, r->V, r->ldv, r->V, r->ldv, nullptr, 0, r->choice, nullptr, 0, 1.0, 1, st, false};
   Job j;
@@ -912,6 +920,7 @@ int ots_reflector_tsolve_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, double*
                              void* stream) {
   if (!ctx || !r) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   SmallState s = r->s;
   CK(launch_tsolve(s, B, (int)ldb, (int)m, adjoint, (cudaStream_t)stream));
   CK(cudaStreamSynchronize((cudaStream_t)stream));
@@ -931,6 +940,7 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, 
                            int64_t ldq, double* R, int64_t ldr, int nonneg_diag, void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (m < k) return fail(ctx, OTS_E_DIMENSION, "need rows >= cols");
   if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
@@ -977,6 +987,7 @@ int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, con
                              double* S, int64_t lds, double* diag_host, void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
   if (k > 64 || k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
@@ -1021,6 +1032,7 @@ int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double
                                 int64_t ldq, double* R, int64_t ldr, void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (m < k) return fail(ctx, OTS_E_DIMENSION, "need rows >= cols");
   if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
@@ -1046,6 +1058,7 @@ int ots_modified_lu_f64(ots_ctx* ctx, int64_t n, const double* Z, int64_t ldz, d
                         void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (n <= 0) return OTS_OK;
   if (n > 512) return fail(ctx, OTS_E_UNSUPPORTED, "n > 512");
@@ -1065,6 +1078,7 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
                    int64_t ldv, const double* A, int64_t lda, double* Q, int64_t ldq, int choice,
                    const double* P, int64_t ldp, double orth_tol, void* stream) {
   cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   if (k > 64 || k0 > 512 || k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "shape not in this build");
   if (row0 == 0 && n_local < k0 + k) return fail(ctx, OTS_E_DIMENSION, "rank 0 must own >= k0+k rows");
   int rc;

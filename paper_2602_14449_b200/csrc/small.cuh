@@ -65,6 +65,11 @@ cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, lo
                              int augmented, double* work, double* out3, cudaStream_t st);
 cudaError_t launch_neg_copy(const double* X, long ldx, int r, int c, double* Y, long ldy, cudaStream_t st);
 cudaError_t launch_zseed(const ZState& z, cudaStream_t st);
+cudaError_t launch_zcholqr_step(const double* Gr, long ldg, int k, long m, int shift, void* W, int ld,
+                                double* Zx, int ldzx, void* R, int* status, cudaStream_t st);
+cudaError_t launch_zmlu(const void* Z, int ldz, int n, void* LU, double* p, double* work, int* status,
+                        cudaStream_t st);
+cudaError_t launch_zidentity(void* D, int n, int ld, cudaStream_t st);
 cudaError_t launch_zz2(const ZState& z, const double* Y2r, long ldy, void* Qtop, long ldq, cudaStream_t st);
 cudaError_t launch_zsign(const ZState& z, const void* Qtop, long ldq, const void* Rfin, int ldr, void* Rout,
                          long ldro, cudaStream_t st);

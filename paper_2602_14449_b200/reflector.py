@@ -180,22 +180,22 @@ def modified_lu(z):
     k = z.shape[0]
     if z.shape[0] != z.shape[1]:
         raise E.DimensionError(f"modified_lu needs a square matrix, got {tuple(z.shape)}")
-    if is_complex(z):
-        raise NotImplementedError("complex modified_lu: not in this build")
+    cplx = is_complex(z)
     if k == 0:
-        e = np.zeros((0, 0))
+        e = np.zeros((0, 0), dtype=np.complex128 if cplx else np.float64)
         return MLUResult(np.ones(0), e, e)
     dev = D.pick_device(z)
     ctx = D.ctx(dev)
-    Z = D.to_device(z, dev)
+    Z = (D.cto_device if cplx else D.to_device)(z, dev)
     t = D.torch()
-    LU = t.empty((k, k), dtype=t.float64, device=f"cuda:{dev}")
+    dt = t.complex128 if cplx else t.float64
+    LU = t.empty((k, k), dtype=dt, device=f"cuda:{dev}")
     p = t.empty((k,), dtype=t.float64, device=f"cuda:{dev}")
     import ctypes as C
-    rc = lib().ots_modified_lu_f64(ctx, k, Z.ptr, Z.ld, C.c_void_p(LU.data_ptr()),
-                                   C.c_void_p(p.data_ptr()), D.stream_ptr(dev))
+    fn = lib().ots_modified_lu_c128 if cplx else lib().ots_modified_lu_f64
+    rc = fn(ctx, k, Z.ptr, Z.ld, C.c_void_p(LU.data_ptr()), C.c_void_p(p.data_ptr()), D.stream_ptr(dev))
     check(rc, ctx)
-    lo = t.tril(LU, -1) + t.eye(k, dtype=t.float64, device=LU.device)
+    lo = t.tril(LU, -1) + t.eye(k, dtype=dt, device=LU.device)
     up = t.triu(LU)
     if was_torch:
         return MLUResult(p, lo, up)

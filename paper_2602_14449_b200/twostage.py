@@ -94,8 +94,6 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         raise E.ParameterError(f"unknown intra method {intra!r}; expected {INTRA_METHODS}")
     dev = D.pick_device(v, a)
     ctx = D.ctx(dev)
-    if cplx and intra != "householder":
-        raise NotImplementedError("complex intra='cholshift': not in this build")
     todev = D.cto_device if cplx else D.to_device
     V = todev(v, dev)
     A = todev(a, dev)

@@ -141,3 +141,45 @@ def test_complex_binner_diag_config4_like():
     W = np.hstack([v, res.q])
     G = W.conj().T @ (d[:, None] * W)
     assert np.abs(G - np.eye(k0 + k)).max() <= 10 * n * U
+
+
+@pytest.mark.parametrize("shape", [(500, 8), (20000, 48), (100000, 64)])
+def test_complex_shifted_cholesky_qr(shape):
+    """core.py:177-202 on c128 (shifted CholeskyQR + 2 refinements)."""
+    rng = np.random.default_rng(shape[1])
+    a = cgauss(rng, *shape)
+    q0, r0 = O.cholqr_shifted(a)
+    res = P.shifted_cholesky_qr(a)
+    assert rel(res.r, r0) < 1e-10
+    assert rel(res.q, q0) < 1e-10
+    assert np.all(np.diag(res.r).real > 0)
+
+
+def test_complex_shifted_cholesky_breakdown():
+    a = np.zeros((100, 4), dtype=np.complex128)
+    a[:, 0] = 1.0
+    with pytest.raises(P.NotPositiveDefinite):
+        P.shifted_cholesky_qr(a)
+
+
+@pytest.mark.parametrize("choice", ["qr", "mlu"])
+def test_complex_two_stage_cholshift_oracle(choice):
+    rng = np.random.default_rng(17)
+    n, k0, k = 8000, 24, 16
+    v, _ = np.linalg.qr(cgauss(rng, n, k0))
+    a = cgauss(rng, n, k)
+    ref = O.two_stage(v, a, choice, intra_method="cholshift")
+    res = P.two_stage_qr(v, a, choice=choice, intra="cholshift")
+    assert rel(res.q, ref["q"]) < 1e-10
+    assert rel(res.r, ref["r"]) < 1e-10
+    assert rel(res.s, ref["s"]) < 1e-10
+
+
+@pytest.mark.parametrize("n", [1, 5, 40])
+def test_complex_modified_lu(n):
+    rng = np.random.default_rng(n)
+    z = np.linalg.qr(cgauss(rng, 2 * n, n))[0][:n]   # ||z|| <= 1
+    p0, l0, u0 = O.mlu(z)
+    res = P.modified_lu(z)
+    assert np.array_equal(np.asarray(res.p_diag), p0)
+    assert rel(res.l, l0) < 1e-12 and rel(res.u_tri, u0) < 1e-12
