@@ -68,8 +68,6 @@ def lib():
                 L.ots_two_stage_c128.argtypes = L.ots_two_stage_f64.argtypes
                 L.ots_householder_qr_c128.argtypes = L.ots_householder_qr_f64.argtypes
                 L.ots_b_two_stage_diag_c128.argtypes = L.ots_b_two_stage_diag_f64.argtypes
-                L.ots_shifted_cholesky_qr_c128.argtypes = L.ots_shifted_cholesky_qr_f64.argtypes
-                L.ots_modified_lu_c128.argtypes = L.ots_modified_lu_f64.argtypes
                 L.ots_stability_f64.argtypes = [
                     _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int,
                     _vp, _i64, C.POINTER(_dbl), _vp]
@@ -88,9 +86,17 @@ def lib():
                 L.ots_dist_tree.argtypes = [_vp, _vp, _int, _int]
                 L.ots_dist_qform.argtypes = [_vp, _vp, _vp]
                 L.ots_dist_finish.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _i64, C.POINTER(_dbl)]
+                # complex variants share their real twins' signatures (set above)
+                L.ots_shifted_cholesky_qr_c128.argtypes = L.ots_shifted_cholesky_qr_f64.argtypes
+                L.ots_modified_lu_c128.argtypes = L.ots_modified_lu_f64.argtypes
+                for fn in EXPORTED_SYMBOLS:
+                    if fn.startswith("ots_") and getattr(L, fn).argtypes is None and fn not in _NO_ARGS:
+                        raise E.NativeUnavailable(f"{fn}: argtypes not declared")
                 _lib = L
     return _lib
 
+
+_NO_ARGS = {"ots_version"}
 
 EXPORTED_SYMBOLS = [
     "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_version",

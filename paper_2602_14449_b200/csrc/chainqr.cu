@@ -219,7 +219,8 @@ struct BlkCfg {
   static constexpr int NP = KT / NB;     // panels (= warps that own columns)
   static constexpr int YS = 12;          // Y slot row stride: 2 wavefronts per 32-lane access
   static constexpr int YSLOT = B * YS;
-  static constexpr int XS0 = (2 * KT * KT + KT > 2 * YSLOT) ? 2 * KT * KT + KT : 2 * YSLOT;
+  static constexpr int NSLOT = 3;       // Y ring: a deferred apply reads Y_p one panel later
+  static constexpr int XS0 = (2 * KT * KT + KT > NSLOT * YSLOT) ? 2 * KT * KT + KT : NSLOT * YSLOT;
   static constexpr int XS = (XS0 > KT * (KT + 4) ? XS0 : KT * (KT + 4)) + 64;  // head U|T, Y slots, Tw
   static constexpr int SMEM = (KT * KT + XS + NP * 64 + 8 * 64) * 8;
 };
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   // ---- structured tiles (register-resident, see BlkCfg)
   const bool owner = warp < NP;
   const int mycol = 8 * warp + ((tid & 31) >> 2);
-  double* Ys = Xs;                                  // 2 panel slots of Y
+  double* Ys = Xs;                                  // NSLOT panel slots of Y
   double x[16][2];
   if (owner && ntiles > 0) {
     const long g0 = r0 + KT;
@@ -591,11 +592,16 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     const long rem = a.G.nrows - gr0;
     const int nb = (int)(rem < b ? rem : b);
     TSTAMP(t1);
+    // The owner of the next panel (p+1) shares its SM sub-partition with warp
+    // (p+1)^4; that warp defers its DMMA apply of panel p by one iteration so
+    // the latency-bound panel factorisation does not queue behind its DMMAs
+    // on the shared FP64 pipe.  A 3-slot Y ring keeps Y_p alive for it.
+    int pending = -1;
     for (int p = 0; p < NP; ++p) {
 #ifdef OTS_TIMING
       long long q0 = clock64();
 #endif
-      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p & 1) * C::YSLOT, Tp, tau_s, scr + warp * 64);
+      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tp, tau_s, scr + warp * 64);
 #ifdef OTS_TIMING
       if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
 #endif
@@ -603,12 +609,21 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
 #ifdef OTS_TIMING
       long long q1 = clock64();
 #endif
-      if (owner && warp != p) panel_apply<KT>(p, warp, x, S, Ys + (p & 1) * C::YSLOT, Tp);
+      if (owner && warp != p) {
+        const int defer_w = (p + 1 < NP) ? ((p + 1) ^ 4) : -1;
+        if (pending >= 0) {
+          panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tp);
+          pending = -1;
+        }
+        if (warp == defer_w) pending = p;
+        else panel_apply<KT>(p, warp, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tp);
+      }
 #ifdef OTS_TIMING
       if (warp == p + 1 && (tid & 31) == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - q1));
       if (tid == 0) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - q0));
 #endif
     }
+    if (pending >= 0) panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tp);
     __syncthreads();
     TSTAMP(t2);
     TACC(1, t1, t2);
