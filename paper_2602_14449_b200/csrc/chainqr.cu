@@ -221,7 +221,9 @@ struct BlkCfg {
   static constexpr int YSLOT = B * YS;
   static constexpr int NSLOT = 3;       // Y ring: a deferred apply reads Y_p one panel later
   static constexpr int XS0 = (2 * KT * KT + KT > NSLOT * YSLOT) ? 2 * KT * KT + KT : NSLOT * YSLOT;
-  static constexpr int XS = (XS0 > KT * (KT + 4) ? XS0 : KT * (KT + 4)) + 64;  // head U|T, Y slots, Tw
+  static constexpr int XS1 = NSLOT * YSLOT + NP * 64;   // Y slots + per-warp Gram scratch
+  static constexpr int XS2 = XS0 > XS1 ? XS0 : XS1;
+  static constexpr int XS = (XS2 > KT * (KT + 4) ? XS2 : KT * (KT + 4)) + 64;  // head U|T, Y slots, Tw
   static constexpr int SMEM = (KT * KT + XS + NP * 64 + 8 * 64) * 8;
 };
 
@@ -330,17 +332,9 @@ __device__ __forceinline__ bool panel_core(int p, double (&xr)[4][8], double* S,
     double rrow[8];
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) rrow[cc] = (cc >= jj) ? S[j * KT + j0 + cc] : 0.0;
-    double s2 = s2n;
-    if (EXACT || jj == 0) {
-      double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-      for (int i = 0; i < 4; i += 2) { s0 = fma(xr[i][jj], xr[i][jj], s0); s1 = fma(xr[i + 1][jj], xr[i + 1][jj], s1); }
-      s2 = warp_sum(s0 + s1);
-    }
-    double beta, tj, scal;
-    dlarfg_nb(rrow[jj], s2, beta, tj, scal);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) xr[i][jj] *= scal;
+    // Raw dots x_jj . x_cc of the UNSCALED column: they do not depend on the
+    // reflector scalars, so the warp reduction runs concurrently with dlarfg
+    // and the step's critical path is one reduction, not dlarfg + reduction.
     double d[8];
 #pragma unroll
     for (int cc = 0; cc < 8; ++cc) {
@@ -353,7 +347,21 @@ __device__ __forceinline__ bool panel_core(int p, double (&xr)[4][8], double* S,
         for (int i = 0; i < 4; ++i) d[cc] = fma(xr[i][jj + 1], xr[i][jj + 1], d[cc]);
       }
     }
+    double s2 = s2n;
+    if (EXACT || jj == 0) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < 4; i += 2) { s0 = fma(xr[i][jj], xr[i][jj], s0); s1 = fma(xr[i + 1][jj], xr[i + 1][jj], s1); }
+      s2 = warp_sum(s0 + s1);
+    }
     warp_sum8(d);
+    double beta, tj, scal;
+    dlarfg_nb(rrow[jj], s2, beta, tj, scal);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) xr[i][jj] *= scal;
+#pragma unroll
+    for (int cc = 0; cc < 8; ++cc)
+      if (cc != jj) d[cc] *= scal;            // v . x_cc  (G entries for cc < jj)
     if (jj + 1 < 8) {
       const double N = d[jj];
       const double vv = s2 * scal * scal;
@@ -391,6 +399,138 @@ __device__ __forceinline__ bool panel_core(int p, double (&xr)[4][8], double* S,
   return bad;
 }
 
+// Gram-form panel sweep (the fast path).  The 8 Householder steps of the
+// structured panel QR([R_pp; X_p]) only need, per step jj, the norm of the
+// current tile column x_jj and its dots with the later columns; all of them
+// follow from the panel Gram M = X_p^T X_p by exact rank-2 algebra:
+//   y_jj = scal x_jj,  x_b <- x_b - w_b y_jj  (b > jj),  w_b = tau (R_jb + y_jj.x_b)
+//   M[a][b] -= w_a c_b + w_b c_a          (jj < a <= b),  c_b = u_b - w_b yy/2
+//   M[a][b] -= w_b G[a][jj]               (a < jj < b),   G[a][jj] = scal M[a][jj]
+// with u_b = scal M[jj][b], yy = |y_jj|^2.  M comes from 32 DMMAs on the
+// quad-layout registers (no reduction tree), the 8 steps are uniform scalar
+// work in every lane (no shuffles on the step chain), and Y is formed
+// afterwards from the stored w / scal with the same FMAs as the exact sweep.
+// Accuracy: M's rounding is absolute in the panel-start norms, so every
+// pivot must keep at least half of its panel-start norm^2 (else the caller
+// replays the panel with the exact per-column reductions of panel_core<KT,true>).
+#define PANEL_SCAL(jj) ((jj) == 0 ? 56 : (jj) * 9 - 1)   // strict-lower slot of scr for scal_jj
+
+template <int KT>
+__device__ __forceinline__ bool panel_gram(int p, const double (&x)[16][2], double* S, double* T8,
+                                           double* tau_s, double* scr) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int j0 = p * 8;
+  const int lr = lane < 8 ? lane : 7;
+  {
+    double acc[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+    for (int f = 0; f < 16; ++f)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) dmma(acc[(2 * f + h) & 3], x[f][h], x[f][h]);
+    scr[g * 8 + 2 * t] = (acc[0][0] + acc[1][0]) + (acc[2][0] + acc[3][0]);
+    scr[g * 8 + 2 * t + 1] = (acc[0][1] + acc[1][1]) + (acc[2][1] + acc[3][1]);
+  }
+  __syncwarp();
+  double m[8][8];   // upper triangle used (compile-time indices after unrolling)
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; b += 2) {
+      if (b + 1 < a) continue;
+      const double2 v = *reinterpret_cast<const double2*>(scr + a * 8 + b);
+      m[a][b] = v.x;
+      m[a][b + 1] = v.y;
+    }
+  // scr keeps the panel-start diagonal M0[a][a] (at a*9) for the checks; the
+  // strict upper part then takes w[jj][b], the slot SCAL(jj) in the strict
+  // lower part scal_jj.  All lanes store the same uniform values (no branch
+  // splits the step chain into basic blocks).
+  __syncwarp();
+  double trow[8];                     // lane ii < 8: row ii of T_p
+#pragma unroll
+  for (int l = 0; l < 8; ++l) trow[l] = 0.0;
+  bool bad = false;
+  double rnext[8];
+#pragma unroll
+  for (int b = 0; b < 8; ++b) rnext[b] = S[j0 * KT + j0 + b];
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const int j = j0 + jj;
+    double rrow[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) rrow[b] = rnext[b];
+    if (jj + 1 < 8) {                 // prefetch R row j+1 (not written by this panel yet)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) rnext[b] = (b > jj) ? S[(j + 1) * KT + j0 + b] : 0.0;
+    }
+    const double s2 = m[jj][jj];
+    bad = bad || !(s2 >= 0.5 * scr[jj * 9]);
+    double beta, tj, scal;
+    dlarfg_nb(rrow[jj], s2, beta, tj, scal);
+    const double yy = scal * scal * s2;
+    double w[8], c[8], gcol[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      w[b] = c[b] = gcol[b] = 0.0;
+      if (b > jj) {
+        const double u = scal * m[jj][b];
+        w[b] = tj * (rrow[b] + u);
+        c[b] = fma(-0.5 * w[b], yy, u);
+      } else if (b < jj) {
+        gcol[b] = scal * m[b][jj];    // G[b][jj] = y_b . y_jj
+      }
+    }
+#pragma unroll
+    for (int b = jj + 1; b < 8; ++b) {
+#pragma unroll
+      for (int a = 0; a < jj; ++a) m[a][b] = fma(-w[b], gcol[a], m[a][b]);
+      m[jj][b] = fma(-0.5 * w[b], yy, c[b]);
+#pragma unroll
+      for (int a = jj + 1; a <= b; ++a) m[a][b] = fma(-w[a], c[b], fma(-w[b], c[a], m[a][b]));
+    }
+    // outputs: S row j (G | beta | R - w), tau, T_p row per lane, w / scal
+#pragma unroll
+    for (int b = 0; b < 8; b += 2) {
+      const double v0 = b < jj ? gcol[b] : (b == jj ? beta : rrow[b] - w[b]);
+      const double v1 = b + 1 < jj ? gcol[b + 1] : (b + 1 == jj ? beta : rrow[b + 1] - w[b + 1]);
+      *reinterpret_cast<double2*>(S + j * KT + j0 + b) = make_double2(v0, v1);
+    }
+    tau_s[j] = tj;
+#pragma unroll
+    for (int b = jj + 1; b < 8; ++b) scr[jj * 8 + b] = w[b];
+    scr[PANEL_SCAL(jj)] = scal;
+    double sacc = 0.0;
+#pragma unroll
+    for (int l = 0; l < jj; ++l) sacc = fma((l >= lr) ? trow[l] : 0.0, gcol[l], sacc);
+    trow[jj] = (lr == jj) ? tj : ((lr < jj) ? -tj * sacc : 0.0);
+  }
+  if (lane < 8) {
+#pragma unroll
+    for (int l = 0; l < 8; ++l) T8[lane * 8 + l] = trow[l];
+  }
+  __syncwarp();
+  return bad;
+}
+
+// Y_p from the stored w / scal (lane-per-row layout): y_jj = scal_jj x_jj,
+// x_b -= w_b y_jj -- the same FMAs, in the same order, as the exact sweep.
+__device__ __forceinline__ void panel_form_y(double (&xr)[4][8], const double* scr) {
+#pragma unroll
+  for (int jj = 0; jj < 8; ++jj) {
+    const double sc = scr[PANEL_SCAL(jj)];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) xr[i][jj] *= sc;
+#pragma unroll
+    for (int b = jj + 1; b < 8; ++b) {
+      const double w = scr[jj * 8 + b];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) xr[i][b] = fma(-w, xr[i][jj], xr[i][b]);
+    }
+  }
+}
+
 // Panel factorization by the owning warp.  The panel is transposed through
 // its Y slot into the lane-per-row layout so that v stays lane-local and the
 // 7 dot products of a step are one reduce-scatter over the warp; the
@@ -398,7 +538,7 @@ __device__ __forceinline__ bool panel_core(int p, double (&xr)[4][8], double* S,
 // layout of the registers.
 template <int KT>
 __device__ __forceinline__ void panel_factor(int p, double (&x)[16][2], double* S, double* Ys,
-                                             double* Tp, double* tau_s, double* save) {
+                                             double* Tp, double* tau_s, double* save, double* gscr) {
   constexpr int YS = BlkCfg<KT>::YS;
   const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int j0 = p * 8;
@@ -416,6 +556,9 @@ __device__ __forceinline__ void panel_factor(int p, double (&x)[16][2], double* 
   save[lane] = S[(j0 + (lane >> 3)) * KT + j0 + (lane & 7)];
   save[lane + 32] = S[(j0 + 4 + (lane >> 3)) * KT + j0 + (lane & 7)];
   __syncwarp();
+  PMARK(8);
+  double* T8 = Tp + p * 64;
+#ifdef OTS_PANEL_EXACT
   double xr[4][8];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -425,11 +568,22 @@ __device__ __forceinline__ void panel_factor(int p, double (&x)[16][2], double* 
       xr[i][c] = u.x;
       xr[i][c + 1] = u.y;
     }
-  PMARK(8);
-  double* T8 = Tp + p * 64;
   const bool bad = panel_core<KT, false>(p, xr, S, T8, tau_s);
+#else
+  const bool bad = panel_gram<KT>(p, x, S, T8, tau_s, gscr);
+  double xr[4][8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int c = 0; c < 8; c += 2) {
+      const double2 u = *reinterpret_cast<const double2*>(Ys + (lane + 32 * i) * YS + c);
+      xr[i][c] = u.x;
+      xr[i][c + 1] = u.y;
+    }
+  if (!bad) panel_form_y(xr, gscr);
+#endif
   PMARK(9);
-  if (__any_sync(0xffffffffu, bad)) {   // rare: replay with exact norms
+  if (__any_sync(0xffffffffu, bad)) {   // rare: replay with exact per-column reductions
     __syncwarp();
     S[(j0 + (lane >> 3)) * KT + j0 + (lane & 7)] = save[lane];
     S[(j0 + 4 + (lane >> 3)) * KT + j0 + (lane & 7)] = save[lane + 32];
@@ -592,6 +746,17 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     const long rem = a.G.nrows - gr0;
     const int nb = (int)(rem < b ? rem : b);
     TSTAMP(t1);
+    if (t < ntiles) {   // next tile -> L2 while this one is factored (its load is on the chain)
+      const long g1 = gr0 + b;
+      const long rem1 = a.G.nrows - g1;
+      const int nb1 = (int)(rem1 < b ? rem1 : b);
+      const int lpr = (a.ncols * 8 + 127) / 128;          // 128-byte lines per row
+      for (int i = tid; i < nb1 * lpr; i += 256) {
+        const int r = i / lpr, l = i - r * lpr;
+        const double* ptr = a.D + (g1 + r) * a.ldd + l * 16;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+      }
+    }
     // The owner of the next panel (p+1) shares its SM sub-partition with warp
     // (p+1)^4; that warp defers its DMMA apply of panel p by one iteration so
     // the latency-bound panel factorisation does not queue behind its DMMAs
@@ -601,7 +766,8 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
 #ifdef OTS_TIMING
       long long q0 = clock64();
 #endif
-      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tp, tau_s, scr + warp * 64);
+      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tp, tau_s, scr + warp * 64,
+                                      Xs + C::NSLOT * C::YSLOT + warp * 64);
 #ifdef OTS_TIMING
       if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
 #endif
