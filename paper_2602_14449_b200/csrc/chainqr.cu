@@ -221,10 +221,11 @@ struct BlkCfg {
   static constexpr int YSLOT = B * YS;
   static constexpr int NSLOT = 3;       // Y ring: a deferred apply reads Y_p one panel later
   static constexpr int XS0 = (2 * KT * KT + KT > NSLOT * YSLOT) ? 2 * KT * KT + KT : NSLOT * YSLOT;
-  static constexpr int XS1 = NSLOT * YSLOT + NP * 64;   // Y slots + per-warp Gram scratch
+  static constexpr int TWOFF = NSLOT * YSLOT + NP * 64;                  // packed T blocks
+  static constexpr int XS1 = TWOFF + (NP * (NP - 1) / 2) * 64;   // Y slots | Gram scratch | T blocks
   static constexpr int XS2 = XS0 > XS1 ? XS0 : XS1;
   static constexpr int XS = (XS2 > KT * (KT + 4) ? XS2 : KT * (KT + 4)) + 64;  // head U|T, Y slots, Tw
-  static constexpr int SMEM = (KT * KT + XS + NP * 64 + 8 * 64) * 8;
+  static constexpr int SMEM = (KT * KT + XS + 2 * NP * 64 + 8 * 64) * 8;
 };
 
 __device__ __forceinline__ void tile_regs_load(double (&x)[16][2], const double* D, long ldd, long gr0,
@@ -664,43 +665,42 @@ __device__ __forceinline__ void panel_apply(int p, int w, double (&x)[16][2], do
 }
 
 // T of a tile from tau (diag) and G (lower part of S), blockwise with DMMA:
-// T[q-block][p-block] = -(sum_{q'=q}^{p-1} T[q][q'] G[q'][p]) T_pp, one warp
-// per row block q < p, columns p = 1..NP-1 in order.  Tw stride KT+4.
+//   T[q][p] = -(sum_{q'=q}^{p-1} T[q][q'] G[q'][p]) T_pp      (q < p)
+// One warp per row block q.  The diagonal blocks are the panels' T_pp (Tpv);
+// the off-diagonal ones are packed 8x8 blocks in Tw.  Phase p of tile t only
+// reads G row block p, which tile t+1 overwrites after its panel-p barrier,
+// so the phases of tile t run on the warps q < p that are idle while tile
+// t+1's panel p is factored (off the chain's critical path).
+__device__ __forceinline__ int tw_off(int q, int p) { return ((p * (p - 1)) / 2 + q) * 64; }
+
 template <int KT>
-__device__ __forceinline__ void build_t(const double* S, const double* Tp, double* Tw, double* Tg,
-                                        double* scr) {
-  constexpr int NP = KT / 8, TL = KT + 4;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  for (int e = tid; e < KT * KT; e += 256) {
-    const int i = e / KT, j = e - i * KT;
-    Tw[i * TL + j] = ((i >> 3) == (j >> 3)) ? Tp[(i >> 3) * 64 + (i & 7) * 8 + (j & 7)] : 0.0;
-  }
-  __syncthreads();
-  double* sc = scr + warp * 64;
-  for (int p = 1; p < NP; ++p) {
-    if (warp < p) {
-      const int q = warp;
-      double m[2] = {0.0, 0.0};
-      for (int qq = q; qq < p; ++qq) {
+__device__ __forceinline__ void t_block(int q, int p, const double* S, const double* Tpv, double* Tw,
+                                        double* sc) {
+  const int lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  double m[2] = {0.0, 0.0};
+  for (int qq = q; qq < p; ++qq) {
+    const double* Tq = (qq == q) ? Tpv + q * 64 : Tw + tw_off(q, qq);
 #pragma unroll
-        for (int k0 = 0; k0 < 8; k0 += 4)
-          dmma(m, Tw[(8 * q + g) * TL + 8 * qq + k0 + t], S[(8 * p + g) * KT + 8 * qq + k0 + t]);
-      }
-      sc[g * 8 + 2 * t] = m[0];
-      sc[g * 8 + 2 * t + 1] = m[1];
-      __syncwarp();
-      double o[2] = {0.0, 0.0};
-#pragma unroll
-      for (int k0 = 0; k0 < 8; k0 += 4) dmma(o, sc[g * 8 + k0 + t], Tp[p * 64 + (k0 + t) * 8 + g]);
-      Tw[(8 * q + g) * TL + 8 * p + 2 * t] = -o[0];
-      Tw[(8 * q + g) * TL + 8 * p + 2 * t + 1] = -o[1];
-      __syncwarp();
-    }
-    __syncthreads();
+    for (int k0 = 0; k0 < 8; k0 += 4) dmma(m, Tq[g * 8 + k0 + t], S[(8 * p + g) * KT + 8 * qq + k0 + t]);
   }
-  for (int e = tid; e < KT * KT; e += 256) {
-    const int i = e / KT, j = e - i * KT;
-    Tg[e] = Tw[i * TL + j];
+  sc[g * 8 + 2 * t] = m[0];
+  sc[g * 8 + 2 * t + 1] = m[1];
+  __syncwarp();
+  double o[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k0 = 0; k0 < 8; k0 += 4) dmma(o, sc[g * 8 + k0 + t], Tpv[p * 64 + (k0 + t) * 8 + g]);
+  double* dst = Tw + tw_off(q, p) + g * 8 + 2 * t;
+  dst[0] = -o[0];
+  dst[1] = -o[1];
+  __syncwarp();
+}
+
+// full KT x KT T (upper block triangular, zeros below) -> global
+template <int KT>
+__device__ __forceinline__ void t_store(const double* Tpv, const double* Tw, double* Tg) {
+  for (int e = threadIdx.x; e < KT * KT; e += 256) {
+    const int i = e / KT, j = e - i * KT, qi = i >> 3, pj = j >> 3, r = (i & 7) * 8 + (j & 7);
+    Tg[e] = qi == pj ? Tpv[qi * 64 + r] : (qi < pj ? Tw[tw_off(qi, pj) + r] : 0.0);
   }
 }
 
@@ -710,8 +710,9 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   constexpr int NP = C::NP;
   extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
   double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
-  double* Tp = Xs + C::XS;                        // NP x 64
-  double* scr = Tp + NP * 64;                     // 8 warps x 64
+  double* Tp = Xs + C::XS;                        // 2 x NP x 64: panel T_pp, by tile parity
+  double* scr = Tp + 2 * NP * 64;                 // 8 warps x 64
+  double* Tw = Xs + C::TWOFF;                     // packed off-diagonal T blocks (previous tile)
   __shared__ double tau_s[KT];
   const int tid = threadIdx.x, warp = tid >> 5;
   const int chain = blockIdx.x;
@@ -742,6 +743,8 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
   }
   for (int t = 1; t <= ntiles; ++t) {
+    double* Tpc = Tp + (t & 1) * NP * 64;           // this tile's T_pp
+    const double* Tpp = Tp + ((t - 1) & 1) * NP * 64;   // previous tile's (its T is built now)
     const long gr0 = r0 + KT + (long)(t - 1) * b;
     const long rem = a.G.nrows - gr0;
     const int nb = (int)(rem < b ? rem : b);
@@ -766,8 +769,9 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
 #ifdef OTS_TIMING
       long long q0 = clock64();
 #endif
-      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tp, tau_s, scr + warp * 64,
+      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tpc, tau_s, scr + warp * 64,
                                       Xs + C::NSLOT * C::YSLOT + warp * 64);
+      else if (t > 1 && warp < p) t_block<KT>(warp, p, S, Tpp, Tw, scr + warp * 64);
 #ifdef OTS_TIMING
       if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
 #endif
@@ -778,18 +782,18 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
       if (owner && warp != p) {
         const int defer_w = (p + 1 < NP) ? ((p + 1) ^ 4) : -1;
         if (pending >= 0) {
-          panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tp);
+          panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tpc);
           pending = -1;
         }
         if (warp == defer_w) pending = p;
-        else panel_apply<KT>(p, warp, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tp);
+        else panel_apply<KT>(p, warp, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tpc);
       }
 #ifdef OTS_TIMING
       if (warp == p + 1 && (tid & 31) == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - q1));
       if (tid == 0) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - q0));
 #endif
     }
-    if (pending >= 0) panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tp);
+    if (pending >= 0) panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tpc);
     __syncthreads();
     TSTAMP(t2);
     TACC(1, t1, t2);
@@ -804,11 +808,21 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     }
     TSTAMP(t3);
     TACC(2, t2, t3);
-    build_t<KT>(S, Tp, Xs, Tbase + (long)t * KT * KT, scr);
-    __syncthreads();
+    if (t > 1) {                    // previous tile's T is complete (phase NP-1 ran in panel NP-1)
+      t_store<KT>(Tpp, Tw, Tbase + (long)(t - 1) * KT * KT);
+      __syncthreads();              // Tpp is this parity's buffer for tile t+1
+    }
     TSTAMP(t4);
     TACC(3, t3, t4);
     if (threadIdx.x == 0) TACC(4, 0, 1);
+  }
+  if (ntiles > 0) {                 // last tile: its T phases in sequence
+    const double* Tpl = Tp + (ntiles & 1) * NP * 64;
+    for (int p = 1; p < NP; ++p) {
+      if (warp < p) t_block<KT>(warp, p, S, Tpl, Tw, scr + warp * 64);
+      __syncthreads();
+    }
+    t_store<KT>(Tpl, Tw, Tbase + (long)ntiles * KT * KT);
   }
 
   // ---- chain R (upper triangle, exact zeros below)
