@@ -54,7 +54,12 @@ tsgemm_tn_kernel(TnArgs a) {
   int mi = 0, ni = 0, nhalf = 0;
   bool fromP = false, half = false;
   {
+    // Diagonal Gram blocks only form their lower-triangular fragments (10 of
+    // 16 DMMAs; every consumer reads the lower triangle), which unbalances the
+    // SM sub-partitions (warp w -> SMSP w % 4); for the hot 128 | 64 shape a
+    // swap of tasks 3 and 9 restores 66 DMMA units on each SMSP.
     int w = warp;
+    if (PW == 128 && BW == 64 && ALIAS && SYM) w = (warp == 3) ? 9 : (warp == 9 ? 3 : warp);
     if (C::NSPLIT && w >= C::NFULL - C::NSPLIT) {
       const int hw = w - (C::NFULL - C::NSPLIT);     // 0 .. 2*NSPLIT-1
       w = C::NFULL - C::NSPLIT + hw / 2;
@@ -127,7 +132,21 @@ tsgemm_tn_kernel(TnArgs a) {
     const double* Bs = fromP ? Ps : stage_b(s);
     const int BWs = fromP ? PW : (BW > 0 ? BW : 32);
     const int nb0 = fromP ? 32 * ni : 32 * ni;
-    if (!half) {
+    if (SYM && fromP && mi == ni && !half) {   // diagonal block: fragments i >= j only
+#pragma unroll
+      for (int kk = 0; kk < C::RT / 4; ++kk) {
+        const int r = 4 * kk + t;
+        double af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, nb0 + 8 * j + g, BWs)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+    } else if (!half) {
 #pragma unroll
       for (int kk = 0; kk < C::RT / 4; ++kk) {
         const int r = 4 * kk + t;
