@@ -23,6 +23,7 @@ struct NnArgs {
   int ncols;
   long row_begin, row_end;
   const double* colscale;                     // device, ncols entries of +-1, or null
+  int* tile_counter;                          // device ticket counter (dynamic tiles) or null
 };
 
 struct ChainGeom {

@@ -101,8 +101,10 @@ struct Level {
 struct ots_ctx {
   int device = 0;
   int nsm = 148;
-  cudaStream_t side = nullptr;
+  cudaStream_t side = nullptr;   // highest priority: its few CTAs go first, the
+                                 // dynamically scheduled apply1 tiles fill around them
   cudaEvent_t ev_seed = nullptr, ev_diag = nullptr;
+  int* nn_counter = nullptr;     // tile tickets of the NN updates
   char* ws = nullptr;
   size_t ws_size = 0;
   int* h_status = nullptr;   // pinned
@@ -460,6 +462,7 @@ int phase_apply1(ots_ctx* ctx, Job& j) {
   a.ncols = (int)c.k;
   a.row_begin = j.qrow0; a.row_end = c.n_local;
   a.colscale = nullptr;
+  a.tile_counter = ctx->nn_counter;
   CK(launch_tsgemm_nn(a, j.KT, ctx->nsm, c.st));
   return OTS_OK;
 }
@@ -504,6 +507,7 @@ int phase_apply2(ots_ctx* ctx, Job& j) {
   a.ncols = (int)c.k;
   a.row_begin = j.qrow0; a.row_end = c.n_local;
   a.colscale = j.svec;
+  a.tile_counter = ctx->nn_counter;
   CK(launch_tsgemm_nn(a, j.KT, ctx->nsm, c.st));
   return OTS_OK;
 }
@@ -645,10 +649,22 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   CK(launch_seed(j.s, st));
   CK(cudaEventRecord(ctx->ev_seed, st));
   prof_mark(ctx, st, "seed");
+  // The diagnostics (3 CTAs, ~2 ms) go on the main stream right behind the
+  // seed so they own their SMs before apply1's CTAs (side stream, released by
+  // an event a little later) fill the rest; apply1 hands out its tiles
+  // dynamically, so those 3 SMs simply take fewer.  The factor then starts on
+  // an idle GPU instead of waiting for the diagnostics' SMs.
+  CK(launch_diag(j.s, st));
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
-  CK(launch_diag(j.s, ctx->side));
-  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
-  if ((rc = phase_apply1(ctx, j))) return rc;
+  {
+    JobCfg c1 = j.c;
+    j.c.st = ctx->side;
+    rc = phase_apply1(ctx, j);
+    j.c = c1;
+    if (rc) return rc;
+  }
+  CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply1 done
+  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   prof_mark(ctx, st, "apply1");
   if (intra == OTS_INTRA_HOUSEHOLDER) {
     if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
@@ -676,7 +692,6 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     b_rsign_kernel<<<1, 256, 0, st>>>(R, ldr, (int)k);
     prof_mark(ctx, st, "b_epilogue");
   }
-  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   prof_mark(ctx, st, "tail");
   ctx->launches = 14 + 3 * (int)j.lv.size() + (bh ? 2 : 0);
   rc = read_status(ctx, j, diag_host);
@@ -698,7 +713,12 @@ int ots_ctx_create(int device, ots_ctx** out) {
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { c->err = cudaGetErrorString(e); *out = c; return OTS_E_CUDA; }
   cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device);
-  cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi);
+  }
+  cudaMalloc(&c->nn_counter, 256);
   cudaEventCreateWithFlags(&c->ev_seed, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_diag, cudaEventDisableTiming);
   cudaMallocHost(&c->h_status, 64);
@@ -716,6 +736,7 @@ void ots_ctx_destroy(ots_ctx* c) {
   if (c->b_ws) cudaFree(c->b_ws);
   if (c->z_ws) cudaFree(c->z_ws);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->nn_counter) cudaFree(c->nn_counter);
   if (c->ev_seed) cudaEventDestroy(c->ev_seed);
   if (c->ev_diag) cudaEventDestroy(c->ev_diag);
   if (c->h_status) cudaFreeHost(c->h_status);

@@ -238,14 +238,25 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
   const long nrows = a.row_end - a.row_begin;
   const long ntiles_total = (nrows + C::RT - 1) / C::RT;
   const int nchunks = (a.kdim + C::KC - 1) / C::KC;
-  const long my_tiles = ntiles_total > blockIdx.x ? (ntiles_total - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-  const long nit = my_tiles * nchunks;
-
-  auto tile_r0 = [&](long lt) { return a.row_begin + (blockIdx.x + lt * gridDim.x) * (long)C::RT; };
+  // Tiles: the CTA's first tile is blockIdx.x; with a ticket counter the later
+  // ones are handed out dynamically (gridDim.x + ticket), so CTAs that start
+  // late -- e.g. on SMs held by the concurrent diagnostics kernel -- take fewer
+  // tiles instead of stretching the tail.  Without it: static stride.
+  // 3-slot ring: slot (lt % 3) holds local tile lt; tile lt+2 is fetched at
+  // chunk 0 of tile lt, after a barrier that retires tile lt-1's slot.
+  __shared__ long s_tile[3];
+  const bool dyn = a.tile_counter != nullptr;
+  if (tid == 0) {
+    s_tile[0] = blockIdx.x;
+    s_tile[1] = dyn ? gridDim.x + atomicAdd(a.tile_counter, 1) : blockIdx.x + (long)gridDim.x;
+  }
+  __syncthreads();
+  auto tile_of = [&](long lt) { return s_tile[lt % 3]; };
+  auto tile_r0 = [&](long lt) { return a.row_begin + tile_of(lt) * (long)C::RT; };
   auto issue = [&](long it) {
-    if (it < nit) {
+    const long lt = it / nchunks;
+    if (tile_of(lt) < ntiles_total) {
       int s = (int)(it % C::NSTAGE);
-      long lt = it / nchunks;
       int ch = (int)(it - lt * nchunks);
       double* Ps = smem + s * C::STAGE;
       double* Zs = Ps + C::RT * C::KC;
@@ -309,9 +320,9 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
   };
 
   if (nchunks == 0) {  // X = B * colscale
-    for (long lt = 0; lt < my_tiles; ++lt) {
-      acc_from_b(tile_r0(lt));
-      epilogue_store(tile_r0(lt));
+    for (long r0 = a.row_begin + (long)blockIdx.x * C::RT; r0 < a.row_end; r0 += (long)gridDim.x * C::RT) {
+      acc_from_b(r0);
+      epilogue_store(r0);
     }
     return;
   }
@@ -319,12 +330,15 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
 #pragma unroll
   for (int s = 0; s < C::NSTAGE - 1; ++s) issue(s);
 
-  for (long it = 0; it < nit; ++it) {
+  for (long it = 0;; ++it) {
     const long lt = it / nchunks;
     const int ch = (int)(it - lt * nchunks);
+    if (tile_of(lt) >= ntiles_total) break;
     if (ch == 0) acc_from_b(tile_r0(lt));
     cp_async_wait<C::NSTAGE - 2>();
     __syncthreads();
+    if (ch == 0 && tid == 0)
+      s_tile[(lt + 2) % 3] = dyn ? gridDim.x + atomicAdd(a.tile_counter, 1) : tile_of(lt + 1) + gridDim.x;
     issue(it + C::NSTAGE - 1);
     const int s = (int)(it % C::NSTAGE);
     const double* Ps = smem + s * C::STAGE;
@@ -422,6 +436,10 @@ static cudaError_t launch_nn_t(const NnArgs& a, int nsm, cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   long tiles = (rows + C::RT - 1) / C::RT;
   int grid = (int)(tiles < 2L * nsm ? tiles : 2L * nsm);
+  if (a.tile_counter) {
+    cudaError_t e = cudaMemsetAsync(a.tile_counter, 0, sizeof(int), st);
+    if (e != cudaSuccess) return e;
+  }
   k<<<grid, C::NT, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
