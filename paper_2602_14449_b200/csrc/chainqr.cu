@@ -726,11 +726,18 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  householder_sweep<KT, true, KT>(S, 0, Xs, tau_s);   // U -> Xs (ld KT+1)
-  store_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
-  __syncthreads();
-  u_to_t_block<KT>(Xs, Xs + KT * (KT + 1), Tbase);
-  __syncthreads();
+  if (a.head_tri) {
+    // Tree levels: the head is an R factor (exact zeros below the diagonal),
+    // so every dlarfg sees |x| = 0: tau = 0, beta = alpha (LAPACK's shortcut),
+    // R = head, Y = 0, T = 0 -- the unblocked sweep would compute exactly that.
+    for (int e = tid; e < KT * KT; e += 256) Tbase[e] = 0.0;
+  } else {
+    householder_sweep<KT, true, KT>(S, 0, Xs, tau_s);   // U -> Xs (ld KT+1)
+    store_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
+    __syncthreads();
+    u_to_t_block<KT>(Xs, Xs + KT * (KT + 1), Tbase);
+    __syncthreads();
+  }
 
   // ---- structured tiles (register-resident, see BlkCfg)
   const bool owner = warp < NP;

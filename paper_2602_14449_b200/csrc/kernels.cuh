@@ -39,6 +39,7 @@ struct FactorArgs {
   ChainGeom G;
   double* U;             // per tile KT*KT, tile id = chain*(L+1) + t
   double* Rout;          // stacked chain R's: chain*KT rows, ld KT
+  int head_tri;          // input rows are stacked upper-triangular R's (tree levels)
 };
 
 struct QformArgs {

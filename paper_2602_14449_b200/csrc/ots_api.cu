@@ -292,9 +292,12 @@ int ensure_ws(ots_ctx* ctx, size_t bytes) {
   return OTS_OK;
 }
 
-int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st) {
-  for (auto& L : lv) {
-    FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R};
+// tri_first: level 0's rows are already stacked R factors (the global tree);
+// levels >= 1 always are.
+int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st, bool tri_first = false) {
+  for (size_t l = 0; l < lv.size(); ++l) {
+    Level& L = lv[l];
+    FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, (l > 0 || tri_first) ? 1 : 0};
     CK(launch_chain_factor(fa, KT, st));
   }
   return OTS_OK;
@@ -1213,7 +1216,7 @@ int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank) {
   }
   j.glv = g;
   int rc;
-  if ((rc = run_factor_levels(ctx, j.glv, KT, st))) return rc;
+  if ((rc = run_factor_levels(ctx, j.glv, KT, st, true))) return rc;
   j.Rfinal = j.glv.back().R;
   set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
   if ((rc = run_qform_levels(ctx, j.glv, KT, j.ident, st))) return rc;
