@@ -103,7 +103,7 @@ struct ots_ctx {
   int nsm = 148;
   cudaStream_t side = nullptr;   // highest priority: its few CTAs go first, the
                                  // dynamically scheduled apply1 tiles fill around them
-  cudaEvent_t ev_seed = nullptr, ev_diag = nullptr;
+  cudaEvent_t ev_seed = nullptr, ev_diag = nullptr, ev_seedA = nullptr;
   int* nn_counter = nullptr;     // tile tickets of the NN updates
   char* ws = nullptr;
   size_t ws_size = 0;
@@ -646,10 +646,27 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   const int KT = j.KT;
   if (bh) { j.s.Gu = bh->Gu; j.s.ldgu = bh->ldgu; j.s.dinv_top = bh->dinv_top; }
   prof_begin(ctx, st);
+  j.s.Sout = S; j.s.lds_out = (int)lds;
+  // The V_t-only part of the seed (QR / LU / polar of the k0 x k0 top block)
+  // runs on one SM, on the side stream, while the single-wave Gram kernel
+  // streams on the other nsm-1 SMs; the Gram-dependent checks and Z1, S
+  // follow the Gram (validation order kept: defect > non-finite > seed).
+  const bool split_seed = c.k0 <= 128 && ctx->nsm > 8;
+  if (split_seed) {
+    CK(cudaEventRecord(ctx->ev_seedA, st));          // inputs ready on st
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
+    CK(launch_seed_split(j.s, 0, ctx->side));
+    CK(cudaEventRecord(ctx->ev_seedA, ctx->side));
+    j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, ctx->nsm - 1);
+  }
   if ((rc = phase_gram(ctx, j))) return rc;
   prof_mark(ctx, st, "gram");
-  j.s.Sout = S; j.s.lds_out = (int)lds;
-  CK(launch_seed(j.s, st));
+  if (split_seed) {
+    CK(cudaStreamWaitEvent(st, ctx->ev_seedA, 0));
+    CK(launch_seed_split(j.s, 1, st));
+  } else {
+    CK(launch_seed(j.s, st));
+  }
   CK(cudaEventRecord(ctx->ev_seed, st));
   prof_mark(ctx, st, "seed");
   // The diagnostics (3 CTAs, ~2 ms) go on the main stream right behind the
@@ -724,6 +741,7 @@ int ots_ctx_create(int device, ots_ctx** out) {
   cudaMalloc(&c->nn_counter, 256);
   cudaEventCreateWithFlags(&c->ev_seed, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_diag, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_seedA, cudaEventDisableTiming);
   cudaMallocHost(&c->h_status, 64);
   cudaMallocHost(&c->h_diag, 64);
   *out = c;
@@ -742,6 +760,7 @@ void ots_ctx_destroy(ots_ctx* c) {
   if (c->nn_counter) cudaFree(c->nn_counter);
   if (c->ev_seed) cudaEventDestroy(c->ev_seed);
   if (c->ev_diag) cudaEventDestroy(c->ev_diag);
+  if (c->ev_seedA) cudaEventDestroy(c->ev_seedA);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_diag) cudaFreeHost(c->h_diag);
   for (auto e : c->pev) cudaEventDestroy(e);

@@ -743,11 +743,15 @@ __device__ int seed_polar(const SmallState& s, double* red) {
   return st;
 }
 
-__global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
-  __shared__ double red[64];
-  __shared__ int ired[64];
+// The seed pipeline in three pieces (reflector.py:207-228 + twostage.py:90-92):
+//   seed_checks  Gram-dependent validation: orthonormality defect, non-finite
+//   seed_build   V_t-only: P, T (and its factors) for the chosen seed, W_t
+//   seed_finish  Z1 = T^{-T}(W_t^T A_t - V_b^T A_b), S = P^T (A_t - W_t Z1)
+// seed_kernel runs them in the reference's validation order; the headline
+// pipeline runs seed_build on one SM while the Gram kernel streams on the
+// others (seedA_kernel) and the rest after the Gram (seedB_kernel).
+__device__ bool seed_checks(SmallState& s, double* red) {
   const int n = s.k0, k = s.k, ld = s.ld;
-  if (threadIdx.x == 0) { s.status[0] = 0; }
   // 1. symmetric Gram (lower blocks valid) and V_b^T A_b
   BLK_FOR(e, n * n) {
     int i = e / n, j = e - i * n;
@@ -766,7 +770,7 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
   if (threadIdx.x == 0) s.diag[2] = defect;
   if (defect > s.orth_tol && !s.allow_defect) {
     if (threadIdx.x == 0) s.status[0] = OTS_E_ORTHONORMALITY;
-    return;
+    return false;
   }
   // Non-finite V or A (core.py:72-73, reached by the reference at the intra
   // QR): any NaN/Inf entry poisons the Gram block [V^T V | V_b^T A_b] or the
@@ -780,9 +784,14 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
     }
     if (__syncthreads_or(bad)) {
       if (threadIdx.x == 0) s.status[0] = OTS_E_VALUE;
-      return;
+      return false;
     }
   }
+  return true;
+}
+
+__device__ int seed_build(SmallState& s, double* red, int* ired) {
+  const int n = s.k0, k = s.k, ld = s.ld;
   // 3. V_t, A_t
   BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.Vt[i * ld + j] = s.V[(long)i * s.ldv + j]; }
   BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.At[i * ld + j] = s.A[(long)i * s.lda + j]; }
@@ -862,10 +871,11 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
       st = OTS_E_PARAMETER;
   }
   __syncthreads();
-  if (st != 0) {
-    if (threadIdx.x == 0) s.status[0] = st;
-    return;
-  }
+  return st;
+}
+
+__device__ void seed_finish(SmallState& s) {
+  const int n = s.k0, k = s.k, ld = s.ld;
   // 5. W_t = fl(P - V_t)
   BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.Wt[i * ld + j] = s.P[i * ld + j] - s.Vt[i * ld + j]; }
   __syncthreads();
@@ -880,6 +890,37 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
   BLK_FOR(e, n * k) { int i = e / k, j = e - i * k; s.X1[i * ld + j] = s.At[i * ld + j] - s.X1[i * ld + j]; }
   __syncthreads();
   blk_gemm(s.Sout, s.lds_out, s.P, ld, true, s.X1, ld, false, n, k, n, 1.0, 0.0);
+}
+
+__global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
+  __shared__ double red[64];
+  __shared__ int ired[64];
+  if (threadIdx.x == 0) { s.status[0] = 0; }
+  if (!seed_checks(s, red)) return;
+  const int st = seed_build(s, red, ired);
+  if (st != 0) {
+    if (threadIdx.x == 0) s.status[0] = st;
+    return;
+  }
+  seed_finish(s);
+}
+
+__global__ void __launch_bounds__(SMALL_NT) seedA_kernel(SmallState s) {
+  __shared__ double red[64];
+  __shared__ int ired[64];
+  const int st = seed_build(s, red, ired);
+  if (threadIdx.x == 0) s.status[1] = st;
+}
+
+__global__ void __launch_bounds__(SMALL_NT) seedB_kernel(SmallState s) {
+  __shared__ double red[64];
+  if (threadIdx.x == 0) { s.status[0] = 0; }
+  if (!seed_checks(s, red)) return;
+  if (s.status[1] != 0) {                 // seed errors come after the Gram checks
+    if (threadIdx.x == 0) s.status[0] = s.status[1];
+    return;
+  }
+  seed_finish(s);
 }
 
 // Diagnostics from k0 x k0 data (reflector.py:241-247):
@@ -1074,6 +1115,13 @@ cudaError_t launch_cholqr_step(const double* Gf, int ldg, int k, long m, int shi
                                double* Z, double* R, int* status, cudaStream_t st) {
   cudaFuncSetAttribute(cholqr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
   cholqr_step_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(Gf, ldg, k, m, shift, W, ld, Z, R, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seed_split(const SmallState& s, int part, cudaStream_t st) {
+  auto k = part == 0 ? seedA_kernel : seedB_kernel;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  k<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 

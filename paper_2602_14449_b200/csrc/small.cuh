@@ -60,6 +60,8 @@ struct ZState {
 };
 
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st);
+// part 0: V_t-only seed construction (status[1]); part 1: Gram checks + Z1, S
+cudaError_t launch_seed_split(const SmallState& s, int part, cudaStream_t st);
 cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, long ldvq, const double* Gqq,
                              long ldqq, const double* Gee, long ldee, const double* Gaa, long ldaa, int k0, int k,
                              int augmented, double* work, double* out3, cudaStream_t st);
