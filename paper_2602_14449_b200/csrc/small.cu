@@ -1047,15 +1047,37 @@ __global__ void __launch_bounds__(SMALL_NT) sign_kernel(SmallState s, const doub
 }
 
 // Q_top = -(W_t Z2) diag(svec)
-__global__ void __launch_bounds__(SMALL_NT) qtop_kernel(SmallState s, double* Q, long ldq) {
+// Q_t = -W_t Z2 diag(s): QTOP_ROWS rows of Q_t per CTA, one output per
+// thread (k <= 64 columns); W_t rows and Z2 staged through shared memory in
+// chunks of QTOP_LC rows of the reduction.
+constexpr int QTOP_ROWS = 8, QTOP_LC = 128;
+__global__ void __launch_bounds__(QTOP_ROWS * 64) qtop_kernel(SmallState s, double* Q, long ldq) {
   if (s.status[0] != 0) return;
   const int n = s.k0, k = s.k, ld = s.ld;
-  BLK_FOR(e, n * k) {
-    int i = e / k, j = e - i * k;
-    double acc = 0.0;
-    for (int l = 0; l < n; ++l) acc = fma(s.Wt[i * ld + l], s.Z2[l * ld + j], acc);
-    Q[(long)i * ldq + j] = -acc * s.svec[j];
+  const int i0 = blockIdx.x * QTOP_ROWS;
+  double* Zs = dsm;                       // QTOP_LC x k
+  double* Ws = dsm + QTOP_LC * k;         // QTOP_ROWS x QTOP_LC
+  const int r = threadIdx.x / 64, j = threadIdx.x % 64;
+  double a0 = 0.0, a1 = 0.0;
+  for (int l0 = 0; l0 < n; l0 += QTOP_LC) {
+    const int lc = n - l0 < QTOP_LC ? n - l0 : QTOP_LC;
+    __syncthreads();
+    for (int e = threadIdx.x; e < lc * k; e += blockDim.x) Zs[e] = s.Z2[(l0 + e / k) * ld + e % k];
+    for (int e = threadIdx.x; e < QTOP_ROWS * lc; e += blockDim.x) {
+      const int rr = i0 + e / lc;
+      Ws[e] = rr < n ? s.Wt[rr * ld + l0 + e % lc] : 0.0;
+    }
+    __syncthreads();
+    if (j < k) {
+      int l = 0;
+      for (; l + 1 < lc; l += 2) {
+        a0 = fma(Ws[r * lc + l], Zs[l * k + j], a0);
+        a1 = fma(Ws[r * lc + l + 1], Zs[(l + 1) * k + j], a1);
+      }
+      if (l < lc) a0 = fma(Ws[r * lc + l], Zs[l * k + j], a0);
+    }
   }
+  if (i0 + r < n && j < k) Q[(long)(i0 + r) * ldq + j] = -(a0 + a1) * s.svec[j];
 }
 
 // Standalone modified LU (the `modified_lu` API, reflector.py:53-77), with
@@ -1158,7 +1180,10 @@ cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const
   return cudaGetLastError();
 }
 cudaError_t launch_qtop(const SmallState& s, double* Q, long ldq, cudaStream_t st) {
-  qtop_kernel<<<1, SMALL_NT, 0, st>>>(s, Q, ldq);
+  if (s.k > 64) return cudaErrorInvalidValue;
+  const int smem = (QTOP_LC * s.k + QTOP_ROWS * QTOP_LC) * 8;
+  cudaFuncSetAttribute(qtop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  qtop_kernel<<<(s.k0 + QTOP_ROWS - 1) / QTOP_ROWS, QTOP_ROWS * 64, smem, st>>>(s, Q, ldq);
   return cudaGetLastError();
 }
 cudaError_t launch_mlu(const double* Z, int ldz, int n, double* LU, double* p, double* work, int* status,
