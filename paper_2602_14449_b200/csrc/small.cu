@@ -1024,9 +1024,13 @@ __global__ void __launch_bounds__(SMALL_NT) tsolve_kernel(SmallState s, double* 
 }
 
 // Z2 = T^{-1} Y2
+// Z2 = T^{-1} Y2, Z2_COLS right-hand sides per CTA (the solves are column-separable)
+constexpr int Z2_COLS = 8;
 __global__ void __launch_bounds__(SMALL_NT) z2_kernel(SmallState s) {
   if (s.status[0] != 0) return;
-  t_solve(s, s.Z2, s.ld, s.k, false);
+  const int c0 = blockIdx.x * Z2_COLS;
+  const int m = s.k - c0 < Z2_COLS ? s.k - c0 : Z2_COLS;
+  if (m > 0) t_solve(s, s.Z2 + c0, s.ld, m, false);
 }
 
 // LAPACK sign recovery on Q_ top k x k and R output
@@ -1171,7 +1175,7 @@ cudaError_t launch_tsolve(const SmallState& s, double* B, int ldb, int m, int ad
 
 cudaError_t launch_z2(const SmallState& s, cudaStream_t st) {
   cudaFuncSetAttribute(z2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
-  z2_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
+  z2_kernel<<<(s.k + Z2_COLS - 1) / Z2_COLS, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 cudaError_t launch_sign(const SmallState& s, const double* Qtop, long ldq, const double* Rfin, int ldr,
