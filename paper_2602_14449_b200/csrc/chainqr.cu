@@ -695,12 +695,20 @@ __device__ __forceinline__ void t_block(int q, int p, const double* S, const dou
   __syncwarp();
 }
 
-// full KT x KT T (upper block triangular, zeros below) -> global
+// T (upper block triangular) -> global.  Only the blocks on and above the
+// diagonal are written: the Q-formation reads T as upper triangular.
 template <int KT>
 __device__ __forceinline__ void t_store(const double* Tpv, const double* Tw, double* Tg) {
-  for (int e = threadIdx.x; e < KT * KT; e += 256) {
-    const int i = e / KT, j = e - i * KT, qi = i >> 3, pj = j >> 3, r = (i & 7) * 8 + (j & 7);
-    Tg[e] = qi == pj ? Tpv[qi * 64 + r] : (qi < pj ? Tw[tw_off(qi, pj) + r] : 0.0);
+  constexpr int NP = KT / 8;
+  for (int e = threadIdx.x; e < (NP * (NP + 1) / 2) * 32; e += 256) {   // 2 doubles per unit
+    const int blk = e >> 5, u = e & 31;
+    int pj = 0;
+    while ((pj + 1) * (pj + 2) / 2 <= blk) ++pj;                  // block column
+    const int qi = blk - pj * (pj + 1) / 2;                       // block row (<= pj)
+    const int r = (u >> 2), c = (u & 3) * 2;
+    const double* src = qi == pj ? Tpv + qi * 64 : Tw + tw_off(qi, pj);
+    *reinterpret_cast<double2*>(Tg + (8 * qi + r) * KT + 8 * pj + c) =
+        *reinterpret_cast<const double2*>(src + r * 8 + c);
   }
 }
 
