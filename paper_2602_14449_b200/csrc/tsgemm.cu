@@ -33,7 +33,10 @@ struct TnCfg {
   static constexpr int NSPLIT = (NFULL % 4 == 2 && NFULL > 4) ? 2 : 0;
   static constexpr int NTASK = NFULL + NSPLIT;      // warps
   static constexpr int NT = NTASK * 32;
-  static constexpr int RT = 32;
+  // 64-row stages (two in flight) for the wide headline shapes: half the
+  // ring hand-offs per DMMA of 32-row stages (measured: gram 19.5 -> 18.4 ms)
+  // (for the cross product V^T Q_ it measured slower: 8.87 -> 9.15 ms)
+  static constexpr int RT = (PW == 128 && BW == 64 && ALIAS) ? 64 : 32;
   static constexpr int STAGE = RT * (PW + BW);
   static constexpr int NSTAGE_RAW = (200 * 1024) / (STAGE * 8);
   static constexpr int NSTAGE = NSTAGE_RAW > 4 ? 4 : (NSTAGE_RAW < 2 ? 2 : NSTAGE_RAW);
