@@ -78,6 +78,29 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
                       double* Q, int64_t ldq, double* R, int64_t ldr,
                       double* S, int64_t lds, double* diag_host, void* stream);
 
+/* InnerProduct.weighted(b) for a dense SPD b      -- oblique.py:48-56
+ * the reference's chol_b = cholesky(b) (core.py:87-105): lower L (strict
+ * upper stored as zeros); OTS_E_NOT_PD when a pivot is not positive. */
+int ots_dense_cholesky_f64(ots_ctx* ctx, int64_t n, const double* B, int64_t ldb,
+                           double* L, int64_t ldl, void* stream);
+/* X <- L^{-T} X (n x m); with X = [I_m; 0] this is initial_b_basis(b, m)
+ * (oblique.py:93-108: the top block L_m^{-T} over zero rows) */
+int ots_dense_trsm_lt_f64(ots_ctx* ctx, int64_t n, int64_t m, const double* L, int64_t ldl,
+                          double* X, int64_t ldx, void* stream);
+/* Y = L^T X (n x m): the map under which the b-inner product is Euclidean */
+int ots_dense_trmm_lt_f64(ots_ctx* ctx, int64_t n, int64_t m, const double* L, int64_t ldl,
+                          const double* X, int64_t ldx, double* Y, int64_t ldy, void* stream);
+/* b_two_stage_qr(v, a, u, inner, choice)          -- oblique.py:279-315
+ * for a dense SPD b = L L^T (L from ots_dense_cholesky_f64) with the
+ * canonical u = initial_b_basis(inner, k0+k): the Euclidean path on
+ * (L^T V, L^T A), Q = L^{-T} Q' sgn, R = sgn R', S unchanged. */
+int ots_b_two_stage_dense_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                              const double* V, int64_t ldv, const double* A, int64_t lda,
+                              const double* L, int64_t ldl, int choice,
+                              const double* P, int64_t ldp, double orth_tol,
+                              double* Q, int64_t ldq, double* R, int64_t ldr,
+                              double* S, int64_t lds, double* diag_host, void* stream);
+
 /* b_two_stage_qr(v, a, u, inner, choice)          -- oblique.py:279-315
  * for the weighted inner product M = diag(d) (d > 0, device, n values) with
  * u = initial_b_basis(inner, k0+k) (oblique.py:93-108): computed as the

@@ -55,6 +55,12 @@ def lib():
                 L.ots_b_two_stage_diag_f64.argtypes = [
                     _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _int, _vp, _i64, _dbl,
                     _vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
+                L.ots_dense_cholesky_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _i64, _vp]
+                L.ots_dense_trsm_lt_f64.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp]
+                L.ots_dense_trmm_lt_f64.argtypes = [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp]
+                L.ots_b_two_stage_dense_f64.argtypes = [
+                    _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp, _i64, _dbl,
+                    _vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
                 L.ots_build_reflector_f64.argtypes = [
                     _vp, _i64, _i64, _vp, _i64, _int, _vp, _i64, _dbl, _int, C.POINTER(_vp),
                     C.POINTER(_dbl), _vp]
@@ -110,6 +116,7 @@ EXPORTED_SYMBOLS = [
     "ots_debug_counters",
     "ots_dist_begin", "ots_dist_sizes", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",
     "ots_dist_tree", "ots_dist_qform", "ots_dist_finish",
+    "ots_dense_cholesky_f64", "ots_dense_trsm_lt_f64", "ots_dense_trmm_lt_f64", "ots_b_two_stage_dense_f64",
 ]
 
 

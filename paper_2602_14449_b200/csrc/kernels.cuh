@@ -65,5 +65,11 @@ cudaError_t launch_zchain_qform(const ZQformArgs& a, int KT, cudaStream_t st);
 int zchain_bmax();
 int chain_bmax(int KT);
 int debug_counters(unsigned long long* out, int reset);
+// dense SPD weights (dense.cu): in-place lower Cholesky, Y = L^T X, X <- L^{-T} X
+cudaError_t launch_dense_cholesky(double* A, long ld, int n, int* status, cudaStream_t st);
+cudaError_t launch_trmm_lt(const double* L, long ldl, const double* X, long ldx, double* Y, long ldy, int n, int m,
+                           cudaStream_t st);
+cudaError_t launch_trsm_lt(const double* L, long ldl, double* X, long ldx, int n, int m, cudaStream_t st);
+cudaError_t launch_colsign(double* Q, long ldq, long n, int k, const double* R, long ldr, cudaStream_t st);
 
 }  // namespace ots

@@ -597,10 +597,13 @@ int validate_layout(ots_ctx* ctx, const void* p, long ld, const char* name) {
 
 }  // namespace
 
-struct BHook {                 // B-inner (diagonal M) extension of the pipeline
+struct BHook {                 // B-inner extension of the pipeline
   const double* Gu; int ldgu;   // unweighted Gram of the original V
-  const double* dinv_top;       // 1/d on the top k0 rows
-  const double* d; long n;      // full weights (for the Q epilogue)
+  const double* dinv_top;       // diagonal M: 1/d on the top k0 rows
+  const double* d; long n;      // diagonal M: full weights (for the Q epilogue)
+  const double* L = nullptr; long ldl = 0;          // dense B = L L^T (Q epilogue: L^{-T})
+  const double* Ltinv = nullptr; int ldlt = 0;      // dense: L_m^{-T} (diagnostics)
+  const double* Vorig = nullptr; long ldvo = 0;     // dense: original V (diagnostics)
 };
 
 __global__ void b_unscale_kernel(double* Q, long ldq, long n, int k, const double* d, const double* R,
@@ -644,7 +647,10 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   int rc;
   if ((rc = job_setup(ctx, j, c))) return rc;
   const int KT = j.KT;
-  if (bh) { j.s.Gu = bh->Gu; j.s.ldgu = bh->ldgu; j.s.dinv_top = bh->dinv_top; }
+  if (bh) {
+    j.s.Gu = bh->Gu; j.s.ldgu = bh->ldgu; j.s.dinv_top = bh->dinv_top;
+    j.s.Ltinv = bh->Ltinv; j.s.ldlt = bh->ldlt; j.s.Vorig = bh->Vorig; j.s.ldvo = bh->ldvo;
+  }
   prof_begin(ctx, st);
   j.s.Sout = S; j.s.lds_out = (int)lds;
   // The V_t-only part of the seed (QR / LU / polar of the k0 x k0 top block)
@@ -708,7 +714,12 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   CK(launch_qtop(j.s, Q, ldq, st));
   if (bh) {
     const int nb = (int)std::min<long>(4096, (n * k + 255) / 256);
-    b_unscale_kernel<<<nb, 256, 0, st>>>(Q, ldq, n, (int)k, bh->d, R, ldr);
+    if (bh->L != nullptr) {       // dense B: Q = L^{-T} Q' sgn
+      CK(launch_colsign(Q, ldq, n, (int)k, R, ldr, st));
+      CK(launch_trsm_lt(bh->L, bh->ldl, Q, ldq, (int)n, (int)k, st));
+    } else {
+      b_unscale_kernel<<<nb, 256, 0, st>>>(Q, ldq, n, (int)k, bh->d, R, ldr);
+    }
     b_rsign_kernel<<<1, 256, 0, st>>>(R, ldr, (int)k);
     prof_mark(ctx, st, "b_epilogue");
   }
@@ -1022,6 +1033,94 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, 
   prof_end(ctx);
   CK(cudaGetLastError());
   return OTS_OK;
+}
+
+// Dense SPD weight B (n x n): lower Cholesky factor into L (B unchanged when
+// L != B).  OTS_E_NOT_PD when a pivot is not positive.
+int ots_dense_cholesky_f64(ots_ctx* ctx, int64_t n, const double* B, int64_t ldb, double* L, int64_t ldl,
+                           void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 0) return fail(ctx, OTS_E_DIMENSION, "n must be >= 0");
+  if (n == 0) return OTS_OK;
+  if (L != B) CK(cudaMemcpy2DAsync(L, ldl * 8, B, ldb * 8, n * 8, n, cudaMemcpyDeviceToDevice, st));
+  int* dstat = ctx->nn_counter + 16;   // spare device word of the context
+  CK(launch_dense_cholesky(L, ldl, (int)n, dstat, st));
+  CK(cudaMemcpyAsync(ctx->h_status, dstat, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (ctx->h_status[0] == OTS_E_NOT_PD) return fail(ctx, OTS_E_NOT_PD, "weight matrix is not positive definite");
+  return OTS_OK;
+}
+
+// X (n x m) <- L^{-T} X  (L lower, from ots_dense_cholesky_f64)
+int ots_dense_trsm_lt_f64(ots_ctx* ctx, int64_t n, int64_t m, const double* L, int64_t ldl, double* X,
+                          int64_t ldx, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();
+  CK(launch_trsm_lt(L, ldl, X, ldx, (int)n, (int)m, (cudaStream_t)stream));
+  return OTS_OK;
+}
+
+// Y (n x m) = L^T X
+int ots_dense_trmm_lt_f64(ots_ctx* ctx, int64_t n, int64_t m, const double* L, int64_t ldl, const double* X,
+                          int64_t ldx, double* Y, int64_t ldy, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();
+  CK(launch_trmm_lt(L, ldl, X, ldx, Y, ldy, (int)n, (int)m, (cudaStream_t)stream));
+  return OTS_OK;
+}
+
+// b_two_stage_qr (oblique.py:279-315) for a dense SPD B = L L^T with the
+// canonical basis u = initial_b_basis(B, k0+k) = [L_m^{-T}; 0]: Algorithm 1 on
+// (L^T V, L^T A), Q = L^{-T} Q' sgn, R = sgn R', S unchanged.
+int ots_b_two_stage_dense_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const double* V, int64_t ldv,
+                              const double* A, int64_t lda, const double* L, int64_t ldl, int choice,
+                              const double* P, int64_t ldp, double orth_tol, double* Q, int64_t ldq, double* R,
+                              int64_t ldr, double* S, int64_t lds, double* diag_host, void* stream) {
+  if (!ctx) return OTS_E_VALUE;
+  cudaSetDevice(ctx->device);
+  (void)cudaGetLastError();
+  cudaStream_t st = (cudaStream_t)stream;
+  if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
+  if (k > 64 || k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
+  if (k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "b_two_stage_dense needs k0, k >= 1");
+  if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
+  int rc;
+  if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
+  if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
+  if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
+  const long ldv2 = (k0 + 1) & ~1L, lda2 = (k + 1) & ~1L, ldt = (k0 + 1) & ~1L;
+  const int PWv = pad32(k0);
+  const int gridu = grid_for_tn(PWv, 0, true, true, ctx->nsm);
+  size_t need = ((size_t)n * (ldv2 + lda2) + (size_t)gridu * PWv * PWv + (size_t)PWv * PWv +
+                 (size_t)k0 * ldt + 256) * 8 + 4096;
+  if (need > ctx->b_size) {
+    if (ctx->b_ws) cudaFree(ctx->b_ws);
+    ctx->b_ws = nullptr; ctx->b_size = 0;
+    CK(cudaMalloc(&ctx->b_ws, need));
+    ctx->b_size = need;
+  }
+  double* V2 = reinterpret_cast<double*>(ctx->b_ws);
+  double* A2 = V2 + (size_t)n * ldv2;
+  double* part = A2 + (size_t)n * lda2;
+  double* Gu = part + (size_t)gridu * PWv * PWv;
+  double* Lti = Gu + (size_t)PWv * PWv;                 // L_m^{-T}, k0 x k0
+  CK(launch_trmm_lt(L, ldl, V, ldv, V2, ldv2, (int)n, (int)k0, st));
+  CK(launch_trmm_lt(L, ldl, A, lda, A2, lda2, (int)n, (int)k, st));
+  set_identity_ld_kernel<<<16, 256, 0, st>>>(Lti, (int)k0, (int)ldt);
+  CK(launch_trsm_lt(L, ldl, Lti, ldt, (int)k0, (int)k0, st));     // (L^{-T})_{top} = L_m^{-T}
+  TnArgs a{};
+  a.P = V; a.ldp = ldv; a.pc0 = 0; a.pcols = (int)k0;
+  a.row_begin = 0; a.row_end = n; a.partial = part;
+  CK(launch_tsgemm_tn(a, PWv, 0, true, true, gridu, st));
+  CK(launch_reduce(part, gridu, (long)PWv * PWv, Gu, 1.0, st));
+  BHook bh{Gu, PWv, nullptr, nullptr, n, L, ldl, Lti, (int)ldt, V, ldv};
+  JobCfg c{n, 0, k0, k, V2, ldv2, A2, lda2, Q, ldq, choice, P, ldp, orth_tol, 0, st, false};
+  return two_stage_pipeline(ctx, c, OTS_INTRA_HOUSEHOLDER, Q, ldq, R, ldr, S, lds, diag_host, &bh);
 }
 
 int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const double* V, int64_t ldv,

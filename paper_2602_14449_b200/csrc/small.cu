@@ -962,6 +962,24 @@ __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
       blk_gemm(WW, ld, s.Wt, ld, true, s.Wt, ld, false, n, n, n, 1.0, 0.0);
       blk_gemm(WW, ld, s.Vt, ld, true, s.Vt, ld, false, n, n, n, -1.0, 1.0);
       BLK_FOR(e2, n * n) { int i = e2 / n, j = e2 - i * n; WW[i * ld + j] += s.G[i * ld + j]; }
+    } else if (s.Ltinv != nullptr) {  // B-inner, dense B = L L^T: unweighted W = u0 p - v
+      const double* Vo = s.Vorig;      // original top rows (global)
+      blk_gemm(H, ld, s.Ltinv, s.ldlt, false, s.P, ld, false, n, n, n, 1.0, 0.0);   // L_m^{-T} P
+      BLK_FOR(e2, n * n) { int i = e2 / n, j = e2 - i * n; H[i * ld + j] -= Vo[(long)i * s.ldvo + j]; }
+      __syncthreads();
+      blk_gemm(WW, ld, H, ld, true, H, ld, false, n, n, n, 1.0, 0.0);
+      BLK_FOR(e2, n * n) {             // - V_t^T V_t
+        int i = e2 / n, j = e2 - i * n;
+        double acc = 0.0;
+        for (int l = 0; l < n; ++l) acc = fma(Vo[(long)l * s.ldvo + i], Vo[(long)l * s.ldvo + j], acc);
+        WW[i * ld + j] -= acc;
+      }
+      __syncthreads();
+      BLK_FOR(e2, n * n) {
+        int i = e2 / n, j = e2 - i * n;
+        WW[i * ld + j] += (j <= i) ? s.Gu[(long)i * s.ldgu + j] : s.Gu[(long)j * s.ldgu + i];
+      }
+      __syncthreads();
     } else {  // B-inner, M = diag(d): unweighted W = D^{-1/2} W'
       BLK_FOR(e2, n * n) { int i = e2 / n, j = e2 - i * n; H[i * ld + j] = s.dinv_top[i] * s.Wt[i * ld + j]; }
       blk_gemm(WW, ld, s.Wt, ld, true, H, ld, false, n, n, n, 1.0, 0.0);

@@ -27,6 +27,10 @@ struct SmallState {
   // W^T W = W_t'^T D_t^{-1} W_t' + V^T V (unweighted Gram Gu) - V_t'^T D_t^{-1} V_t'
   const double* Gu; int ldgu;  // null for the Euclidean path
   const double* dinv_top;      // 1/d on the k0 top rows
+  // dense B = L L^T: W_top = L_m^{-T} P - V_t (unweighted), W^T W = W_top^T
+  // W_top + Gu - V_t^T V_t with V_t the ORIGINAL top rows (dinv_top unused)
+  const double* Ltinv; int ldlt;     // L_m^{-T} (k0 x k0, upper), or null
+  const double* Vorig; long ldvo;    // original V (top k0 rows read)
   double* dg[6];               // diagnostics scratch (k0 x k0 each, ld)
   double* dlam;                // [3] per-CTA eigenvalues of the diagnostics kernel
   int* dcount;                 // CTA completion counter of the diagnostics kernel

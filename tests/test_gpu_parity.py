@@ -183,6 +183,60 @@ def test_binner_diag_golden(golden, ch):
     assert abs(res.diagnostics.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
 
 
+@pytest.mark.parametrize("ch", ["mlu", "qr", "polar"])
+def test_binner_dense_golden(golden, ch):
+    # dense SPD B (oblique.py:48-56): Cholesky transform on the GPU
+    g = lambda key: golden[f"binner_dense/{ch}/{key}"]
+    ip = P.InnerProduct.weighted(g("b"))
+    k0, k = g("v").shape[1], g("a").shape[1]
+    u = P.initial_b_basis(ip, k0 + k)
+    assert rel(u, g("u")) < 1e-12
+    res = P.b_two_stage_qr(g("v"), g("a"), g("u"), ip, choice=ch)
+    assert rel(res.q, g("q")) < 1e-10
+    assert rel(res.r, g("r")) < 1e-10
+    assert rel(res.s, g("s")) < 1e-10
+    assert np.all(np.diag(res.r) > 0)
+    assert abs(res.diagnostics.kappa_t - float(g("kappa_t"))) < 1e-10 * float(g("kappa_t"))
+    assert abs(res.diagnostics.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
+
+
+@pytest.mark.parametrize("n,k0,k,choice", [(700, 24, 16, "qr"), (1500, 64, 64, "mlu"), (2048, 96, 32, "polar")])
+def test_binner_dense_vs_oracle(n, k0, k, choice):
+    rng = W.make_rng(71 + n)
+    X = W.normal_matrix(rng, n, n)
+    b = X @ X.T / n + np.eye(n)                       # SPD, cond ~ 5
+    ip = P.InnerProduct.weighted(b)
+    ref_in = O.BInner(b=b)
+    lo = np.linalg.cholesky(b)
+    v = np.linalg.solve(lo.T, np.linalg.qr(W.normal_matrix(rng, n, k0))[0])   # B-orthonormal
+    a = W.normal_matrix(rng, n, k)
+    u = P.initial_b_basis(ip, k0 + k)
+    res = P.b_two_stage_qr(v, a, u, ip, choice=choice)
+    ref = O.b_two_stage(v, a, u, ref_in, choice, diagnostics=True)
+    assert rel(res.q, ref["q"]) < 1e-10 and rel(res.r, ref["r"]) < 1e-10 and rel(res.s, ref["s"]) < 1e-10
+    assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) < 1e-10 * ref["wt_inv_norm"]
+    # k0 = 0: B-orthonormal QR of A
+    r0 = P.b_two_stage_qr(np.zeros((n, 0)), a, u, ip)
+    ref0 = O.b_two_stage(np.zeros((n, 0)), a, u, ref_in, "qr", diagnostics=False)
+    assert rel(r0.q, ref0["q"]) < 1e-10 and rel(r0.r, ref0["r"]) < 1e-10
+
+
+def test_binner_dense_errors():
+    n = 64
+    b = np.eye(n); b[0, 1] = 1.0                      # not symmetric
+    with pytest.raises(P.NotHermitian):
+        P.InnerProduct.weighted(b)
+    b = np.eye(n); b[3, 3] = -1.0; b[0, 1] = b[1, 0] = 0.1   # symmetric, indefinite
+    with pytest.raises(P.NotPositiveDefinite):
+        P.InnerProduct.weighted(b)
+    b = np.eye(n) + 0.01 * np.ones((n, n))
+    ip = P.InnerProduct.weighted(b)
+    v = np.zeros((n, 2)); v[0, 0] = v[1, 1] = 1.0
+    u = np.eye(n)[:, :5]                              # not the canonical basis of this B
+    with pytest.raises(NotImplementedError):
+        P.b_two_stage_qr(v, np.ones((n, 3)), u, ip)
+
+
 def test_binner_diag_vs_oracle_large():
     n, k0, k = 1 << 18, 64, 64
     d = 10.0 ** W.uniform(W.make_rng(43), 0.0, 4.0, n)
