@@ -724,7 +724,9 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     prof_mark(ctx, st, "b_epilogue");
   }
   prof_mark(ctx, st, "tail");
-  ctx->launches = 14 + 3 * (int)j.lv.size() + (bh ? 2 : 0);
+  // gram, reduce, seed(B), diag, apply1, identity, sign, gram2, reduce, copy_y2,
+  // z2, apply2, qtop + a factor and a qform launch per level (+ seedA, B epilogue)
+  ctx->launches = 13 + 2 * (int)j.lv.size() + (bh ? 2 : 0) + (split_seed ? 1 : 0);
   rc = read_status(ctx, j, diag_host);
   prof_end(ctx);
   return rc;
