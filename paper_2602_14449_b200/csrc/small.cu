@@ -637,10 +637,7 @@ __device__ void t_solve_core(const SmallState& s, const double* F, int ld, doubl
     case CHOICE_QR:  // lower triangular T
       blk_trsm(F, ld, true, adjoint, false, X, ldx, n, m);
       break;
-    case CHOICE_POLAR:  // T = L L^T
-      blk_trsm(F, ld, true, false, false, X, ldx, n, m);
-      blk_trsm(F, ld, true, true, false, X, ldx, n, m);
-      break;
+
     case CHOICE_MLU:
       if (adjoint) {  // diag(p) L U x = b
         BLK_FOR(e, n * m) { int i = e / m; X[i * ldx + (e - i * m)] *= s.pvec[i]; }
@@ -653,6 +650,7 @@ __device__ void t_solve_core(const SmallState& s, const double* F, int ld, doubl
         BLK_FOR(e, n * m) { int i = e / m; X[i * ldx + (e - i * m)] *= s.pvec[i]; }
       }
       break;
+    case CHOICE_POLAR:     // pivoted LU of T = I - V_t^T P (see seed_polar)
     case CHOICE_EXPLICIT:  // P_piv L U = T (getrf); getrs semantics
       if (!adjoint) {
         for (int i = 0; i < n; ++i) {  // apply row swaps forward
@@ -683,7 +681,7 @@ __device__ void t_solve_core(const SmallState& s, const double* F, int ld, doubl
 // Seed: Gram check, P/T construction, W_top, Z1 = T^{-T}(W^T A), S = P^T (H^T A)_top
 // polar V_t = U H via one-sided Jacobi SVD (core.py:108-120):
 // P = -U, Tdense = T = I + H, Tf = chol(T).  Returns a status code.
-__device__ int seed_polar(const SmallState& s, double* red) {
+__device__ int seed_polar(const SmallState& s, double* red, int* ired) {
   const int n = s.k0, ld = s.ld;
   int st = 0;
   // rows of X1 := columns of V_t ; X2 := I (accumulates J^T)
@@ -731,15 +729,24 @@ __device__ int seed_polar(const SmallState& s, double* red) {
     s.Tdense[a * ld + b] = h;
   }
   __syncthreads();
-  BLK_FOR(e, n * n) {  // symmetrise H, T = I + H
-    int a = e / n, b = e - a * n;
-    double h = 0.5 * (s.Tdense[a * ld + b] + s.Tdense[b * ld + a]);
-    s.Tf[a * ld + b] = h + (a == b ? 1.0 : 0.0);
-  }
   __syncthreads();
-  blk_copy(s.Tdense, ld, s.Tf, ld, n, n);
+  // One-sided Jacobi leaves U orthogonal only to its tolerance (~4 n u), and
+  // the reflector is orthogonal only as far as P is and T = I - V_t^T P holds
+  // (SURVEY §3.1); so refine P by one Newton-Schulz step P <- P (3I - P^T P)/2
+  // (orthogonal to rounding) and form T from that P itself.  T is then
+  // symmetric only up to the Jacobi error, so it is factored by pivoted LU
+  // (the 'explicit' solver) rather than Cholesky; it is I + H with H PSD in
+  // exact arithmetic, so positive definite.
+  blk_gemm(s.X1, ld, s.P, ld, true, s.P, ld, false, n, n, n, 1.0, 0.0);
+  BLK_FOR(e, n * n) { int a = e / n, b = e - a * n; s.X1[a * ld + b] = (a == b ? 1.5 : 0.0) - 0.5 * s.X1[a * ld + b]; }
+  blk_gemm(s.X2, ld, s.P, ld, false, s.X1, ld, false, n, n, n, 1.0, 0.0);
+  blk_copy(s.P, ld, s.X2, ld, n, n);
+  blk_gemm(s.Tdense, ld, s.Vt, ld, true, s.P, ld, false, n, n, n, -1.0, 0.0);
+  BLK_FOR(i, n) s.Tdense[i * ld + i] += 1.0;
   __syncthreads();
-  if (!blk_cholesky(s.Tf, ld, n, red)) st = OTS_E_NOT_PD;
+  blk_copy(s.Tf, ld, s.Tdense, ld, n, n);
+  __syncthreads();
+  if (!blk_getrf(s.Tf, ld, n, s.piv, red, ired)) st = OTS_E_SINGULAR_T;
   return st;
 }
 
@@ -842,7 +849,7 @@ __device__ int seed_build(SmallState& s, double* red, int* ired) {
       break;
     }
     case CHOICE_POLAR:
-      st = seed_polar(s, red);
+      st = seed_polar(s, red, ired);
       break;
     case CHOICE_EXPLICIT: {
       blk_copy(s.P, ld, s.Pexp, s.ldpe, n, n);
