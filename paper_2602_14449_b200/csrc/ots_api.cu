@@ -199,6 +199,7 @@ struct Job {
   JobCfg c;
   int PW = 32, BWa = 32, KT = 16, NTOT1 = 64, ld = 32;
   int grid_tn = 148, grid_tn2 = 148;
+  int gram_nsm = 0;      // SMs of the Gram kernels (nsm - 1 when the seed runs beside them)
   long qrow0 = 0;        // first local row of the QR block (k0 on rank 0)
   long m = 0;            // local QR rows
   double *partial = nullptr, *Gfull = nullptr, *Y2full = nullptr, *top = nullptr;
@@ -407,6 +408,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
 int phase_gram(ots_ctx* ctx, Job& j) {
   const JobCfg& c = j.c;
   const int k0 = (int)c.k0, k = (int)c.k;
+  const int gnsm = j.gram_nsm > 0 ? j.gram_nsm : ctx->nsm;   // SMs the Gram kernels may use
   if (k0 <= 128) {
     TnArgs a{};
     a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = k0;
@@ -430,12 +432,12 @@ int phase_gram(ots_ctx* ctx, Job& j) {
       int grid, ldp;
       if (ab == bb) {
         a.B = nullptr; a.ldb = 0; a.bc0 = 0; a.bcols = 0;
-        grid = grid_for_tn(PWa, 0, true, true, ctx->nsm);
+        grid = grid_for_tn(PWa, 0, true, true, gnsm);
         ldp = PWa;
         CK(launch_tsgemm_tn(a, PWa, 0, true, true, grid, c.st));
       } else {
         a.B = c.V; a.ldb = c.ldv; a.bc0 = b0; a.bcols = bw;
-        grid = grid_for_tn(PWa, PWb, false, false, ctx->nsm);
+        grid = grid_for_tn(PWa, PWb, false, false, gnsm);
         ldp = PWb;
         CK(launch_tsgemm_tn(a, PWa, PWb, false, false, grid, c.st));
       }
@@ -447,7 +449,7 @@ int phase_gram(ots_ctx* ctx, Job& j) {
     a.B = c.A; a.ldb = c.lda; a.bc0 = 0; a.bcols = k;
     a.row_begin = 0; a.row_end = c.n_local; a.b_row_begin = j.qrow0; a.p_row_begin = 0;
     a.partial = j.partial;
-    const int grid = grid_for_tn(PWa, j.BWa, false, false, ctx->nsm);
+    const int grid = grid_for_tn(PWa, j.BWa, false, false, gnsm);
     CK(launch_tsgemm_tn(a, PWa, j.BWa, false, false, grid, c.st));
     CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Gfull + (long)a0 * j.NTOT1 + j.PW, j.NTOT1, 1.0,
                              c.st));
@@ -657,13 +659,14 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // runs on one SM, on the side stream, while the single-wave Gram kernel
   // streams on the other nsm-1 SMs; the Gram-dependent checks and Z1, S
   // follow the Gram (validation order kept: defect > non-finite > seed).
-  const bool split_seed = c.k0 <= 128 && ctx->nsm > 8;
+  const bool split_seed = ctx->nsm > 8;
   if (split_seed) {
     CK(cudaEventRecord(ctx->ev_seedA, st));          // inputs ready on st
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
     CK(launch_seed_split(j.s, 0, ctx->side));
     CK(cudaEventRecord(ctx->ev_seedA, ctx->side));
-    j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, ctx->nsm - 1);
+    j.gram_nsm = ctx->nsm - 1;
+    j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, j.gram_nsm);
   }
   if ((rc = phase_gram(ctx, j))) return rc;
   prof_mark(ctx, st, "gram");
