@@ -1289,14 +1289,24 @@ int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows) 
   j.s.Sout = j.s.Sd;  // S kept on device until finish
   j.s.lds_out = j.ld;
   CK(launch_seed(j.s, j.c.st));
-  CK(launch_diag(j.s, j.c.st));
+  CK(cudaEventRecord(ctx->ev_seed, j.c.st));
+  CK(launch_diag(j.s, j.c.st));      // owns its SMs before apply1 (side stream) starts
   return OTS_OK;
 }
 
 int ots_dist_factor(ots_ctx* ctx, double* r_local_out) {
   Job& j = *ctx->job;
+  // apply1 on the side stream beside the diagnostics (as in the one-GPU
+  // pipeline): its tiles are handed out dynamically around their SMs, and
+  // the factor starts once both are done
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
+  const cudaStream_t st = j.c.st;
+  j.c.st = ctx->side;
   int rc = phase_apply1(ctx, j);
+  j.c.st = st;
   if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
+  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   if ((rc = run_factor_levels(ctx, j.lv, j.KT, j.c.st))) return rc;
   if (r_local_out)
     CK(cudaMemcpyAsync(r_local_out, j.lv.back().R, (size_t)j.KT * j.KT * 8, cudaMemcpyDeviceToDevice, j.c.st));
