@@ -235,6 +235,9 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
 int ots_dist_sizes(ots_ctx* ctx, int64_t* out4);
 int ots_dist_gram(ots_ctx* ctx, double* gram_out);
 int ots_dist_top_rows(ots_ctx* ctx, double* top_rows_out);   /* rank 0 writes */
+/* optional, between ots_dist_top_rows (+ broadcast) and ots_dist_gram: start
+ * the V_t-only part of the seed beside this rank's Gram */
+int ots_dist_seed_early(ots_ctx* ctx, const double* top_rows);
 int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows);
 int ots_dist_factor(ots_ctx* ctx, double* r_local_out);      /* KT x KT */
 int ots_dist_tree(ots_ctx* ctx, const double* r_all, int nranks, int rank);

@@ -88,6 +88,7 @@ def lib():
                 L.ots_dist_gram.argtypes = [_vp, _vp]
                 L.ots_dist_top_rows.argtypes = [_vp, _vp]
                 L.ots_dist_seed.argtypes = [_vp, _vp, _vp]
+                L.ots_dist_seed_early.argtypes = [_vp, _vp]
                 L.ots_dist_factor.argtypes = [_vp, _vp]
                 L.ots_dist_tree.argtypes = [_vp, _vp, _int, _int]
                 L.ots_dist_qform.argtypes = [_vp, _vp, _vp]
@@ -114,7 +115,7 @@ EXPORTED_SYMBOLS = [
     "ots_reflector_diagnostics_f64", "ots_reflector_tsolve_f64", "ots_reflector_get_f64",
     "ots_set_profiling", "ots_last_profile", "ots_last_launch_count", "ots_fp64_peak",
     "ots_debug_counters",
-    "ots_dist_begin", "ots_dist_sizes", "ots_dist_gram", "ots_dist_seed", "ots_dist_top_rows", "ots_dist_factor",
+    "ots_dist_begin", "ots_dist_sizes", "ots_dist_gram", "ots_dist_seed", "ots_dist_seed_early", "ots_dist_top_rows", "ots_dist_factor",
     "ots_dist_tree", "ots_dist_qform", "ots_dist_finish",
     "ots_dense_cholesky_f64", "ots_dense_trsm_lt_f64", "ots_dense_trmm_lt_f64", "ots_b_two_stage_dense_f64",
 ]

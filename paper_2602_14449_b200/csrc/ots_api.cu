@@ -200,6 +200,7 @@ struct Job {
   int PW = 32, BWa = 32, KT = 16, NTOT1 = 64, ld = 32;
   int grid_tn = 148, grid_tn2 = 148;
   int gram_nsm = 0;      // SMs of the Gram kernels (nsm - 1 when the seed runs beside them)
+  bool seeded_early = false;   // row-sharded path: seedA already launched beside the Gram
   long qrow0 = 0;        // first local row of the QR block (k0 on rank 0)
   long m = 0;            // local QR rows
   double *partial = nullptr, *Gfull = nullptr, *Y2full = nullptr, *top = nullptr;
@@ -1276,19 +1277,44 @@ int ots_dist_top_rows(ots_ctx* ctx, double* top_out) {
   return OTS_OK;
 }
 
+// V_t-only seed (seedA) from the broadcast top rows, on the side stream; the
+// Gram that follows uses nsm-1 CTAs so seedA has its SM (as in the one-GPU
+// pipeline).  Optional: ots_dist_seed then runs only the Gram-dependent part.
+int ots_dist_seed_early(ots_ctx* ctx, const double* top_rows) {
+  Job& j = *ctx->job;
+  if (!top_rows || ctx->nsm <= 8) return OTS_OK;
+  const long k0 = j.c.k0, k = j.c.k;
+  const int ldt = (int)((k0 + k + 1) & ~1L);
+  CK(cudaMemcpyAsync(j.top, top_rows, (size_t)k0 * ldt * 8, cudaMemcpyDeviceToDevice, j.c.st));
+  j.s.V = j.top; j.s.ldv = ldt; j.s.A = j.top + k0; j.s.lda = ldt;
+  CK(cudaEventRecord(ctx->ev_seedA, j.c.st));
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
+  CK(launch_seed_split(j.s, 0, ctx->side));
+  CK(cudaEventRecord(ctx->ev_seedA, ctx->side));
+  j.gram_nsm = ctx->nsm - 1;
+  j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, j.gram_nsm);
+  j.seeded_early = true;
+  return OTS_OK;
+}
+
 int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows) {
   Job& j = *ctx->job;
   const long k0 = j.c.k0, k = j.c.k;
   const int ldt = (int)((k0 + k + 1) & ~1L);
   if (gram_sum && gram_sum != j.Gfull)
     CK(cudaMemcpyAsync(j.Gfull, gram_sum, (size_t)j.PW * j.NTOT1 * 8, cudaMemcpyDeviceToDevice, j.c.st));
-  if (top_rows) {
+  if (top_rows && !j.seeded_early) {
     CK(cudaMemcpyAsync(j.top, top_rows, (size_t)k0 * ldt * 8, cudaMemcpyDeviceToDevice, j.c.st));
     j.s.V = j.top; j.s.ldv = ldt; j.s.A = j.top + k0; j.s.lda = ldt;
   }
   j.s.Sout = j.s.Sd;  // S kept on device until finish
   j.s.lds_out = j.ld;
-  CK(launch_seed(j.s, j.c.st));
+  if (j.seeded_early) {
+    CK(cudaStreamWaitEvent(j.c.st, ctx->ev_seedA, 0));
+    CK(launch_seed_split(j.s, 1, j.c.st));
+  } else {
+    CK(launch_seed(j.s, j.c.st));
+  }
   CK(cudaEventRecord(ctx->ev_seed, j.c.st));
   CK(launch_diag(j.s, j.c.st));      // owns its SMs before apply1 (side stream) starts
   return OTS_OK;

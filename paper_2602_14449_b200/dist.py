@@ -154,6 +154,9 @@ class NativePhases:
         check(self.L.ots_dist_top_rows(self.ctx, C.c_void_p(t.data_ptr())), self.ctx)
         return t
 
+    def seed_early(self, top):
+        check(self.L.ots_dist_seed_early(self.ctx, C.c_void_p(top.data_ptr())), self.ctx)
+
     def seed(self, gram_sum, top):
         check(self.L.ots_dist_seed(self.ctx, C.c_void_p(gram_sum.data_ptr()),
                                    C.c_void_p(top.data_ptr())), self.ctx)
@@ -191,9 +194,11 @@ def run_phases(be, comm, n_local, row0, k0, k, V, A, Q, R, S, choice="qr", P=Non
     if row0 == 0 and n_local < k0 + k:
         raise E.DimensionError("rank 0 must own at least k0 + k rows")
     be.begin(n_local, row0, k0, k, V, A, Q, choice, P, orth_tol)
+    top = be.top_rows()                  # inputs: broadcast before the Gram, so the
+    top = comm.broadcast(top, src=0)     # V_t-only seed can run beside it
+    if hasattr(be, "seed_early"):
+        be.seed_early(top)
     g = comm.allreduce_sum(be.gram())
-    top = be.top_rows()
-    top = comm.broadcast(top, src=0)
     be.seed(g, top)
     r_all = comm.allgather_cat(be.factor())
     be.tree(r_all, comm.world, comm.rank)
