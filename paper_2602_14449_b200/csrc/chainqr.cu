@@ -1255,6 +1255,7 @@ static cudaError_t qform_t(const QformArgs& a, cudaStream_t st) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (a.grid_max > 0 && a.grid_max < nsm) nsm = a.grid_max;
   const int grid = a.G.nchains < nsm ? a.G.nchains : nsm;
   k<<<grid, C::NT, C::SMEM, st>>>(a);
   return cudaGetLastError();

@@ -47,6 +47,7 @@ struct QformArgs {
   ChainGeom G;
   const double* T;       // per tile KT*KT
   const double* Cin;     // stacked chain C's (chain*KT rows, ld KT)
+  int grid_max = 0;      // CTAs at most (0: one per SM)
 };
 
 cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid, cudaStream_t st);

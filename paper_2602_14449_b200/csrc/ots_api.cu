@@ -191,6 +191,7 @@ struct JobCfg {
   double orth_tol; int allow_defect;
   cudaStream_t st;
   bool distributed;
+  int nsm_avail = 0;     // SMs the row-parallel phases may plan for (0: all)
 };
 
 }  // namespace
@@ -201,6 +202,7 @@ struct Job {
   int grid_tn = 148, grid_tn2 = 148;
   int gram_nsm = 0;      // SMs of the Gram kernels (nsm - 1 when the seed runs beside them)
   bool seeded_early = false;   // row-sharded path: seedA already launched beside the Gram
+  int nsm_use = 0;             // SMs the row-parallel phases are planned for
   long qrow0 = 0;        // first local row of the QR block (k0 on rank 0)
   long m = 0;            // local QR rows
   double *partial = nullptr, *Gfull = nullptr, *Y2full = nullptr, *top = nullptr;
@@ -306,11 +308,12 @@ int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t
 }
 
 // Q-form from the top level (whose single chain gets C = Ctop) down to level 0.
-int run_qform_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, const double* Ctop, cudaStream_t st) {
+int run_qform_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, const double* Ctop, cudaStream_t st,
+                     int grid_max = 0) {
   const double* Cin = Ctop;
   for (int l = (int)lv.size() - 1; l >= 0; --l) {
     Level& L = lv[l];
-    QformArgs qa{L.D, L.ldd, L.ncols, L.G, L.UT, Cin};
+    QformArgs qa{L.D, L.ldd, L.ncols, L.G, L.UT, Cin, grid_max};
     CK(launch_chain_qform(qa, KT, st));
     Cin = L.D;  // output rows of level l are the C's of level l-1's chains
   }
@@ -345,7 +348,9 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   j.qrow0 = (c.row0 == 0) ? k0 : 0;
   j.m = c.n_local - j.qrow0;
   j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, ctx->nsm);
-  j.grid_tn2 = grid_for_tn(j.PW, j.BWa, false, false, ctx->nsm);
+  const int nsm_use = (c.nsm_avail > 0 && c.nsm_avail < ctx->nsm) ? c.nsm_avail : ctx->nsm;
+  j.nsm_use = nsm_use;
+  j.grid_tn2 = grid_for_tn(j.PW, j.BWa, false, false, nsm_use);
   const int ld = j.ld, KT = j.KT;
   const int gmax = std::max(j.grid_tn, j.grid_tn2);
   const int PWk = pad32(std::max<long>(k, 1));
@@ -365,7 +370,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   bytes += (size_t)22 * ld * ld * 8 + 22 * 256;                    // small matrices + diag scratch
   bytes += (size_t)8 * ld * 8 + 10 * 256;                          // vectors, dlam, dcount
   bytes += (size_t)KT * KT * 8 * 2 + 1024;                         // ident, svec
-  bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, ctx->nsm);
+  bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, nsm_use);
   bytes += (size_t)64 * KT * KT * 8 * 4 + 4096;                    // global tree (<=64 ranks)
   bytes += 64;
   int rc = ensure_ws(ctx, bytes);
@@ -396,7 +401,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   s.status = ar.take<int>(4);
   j.ident = ar.take<double>((size_t)KT * KT);
   j.svec = s.svec;
-  j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, ctx->nsm);
+  j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, nsm_use);
   j.Rall = ar.take<double>((size_t)64 * KT * KT);
   j.Cglob = ar.take<double>((size_t)64 * KT * KT);
   if (ar.off > ctx->ws_size) return fail(ctx, OTS_E_CUDA, "workspace plan overflow");
@@ -489,7 +494,7 @@ int phase_vtb(ots_ctx* ctx, Job& j, const double* Bm, long ldb, double alpha) {
     a.row_begin = j.qrow0; a.row_end = c.n_local;
     a.b_row_begin = j.qrow0; a.p_row_begin = j.qrow0;
     a.partial = j.partial;
-    const int grid = (nbk == 1) ? j.grid_tn2 : grid_for_tn(PWa, j.BWa, false, false, ctx->nsm);
+    const int grid = (nbk == 1) ? j.grid_tn2 : grid_for_tn(PWa, j.BWa, false, false, j.nsm_use > 0 ? j.nsm_use : ctx->nsm);
     CK(launch_tsgemm_tn(a, PWa, j.BWa, false, false, grid, c.st));
     CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Y2full + (long)a0 * j.BWa, j.BWa, alpha, c.st));
   }
@@ -648,7 +653,14 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   cudaStream_t st = c.st;
   Job j;
   int rc;
-  if ((rc = job_setup(ctx, j, c))) return rc;
+  // k0 > 128: the k0 x k0 diagnostics take tens of ms on three single-CTA
+  // eigenvalue problems; they then run on the side stream beside everything
+  // after the seed, and the row-parallel phases are planned for nsm - 3 SMs
+  // (chains, qform and Gram grids; the NN updates balance dynamically).
+  const bool diag_side = k0 > 128 && ctx->nsm > 16;
+  JobCfg c2 = c;
+  if (diag_side) c2.nsm_avail = ctx->nsm - 3;
+  if ((rc = job_setup(ctx, j, c2))) return rc;
   const int KT = j.KT;
   if (bh) {
     j.s.Gu = bh->Gu; j.s.ldgu = bh->ldgu; j.s.dinv_top = bh->dinv_top;
@@ -684,23 +696,28 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // an event a little later) fill the rest; apply1 hands out its tiles
   // dynamically, so those 3 SMs simply take fewer.  The factor then starts on
   // an idle GPU instead of waiting for the diagnostics' SMs.
-  CK(launch_diag(j.s, st));
-  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
-  {
+  if (diag_side) {
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
+    CK(launch_diag(j.s, ctx->side));
+    CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // waited for before the status read
+    if ((rc = phase_apply1(ctx, j))) return rc;
+  } else {
+    CK(launch_diag(j.s, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
     JobCfg c1 = j.c;
     j.c.st = ctx->side;
     rc = phase_apply1(ctx, j);
     j.c = c1;
     if (rc) return rc;
+    CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply1 done
+    CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   }
-  CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply1 done
-  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   prof_mark(ctx, st, "apply1");
   if (intra == OTS_INTRA_HOUSEHOLDER) {
     if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
     prof_mark(ctx, st, "factor");
     set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
-    if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st))) return rc;
+    if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st, diag_side ? j.nsm_use : 0))) return rc;
     prof_mark(ctx, st, "qform");
     CK(launch_sign(j.s, Q + k0 * ldq, ldq, j.lv.back().R, KT, R, (int)ldr, st));
   } else {
@@ -727,6 +744,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     b_rsign_kernel<<<1, 256, 0, st>>>(R, ldr, (int)k);
     prof_mark(ctx, st, "b_epilogue");
   }
+  if (diag_side) CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   prof_mark(ctx, st, "tail");
   // gram, reduce, seed(B), diag, apply1, identity, sign, gram2, reduce, copy_y2,
   // z2, apply2, qtop + a factor and a qform launch per level (+ seedA, B epilogue)
