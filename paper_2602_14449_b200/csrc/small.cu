@@ -253,6 +253,73 @@ __device__ void blk_org2r(double* A, int lda, int m, int n, const double* tau, d
   }
 }
 
+// Column-major twins (A[c * lda + r] holds entry (r, c)): the same
+// Householder sweep with every column contiguous, so the one-warp-per-column
+// dots and updates are coalesced when the matrix lives in global memory
+// (k0 x k0 seeds too large for shared memory).
+__device__ void blk_geqr2_cm(double* A, int lda, int m, int n, double* tau, double* red) {
+  for (int j = 0; j < n; ++j) {
+    double s2 = 0.0;
+    for (int r = j + 1 + (int)threadIdx.x; r < m; r += blockDim.x) { double x = A[(j) * lda + (r)]; s2 = fma(x, x, s2); }
+    s2 = block_sum(s2, red);
+    const double alpha = A[(j) * lda + (j)];
+    double beta = alpha, tj = 0.0, scal = 0.0;
+    if (s2 != 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+      tj = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
+    }
+    __syncthreads();
+    if (s2 != 0.0)
+      for (int r = j + 1 + (int)threadIdx.x; r < m; r += blockDim.x) A[(j) * lda + (r)] *= scal;
+    if (threadIdx.x == 0) { A[(j) * lda + (j)] = beta; tau[j] = tj; }
+    __syncthreads();
+    if (tj != 0.0) {
+      // trailing columns c > j: w = v^T A[:, c]; A[:,c] -= tau w v   (one warp per column)
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int c = j + 1 + w; c < n; c += nw) {
+        double d = 0.0;
+        for (int r = j + 1 + l; r < m; r += 32) d = fma(A[(j) * lda + (r)], A[(c) * lda + (r)], d);
+        d = warp_sum(d) + A[(c) * lda + (j)];
+        const double wc = tj * d;
+        if (l == 0) A[(c) * lda + (j)] -= wc;
+        for (int r = j + 1 + l; r < m; r += 32) A[(c) * lda + (r)] = fma(-wc, A[(j) * lda + (r)], A[(c) * lda + (r)]);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// dorg2r: Q (m x n) from the reflectors stored in A (in place -> Q); W scratch n*... unused
+__device__ void blk_org2r_cm(double* A, int lda, int m, int n, const double* tau, double* red) {
+  // Q = H_0 ... H_{n-1} [I; 0], accumulated backwards in place like dorg2r.
+  for (int j = n - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    // apply H_j to Q[j:m, j+1:n]  (columns right of j already hold Q columns)
+    if (j < n - 1 && tj != 0.0) {
+      const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+      for (int c = j + 1 + w; c < n; c += nw) {
+        double d = 0.0;
+        for (int r = j + 1 + l; r < m; r += 32) d = fma(A[(j) * lda + (r)], A[(c) * lda + (r)], d);
+        d = warp_sum(d) + A[(c) * lda + (j)];
+        const double wc = tj * d;
+        if (l == 0) A[(c) * lda + (j)] -= wc;
+        for (int r = j + 1 + l; r < m; r += 32) A[(c) * lda + (r)] = fma(-wc, A[(j) * lda + (r)], A[(c) * lda + (r)]);
+      }
+    } else if (j < n - 1) {
+      // tau == 0: H_j = I, nothing to do for the trailing columns
+    }
+    __syncthreads();
+    // column j: Q[j:, j] = e_j - tau v ; Q[0:j, j] = 0
+    for (int r = (int)threadIdx.x; r < m; r += blockDim.x) {
+      if (r < j) A[(j) * lda + (r)] = 0.0;
+      else if (r == j) A[(j) * lda + (r)] = 1.0 - tj;
+      else A[(j) * lda + (r)] = -tj * A[(j) * lda + (r)];
+    }
+    __syncthreads();
+  }
+}
+
 // Modified LU (reflector.py:53-77 / paper Alg. 2) in place:
 // Z -> L (strict lower, unit diag implied) and U (upper), p[n].
 // signrec=true applies the LAPACK-sign-recovery variant: a pivot
@@ -808,15 +875,30 @@ __device__ int seed_build(SmallState& s, double* red, int* ired) {
   switch (s.choice) {
     case CHOICE_QR: {
       // nonneg-diagonal QR of V_t (core.py:61-84): P = -Q1, T = I + R1^T
-      double* Wq = (n * (n + 1) <= SMALL_SMEM_DOUBLES) ? dsm : s.X1;
-      const int lq = (Wq == dsm) ? n + 1 : ld;
-      blk_copy(Wq, lq, s.Vt, ld, n, n);
-      __syncthreads();
-      blk_geqr2(Wq, lq, n, n, s.tau, red);
-      BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? Wq[i * lq + j] : 0.0; }
-      __syncthreads();
-      blk_org2r(Wq, lq, n, n, s.tau, red);  // Q1
-      if (Wq != s.X1) { blk_copy(s.X1, ld, Wq, lq, n, n); __syncthreads(); }
+      if (n * (n + 1) <= SMALL_SMEM_DOUBLES) {   // in shared memory
+        double* Wq = dsm;
+        const int lq = n + 1;
+        blk_copy(Wq, lq, s.Vt, ld, n, n);
+        __syncthreads();
+        blk_geqr2(Wq, lq, n, n, s.tau, red);
+        BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? Wq[i * lq + j] : 0.0; }
+        __syncthreads();
+        blk_org2r(Wq, lq, n, n, s.tau, red);  // Q1
+        blk_copy(s.X1, ld, Wq, lq, n, n);
+        __syncthreads();
+      } else {                                    // global memory: column-major (coalesced)
+        BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[j * ld + i] = s.Vt[i * ld + j]; }
+        __syncthreads();
+        blk_geqr2_cm(s.X1, ld, n, n, s.tau, red);
+        BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? s.X1[j * ld + i] : 0.0; }
+        __syncthreads();
+        blk_org2r_cm(s.X1, ld, n, n, s.tau, red);  // Q1, column-major
+        BLK_FOR(e, n * n) {                        // -> row-major in place
+          int i = e / n, j = e - i * n;
+          if (i < j) { const double a = s.X1[i * ld + j]; s.X1[i * ld + j] = s.X1[j * ld + i]; s.X1[j * ld + i] = a; }
+        }
+        __syncthreads();
+      }
       BLK_FOR(i, n) { double d = s.X2[i * ld + i]; s.pvec[i] = (d < 0.0) ? -1.0 : 1.0; }
       __syncthreads();
       BLK_FOR(e, n * n) {

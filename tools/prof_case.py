@@ -15,12 +15,16 @@ ap.add_argument("--k0", type=int, default=128)
 ap.add_argument("--k", type=int, default=64)
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--choice", default="qr")
-ap.add_argument("--vgen", default="ots", help="ots | torch (cuSOLVER QR) | eye ([I; 0]); the last two keep our kernels out of the setup")
+ap.add_argument("--vgen", default="ots", help="ots | torch (cuSOLVER QR) | eye ([I; 0]) | rot ([W; 0], W random orthogonal)")
 a = ap.parse_args()
 g = torch.Generator(device="cuda:0")
 g.manual_seed(1)
 G = torch.randn((a.n, a.k0), generator=g, dtype=torch.float64, device="cuda:0")
-if a.vgen == "eye":      # exactly orthonormal [I; 0] (no setup kernels)
+if a.vgen == "rot":      # [W; 0] with W a random orthogonal k0 x k0: a non-trivial seed
+    V = torch.zeros((a.n, a.k0), dtype=torch.float64, device="cuda:0")
+    V[:a.k0].copy_(torch.linalg.qr(torch.randn((a.k0, a.k0), generator=g, dtype=torch.float64,
+                                               device="cuda:0"))[0])
+elif a.vgen == "eye":      # exactly orthonormal [I; 0] (no setup kernels)
     V = torch.zeros((a.n, a.k0), dtype=torch.float64, device="cuda:0")
     V[:a.k0].copy_(torch.eye(a.k0, dtype=torch.float64))
 elif a.vgen == "torch":
