@@ -1255,6 +1255,10 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
   ctx->job = new Job();
   JobCfg c{n_local, row0, k0, k, V, ldv, A, lda, Q, ldq, choice, P, ldp, orth_tol, 0,
            (cudaStream_t)stream, true};
+  // per rank the row-parallel work is short, so the diagnostics (side stream,
+  // three CTAs) run beside apply1 and the factor, which are planned for the
+  // remaining SMs
+  if (ctx->nsm > 16) c.nsm_avail = ctx->nsm - 3;
   return job_setup(ctx, *ctx->job, c);
 }
 
@@ -1334,23 +1338,18 @@ int ots_dist_seed(ots_ctx* ctx, const double* gram_sum, const double* top_rows) 
     CK(launch_seed(j.s, j.c.st));
   }
   CK(cudaEventRecord(ctx->ev_seed, j.c.st));
-  CK(launch_diag(j.s, j.c.st));      // owns its SMs before apply1 (side stream) starts
+  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
+  CK(launch_diag(j.s, ctx->side));   // beside apply1 / factor; waited for in ots_dist_finish
+  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
   return OTS_OK;
 }
 
 int ots_dist_factor(ots_ctx* ctx, double* r_local_out) {
   Job& j = *ctx->job;
-  // apply1 on the side stream beside the diagnostics (as in the one-GPU
-  // pipeline): its tiles are handed out dynamically around their SMs, and
-  // the factor starts once both are done
-  CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
-  const cudaStream_t st = j.c.st;
-  j.c.st = ctx->side;
+  // apply1 (dynamic tiles) and the factor (chains planned for nsm - 3 SMs)
+  // run beside the diagnostics launched by ots_dist_seed
   int rc = phase_apply1(ctx, j);
-  j.c.st = st;
   if (rc) return rc;
-  CK(cudaEventRecord(ctx->ev_diag, ctx->side));
-  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   if ((rc = run_factor_levels(ctx, j.lv, j.KT, j.c.st))) return rc;
   if (r_local_out)
     CK(cudaMemcpyAsync(r_local_out, j.lv.back().R, (size_t)j.KT * j.KT * 8, cudaMemcpyDeviceToDevice, j.c.st));
@@ -1406,7 +1405,7 @@ int ots_dist_qform(ots_ctx* ctx, double* y2_out, double* sign_out) {
   Job& j = *ctx->job;
   cudaStream_t st = j.c.st;
   int rc;
-  if ((rc = run_qform_levels(ctx, j.lv, j.KT, j.Cglob, st))) return rc;
+  if ((rc = run_qform_levels(ctx, j.lv, j.KT, j.Cglob, st, j.nsm_use))) return rc;
   if (j.c.row0 == 0) {
     CK(launch_sign(j.s, j.c.Q + j.c.k0 * j.c.ldq, j.c.ldq, j.Rfinal, j.KT, j.s.D1 /*scratch R*/, j.ld, st));
     if (sign_out) CK(cudaMemcpyAsync(sign_out, j.svec, j.c.k * 8, cudaMemcpyDeviceToDevice, st));
@@ -1452,6 +1451,7 @@ int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign, doub
     ctx->launches = gram + (top ? 1 : 0) + 2 + 1 + 2 * (int)j.lv.size() + 2 * (int)j.glv.size() + 1 +
                     (top ? 1 : 0) + 2 * nb + 3 + (top ? 1 : 0) + (R ? 1 : 0) + (S ? 1 : 0);
   }
+  CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));   // diagnostics (side stream)
   return read_status(ctx, j, diag_host);
 }
 
