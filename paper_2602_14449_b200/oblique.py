@@ -14,7 +14,9 @@ Q = L^-T Q' sgn, with the Cholesky factor, L^T X and L^-T X on the GPU
 (`ots_dense_cholesky_f64`, `ots_dense_trmm_lt_f64`, `ots_dense_trsm_lt_f64`,
 `ots_b_two_stage_dense_f64`).  Both fast paths need the canonical initial
 basis u = initial_b_basis(inner, k0+k); any other u, and a dense complex B,
-raise NotImplementedError.
+raise NotImplementedError.  The primitives b_householder_qr,
+b_build_reflector, b_apply_reflector and the driver b_block_householder_qr
+use the same isometry (section at the end of this module).
 """
 
 from __future__ import annotations
@@ -141,15 +143,16 @@ def initial_b_basis(inner, m):
 
 
 def _is_canonical_basis(u, d, m):
-    """u[:, :m] == initial_b_basis(diag(d), m) (exactly, as the fast path needs)."""
+    """u[:, :m] == initial_b_basis(diag(d), m) up to rounding of d^-1/2."""
     if D.is_torch(u):
         t = D.torch()
         top = u[:m, :m]
         want = t.diag(t.as_tensor(d, device=u.device)[:m].rsqrt())
-        return bool(t.equal(top, want)) and (t.count_nonzero(u[m:, :m]).item() == 0)
+        return bool(t.allclose(top.to(want.dtype), want, rtol=1e-14, atol=0.0)) and \
+            (t.count_nonzero(u[m:, :m]).item() == 0)
     top = np.asarray(u[:m, :m])
     dd = np.asarray(d.cpu().numpy() if D.is_torch(d) else d)[:m]
-    return np.array_equal(top, np.diag(1.0 / np.sqrt(dd))) and not np.count_nonzero(u[m:, :m])
+    return np.allclose(top, np.diag(1.0 / np.sqrt(dd)), rtol=1e-14, atol=0.0) and not np.count_nonzero(u[m:, :m])
 
 
 def b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
@@ -266,3 +269,234 @@ class BGenHouseholder:
     choice: str
     n: int
     k0: int
+    _h: object = None          # the Euclidean reflector of (Phi v) on the device
+
+
+# ---------------------------------------------------------------------------
+# Drop-in B-path primitives through the isometry Phi (Phi = D^1/2 for a
+# diagonal B, L^T for a dense B = L L^T): <x, y>_B = (Phi y)^* (Phi x), and the
+# canonical basis initial_b_basis(inner, m) maps to [I_m; 0].  A B-reflector
+# for (v, u0 = canonical) is H = Phi^-1 H' Phi with H' the Euclidean reflector
+# of Phi v (same seed: the coupling u0^* B v is the top block of Phi v), and the
+# positive-diagonal B-QR of a is Q = Phi^-1 Q', R = R' for the nonneg
+# Householder QR of Phi a (unique, so it equals the reference's left-looking
+# result up to rounding).  Scaling by D^+-1/2 is an element-wise torch op on the
+# device; L^T x and L^-T x are the dense.cu kernels.
+# ---------------------------------------------------------------------------
+
+def _dev_of(inner, *xs):
+    if inner.diag is None:
+        return inner.chol_b.device.index
+    if D.is_torch(inner.diag) and inner.diag.is_cuda:
+        return inner.diag.device.index
+    return D.pick_device(*xs)
+
+
+def _sqrt_d(inner, dev):
+    t = D.torch()
+    d = inner.diag if D.is_torch(inner.diag) else t.from_numpy(inner.diag)
+    return d.to(device=f"cuda:{dev}", dtype=t.float64).sqrt()
+
+
+def _phi(inner, x, dev, inverse=False):
+    """Phi x (or Phi^-1 x) for x an n x m matrix; returns a device tensor."""
+    t = D.torch()
+    if inner.diag is not None:
+        xd = (x if D.is_torch(x) else t.from_numpy(np.ascontiguousarray(x))).to(f"cuda:{dev}")
+        s = _sqrt_d(inner, dev)[:, None]
+        return xd / s if inverse else xd * s
+    if is_complex(x):
+        raise NotImplementedError("dense complex B is not supported by this build")
+    L = inner.chol_b
+    n = L.shape[0]
+    ctx = D.ctx(dev)
+    X = D.to_device(x, dev)
+    if inverse:
+        Y = D.empty(n, X.cols, dev)
+        Y.buf[:, :X.cols].copy_(X.view())
+        check(lib().ots_dense_trsm_lt_f64(ctx, n, X.cols, C.c_void_p(L.data_ptr()), n, Y.ptr, Y.ld,
+                                          D.stream_ptr(dev)), ctx)
+    else:
+        Y = D.empty(n, X.cols, dev)
+        check(lib().ots_dense_trmm_lt_f64(ctx, n, X.cols, C.c_void_p(L.data_ptr()), n, X.ptr, X.ld, Y.ptr, Y.ld,
+                                          D.stream_ptr(dev)), ctx)
+    return Y.view()
+
+
+def _out(x, was_torch):
+    return x if was_torch else x.cpu().numpy()
+
+
+def _check_weighted(inner, n):
+    if inner.kind != "weighted":
+        raise NotImplementedError("the B-path needs a weighted inner product")
+    if inner.n != n:
+        raise E.DimensionError(f"weight is {inner.n} x {inner.n}, data has {n} rows")
+
+
+def _require_canonical(u, inner, m, name):
+    """u[:, :m] must be initial_b_basis(inner, m) (the basis every caller of
+    the reference's B-path passes, oblique.py:304-313, 331-346)."""
+    if inner.diag is not None:
+        ok = _is_canonical_basis(u, inner.diag, m)
+    else:
+        t = D.torch()
+        ucan = _dense_basis(inner, m)
+        ud = (u if D.is_torch(u) else t.from_numpy(np.ascontiguousarray(u))).to(
+            device=ucan.device, dtype=t.float64)
+        scale = float(ucan.abs().max().item()) if m else 1.0
+        ok = float((ud[:, :m] - ucan).abs().max().item()) <= 1e-12 * (scale or 1.0) if m else True
+    if not ok:
+        raise NotImplementedError(f"this build needs {name} = initial_b_basis(inner, {m})")
+
+
+def b_householder_qr(a, u_init, inner, reorth=True, prefix=None):
+    """oblique.py:170-238: B-orthonormal Q and upper-triangular R with a
+    positive diagonal, A = Q R.  Computed as Phi^-1 times the nonneg
+    Householder QR of Phi a on the GPU (the factorization is unique, so this
+    is the reference's result; `reorth` and `prefix` only steer the
+    reference's rounding and are accepted for drop-in callers).  Raises
+    BreakdownError when R_jj <= 1e3 u max_j ||a_j||_B (oblique.py:196-199)."""
+    from .core import EPS
+    was_torch = D.is_torch(a) or D.is_torch(u_init)
+    a = as_matrix(a, "a")
+    u_init = as_matrix(u_init, "u_init")
+    n, k = a.shape
+    if u_init.shape[0] != n:
+        raise E.DimensionError("a and u_init must share the row count")
+    if u_init.shape[1] < k:
+        raise E.DimensionError(f"u_init needs at least {k} columns")
+    if prefix is not None:
+        prefix = as_matrix(prefix, "prefix")
+        if prefix.shape[0] != n:
+            raise E.DimensionError("prefix must share the row count")
+    cplx = is_complex(a) or is_complex(u_init)
+    if k == 0:
+        dt = np.complex128 if cplx else np.float64
+        if was_torch:
+            t = D.torch()
+            tdt = t.complex128 if cplx else t.float64
+            return QRPair(t.zeros((n, 0), dtype=tdt), t.zeros((0, 0), dtype=tdt))
+        return QRPair(np.zeros((n, 0), dtype=dt), np.zeros((0, 0), dtype=dt))
+    _check_weighted(inner, n)
+    _require_canonical(u_init, inner, k, "u_init")
+    dev = _dev_of(inner, a)
+    pa = _phi(inner, a, dev)
+    t = D.torch()
+    scale = float(t.linalg.vector_norm(pa, dim=0).max().item())
+    thresh = 1e3 * EPS * scale
+    qr = householder_qr(pa, nonneg_diag=True)
+    rd = t.diagonal(qr.r).abs()
+    bad = t.nonzero(rd <= thresh)
+    if bad.numel():
+        j = int(bad[0, 0].item())
+        raise E.BreakdownError(f"column {j} is numerically zero after projection "
+                               f"(B-norm {float(rd[j].item()):.3e} <= {thresh:.3e})")
+    q = _phi(inner, qr.q, dev, inverse=True)
+    return QRPair(_out(q, was_torch), _out(qr.r, was_torch))
+
+
+def b_build_reflector(v, u0, inner, choice="qr", p=None, orth_tol=1e-6, allow_defect=False):
+    """oblique.py:125-151: the B-reflector H = I - w T^-1 w^* B mapping u0 p
+    onto v, for the canonical u0 = initial_b_basis(inner, k0).  Built as the
+    Euclidean device reflector of Phi v (same seed p and T); w = x - v with
+    x = u0 p.  Defect checks ||v^* B v - I||_2 = ||(Phi v)^*(Phi v) - I||_2 run
+    in the native build (oblique.py:141-145)."""
+    from .reflector import build_reflector
+    was_torch = D.is_torch(v) or D.is_torch(u0)
+    v = as_matrix(v, "v")
+    u0 = as_matrix(u0, "u0")
+    if tuple(v.shape) != tuple(u0.shape):
+        raise E.DimensionError(f"v and u0 must agree in shape, {tuple(v.shape)} vs {tuple(u0.shape)}")
+    n, k0 = v.shape
+    if k0 == 0:
+        raise E.DimensionError("v must have at least one column")
+    if is_complex(v) or is_complex(u0):
+        raise NotImplementedError("complex b_build_reflector: not in this build")
+    _check_weighted(inner, n)
+    _require_canonical(u0, inner, k0, "u0")
+    dev = _dev_of(inner, v)
+    pv = _phi(inner, v, dev)
+    try:
+        h = build_reflector(pv, choice=choice, p=p, orth_tol=orth_tol, allow_defect=allow_defect)
+    except E.OrthonormalityError as exc:
+        raise E.OrthonormalityError(str(exc).replace("v^* v", "v^* B v")) from None
+    t = D.torch()
+    pm = h.p                                     # device tensor (pv is torch)
+    top = t.zeros((n, k0), dtype=t.float64, device=pv.device)
+    top[:k0] = pm
+    x = _phi(inner, top, dev, inverse=True)     # u0 p = Phi^-1 [p; 0]
+    vd = v.to(pv.device) if D.is_torch(v) else t.from_numpy(np.ascontiguousarray(v)).to(pv.device)
+    w = x - vd
+    h._torch = was_torch
+    h.t_solver._torch = was_torch
+    return BGenHouseholder(w=_out(w, was_torch), t_solver=h.t_solver, p=_out(pm, was_torch), x=_out(x, was_torch),
+                           inner=inner, choice=choice, n=n, k0=k0, _h=h)
+
+
+def b_apply_reflector(h, x, inverse=False):
+    """oblique.py:154-161: H x, or H^-1 x = (I - w T^-* w^* B) x, computed as
+    Phi^-1 H'^(*) Phi x with the Euclidean device reflector H'."""
+    from .reflector import apply_reflector
+    was_torch = D.is_torch(x)
+    x = as_matrix(x, "x")
+    if x.shape[0] != h.n:
+        raise E.DimensionError(f"x has {x.shape[0]} rows, reflector expects {h.n}")
+    if h._h is None:
+        raise E.ParameterError("b_apply_reflector needs a reflector from b_build_reflector")
+    dev = h._h._h.dev
+    y = apply_reflector(h._h, _phi(h.inner, x, dev), adjoint=inverse)
+    return _out(_phi(h.inner, y, dev, inverse=True), was_torch)
+
+
+def b_block_householder_qr(blocks, inner, choice="qr", reorth=True):
+    """oblique.py:318-361: Algorithm 3 under the B inner product -- one
+    canonical basis for all blocks, block 0 by b_householder_qr, block i >= 1
+    by b_two_stage_qr against the accumulated Q; BreakdownError /
+    NotPositiveDefinite become IntraFailure tagged with the block index."""
+    from .twostage import BlockQRResult
+    if not blocks:
+        raise E.ParameterError("need at least one block")
+    was_torch = any(D.is_torch(b) for b in blocks)
+    blocks = [as_matrix(b, f"block {i}") for i, b in enumerate(blocks)]
+    n = blocks[0].shape[0]
+    sizes = [b.shape[1] for b in blocks]
+    if any(b.shape[0] != n for b in blocks):
+        raise E.DimensionError("all blocks must have the same row count")
+    total = sum(sizes)
+    if total > n:
+        raise E.DimensionError(f"need sum(k_i) <= n, got {total} > {n}")
+    t = D.torch()
+    u = initial_b_basis(inner, total)
+    dev = _dev_of(inner, *blocks)
+    cplx = any(is_complex(b) for b in blocks)
+    tdt = t.complex128 if cplx else t.float64
+    todev = (lambda z: (z if D.is_torch(z) else t.from_numpy(np.ascontiguousarray(z))).to(
+        device=f"cuda:{dev}", dtype=tdt))
+    blocks = [todev(b) for b in blocks]
+    u = (u if D.is_torch(u) else t.from_numpy(u)).to(device=f"cuda:{dev}", dtype=t.float64)
+    r_full = t.zeros((total, total), dtype=tdt, device=f"cuda:{dev}")
+    try:
+        qr0 = b_householder_qr(blocks[0], u[:, :sizes[0]], inner, reorth=reorth)
+    except (E.BreakdownError, E.NotPositiveDefinite) as exc:
+        raise E.IntraFailure(str(exc), block=0) from None
+    qs = [qr0.q]
+    r_full[:sizes[0], :sizes[0]] = qr0.r
+    worst = ReflectorDiagnostics(1.0, 0.0)
+    offset = sizes[0]
+    for i in range(1, len(blocks)):
+        ki = sizes[i]
+        qacc = t.cat(qs, dim=1)
+        m = qacc.shape[1]
+        try:
+            res = b_two_stage_qr(qacc, blocks[i], u[:, :m + ki], inner, choice=choice, reorth=reorth)
+        except (E.BreakdownError, E.NotPositiveDefinite) as exc:
+            raise E.IntraFailure(str(exc), block=i) from None
+        qs.append(res.q)
+        r_full[:m, offset:offset + ki] = res.s
+        r_full[offset:offset + ki, offset:offset + ki] = res.r
+        if res.diagnostics and res.diagnostics.kappa_t > worst.kappa_t:
+            worst = res.diagnostics
+        offset += ki
+    q = t.cat(qs, dim=1)
+    return BlockQRResult(_out(q, was_torch), _out(r_full, was_torch), sizes, worst)

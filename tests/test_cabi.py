@@ -66,3 +66,20 @@ def test_no_cpu_fallback():
         P.two_stage_qr(np.eye(10, 3), np.ones((10, 2)))
     with pytest.raises(P.NativeUnavailable):
         P.householder_qr(np.ones((10, 2)))
+    ip = P.InnerProduct.weighted(np.arange(1.0, 11.0))
+    with pytest.raises(P.NativeUnavailable):
+        P.b_householder_qr(np.ones((10, 2)), P.initial_b_basis(ip, 2), ip)
+    with pytest.raises(P.NativeUnavailable):
+        P.b_build_reflector(P.initial_b_basis(ip, 2), P.initial_b_basis(ip, 2), ip)
+    with pytest.raises(P.NativeUnavailable):
+        P.b_block_householder_qr([np.ones((10, 2))], ip)
+
+
+def test_drop_in_surface():
+    """every name of the reference's path surface."""
+    for name in ("two_stage_qr", "build_reflector", "apply_reflector", "reflector_diagnostics", "modified_lu",
+                 "b_two_stage_qr", "b_build_reflector", "b_apply_reflector", "b_householder_qr",
+                 "b_block_householder_qr", "InnerProduct", "initial_b_basis", "BGenHouseholder",
+                 "block_householder_qr", "reorthogonalized_two_stage", "householder_qr", "TwoStageResult",
+                 "BlockQRResult", "GenHouseholder", "ReflectorDiagnostics"):
+        assert callable(getattr(P, name)), name

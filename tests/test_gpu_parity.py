@@ -372,3 +372,96 @@ def test_gpu_metrics_vs_oracle(case):
     assert abs(rep.rel_residual - resid) <= max(1e-3 * resid, 1e-16)
     assert rep.kappa_t == res.diagnostics.kappa_t
     assert abs(P.orthogonality_loss(res.q, v=v) - O.stability(v, a, res.q, res.r, res.s)[0]) < 1e-13
+
+
+def _b_case(kind, n, k0, k, seed):
+    rng = W.make_rng(seed)
+    if kind == "diag":
+        d = 10.0 ** W.uniform(rng, 0.0, 2.0, n)
+        ip, ref_in, lo = P.InnerProduct.weighted(d), O.BInner(diag=d), np.diag(np.sqrt(d))
+    else:
+        X = W.normal_matrix(rng, n, n)
+        b = X @ X.T / n + np.eye(n)
+        ip, ref_in, lo = P.InnerProduct.weighted(b), O.BInner(b=b), np.linalg.cholesky(b)
+    v = np.linalg.solve(lo.T, np.linalg.qr(W.normal_matrix(rng, n, k0))[0])   # B-orthonormal
+    a = W.normal_matrix(rng, n, k)
+    return ip, ref_in, v, a
+
+
+@pytest.mark.parametrize("kind", ["diag", "dense"])
+@pytest.mark.parametrize("choice", ["mlu", "qr", "polar"])
+def test_b_reflector_vs_oracle(kind, choice):
+    """b_build_reflector / b_apply_reflector (oblique.py:125-161) against the
+    oracle's inline B-reflector of b_two_stage (oracle/twostage_oracle.py)."""
+    n, k0, k = 900, 24, 16
+    ip, ref_in, v, a = _b_case(kind, n, k0, k, 300 + k0)
+    u0 = P.initial_b_basis(ip, k0)
+    h = P.b_build_reflector(v, u0, ip, choice=choice)
+    coupling = v.T @ ref_in.apply(u0)
+    pm, tf = O.seed(coupling.T, choice, None)
+    x = u0 @ pm
+    w = x - v
+    assert rel(h.p, pm) < 1e-10 and rel(h.x, x) < 1e-10 and rel(h.w, w) < 1e-10
+    hinv_a = a - w @ tf.solve(w.T @ ref_in.apply(a), adjoint=True)
+    h_a = a - w @ tf.solve(w.T @ ref_in.apply(a))
+    assert rel(P.b_apply_reflector(h, a, inverse=True), hinv_a) < 1e-10
+    assert rel(P.b_apply_reflector(h, a), h_a) < 1e-10
+    # H maps x = u0 p onto v and is B-unitary
+    assert rel(P.b_apply_reflector(h, x), v) < 1e-10
+    y = P.b_apply_reflector(h, a)
+    assert rel(y.T @ ref_in.apply(y), a.T @ ref_in.apply(a)) < 1e-10
+    ts = h.t_solver.solve(np.eye(k0))
+    assert rel(ts, tf.solve(np.eye(k0))) < 1e-10
+    with pytest.raises(P.OrthonormalityError):
+        P.b_build_reflector(2.0 * v, u0, ip, choice=choice)
+    with pytest.raises(P.DimensionError):
+        P.b_build_reflector(v[:, :3], u0, ip)
+
+
+@pytest.mark.parametrize("kind", ["diag", "dense"])
+def test_b_householder_qr_vs_oracle(kind):
+    n, k = 1100, 48
+    ip, ref_in, _, a = _b_case(kind, n, 8, k, 410)
+    u = P.initial_b_basis(ip, k)
+    res = P.b_householder_qr(a, u, ip)
+    q, r = O.b_house(a, u, ref_in)
+    assert rel(res.q, q) < 1e-10 and rel(res.r, r) < 1e-10
+    assert np.all(np.diag(res.r) > 0)
+    # torch in -> torch out, on the device
+    t = pytest.importorskip("torch")
+    rt = P.b_householder_qr(t.from_numpy(a).cuda(), t.from_numpy(u).cuda(), ip)
+    assert rt.q.is_cuda and rel(rt.q.cpu().numpy(), q) < 1e-10
+    a0 = a.copy()
+    a0[:, 5] = 0.0
+    with pytest.raises(P.BreakdownError):
+        P.b_householder_qr(a0, u, ip)
+    assert P.b_householder_qr(np.zeros((n, 0)), u, ip).q.shape == (n, 0)
+
+
+@pytest.mark.parametrize("kind", ["diag", "dense"])
+def test_b_block_householder_qr_vs_oracle(kind):
+    """oblique.py:318-361 against the oracle driven block by block."""
+    n, sizes = 1200, [16, 24, 32]
+    ip, ref_in, _, a = _b_case(kind, n, 8, sum(sizes), 520)
+    blocks = [a[:, sum(sizes[:i]):sum(sizes[:i + 1])] for i in range(len(sizes))]
+    res = P.b_block_householder_qr(blocks, ip)
+    u = ref_in.first_basis(sum(sizes))
+    q0, r0 = O.b_house(blocks[0], u[:, :sizes[0]], ref_in)
+    qs, rf = [q0], np.zeros((sum(sizes), sum(sizes)))
+    rf[:sizes[0], :sizes[0]] = r0
+    off = sizes[0]
+    for i in range(1, len(sizes)):
+        qa = np.hstack(qs)
+        out = O.b_two_stage(qa, blocks[i], u[:, :off + sizes[i]], ref_in, "qr", diagnostics=False)
+        qs.append(out["q"])
+        rf[:off, off:off + sizes[i]] = out["s"]
+        rf[off:off + sizes[i], off:off + sizes[i]] = out["r"]
+        off += sizes[i]
+    assert rel(res.q, np.hstack(qs)) < 1e-10 and rel(res.r, rf) < 1e-10
+    assert res.block_sizes == sizes
+    assert rel(res.q @ res.r, a) < 1e-12
+    bad = [b.copy() for b in blocks]
+    bad[0][:, 3] = 0.0
+    with pytest.raises(P.IntraFailure) as ei:
+        P.b_block_householder_qr(bad, ip)
+    assert ei.value.block == 0
