@@ -41,9 +41,13 @@ __device__ __forceinline__ cplx cshfl_xor(unsigned mask, cplx v, int o) {
   return cmk(__shfl_xor_sync(mask, v.x, o), __shfl_xor_sync(mask, v.y, o));
 }
 
+#ifndef ZNT
+#define ZNT 512
+#endif
+
 template <int KT>
 struct ZCfg {
-  static constexpr int NT = 256;
+  static constexpr int NT = ZNT;       // factor threads per CTA
   static constexpr int B = 64;            // structured tile rows (BMAX)
   static constexpr int TPC = NT / KT;     // threads per column
   static constexpr int LDS = KT + 1;      // smem row stride (complex units)
@@ -149,34 +153,104 @@ __device__ void zsweep(cplx* A, int nb, cplx* U, cplx* tau_s) {
   }
 }
 
+// Structured-tile sweep (rows 0..KT-1 hold R, rows KT..KT+B-1 the tile, zero
+// beyond nb): thread (c, q) keeps rows KT+q+TPC*i of column c in registers, so
+// each step reads only the pivot column from shared memory.  A column's
+// scaled reflector is written back when it becomes the pivot (phase_a).
+template <int KT>
+__device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s) {
+  using C = ZCfg<KT>;
+  constexpr int TPC = C::TPC, LDS = C::LDS, UL = C::UL, RPT = C::B / TPC;
+  const int tid = threadIdx.x;
+  const int c = tid / TPC, q = tid % TPC;
+  const unsigned gmask = (TPC >= 32) ? 0xffffffffu : (((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1)));
+  cplx x[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) x[i] = A[(KT + q + TPC * i) * LDS + c];
+
+  auto phase_a = [&](int j) {   // owners of column j (c == j): zlarfg on x
+    const cplx alpha = A[j * LDS + j];
+    double s2 = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) s2 = fma(x[i].x, x[i].x, fma(x[i].y, x[i].y, s2));
+    s2 = gsum<TPC>(s2, gmask);
+    cplx tau = cmk(0.0, 0.0);
+    cplx beta = alpha;
+    if (s2 != 0.0 || alpha.y != 0.0) {
+      const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
+      tau = cmk((bt - alpha.x) / bt, -alpha.y / bt);
+      const cplx scal = crecip(csub(alpha, cmk(bt, 0.0)));
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) x[i] = cmul(x[i], scal);
+      beta = cmk(bt, 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) A[(KT + q + TPC * i) * LDS + j] = x[i];
+    __syncwarp(gmask);
+    if (q == 0) { A[j * LDS + j] = beta; tau_s[j] = tau; }
+  };
+
+  if (c == 0) phase_a(0);
+  __syncthreads();
+  for (int j = 0; j < KT; ++j) {
+    if (c != j) {
+      cplx v[RPT];
+      cplx d = cmk(0.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) {
+        v[i] = A[(KT + q + TPC * i) * LDS + j];
+        d = cfmac(v[i], x[i], d);
+      }
+      d = gsumc<TPC>(d, gmask);
+      if (c > j) {
+        d = cadd(d, A[j * LDS + c]);
+        const cplx w = cmul(conjc(tau_s[j]), d);     // conj(tau) v^H a
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) x[i] = csub(x[i], cmul(w, v[i]));
+        if (q == 0) A[j * LDS + c] = csub(A[j * LDS + c], w);
+        if (c == j + 1) {
+          __syncwarp(gmask);
+          phase_a(j + 1);
+        }
+      } else {
+        if (q == 0) U[c * UL + j] = conjc(d);        // U[c][j] = v_c^H v_j
+      }
+    } else {
+      if (q == 0) U[j * UL + j] = tau_s[j];
+    }
+    __syncthreads();
+  }
+}
+
 // T (zlarft forward, columnwise) from U; T -> global Tg (KT x KT, row-major)
 template <int KT>
 __device__ void zu_to_t(cplx* U, cplx* Tg) {
   constexpr int UL = ZCfg<KT>::UL;
+  constexpr int G = ZCfg<KT>::NT / KT;   // threads per row of T (a power of two)
   // in place in U: column j of T over rows i < j uses T[i][l] (l < j, already
   // final in U's upper part; U[i][i] = tau_i = T[i][i]) and U[l][j] (column j
-  // still holds Gram entries); the new column is written after a barrier.
+  // still holds Gram entries); G threads share each row's dot product and the
+  // new column is written after a barrier.
+  const int i = threadIdx.x / G, g = threadIdx.x % G;
+  const unsigned gmask = (G >= 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
   for (int j = 1; j < KT; ++j) {
     const cplx tj = U[j * UL + j];
-    cplx val = cmk(0.0, 0.0);
-    const int i = threadIdx.x;
-    if (i < j) {
-      cplx s = cmk(0.0, 0.0);
-      for (int l = i; l < j; ++l) s = cfma(U[i * UL + l], U[l * UL + j], s);
-      val = cneg(cmul(tj, s));
-    }
+    cplx s = cmk(0.0, 0.0);
+    if (i < j)
+      for (int l = i + g; l < j; l += G) s = cfma(U[i * UL + l], U[l * UL + j], s);
+    s = gsumc<G>(s, gmask);
     __syncthreads();
-    if (i < j) U[i * UL + j] = val;
+    if (i < j && g == 0) U[i * UL + j] = cneg(cmul(tj, s));
     __syncthreads();
   }
   for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
-    const int i = e / KT, j = e - i * KT;
-    Tg[e] = (j >= i) ? U[i * UL + j] : cmk(0.0, 0.0);
+    const int r = e / KT, c = e - r * KT;
+    Tg[e] = (c >= r) ? U[r * UL + c] : cmk(0.0, 0.0);
   }
 }
 
 template <int KT>
-__global__ void __launch_bounds__(256, 1) zchain_factor_kernel(ZFactorArgs a) {
+__global__ void __launch_bounds__(ZNT, 1) zchain_factor_kernel(ZFactorArgs a) {
   using C = ZCfg<KT>;
   constexpr int LDS = C::LDS, UL = C::UL;
   extern __shared__ __align__(16) unsigned char zsm_raw[];
@@ -212,7 +286,7 @@ __global__ void __launch_bounds__(256, 1) zchain_factor_kernel(ZFactorArgs a) {
     const int nb = (int)(rem < b ? rem : b);
     zload_rows<KT>(A, KT, D0, a.ldd, gr0, C::B, gr0 + nb, a.ncols);
     __syncthreads();
-    zsweep<KT, false>(A, nb, U, tau_s);
+    zsweep_tile<KT>(A, U, tau_s);
     zstore_rows<KT>(A, KT, D, a.ldd, gr0, nb, a.G.nrows, a.ncols);
     __syncthreads();
     zu_to_t<KT>(U, Tbase + (long)t * KT * KT);
@@ -339,7 +413,7 @@ cudaError_t zfactor_t(const ZFactorArgs& a, cudaStream_t st) {
   if (a.G.b > C::B || a.G.nchains <= 0) return cudaErrorInvalidValue;
   auto k = zchain_factor_kernel<KT>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  k<<<a.G.nchains, 256, C::SMEM, st>>>(a);
+  k<<<a.G.nchains, C::NT, C::SMEM, st>>>(a);
   return cudaGetLastError();
 }
 template <int KT>
