@@ -53,7 +53,7 @@ struct ZCfg {
   static constexpr int LDS = KT + 1;      // smem row stride (complex units)
   static constexpr int ROWS = KT + B;     // R rows + tile rows
   static constexpr int UL = KT + 1;
-  static constexpr int SMEM = (ROWS * LDS + KT * UL + KT) * 16;
+  static constexpr int SMEM = (ROWS * LDS + KT * UL + KT + 2 * B) * 16;
 };
 
 template <int TPC>
@@ -153,20 +153,42 @@ __device__ void zsweep(cplx* A, int nb, cplx* U, cplx* tau_s) {
   }
 }
 
-// Structured-tile sweep (rows 0..KT-1 hold R, rows KT..KT+B-1 the tile, zero
-// beyond nb): thread (c, q) keeps rows KT+q+TPC*i of column c in registers, so
-// each step reads only the pivot column from shared memory.  A column's
-// scaled reflector is written back when it becomes the pivot (phase_a).
+// next structured tile -> the smem tile buffer (cp.async, zero fill beyond
+// nb rows / ncols columns)
 template <int KT>
-__device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s) {
+__device__ __forceinline__ void zprefetch_tile(cplx* buf, const cplx* D0, long ldd, long gr0, int nb, int ncols) {
+  constexpr int LDS = ZCfg<KT>::LDS, B = ZCfg<KT>::B;
+  for (int e = threadIdx.x; e < B * KT; e += blockDim.x) {
+    const int r = e / KT, c = e - r * KT;
+    const bool ok = r < nb && c < ncols;
+    cp_async16(buf + r * LDS + c, ok ? (const void*)(D0 + (gr0 + r) * ldd + c) : (const void*)D0, ok ? 16 : 0);
+  }
+  cp_async_commit();
+}
+
+// Structured-tile sweep.  Rows 0..KT-1 of A hold R; the tile (landed in the
+// buffer rows KT..KT+B-1 by cp.async, zero beyond nb) is moved to registers:
+// thread (c, q) keeps rows q+TPC*i of column c, and the buffer then receives
+// the next tile while this one is swept.  Each step reads the pivot reflector
+// from a two-column slot ring; a column's final reflector goes from registers
+// straight to global memory.  T (zlarft forward) is built one column behind
+// the Gram entries by the groups left of the pivot, T[i][l] (l > i) kept in
+// U's lower triangle (U[l][i]), tau_i on the diagonal, U[l][j] (l < j) = v_l^H v_j.
+template <int KT>
+__device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, const cplx* D0, long ldd, long gr0,
+                            int nb, int ncols, long nxt_gr0, int nxt_nb, cplx* Tg) {
   using C = ZCfg<KT>;
-  constexpr int TPC = C::TPC, LDS = C::LDS, UL = C::UL, RPT = C::B / TPC;
+  constexpr int TPC = C::TPC, LDS = C::LDS, UL = C::UL, B = C::B, RPT = B / TPC;
   const int tid = threadIdx.x;
   const int c = tid / TPC, q = tid % TPC;
   const unsigned gmask = (TPC >= 32) ? 0xffffffffu : (((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1)));
   cplx x[RPT];
+  cp_async_wait<0>();
+  __syncthreads();
 #pragma unroll
   for (int i = 0; i < RPT; ++i) x[i] = A[(KT + q + TPC * i) * LDS + c];
+  __syncthreads();
+  if (nxt_nb > 0) zprefetch_tile<KT>(A + KT * LDS, D0, ldd, nxt_gr0, nxt_nb, ncols);
 
   auto phase_a = [&](int j) {   // owners of column j (c == j): zlarfg on x
     const cplx alpha = A[j * LDS + j];
@@ -178,27 +200,42 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s) {
     cplx beta = alpha;
     if (s2 != 0.0 || alpha.y != 0.0) {
       const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
-      tau = cmk((bt - alpha.x) / bt, -alpha.y / bt);
-      const cplx scal = crecip(csub(alpha, cmk(bt, 0.0)));
+      const double ib = 1.0 / bt;
+      tau = cmk((bt - alpha.x) * ib, -alpha.y * ib);
+      const double dr = alpha.x - bt;
+      const double id = 1.0 / (dr * dr + alpha.y * alpha.y);
+      const cplx scal = cmk(dr * id, -alpha.y * id);     // 1 / (alpha - beta)
 #pragma unroll
       for (int i = 0; i < RPT; ++i) x[i] = cmul(x[i], scal);
       beta = cmk(bt, 0.0);
     }
+    cplx* sl = slot + (j & 1) * B;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) A[(KT + q + TPC * i) * LDS + j] = x[i];
+    for (int i = 0; i < RPT; ++i) {
+      const int row = q + TPC * i;
+      sl[row] = x[i];
+      if (row < nb && j < ncols) D[(gr0 + row) * ldd + j] = x[i];
+    }
     __syncwarp(gmask);
     if (q == 0) { A[j * LDS + j] = beta; tau_s[j] = tau; }
+  };
+  auto t_col = [&](int jj) {    // T[c][jj] = -tau_jj sum_{l=c}^{jj-1} T[c][l] U[l][jj]  (groups c < jj)
+    cplx sacc = cmk(0.0, 0.0);
+    for (int l = c + q; l < jj; l += TPC) sacc = cfma(U[l * UL + c], U[l * UL + jj], sacc);
+    sacc = gsumc<TPC>(sacc, gmask);
+    if (q == 0) U[jj * UL + c] = cneg(cmul(tau_s[jj], sacc));
   };
 
   if (c == 0) phase_a(0);
   __syncthreads();
   for (int j = 0; j < KT; ++j) {
     if (c != j) {
+      const cplx* vj = slot + (j & 1) * B;
       cplx v[RPT];
       cplx d = cmk(0.0, 0.0);
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
-        v[i] = A[(KT + q + TPC * i) * LDS + j];
+        v[i] = vj[q + TPC * i];
         d = cfmac(v[i], x[i], d);
       }
       d = gsumc<TPC>(d, gmask);
@@ -214,11 +251,18 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s) {
         }
       } else {
         if (q == 0) U[c * UL + j] = conjc(d);        // U[c][j] = v_c^H v_j
+        if (c < j - 1) t_col(j - 1);
       }
     } else {
       if (q == 0) U[j * UL + j] = tau_s[j];
     }
     __syncthreads();
+  }
+  if (c < KT - 1) t_col(KT - 1);
+  __syncthreads();
+  for (int e = tid; e < KT * KT; e += blockDim.x) {
+    const int r = e / KT, cc = e - r * KT;
+    Tg[e] = cc > r ? U[cc * UL + r] : (cc == r ? U[r * UL + r] : cmk(0.0, 0.0));
   }
 }
 
@@ -267,6 +311,17 @@ __global__ void __launch_bounds__(ZNT, 1) zchain_factor_kernel(ZFactorArgs a) {
   if (rem0 > 0) { long t = (rem0 + b - 1) / b; ntiles = (int)(t < a.G.L ? t : a.G.L); }
   cplx* Tbase = reinterpret_cast<cplx*>(a.U) + (long)chain * (a.G.L + 1) * KT * KT;
 
+  cplx* slot = tau_s + KT;
+  auto tile_rows = [&](int t, long& g0) {
+    g0 = r0 + KT + (long)(t - 1) * b;
+    const long rem = a.G.nrows - g0;
+    return (int)(rem < b ? rem : b);
+  };
+  if (ntiles >= 1) {   // tile 1 lands in the buffer while the head is factored
+    long g1;
+    const int nb1 = tile_rows(1, g1);
+    zprefetch_tile<KT>(A + KT * LDS, D0, a.ldd, g1, nb1, a.ncols);
+  }
   // head
   zload_rows<KT>(A, 0, D0, a.ldd, r0, KT, a.G.nrows, a.ncols);
   __syncthreads();
@@ -279,19 +334,13 @@ __global__ void __launch_bounds__(ZNT, 1) zchain_factor_kernel(ZFactorArgs a) {
     const int i = e / KT, j = e - i * KT;
     if (j < i) A[i * LDS + j] = cmk(0.0, 0.0);
   }
-  __syncthreads();
   for (int t = 1; t <= ntiles; ++t) {
-    const long gr0 = r0 + KT + (long)(t - 1) * b;
-    const long rem = a.G.nrows - gr0;
-    const int nb = (int)(rem < b ? rem : b);
-    zload_rows<KT>(A, KT, D0, a.ldd, gr0, C::B, gr0 + nb, a.ncols);
-    __syncthreads();
-    zsweep_tile<KT>(A, U, tau_s);
-    zstore_rows<KT>(A, KT, D, a.ldd, gr0, nb, a.G.nrows, a.ncols);
-    __syncthreads();
-    zu_to_t<KT>(U, Tbase + (long)t * KT * KT);
-    __syncthreads();
+    long gr0, g2 = 0;
+    const int nb = tile_rows(t, gr0);
+    const int nb2 = t < ntiles ? tile_rows(t + 1, g2) : 0;
+    zsweep_tile<KT>(A, U, tau_s, slot, D, D0, a.ldd, gr0, nb, a.ncols, g2, nb2, Tbase + (long)t * KT * KT);
   }
+  __syncthreads();
   cplx* R = reinterpret_cast<cplx*>(a.Rout) + (long)chain * KT * KT;
   for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
     const int i = e / KT, j = e - i * KT;
@@ -299,15 +348,22 @@ __global__ void __launch_bounds__(ZNT, 1) zchain_factor_kernel(ZFactorArgs a) {
   }
 }
 
-// M = T C  (T upper triangular, global; C smem)  into smem M
+// acc[i][jj] += sum_l As[tr+16i][l] Bs[l][tc+16jj]  (KT x KT smem operands,
+// 256 threads as a 16 x 16 grid of (KT/16) x (KT/16) register tiles)
 template <int KT>
-__device__ void z_tc(const cplx* T, const cplx* Cs, cplx* Ms) {
-  constexpr int LDS = ZCfg<KT>::LDS;
-  for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
-    const int i = e / KT, j = e - i * KT;
-    cplx s = cmk(0.0, 0.0);
-    for (int l = i; l < KT; ++l) s = cfma(T[i * KT + l], Cs[l * LDS + j], s);
-    Ms[i * LDS + j] = s;
+__device__ __forceinline__ void zmm(const cplx* As, const cplx* Bs, cplx (&acc)[KT / 16][KT / 16], int tr, int tc) {
+  constexpr int LDS = ZCfg<KT>::LDS, MT = KT / 16;
+#pragma unroll 4
+  for (int l = 0; l < KT; ++l) {
+    cplx av[MT], bv[MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) av[i] = As[(tr + 16 * i) * LDS + l];
+#pragma unroll
+    for (int jj = 0; jj < MT; ++jj) bv[jj] = Bs[l * LDS + tc + 16 * jj];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < MT; ++jj) acc[i][jj] = cfma(av[i], bv[jj], acc[i][jj]);
   }
 }
 
@@ -335,25 +391,51 @@ __global__ void __launch_bounds__(256, 1) zchain_qform_kernel(ZQformArgs a) {
     Cs[i * LDS + j] = Cin[e];
   }
   __syncthreads();
+  constexpr int MT = KT / 16;
+  const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
   for (int t = ntiles; t >= 1; --t) {
     const long gr0 = r0 + KT + (long)(t - 1) * b;
     const long rem = a.G.nrows - gr0;
     const int nb = (int)(rem < b ? rem : b);
-    z_tc<KT>(Tbase + (long)t * KT * KT, Cs, Ms);
+    const cplx* Tt = Tbase + (long)t * KT * KT;
+    for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+      const int i = e / KT, j = e - i * KT;
+      Ys[i * LDS + j] = Tt[e];
+    }
     __syncthreads();
-    for (int c0 = 0; c0 < nb; c0 += 32) {
-      const int nr = (nb - c0 < 32) ? nb - c0 : 32;
-      for (int e = threadIdx.x; e < nr * KT; e += blockDim.x) {
+    {   // M = T C
+      cplx acc[MT][MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) acc[i][jj] = cmk(0.0, 0.0);
+      zmm<KT>(Ys, Cs, acc, tr, tc);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) Ms[(tr + 16 * i) * LDS + tc + 16 * jj] = acc[i][jj];
+    }
+    __syncthreads();
+    for (int c0 = 0; c0 < nb; c0 += KT) {   // out = -Y M, KT rows at a time
+      const int nr = (nb - c0 < KT) ? nb - c0 : KT;
+      for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
         const int r = e / KT, c = e - r * KT;
-        Ys[r * LDS + c] = (c < a.ncols) ? D[(gr0 + c0 + r) * a.ldd + c] : cmk(0.0, 0.0);
+        Ys[r * LDS + c] = (r < nr && c < a.ncols) ? D[(gr0 + c0 + r) * a.ldd + c] : cmk(0.0, 0.0);
       }
       __syncthreads();
-      for (int e = threadIdx.x; e < nr * KT; e += blockDim.x) {
-        const int r = e / KT, c = e - r * KT;
-        cplx s = cmk(0.0, 0.0);
-        for (int l = 0; l < KT; ++l) s = cfma(Ys[r * LDS + l], Ms[l * LDS + c], s);
-        if (c < a.ncols) D[(gr0 + c0 + r) * a.ldd + c] = cneg(s);
-      }
+      cplx acc[MT][MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) acc[i][jj] = cmk(0.0, 0.0);
+      zmm<KT>(Ys, Ms, acc, tr, tc);
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) {
+          const int r = tr + 16 * i, c = tc + 16 * jj;
+          if (r < nr && c < a.ncols) D[(gr0 + c0 + r) * a.ldd + c] = cneg(acc[i][jj]);
+        }
       __syncthreads();
     }
     for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
