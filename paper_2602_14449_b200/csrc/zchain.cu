@@ -190,21 +190,25 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
   __syncthreads();
   if (nxt_nb > 0) zprefetch_tile<KT>(A + KT * LDS, D0, ldd, nxt_gr0, nxt_nb, ncols);
 
-  auto phase_a = [&](int j) {   // owners of column j (c == j): zlarfg on x
-    const cplx alpha = A[j * LDS + j];
-    double s2 = 0.0;
+  auto phase_a = [&](int j, cplx alpha) {   // owners of column j (c == j): zlarfg on x
+    double s2a = 0.0, s2b = 0.0;
 #pragma unroll
-    for (int i = 0; i < RPT; ++i) s2 = fma(x[i].x, x[i].x, fma(x[i].y, x[i].y, s2));
-    s2 = gsum<TPC>(s2, gmask);
+    for (int i = 0; i < RPT; i += 2) {
+      s2a = fma(x[i].x, x[i].x, fma(x[i].y, x[i].y, s2a));
+      if (i + 1 < RPT) s2b = fma(x[i + 1].x, x[i + 1].x, fma(x[i + 1].y, x[i + 1].y, s2b));
+    }
+    const double s2 = gsum<TPC>(s2a + s2b, gmask);
     cplx tau = cmk(0.0, 0.0);
     cplx beta = alpha;
     if (s2 != 0.0 || alpha.y != 0.0) {
       const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
-      const double ib = 1.0 / bt;
-      tau = cmk((bt - alpha.x) * ib, -alpha.y * ib);
-      const double dr = alpha.x - bt;
-      const double id = 1.0 / (dr * dr + alpha.y * alpha.y);
-      const cplx scal = cmk(dr * id, -alpha.y * id);     // 1 / (alpha - beta)
+      // one reciprocal rr = 1 / (bt m), m = |alpha - beta|^2, gives 1/bt = m rr and 1/m = bt rr
+      const double e = bt - alpha.x;
+      const double m = fma(e, e, alpha.y * alpha.y);
+      const double rr = 1.0 / (bt * m);
+      const double ib = m * rr, im = bt * rr;
+      tau = cmk(e * ib, -alpha.y * ib);
+      const cplx scal = cmk(-e * im, -alpha.y * im);     // conj(alpha - beta) / |alpha - beta|^2
 #pragma unroll
       for (int i = 0; i < RPT; ++i) x[i] = cmul(x[i], scal);
       beta = cmk(bt, 0.0);
@@ -226,10 +230,11 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
     if (q == 0) U[jj * UL + c] = cneg(cmul(tau_s[jj], sacc));
   };
 
-  if (c == 0) phase_a(0);
+  if (c == 0) phase_a(0, A[0]);
   __syncthreads();
   for (int j = 0; j < KT; ++j) {
     if (c != j) {
+      const cplx alpha_n = (c == j + 1) ? A[c * LDS + c] : cmk(0.0, 0.0);
       const cplx* vj = slot + (j & 1) * B;
       cplx v[RPT];
       cplx d = cmk(0.0, 0.0);
@@ -247,7 +252,7 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
         if (q == 0) A[j * LDS + c] = csub(A[j * LDS + c], w);
         if (c == j + 1) {
           __syncwarp(gmask);
-          phase_a(j + 1);
+          phase_a(j + 1, alpha_n);
         }
       } else {
         if (q == 0) U[c * UL + j] = conjc(d);        // U[c][j] = v_c^H v_j
