@@ -181,7 +181,6 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
   constexpr int TPC = C::TPC, LDS = C::LDS, UL = C::UL, B = C::B, RPT = B / TPC;
   const int tid = threadIdx.x;
   const int c = tid / TPC, q = tid % TPC;
-  const unsigned gmask = (TPC >= 32) ? 0xffffffffu : (((1u << TPC) - 1u) << ((tid & 31) & ~(TPC - 1)));
   cplx x[RPT];
   cp_async_wait<0>();
   __syncthreads();
@@ -190,80 +189,82 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
   __syncthreads();
   if (nxt_nb > 0) zprefetch_tile<KT>(A + KT * LDS, D0, ldd, nxt_gr0, nxt_nb, ncols);
 
-  auto phase_a = [&](int j, cplx alpha) {   // owners of column j (c == j): zlarfg on x
+  // The whole warp holding column j runs zlarfg (warp-uniform: full-mask
+  // shuffles, no divergence); only the group c == j commits.
+  const int warp = tid >> 5;
+  const int c_first = (warp * 32) / TPC;     // first column of this warp
+  constexpr unsigned FULL = 0xffffffffu;
+  auto phase_a = [&](int j, cplx alpha) {
+    const bool own = (c == j);
     double s2a = 0.0, s2b = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; i += 2) {
       s2a = fma(x[i].x, x[i].x, fma(x[i].y, x[i].y, s2a));
       if (i + 1 < RPT) s2b = fma(x[i + 1].x, x[i + 1].x, fma(x[i + 1].y, x[i + 1].y, s2b));
     }
-    const double s2 = gsum<TPC>(s2a + s2b, gmask);
-    cplx tau = cmk(0.0, 0.0);
-    cplx beta = alpha;
-    if (s2 != 0.0 || alpha.y != 0.0) {
-      const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
-      // one reciprocal rr = 1 / (bt m), m = |alpha - beta|^2, gives 1/bt = m rr and 1/m = bt rr
-      const double e = bt - alpha.x;
-      const double m = fma(e, e, alpha.y * alpha.y);
-      const double rr = 1.0 / (bt * m);
-      const double ib = m * rr, im = bt * rr;
-      tau = cmk(e * ib, -alpha.y * ib);
-      const cplx scal = cmk(-e * im, -alpha.y * im);     // conj(alpha - beta) / |alpha - beta|^2
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) x[i] = cmul(x[i], scal);
-      beta = cmk(bt, 0.0);
-    }
-    cplx* sl = slot + (j & 1) * B;
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int row = q + TPC * i;
-      sl[row] = x[i];
-      if (row < nb && j < ncols) D[(gr0 + row) * ldd + j] = x[i];
-    }
-    __syncwarp(gmask);
-    if (q == 0) { A[j * LDS + j] = beta; tau_s[j] = tau; }
-  };
-  auto t_col = [&](int jj) {    // T[c][jj] = -tau_jj sum_{l=c}^{jj-1} T[c][l] U[l][jj]  (groups c < jj)
-    cplx sacc = cmk(0.0, 0.0);
-    for (int l = c + q; l < jj; l += TPC) sacc = cfma(U[l * UL + c], U[l * UL + jj], sacc);
-    sacc = gsumc<TPC>(sacc, gmask);
-    if (q == 0) U[jj * UL + c] = cneg(cmul(tau_s[jj], sacc));
-  };
-
-  if (c == 0) phase_a(0, A[0]);
-  __syncthreads();
-  for (int j = 0; j < KT; ++j) {
-    if (c != j) {
-      const cplx alpha_n = (c == j + 1) ? A[c * LDS + c] : cmk(0.0, 0.0);
-      const cplx* vj = slot + (j & 1) * B;
-      cplx v[RPT];
-      cplx d = cmk(0.0, 0.0);
+    const double s2 = gsum<TPC>(s2a + s2b, FULL);
+    const bool nz = (s2 != 0.0 || alpha.y != 0.0);
+    const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
+    // one reciprocal rr = 1 / (bt m), m = |alpha - beta|^2, gives 1/bt = m rr and 1/m = bt rr
+    const double e = bt - alpha.x;
+    const double m = fma(e, e, alpha.y * alpha.y);
+    const double rr = 1.0 / (bt * m);
+    const double ib = m * rr, im = bt * rr;
+    const cplx tau = nz ? cmk(e * ib, -alpha.y * ib) : cmk(0.0, 0.0);
+    const cplx scal = cmk(-e * im, -alpha.y * im);     // conj(alpha - beta) / |alpha - beta|^2
+    const cplx beta = nz ? cmk(bt, 0.0) : alpha;
+    if (own) {
+      cplx* sl = slot + (j & 1) * B;
 #pragma unroll
       for (int i = 0; i < RPT; ++i) {
-        v[i] = vj[q + TPC * i];
-        d = cfmac(v[i], x[i], d);
+        if (nz) x[i] = cmul(x[i], scal);
+        const int row = q + TPC * i;
+        sl[row] = x[i];
+        if (row < nb && j < ncols) D[(gr0 + row) * ldd + j] = x[i];
       }
-      d = gsumc<TPC>(d, gmask);
-      if (c > j) {
-        d = cadd(d, A[j * LDS + c]);
-        const cplx w = cmul(conjc(tau_s[j]), d);     // conj(tau) v^H a
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) x[i] = csub(x[i], cmul(w, v[i]));
-        if (q == 0) A[j * LDS + c] = csub(A[j * LDS + c], w);
-        if (c == j + 1) {
-          __syncwarp(gmask);
-          phase_a(j + 1, alpha_n);
-        }
-      } else {
-        if (q == 0) U[c * UL + j] = conjc(d);        // U[c][j] = v_c^H v_j
-        if (c < j - 1) t_col(j - 1);
-      }
-    } else {
-      if (q == 0) U[j * UL + j] = tau_s[j];
+      if (q == 0) { A[j * LDS + j] = beta; tau_s[j] = tau; }
     }
+  };
+  auto t_col = [&](int jj) {    // T[c][jj] = -tau_jj sum_{l=c}^{jj-1} T[c][l] U[l][jj]  (groups c < jj)
+    if (c_first >= jj) return;  // warp-uniform
+    cplx sacc = cmk(0.0, 0.0);
+    if (c < jj)
+      for (int l = c + q; l < jj; l += TPC) sacc = cfma(U[l * UL + c], U[l * UL + jj], sacc);
+    sacc = gsumc<TPC>(sacc, FULL);
+    if (c < jj && q == 0) U[jj * UL + c] = cneg(cmul(tau_s[jj], sacc));
+  };
+
+  if (warp == 0) phase_a(0, A[c * LDS + c]);
+  __syncthreads();
+  for (int j = 0; j < KT; ++j) {
+    const bool crit = (j + 1 < KT) && (((j + 1) * TPC) >> 5) == warp;
+    const cplx alpha_n = crit ? A[c * LDS + c] : cmk(0.0, 0.0);
+    const cplx tj = tau_s[j];
+    const cplx* vj = slot + (j & 1) * B;
+    cplx v[RPT];
+    cplx d = cmk(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      v[i] = vj[q + TPC * i];
+      d = cfmac(v[i], x[i], d);
+    }
+    d = gsumc<TPC>(d, FULL);
+    if (c > j) {
+      d = cadd(d, A[j * LDS + c]);
+      const cplx w = cmul(conjc(tj), d);               // conj(tau) v^H a
+#pragma unroll
+      for (int i = 0; i < RPT; ++i) x[i] = csub(x[i], cmul(w, v[i]));
+      if (q == 0) A[j * LDS + c] = csub(A[j * LDS + c], w);
+    } else if (c < j) {
+      if (q == 0) U[c * UL + j] = conjc(d);            // U[c][j] = v_c^H v_j
+    } else {
+      if (q == 0) U[j * UL + j] = tj;
+    }
+    if (j >= 2) t_col(j - 1);
+    if (crit) phase_a(j + 1, alpha_n);
     __syncthreads();
   }
-  if (c < KT - 1) t_col(KT - 1);
+  t_col(KT - 1);
   __syncthreads();
   for (int e = tid; e < KT * KT; e += blockDim.x) {
     const int r = e / KT, cc = e - r * KT;
