@@ -204,12 +204,19 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
     }
     const double s2 = gsum<TPC>(s2a + s2b, FULL);
     const bool nz = (s2 != 0.0 || alpha.y != 0.0);
-    const double bt = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + s2), alpha.x);
-    // one reciprocal rr = 1 / (bt m), m = |alpha - beta|^2, gives 1/bt = m rr and 1/m = bt rr
+    // beta = -sign(Re alpha) sqrt(h) via one rsqrt (1/beta comes with it);
+    // 1/|alpha - beta|^2 by the MUFU reciprocal seed and two Newton steps
+    // (as dlarfg_fast in chainqr.cu: ~1 ulp, no IEEE division / sqrt paths)
+    const double h = fma(alpha.x, alpha.x, fma(alpha.y, alpha.y, s2));
+    const double r = rsqrt(h);
+    const double bt = -copysign(h * r, alpha.x);
+    const double ib = -copysign(r, alpha.x);
     const double e = bt - alpha.x;
     const double m = fma(e, e, alpha.y * alpha.y);
-    const double rr = 1.0 / (bt * m);
-    const double ib = m * rr, im = bt * rr;
+    double im;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(im) : "d"(m));
+    im = im * fma(-m, im, 2.0);
+    im = im * fma(-m, im, 2.0);
     const cplx tau = nz ? cmk(e * ib, -alpha.y * ib) : cmk(0.0, 0.0);
     const cplx scal = cmk(-e * im, -alpha.y * im);     // conj(alpha - beta) / |alpha - beta|^2
     const cplx beta = nz ? cmk(bt, 0.0) : alpha;
