@@ -36,8 +36,9 @@ class StabilityReport:
 def _weighted(x, inner):
     if inner is None or inner.kind != "weighted":
         return x
-    if inner.diag is None:
-        raise NotImplementedError("dense-B metrics are not in this build")
+    if inner.diag is None:       # dense B = L L^T: the B-metrics are the Euclidean ones of L^T x
+        from .oblique import _phi
+        return _phi(inner, x, x.device.index)
     t = D.torch()
     d = inner.diag if D.is_torch(inner.diag) else t.from_numpy(inner.diag)
     d = d.to(device=x.device, dtype=t.float64)

@@ -465,3 +465,20 @@ def test_b_block_householder_qr_vs_oracle(kind):
     with pytest.raises(P.IntraFailure) as ei:
         P.b_block_householder_qr(bad, ip)
     assert ei.value.block == 0
+
+
+@pytest.mark.parametrize("kind", ["diag", "dense"])
+def test_b_householder_qr_general_basis(kind):
+    """Any B-orthonormal u_init: the positive-diagonal B-QR is unique, so the
+    result matches the reference run with that same u_init."""
+    n, k = 800, 24
+    ip, ref_in, _, a = _b_case(kind, n, 8, k, 610)
+    lo = np.diag(np.sqrt(ref_in.diag)) if kind == "diag" else np.linalg.cholesky(ref_in.b)
+    u = np.linalg.solve(lo.T, np.linalg.qr(W.normal_matrix(W.make_rng(611), n, k))[0])
+    res = P.b_householder_qr(a, u, ip)
+    q, r = O.b_house(a, u, ref_in)
+    assert rel(res.q, q) < 1e-10 and rel(res.r, r) < 1e-10
+    m = P.compute_metrics(None, a, res, inner=ip)
+    assert m.loss_orth < 1e-13 and m.rel_residual < 1e-14
+    with pytest.raises(NotImplementedError):
+        P.b_householder_qr(a, 2.0 * u, ip)
