@@ -183,3 +183,30 @@ def test_complex_modified_lu(n):
     res = P.modified_lu(z)
     assert np.array_equal(np.asarray(res.p_diag), p0)
     assert rel(res.l, l0) < 1e-12 and rel(res.u_tri, u0) < 1e-12
+
+
+def test_complex_b_householder_and_block_driver():
+    """b_householder_qr / b_block_householder_qr (oblique.py:170-238, 318-361)
+    on c128 blocks with M = diag(d), against the oracle block by block."""
+    rng = np.random.default_rng(23)
+    n, sizes = 900, [16, 24, 16]
+    d = 10.0 ** rng.uniform(0.0, 2.0, n)
+    ip, ref_in = P.InnerProduct.weighted(d), O.BInner(diag=d)
+    a = cgauss(rng, n, sum(sizes))
+    u = P.initial_b_basis(ip, sum(sizes))
+    r1 = P.b_householder_qr(a[:, :16], u[:, :16], ip)
+    q1, rr1 = O.b_house(a[:, :16], u[:, :16], ref_in)
+    assert rel(r1.q, q1) < 1e-10 and rel(r1.r, rr1) < 1e-10
+    blocks = [a[:, sum(sizes[:i]):sum(sizes[:i + 1])] for i in range(len(sizes))]
+    res = P.b_block_householder_qr(blocks, ip)
+    qs, off = [q1], sizes[0]
+    rf = np.zeros((sum(sizes), sum(sizes)), dtype=complex)
+    rf[:16, :16] = rr1
+    for i in range(1, len(sizes)):
+        out = O.b_two_stage(np.hstack(qs), blocks[i], u[:, :off + sizes[i]], ref_in, "qr", diagnostics=False)
+        qs.append(out["q"])
+        rf[:off, off:off + sizes[i]] = out["s"]
+        rf[off:off + sizes[i], off:off + sizes[i]] = out["r"]
+        off += sizes[i]
+    assert np.iscomplexobj(res.q)
+    assert rel(res.q, np.hstack(qs)) < 1e-10 and rel(res.r, rf) < 1e-10
