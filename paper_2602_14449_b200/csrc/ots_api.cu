@@ -657,7 +657,10 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // eigenvalue problems; they then run on the side stream beside everything
   // after the seed, and the row-parallel phases are planned for nsm - 3 SMs
   // (chains, qform and Gram grids; the NN updates balance dynamically).
-  const bool diag_side = k0 > 128 && ctx->nsm > 16;
+  // Small calls (apply1 well under the diagnostics' fixed ~0.3-0.6 ms) take
+  // the same route: the diagnostics then hide behind factor..apply2.
+  const bool small_call = (double)n * (double)k0 * (double)k < 2.5e10;
+  const bool diag_side = (k0 > 128 || small_call) && ctx->nsm > 16;
   JobCfg c2 = c;
   if (diag_side) c2.nsm_avail = ctx->nsm - 3;
   if ((rc = job_setup(ctx, j, c2))) return rc;
