@@ -614,6 +614,25 @@ struct BHook {                 // B-inner extension of the pipeline
   const double* Vorig = nullptr; long ldvo = 0;     // dense: original V (diagnostics)
 };
 
+// Y = D^(+-1/2) X, row-oriented (real views, even leading dimensions: 16-byte
+// accesses): one warp per row, the row factor computed once per row, no
+// per-element index division (the element-wise form ran at ~4 TB/s).
+__global__ void row_scale_pairs_kernel(const double* X, long ldx, long n, int cols, const double* d, int inv,
+                                       double* Y, long ldy) {
+  const int lane = threadIdx.x & 31;
+  const long nw = ((long)gridDim.x * blockDim.x) >> 5;
+  const int np = cols >> 1;
+  for (long i = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const double s = inv ? rsqrt(d[i]) : sqrt(d[i]);
+    const double2* xr = reinterpret_cast<const double2*>(X + i * ldx);
+    double2* yr = reinterpret_cast<double2*>(Y + i * ldy);
+    for (int q = lane; q < np; q += 32) {
+      const double2 v = __ldcs(xr + q);
+      __stcs(yr + q, make_double2(v.x * s, v.y * s));
+    }
+    if ((cols & 1) && lane == 0) Y[i * ldy + cols - 1] = X[i * ldx + cols - 1] * s;
+  }
+}
 __global__ void b_unscale_kernel(double* Q, long ldq, long n, int k, const double* d, const double* R,
                                  long ldr) {
   // Q <- D^{-1/2} Q diag(sg), sg_j = sign(R_jj) (0 -> +1): the B-path's
@@ -624,6 +643,8 @@ __global__ void b_unscale_kernel(double* Q, long ldq, long n, int k, const doubl
     Q[i * ldq + j] *= sg * rsqrt(d[i]);
   }
 }
+static int row_grid(long n) { return (int)std::min<long>(148L * 16, (n + 7) / 8); }
+
 __global__ void b_rsign_kernel(double* R, long ldr, int k) {
   // R <- diag(sg) R  (rows), sg from its own diagonal; one block, ordered so
   // the diagonal is read before it is rewritten.
@@ -633,14 +654,6 @@ __global__ void b_rsign_kernel(double* R, long ldr, int k) {
   for (int e = threadIdx.x; e < k * k; e += blockDim.x) {
     int i = e / k, j = e - i * k;
     R[(long)i * ldr + j] *= sg[i];
-  }
-}
-__global__ void row_scale_kernel(const double* X, long ldx, long n, int k, const double* d, double pw,
-                                 double* Y, long ldy) {
-  for (long e = (long)blockIdx.x * blockDim.x + threadIdx.x; e < n * k; e += (long)gridDim.x * blockDim.x) {
-    long i = e / k; int j = (int)(e - i * k);
-    const double s = (pw > 0.0) ? sqrt(d[i]) : rsqrt(d[i]);
-    Y[i * ldy + j] = X[i * ldx + j] * s;
   }
 }
 __global__ void inv_top_kernel(const double* d, int k0, double* out) {
@@ -737,12 +750,11 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   prof_mark(ctx, st, "apply2");
   CK(launch_qtop(j.s, Q, ldq, st));
   if (bh) {
-    const int nb = (int)std::min<long>(4096, (n * k + 255) / 256);
     if (bh->L != nullptr) {       // dense B: Q = L^{-T} Q' sgn
       CK(launch_colsign(Q, ldq, n, (int)k, R, ldr, st));
       CK(launch_trsm_lt(bh->L, bh->ldl, Q, ldq, (int)n, (int)k, st));
     } else {
-      b_unscale_kernel<<<nb, 256, 0, st>>>(Q, ldq, n, (int)k, bh->d, R, ldr);
+      b_unscale_kernel<<<(int)std::min<long>(4096, (n * k + 255) / 256), 256, 0, st>>>(Q, ldq, n, (int)k, bh->d, R, ldr);
     }
     b_rsign_kernel<<<1, 256, 0, st>>>(R, ldr, (int)k);
     prof_mark(ctx, st, "b_epilogue");
@@ -1183,9 +1195,8 @@ int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, con
   double* part = A2 + (size_t)n * lda2;
   double* Gu = part + (size_t)gridu * PWv * PWv;
   double* dinv = Gu + (size_t)PWv * PWv;
-  const int nb = (int)std::min<long>(4096, (n * (k0 + k) + 255) / 256);
-  row_scale_kernel<<<nb, 256, 0, st>>>(V, ldv, n, (int)k0, d, 1.0, V2, ldv2);
-  row_scale_kernel<<<nb, 256, 0, st>>>(A, lda, n, (int)k, d, 1.0, A2, lda2);
+  row_scale_pairs_kernel<<<row_grid(n), 256, 0, st>>>(V, ldv, n, (int)k0, d, 0, V2, ldv2);
+  row_scale_pairs_kernel<<<row_grid(n), 256, 0, st>>>(A, lda, n, (int)k, d, 0, A2, lda2);
   inv_top_kernel<<<1, 128, 0, st>>>(d, (int)k0, dinv);
   TnArgs a{};
   a.P = V; a.ldp = ldv; a.pc0 = 0; a.pcols = (int)k0;

@@ -149,7 +149,7 @@ def _is_canonical_basis(u, d, m):
         top = u[:m, :m]
         want = t.diag(t.as_tensor(d, device=u.device)[:m].rsqrt())
         return bool(t.allclose(top.to(want.dtype), want, rtol=1e-14, atol=0.0)) and \
-            (t.count_nonzero(u[m:, :m]).item() == 0)
+            not bool(u[m:, :m].any().item())
     top = np.asarray(u[:m, :m])
     dd = np.asarray(d.cpu().numpy() if D.is_torch(d) else d)[:m]
     return np.allclose(top, np.diag(1.0 / np.sqrt(dd)), rtol=1e-14, atol=0.0) and not np.count_nonzero(u[m:, :m])
