@@ -148,6 +148,10 @@ def apply_reflector(h, x, adjoint=False):
     x = as_matrix(x, "x")
     if x.shape[0] != h.n:
         raise E.DimensionError(f"x has {x.shape[0]} rows, reflector expects {h.n}")
+    if is_complex(x):   # a real reflector acts on the real and imaginary parts separately
+        re = apply_reflector(h, x.real.contiguous() if was_torch else np.ascontiguousarray(x.real), adjoint)
+        im = apply_reflector(h, x.imag.contiguous() if was_torch else np.ascontiguousarray(x.imag), adjoint)
+        return D.torch().complex(re, im) if was_torch else re + 1j * im
     dev = h._h.dev
     ctx = D.ctx(dev)
     X = D.to_device(x, dev)

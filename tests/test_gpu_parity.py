@@ -482,3 +482,18 @@ def test_b_householder_qr_general_basis(kind):
     assert m.loss_orth < 1e-13 and m.rel_residual < 1e-14
     with pytest.raises(NotImplementedError):
         P.b_householder_qr(a, 2.0 * u, ip)
+
+
+def test_apply_reflector_complex_rhs():
+    """A real reflector applied to complex x (reflector.py:231-238 with numpy
+    promotion): real and imaginary parts independently."""
+    n, k0 = 600, 12
+    rng = W.make_rng(77)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    h = P.build_reflector(v)
+    x = W.normal_matrix(rng, n, 5) + 1j * W.normal_matrix(rng, n, 5)
+    for adj in (False, True):
+        y = P.apply_reflector(h, x, adjoint=adj)
+        assert np.iscomplexobj(y)
+        assert rel(y.real, P.apply_reflector(h, x.real.copy(), adjoint=adj)) < 1e-15
+        assert rel(y.imag, P.apply_reflector(h, x.imag.copy(), adjoint=adj)) < 1e-15
