@@ -46,6 +46,10 @@ class _DeviceTSolver:
 
     def solve(self, b, adjoint=False):
         was_torch = D.is_torch(b)
+        if is_complex(b):   # T is real: real and imaginary parts separately
+            re = self.solve(b.real.contiguous() if was_torch else np.ascontiguousarray(np.real(b)), adjoint)
+            im = self.solve(b.imag.contiguous() if was_torch else np.ascontiguousarray(np.imag(b)), adjoint)
+            return D.torch().complex(re, im) if was_torch else re + 1j * im
         bb = as_matrix(b if (was_torch or np.ndim(b) == 2) else np.asarray(b)[:, None], "b")
         vec = (not was_torch) and np.ndim(b) == 1
         B = D.to_device(bb, self._dev)

@@ -497,3 +497,6 @@ def test_apply_reflector_complex_rhs():
         assert np.iscomplexobj(y)
         assert rel(y.real, P.apply_reflector(h, x.real.copy(), adjoint=adj)) < 1e-15
         assert rel(y.imag, P.apply_reflector(h, x.imag.copy(), adjoint=adj)) < 1e-15
+    b = x[:k0]
+    z = h.t_solver.solve(b, adjoint=True)
+    assert np.iscomplexobj(z) and rel(z.imag, h.t_solver.solve(b.imag.copy(), adjoint=True)) < 1e-15
