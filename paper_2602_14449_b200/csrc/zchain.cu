@@ -406,6 +406,71 @@ __global__ void __launch_bounds__(256, 1) zchain_qform_kernel(ZQformArgs a) {
   __syncthreads();
   constexpr int MT = KT / 16;
   const int tr = threadIdx.x / 16, tc = threadIdx.x % 16;
+  if constexpr (KT == 64) {
+    // Two smem buffers alternate roles: B1 holds T_t, then M_t = T_t C; B2
+    // receives Y_t by cp.async while T_t C is formed.  After out = -Y_t M_t,
+    // T_{t-1} -> B1 and Y_{t-1} -> B2 are issued as separate groups.
+    cplx* B1 = Ys;
+    cplx* B2 = Ms;
+    auto issue_t = [&](int t) {
+      const cplx* Tt = Tbase + (long)t * KT * KT;
+      for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+        const int i = e / KT, j = e - i * KT;
+        cp_async16(B1 + i * LDS + j, Tt + e, 16);
+      }
+      cp_async_commit();
+    };
+    auto issue_y = [&](int t) {
+      const long gr0 = r0 + KT + (long)(t - 1) * b;
+      const long rem = a.G.nrows - gr0;
+      const int nb = (int)(rem < b ? rem : b);
+      for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+        const int r = e / KT, c = e - r * KT;
+        const bool ok = r < nb && c < a.ncols;
+        cp_async16(B2 + r * LDS + c, ok ? (const void*)(D + (gr0 + r) * a.ldd + c) : (const void*)D, ok ? 16 : 0);
+      }
+      cp_async_commit();
+    };
+    if (ntiles >= 1) { issue_t(ntiles); issue_y(ntiles); }
+    for (int t = ntiles; t >= 1; --t) {
+      const long gr0 = r0 + KT + (long)(t - 1) * b;
+      const long rem = a.G.nrows - gr0;
+      const int nb = (int)(rem < b ? rem : b);
+      cp_async_wait<1>();            // T_t landed (Y_t may still be in flight)
+      __syncthreads();
+      cplx acc[MT][MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) acc[i][jj] = cmk(0.0, 0.0);
+      zmm<KT>(B1, Cs, acc, tr, tc);   // M = T C
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) {
+          const int o = (tr + 16 * i) * LDS + tc + 16 * jj;
+          B1[o] = acc[i][jj];
+          Cs[o] = csub(Cs[o], acc[i][jj]);
+        }
+      cp_async_wait<0>();            // Y_t
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) acc[i][jj] = cmk(0.0, 0.0);
+      zmm<KT>(B2, B1, acc, tr, tc);   // Y M
+#pragma unroll
+      for (int i = 0; i < MT; ++i)
+#pragma unroll
+        for (int jj = 0; jj < MT; ++jj) {
+          const int r = tr + 16 * i, c = tc + 16 * jj;
+          if (r < nb && c < a.ncols) D[(gr0 + r) * a.ldd + c] = cneg(acc[i][jj]);
+        }
+      __syncthreads();
+      if (t > 1) { issue_t(t - 1); issue_y(t - 1); }
+    }
+  } else
   for (int t = ntiles; t >= 1; --t) {
     const long gr0 = r0 + KT + (long)(t - 1) * b;
     const long rem = a.G.nrows - gr0;
