@@ -70,7 +70,7 @@ cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, lo
                              long ldqq, const double* Gee, long ldee, const double* Gaa, long ldaa, int k0, int k,
                              int augmented, double* work, double* out3, cudaStream_t st);
 cudaError_t launch_neg_copy(const double* X, long ldx, int r, int c, double* Y, long ldy, cudaStream_t st);
-cudaError_t launch_zseed(const ZState& z, cudaStream_t st);
+cudaError_t launch_zseed(const ZState& z, cudaStream_t st, int part = 0);
 cudaError_t launch_zcholqr_step(const double* Gr, long ldg, int k, long m, int shift, void* W, int ld,
                                 double* Zx, int ldzx, void* R, int* status, cudaStream_t st);
 cudaError_t launch_zmlu(const void* Z, int ldz, int n, void* LU, double* p, double* work, int* status,
