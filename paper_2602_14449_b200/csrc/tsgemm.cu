@@ -451,6 +451,7 @@ cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st) 
   if (KT == 16) return launch_nn_t<16>(a, nsm, st);
   if (KT == 32) return launch_nn_t<32>(a, nsm, st);
   if (KT == 64) return launch_nn_t<64>(a, nsm, st);
+  if (KT == 128) return launch_nn_t<128>(a, nsm, st);   // 64-row tiles (complex real views)
   return cudaErrorInvalidValue;
 }
 
