@@ -83,3 +83,28 @@ def test_drop_in_surface():
                  "block_householder_qr", "reorthogonalized_two_stage", "householder_qr", "TwoStageResult",
                  "BlockQRResult", "GenHouseholder", "ReflectorDiagnostics"):
         assert callable(getattr(P, name)), name
+
+
+def test_b_path_validation_on_host():
+    """Shape / basis checks of the B-path primitives run before any device work
+    (oblique.py:125-151, 170-238 error behaviour)."""
+    from paper_2602_14449_b200.oblique import _is_canonical_basis
+    d = np.arange(1.0, 13.0)
+    ip = P.InnerProduct.weighted(d)
+    u = P.initial_b_basis(ip, 4)
+    assert _is_canonical_basis(u, ip.diag, 4)
+    assert not _is_canonical_basis(2.0 * u, ip.diag, 4)
+    with pytest.raises(P.DimensionError):
+        P.b_householder_qr(np.ones((11, 2)), u, ip)          # row mismatch
+    with pytest.raises(P.DimensionError):
+        P.b_householder_qr(np.ones((12, 5)), u, ip)          # u_init too narrow
+    with pytest.raises(P.DimensionError):
+        P.b_build_reflector(u[:, :3], u, ip)                  # v / u0 shapes differ
+    with pytest.raises(P.DimensionError):
+        P.b_build_reflector(np.zeros((12, 0)), np.zeros((12, 0)), ip)
+    with pytest.raises(P.ParameterError):
+        P.b_block_householder_qr([], ip)
+    with pytest.raises(P.DimensionError):
+        P.b_block_householder_qr([np.ones((12, 8)), np.ones((12, 8))], ip)   # sum k_i > n
+    q = P.b_householder_qr(np.zeros((12, 0)), u, ip)
+    assert q.q.shape == (12, 0) and q.r.shape == (0, 0)
