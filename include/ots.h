@@ -174,6 +174,57 @@ int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k,
                                 const double* A, int64_t lda, double* Q, int64_t ldq,
                                 double* R, int64_t ldr, void* stream);
 
+/* shifted_cholesky_qr(a, refine_passes)          -- core.py:177-202
+ * 1 shifted pass + max(0, refine_passes) unshifted ones (real / c128). */
+int ots_shifted_cholesky_qr_ex_f64(ots_ctx* ctx, int64_t m, int64_t k,
+                                   const double* A, int64_t lda, double* Q, int64_t ldq,
+                                   double* R, int64_t ldr, int refine_passes, void* stream);
+int ots_shifted_cholesky_qr_ex_c128(ots_ctx* ctx, int64_t m, int64_t k,
+                                    const void* A, int64_t lda, void* Q, int64_t ldq,
+                                    void* R, int64_t ldr, int refine_passes, void* stream);
+
+/* compute_metrics / orthogonality_loss for complex128 (metrics.py:25-73):
+ * as ots_stability_f64 on interleaved data (ld in complex elements);
+ * 1 <= k <= 64, k0 <= 256. */
+int ots_stability_c128(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                       const void* V, int64_t ldv, const void* A, int64_t lda,
+                       const void* Q, int64_t ldq, const void* R, int64_t ldr,
+                       const void* S, int64_t lds, int augmented,
+                       void* E, int64_t lde, double* out3, void* stream);
+
+/* orthonormality_defect(v) = ||v^* v - I||_2      -- core.py:43-49
+ * (the check build_reflector makes at reflector.py:220-223); *out on the
+ * host.  k0 <= 1024 (c128: 512). */
+int ots_orthonormality_defect_f64(ots_ctx* ctx, int64_t n, int64_t k0,
+                                  const double* V, int64_t ldv, double* out, void* stream);
+int ots_orthonormality_defect_c128(ots_ctx* ctx, int64_t n, int64_t k0,
+                                   const void* V, int64_t ldv, double* out, void* stream);
+/* {lambda_min, lambda_max} of v^* v (host out2): spectral_norm (core.py:35-40)
+ * = sqrt(lambda_max); InnerProduct.norm/defect (oblique.py:75-90) on L^* x. */
+int ots_gram_extremes_f64(ots_ctx* ctx, int64_t n, int64_t k0,
+                          const double* V, int64_t ldv, double* out2, void* stream);
+int ots_gram_extremes_c128(ots_ctx* ctx, int64_t n, int64_t k0,
+                           const void* V, int64_t ldv, double* out2, void* stream);
+
+/* Streaming block products of the classical comparators (BCGS / BCGS2 /
+ * CholQR, baselines.py:34-175): the inner-product block c = v^* x
+ * (baselines.py:66,113,117,169) and the projector update x - v c
+ * (:67,114,118,173).  Device pointers; DMMA kernels of the two-stage path.
+ *   ots_gram_*   out (p x q, ld ldo) = P^* B over n rows; B null: P^* P
+ *                (full Hermitian).  p, q <= 1024 (c128: 512).
+ *   ots_update_* X (n x m) = B + V Z, Z p x m; B null: X = V Z; B may
+ *                alias X.  p <= 512 (c128: 256). */
+int ots_gram_f64(ots_ctx* ctx, int64_t n, int64_t p, const double* P, int64_t ldp,
+                 int64_t q, const double* B, int64_t ldb, double* out, int64_t ldo, void* stream);
+int ots_gram_c128(ots_ctx* ctx, int64_t n, int64_t p, const void* P, int64_t ldp,
+                  int64_t q, const void* B, int64_t ldb, void* out, int64_t ldo, void* stream);
+int ots_update_f64(ots_ctx* ctx, int64_t n, int64_t p, const double* V, int64_t ldv,
+                   int64_t m, const double* Z, int64_t ldz, const double* B, int64_t ldb,
+                   double* X, int64_t ldx, void* stream);
+int ots_update_c128(ots_ctx* ctx, int64_t n, int64_t p, const void* V, int64_t ldv,
+                    int64_t m, const void* Z, int64_t ldz, const void* B, int64_t ldb,
+                    void* X, int64_t ldx, void* stream);
+
 /* modified_lu(z)                                  -- reflector.py:53-77
  * LU (n x n, L strict-lower unit + U upper, packed, ld n) and p (n). */
 int ots_modified_lu_f64(ots_ctx* ctx, int64_t n, const double* Z, int64_t ldz,

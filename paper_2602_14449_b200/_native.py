@@ -77,6 +77,19 @@ def lib():
                 L.ots_stability_f64.argtypes = [
                     _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int,
                     _vp, _i64, C.POINTER(_dbl), _vp]
+                L.ots_stability_c128.argtypes = L.ots_stability_f64.argtypes
+                L.ots_orthonormality_defect_f64.argtypes = [_vp, _i64, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
+                L.ots_orthonormality_defect_c128.argtypes = L.ots_orthonormality_defect_f64.argtypes
+                L.ots_shifted_cholesky_qr_ex_f64.argtypes = [
+                    _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _int, _vp]
+                L.ots_shifted_cholesky_qr_ex_c128.argtypes = L.ots_shifted_cholesky_qr_ex_f64.argtypes
+                L.ots_gram_f64.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp]
+                L.ots_gram_c128.argtypes = L.ots_gram_f64.argtypes
+                L.ots_update_f64.argtypes = [_vp, _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                                             _vp]
+                L.ots_update_c128.argtypes = L.ots_update_f64.argtypes
+                L.ots_gram_extremes_f64.argtypes = L.ots_orthonormality_defect_f64.argtypes
+                L.ots_gram_extremes_c128.argtypes = L.ots_orthonormality_defect_f64.argtypes
                 L.ots_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), _int]
                 L.ots_modified_lu_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp]
                 L.ots_shifted_cholesky_qr_f64.argtypes = [
@@ -117,21 +130,35 @@ EXPORTED_SYMBOLS = [
     "ots_debug_counters",
     "ots_dist_begin", "ots_dist_sizes", "ots_dist_gram", "ots_dist_seed", "ots_dist_seed_early", "ots_dist_top_rows", "ots_dist_factor",
     "ots_dist_tree", "ots_dist_qform", "ots_dist_finish",
+    "ots_stability_c128", "ots_orthonormality_defect_f64", "ots_orthonormality_defect_c128",
+    "ots_shifted_cholesky_qr_ex_f64", "ots_shifted_cholesky_qr_ex_c128",
+    "ots_gram_f64", "ots_gram_c128", "ots_update_f64", "ots_update_c128",
+    "ots_gram_extremes_f64", "ots_gram_extremes_c128",
     "ots_dense_cholesky_f64", "ots_dense_trsm_lt_f64", "ots_dense_trmm_lt_f64", "ots_b_two_stage_dense_f64",
 ]
 
 
 def context(device):
-    """Per-device C context (created lazily, kept for the process lifetime)."""
-    if device not in _ctx:
+    """C context of (device, calling thread), created lazily.  ots.h: one
+    context per (device, host thread) -- ctypes releases the GIL during a
+    call, so two threads must never share a context's workspace.  Contexts of
+    threads that have exited are destroyed when a new one is created."""
+    key = (int(device), threading.get_ident())
+    h = _ctx.get(key)
+    if h is None:
         L = lib()
+        with _lock:
+            alive = {t.ident for t in threading.enumerate()}
+            for dead in [kk for kk in _ctx if kk[1] not in alive]:
+                L.ots_ctx_destroy(_ctx.pop(dead))
         h = _vp()
         rc = L.ots_ctx_create(int(device), C.byref(h))
         if rc != 0:
             msg = L.ots_last_error(h).decode() if h.value else "ots_ctx_create failed"
             raise E.NativeUnavailable(f"CUDA context on device {device}: {msg}")
-        _ctx[device] = h
-    return _ctx[device]
+        with _lock:
+            _ctx[key] = h
+    return h
 
 
 def new_context(device):

@@ -66,8 +66,7 @@ def householder_qr(a, nonneg_diag=False):
     m, n = a.shape
     if m < n:
         raise E.DimensionError(f"need rows >= cols, got {m}x{n}")
-    if not all_finite(a):
-        raise ValueError("input contains non-finite entries")
+    # non-finite input: ValueError from the device (R check, core.py:72-73)
     dev = D.pick_device(a)
     ctx = D.ctx(dev)
     if is_complex(a):
@@ -90,10 +89,9 @@ def householder_qr(a, nonneg_diag=False):
 
 
 def shifted_cholesky_qr(a, refine_passes=2):
-    """Shifted Cholesky-QR + 2 unshifted refinements on the GPU
+    """Shifted Cholesky-QR + `refine_passes` unshifted refinements on the GPU
     (core.py:177-202).  Breakdown raises NotPositiveDefinite."""
-    if refine_passes != 2:
-        raise NotImplementedError("this build implements the reference's 2 refinement passes")
+    refine_passes = max(0, int(refine_passes))
     was_torch = D.is_torch(a)
     a = as_matrix(a, "a")
     m, n = a.shape
@@ -106,15 +104,117 @@ def shifted_cholesky_qr(a, refine_passes=2):
         Q = D.cempty(m, n, dev)
         R = D.czeros(n, n, dev)
         if n:
-            rc = lib().ots_shifted_cholesky_qr_c128(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
-                                                    D.stream_ptr(dev))
+            rc = lib().ots_shifted_cholesky_qr_ex_c128(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
+                                                       refine_passes, D.stream_ptr(dev))
             check(rc, ctx)
         return QRPair(out_like(was_torch, Q), out_like(was_torch, R))
     A = D.to_device(a, dev)
     Q = D.empty(m, n, dev)
     R = D.zeros(n, n, dev)
     if n:
-        rc = lib().ots_shifted_cholesky_qr_f64(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
-                                               D.stream_ptr(dev))
+        rc = lib().ots_shifted_cholesky_qr_ex_f64(ctx, m, n, A.ptr, A.ld, Q.ptr, Q.ld, R.ptr, R.ld,
+                                                  refine_passes, D.stream_ptr(dev))
         check(rc, ctx)
     return QRPair(out_like(was_torch, Q), out_like(was_torch, R))
+
+
+# ---------------------------------------------------------------------------
+# n-length block products on the device (DMMA kernels of the path), used by
+# the drivers, the comparators (baselines.py) and the weighted inner product
+# ---------------------------------------------------------------------------
+def _dev_of(*xs):
+    return D.pick_device(*xs)
+
+
+def _tdev(x, dev, cplx):
+    t = D.torch()
+    dt = t.complex128 if cplx else t.float64
+    x = x if D.is_torch(x) else t.from_numpy(np.ascontiguousarray(x))
+    return x.to(device=f"cuda:{dev}", dtype=dt)
+
+
+def gram(p, b=None):
+    """p^* b (p n x q1, b n x q2) on the GPU -> CUDA tensor (q1 x q2);
+    b None: the Hermitian p^* p."""
+    t = D.torch()
+    cplx = is_complex(p) or (b is not None and is_complex(b))
+    dev = _dev_of(p, b) if b is not None else _dev_of(p)
+    todev = D.cto_device if cplx else D.to_device
+    P = todev(_tdev(p, dev, cplx), dev)
+    B = todev(_tdev(b, dev, cplx), dev) if b is not None else None
+    q = P.cols if B is None else B.cols
+    out = t.empty((max(P.cols, 1), max(q, 1)), dtype=t.complex128 if cplx else t.float64, device=f"cuda:{dev}")
+    ctx = D.ctx(dev)
+    fn = lib().ots_gram_c128 if cplx else lib().ots_gram_f64
+    rc = fn(ctx, P.rows if p.shape[0] else 0, P.cols, P.ptr, P.ld, q, B.ptr if B is not None else None,
+            B.ld if B is not None else 0, C.c_void_p(out.data_ptr()), out.stride(0), D.stream_ptr(dev))
+    check(rc, ctx)
+    return out[:P.cols, :q]
+
+
+def update(v, z, b=None):
+    """b + v z (v n x p, z p x m, b n x m or None) on the GPU -> CUDA tensor."""
+    cplx = is_complex(v) or is_complex(z) or (b is not None and is_complex(b))
+    dev = _dev_of(v, z, b) if b is not None else _dev_of(v, z)
+    todev = D.cto_device if cplx else D.to_device
+    V = todev(_tdev(v, dev, cplx), dev)
+    Z = todev(_tdev(z, dev, cplx), dev)
+    B = todev(_tdev(b, dev, cplx), dev) if b is not None else None
+    n, m = v.shape[0], z.shape[1]
+    X = (D.cempty if cplx else D.empty)(n, m, dev)
+    ctx = D.ctx(dev)
+    fn = lib().ots_update_c128 if cplx else lib().ots_update_f64
+    rc = fn(ctx, n, V.cols, V.ptr, V.ld, m, Z.ptr, Z.ld, B.ptr if B is not None else None,
+            B.ld if B is not None else 0, X.ptr, X.ld, D.stream_ptr(dev))
+    check(rc, ctx)
+    return X.view()[:n]
+
+
+def gram_extremes(v):
+    """(lambda_min, lambda_max) of v^* v from the device Gram + spectrum."""
+    if v.shape[1] == 0:
+        return 0.0, 0.0
+    v = as_matrix(v, "v")
+    dev = D.pick_device(v)
+    ctx = D.ctx(dev)
+    out = (C.c_double * 2)()
+    if is_complex(v):
+        V = D.cto_device(v, dev)
+        rc = lib().ots_gram_extremes_c128(ctx, v.shape[0], V.cols, V.ptr, V.ld, out, D.stream_ptr(dev))
+    else:
+        V = D.to_device(v, dev)
+        rc = lib().ots_gram_extremes_f64(ctx, v.shape[0], V.cols, V.ptr, V.ld, out, D.stream_ptr(dev))
+    check(rc, ctx)
+    return float(out[0]), float(out[1])
+
+
+def spectral_norm(a):
+    """||a||_2 (core.py:35-40) = sqrt(lambda_max(a^* a)) on the GPU (for the
+    tall blocks of this path; the reference takes an SVD)."""
+    if a.shape[0] == 0 or a.shape[1] == 0:
+        return 0.0
+    return float(np.sqrt(max(gram_extremes(a)[1], 0.0)))
+
+
+def orthonormality_defect(v):
+    """||v^* v - I||_2 (core.py:43-49) on the GPU: DMMA Gram + symmetric
+    spectrum (ots_orthonormality_defect_*)."""
+    was_torch = D.is_torch(v)
+    if not was_torch:
+        v = np.asarray(v)
+    if v.shape[0] == 0 or v.shape[1] == 0:
+        return 0.0
+    v = as_matrix(v, "v")
+    dev = D.pick_device(v)
+    ctx = D.ctx(dev)
+    out = C.c_double()
+    if is_complex(v):
+        V = D.cto_device(v, dev)
+        rc = lib().ots_orthonormality_defect_c128(ctx, v.shape[0], V.cols, V.ptr, V.ld, C.byref(out),
+                                                  D.stream_ptr(dev))
+    else:
+        V = D.to_device(v, dev)
+        rc = lib().ots_orthonormality_defect_f64(ctx, v.shape[0], V.cols, V.ptr, V.ld, C.byref(out),
+                                                 D.stream_ptr(dev))
+    check(rc, ctx)
+    return float(out.value)

@@ -542,14 +542,14 @@ __global__ void ones_kernel(double* v, int n) {
 // Shifted Cholesky-QR with two refinements on X (m x k, in place):
 // core.py:177-202.  R (k x k, ldr) written; status <- INTRA_FAILURE on breakdown.
 int run_cholshift(ots_ctx* ctx, Job& j, double* X, long ldx, long m, int k, double* R, long ldr,
-                  cudaStream_t st) {
+                  cudaStream_t st, int refine_passes = 2) {
   const int PWk = pad32(k);
   const int grid = grid_for_tn(PWk, 0, true, true, ctx->nsm);
   double* W = j.chol_ws;   // small scratch (2 k x ld + k)
   double* Z = j.s.X2;
   double* Racc = j.s.Sd;
   set_identity_ld_kernel<<<4, 256, 0, st>>>(Racc, k, j.ld);
-  for (int pass = 0; pass < 3; ++pass) {
+  for (int pass = 0; pass < 1 + std::max(0, refine_passes); ++pass) {
     TnArgs a{};
     a.P = X; a.ldp = ldx; a.pc0 = 0; a.pcols = k;
     a.B = nullptr; a.ldb = 0; a.bc0 = 0; a.bcols = 0;
@@ -566,6 +566,19 @@ int run_cholshift(ots_ctx* ctx, Job& j, double* X, long ldx, long m, int k, doub
   triu_copy_kernel<<<4, 256, 0, st>>>(Racc, j.ld, R, ldr, k);
   CK(cudaGetLastError());
   return OTS_OK;
+}
+
+// status <- OTS_E_VALUE when the (real view of the) k x k R holds a
+// non-finite entry: a NaN/Inf anywhere in the input reaches every R of the
+// TSQR chain that holds it and from there the final R (core.py:72-73 check,
+// done on k^2 data instead of a pass over the n-length input)
+__global__ void nonfinite_status_kernel(const double* R, long ldr, int rows, int cols, int* status) {
+  int bad = 0;
+  for (int e = threadIdx.x; e < rows * cols; e += blockDim.x) {
+    const int i = e / cols, j = e - i * cols;
+    if (!isfinite(R[(long)i * ldr + j])) bad = 1;
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicCAS(status, 0, OTS_E_VALUE);
 }
 
 int read_status(ots_ctx* ctx, Job& j, double* diag_host) {
@@ -871,8 +884,11 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
   if ((rc = validate_layout(ctx, A, lda, "A"))) return rc;
   if ((rc = validate_layout(ctx, Q, ldq, "Q"))) return rc;
   if (k == 0) return OTS_OK;
-  if (k0 == 0) {
-    rc = ots_householder_qr_f64(ctx, n, k, A, lda, Q, ldq, R, ldr, 0, stream);
+  if (k0 == 0) {   // intra_qr(a, intra) (twostage.py:81-84 -> :45-54)
+    rc = (intra == OTS_INTRA_CHOLSHIFT) ? ots_shifted_cholesky_qr_f64(ctx, n, k, A, lda, Q, ldq, R, ldr, stream)
+                                        : ots_householder_qr_f64(ctx, n, k, A, lda, Q, ldq, R, ldr, 0, stream);
+    if (rc == OTS_E_NOT_PD && intra == OTS_INTRA_CHOLSHIFT)
+      rc = fail(ctx, OTS_E_INTRA_FAILURE, "shifted Cholesky-QR broke down: " + ctx->err);
     if (diag_host) { diag_host[0] = 1.0; diag_host[1] = 0.0; diag_host[2] = 0.0; }
     return rc;
   }
@@ -1065,12 +1081,14 @@ int ots_householder_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, 
     nonneg_q_kernel<<<std::min<long>(1024, (m * k + 255) / 256), 256, 0, st>>>(Q, ldq, m, (int)k, R, ldr);
     nonneg_r_kernel<<<1, 256, 0, st>>>((int)k, R, ldr);
   }
+  nonfinite_status_kernel<<<1, 256, 0, st>>>(R, ldr, (int)k, (int)k, j.s.status);
   prof_mark(ctx, st, "sign");
-  ctx->launches = 3 + 3 * (int)j.lv.size() + (nonneg_diag ? 1 : 0);
+  ctx->launches = 4 + 3 * (int)j.lv.size() + (nonneg_diag ? 1 : 0);
   CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   prof_end(ctx);
   CK(cudaGetLastError());
+  if (ctx->h_status[0] == OTS_E_VALUE) return fail(ctx, OTS_E_VALUE, "input contains non-finite entries");
   return OTS_OK;
 }
 
@@ -1210,6 +1228,11 @@ int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, con
 
 int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, int64_t lda, double* Q,
                                 int64_t ldq, double* R, int64_t ldr, void* stream) {
+  return ots_shifted_cholesky_qr_ex_f64(ctx, m, k, A, lda, Q, ldq, R, ldr, 2, stream);
+}
+
+int ots_shifted_cholesky_qr_ex_f64(ots_ctx* ctx, int64_t m, int64_t k, const double* A, int64_t lda, double* Q,
+                                   int64_t ldq, double* R, int64_t ldr, int refine_passes, void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
   (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
@@ -1225,8 +1248,8 @@ int ots_shifted_cholesky_qr_f64(ots_ctx* ctx, int64_t m, int64_t k, const double
   if ((rc = job_setup(ctx, j, c))) return rc;
   if (A != Q) CK(cudaMemcpy2DAsync(Q, ldq * 8, A, lda * 8, k * 8, m, cudaMemcpyDeviceToDevice, st));
   CK(cudaMemsetAsync(j.s.status, 0, sizeof(int), st));
-  if ((rc = run_cholshift(ctx, j, Q, ldq, m, (int)k, R, ldr, st))) return rc;
-  ctx->launches = 13;
+  if ((rc = run_cholshift(ctx, j, Q, ldq, m, (int)k, R, ldr, st, refine_passes))) return rc;
+  ctx->launches = 1 + 4 * (1 + std::max(0, refine_passes));
   CK(cudaMemcpyAsync(ctx->h_status, j.s.status, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (ctx->h_status[0] == OTS_E_INTRA_FAILURE)

@@ -1367,6 +1367,32 @@ cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, lo
   return cudaGetLastError();
 }
 
+// lambda_min, lambda_max of a symmetric m x m matrix (lower triangle of G
+// read; work: m*m + 4m doubles) -- spectra of Grams for orthonormality_defect
+// and the weighted norms (core.py:35-49, oblique.py:70-90)
+__global__ void __launch_bounds__(SMALL_NT) sym_extremes_kernel(const double* G, long ldg, int m, double* work,
+                                                                double* out2) {
+  __shared__ double red[64];
+  double* M = work;
+  double* vec = work + (long)m * m;
+  BLK_FOR(e, m * m) {
+    const int i = e / m, j = e - i * m;
+    M[e] = (j <= i) ? G[(long)i * ldg + j] : G[(long)j * ldg + i];
+  }
+  double lmin = 0.0, lmax = 0.0;
+  if (m == 1) {
+    __syncthreads();
+    lmin = lmax = M[0];
+  } else if (m > 1) {
+    blk_sym_extremes(M, m, m, vec, red, lmin, lmax);
+  }
+  if (threadIdx.x == 0) { out2[0] = lmin; out2[1] = lmax; }
+}
+cudaError_t launch_sym_extremes(const double* G, long ldg, int m, double* work, double* out2, cudaStream_t st) {
+  sym_extremes_kernel<<<1, SMALL_NT, 0, st>>>(G, ldg, m, work, out2);
+  return cudaGetLastError();
+}
+
 __global__ void neg_copy_kernel(const double* X, long ldx, int r, int c, double* Y, long ldy) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < r * c; e += gridDim.x * blockDim.x) {
     const int i = e / c, j = e - i * c;

@@ -6,9 +6,10 @@ loss = max |lambda([v?, q]^* [v?, q]) - 1|, cross = ||v^* q||_F and the
 relative residual sqrt(lambda_max(E^T E) / lambda_max(A^T A)) with
 E = a - v s - q r formed explicitly (never by Gram expansion).  Grams use the
 DMMA tn kernel, spectra a tridiagonalisation + multisection (C-ABI
-`ots_stability_f64`).  Real f64 data; a diagonal weight is applied as
-D^1/2 scaling of v and q (the cached-Cholesky path of the reference for
-M = diag(d)).
+`ots_stability_f64` / `ots_stability_c128`; complex data runs on the real
+views with the Grams embedded as [[Re, -Im], [Im, Re]]).  A diagonal weight
+is applied as D^1/2 scaling of v and q (the cached-Cholesky path of the
+reference for M = diag(d)).
 """
 
 from __future__ import annotations
@@ -48,42 +49,46 @@ def _weighted(x, inner):
 def _run(v, a, q, r, s, augmented, inner=None):
     t = D.torch()
     dev = D.pick_device(q, a, v)
+    raw = [x for x in (q, a, v, r, s) if x is not None]
+    cplx = any(is_complex(x) for x in raw)      # decided on the raw inputs, before any cast
+    dt = t.complex128 if cplx else t.float64
     to = lambda x: None if x is None else (x if D.is_torch(x) else t.from_numpy(as_matrix(x))).to(
-        device=f"cuda:{dev}", dtype=t.float64)
+        device=f"cuda:{dev}", dtype=dt)
     q, a, v, r, s = to(q), to(a), to(v), to(r), to(s)
-    if any(x is not None and is_complex(x) for x in (q, a, v)):
-        raise NotImplementedError("complex metrics are not in this build")
+    todev = D.cto_device if cplx else D.to_device
+    mk = D.cempty if cplx else D.empty
+    fn = lib().ots_stability_c128 if cplx else lib().ots_stability_f64
     qw = _weighted(q, inner)
     vw = _weighted(v, inner) if v is not None else None
     n, k = q.shape
     k0 = 0 if vw is None else vw.shape[1]
-    Q = D.to_device(qw.contiguous(), dev)
-    V = D.to_device(vw.contiguous(), dev) if vw is not None else None
-    A = D.to_device(a.contiguous(), dev) if a is not None else None
-    R = D.to_device(r, dev) if r is not None else None
-    S = D.to_device(s, dev) if (s is not None and k0) else None
-    Eb = D.empty(n, k, dev)
+    Q = todev(qw.contiguous(), dev)
+    V = todev(vw.contiguous(), dev) if vw is not None else None
+    A = todev(a.contiguous(), dev) if a is not None else None
+    R = todev(r, dev) if r is not None else None
+    S = todev(s, dev) if (s is not None and k0) else None
+    Eb = mk(n, k, dev)
     out = (C.c_double * 3)()
     ctx = D.ctx(dev)
     if A is not None and inner is not None and inner.kind == "weighted":
         # the residual is unweighted (a - v s - q r): use the unscaled q, v
-        Q2 = D.to_device(q.contiguous(), dev)
-        V2 = D.to_device(v.contiguous(), dev) if v is not None else None
-        rc = lib().ots_stability_f64(ctx, n, k0, k, V2.ptr if V2 else None, V2.ld if V2 else 0, A.ptr, A.ld,
-                                     Q2.ptr, Q2.ld, R.ptr, R.ld, S.ptr if S else None, S.ld if S else 0,
-                                     0, Eb.ptr, Eb.ld, out, D.stream_ptr(dev))
+        Q2 = todev(q.contiguous(), dev)
+        V2 = todev(v.contiguous(), dev) if v is not None else None
+        rc = fn(ctx, n, k0, k, V2.ptr if V2 else None, V2.ld if V2 else 0, A.ptr, A.ld,
+                Q2.ptr, Q2.ld, R.ptr, R.ld, S.ptr if S else None, S.ld if S else 0,
+                0, Eb.ptr, Eb.ld, out, D.stream_ptr(dev))
         check(rc, ctx)
         resid = out[2]
-        rc = lib().ots_stability_f64(ctx, n, k0, k, V.ptr if V else None, V.ld if V else 0, None, 0,
-                                     Q.ptr, Q.ld, None, 0, None, 0, 1 if augmented else 0, Eb.ptr, Eb.ld,
-                                     out, D.stream_ptr(dev))
+        rc = fn(ctx, n, k0, k, V.ptr if V else None, V.ld if V else 0, None, 0,
+                Q.ptr, Q.ld, None, 0, None, 0, 1 if augmented else 0, Eb.ptr, Eb.ld,
+                out, D.stream_ptr(dev))
         check(rc, ctx)
         return float(out[0]), float(out[1]), float(resid)
-    rc = lib().ots_stability_f64(ctx, n, k0, k, V.ptr if V else None, V.ld if V else 0,
-                                 A.ptr if A else None, A.ld if A else 0, Q.ptr, Q.ld,
-                                 R.ptr if R else None, R.ld if R else 0, S.ptr if S else None,
-                                 S.ld if S else 0, 1 if augmented else 0, Eb.ptr, Eb.ld, out,
-                                 D.stream_ptr(dev))
+    rc = fn(ctx, n, k0, k, V.ptr if V else None, V.ld if V else 0,
+            A.ptr if A else None, A.ld if A else 0, Q.ptr, Q.ld,
+            R.ptr if R else None, R.ld if R else 0, S.ptr if S else None,
+            S.ld if S else 0, 1 if augmented else 0, Eb.ptr, Eb.ld, out,
+            D.stream_ptr(dev))
     check(rc, ctx)
     return float(out[0]), float(out[1]), float(out[2])
 

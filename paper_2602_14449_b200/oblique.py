@@ -105,6 +105,78 @@ class InnerProduct:
             return int(self.diag.shape[0])
         return None if self.chol_b is None else int(self.chol_b.shape[0])
 
+    # -- oblique.py:62-90 (n-length work on the device; numpy in -> numpy out)
+    def apply(self, x):
+        """B x (identity for the Euclidean kind) -- oblique.py:62-64."""
+        if self.kind == "euclidean":
+            return x
+        was_torch = D.is_torch(x)
+        dev = _dev_of(self, x)
+        t = D.torch()
+        xd = (x if was_torch else t.from_numpy(np.ascontiguousarray(x))).to(f"cuda:{dev}")
+        if self.diag is not None:
+            d = _sqrt_d(self, dev) ** 2
+            y = xd * (d[:, None] if xd.dim() == 2 else d)
+        else:
+            y = self.b.to(xd.dtype) @ xd
+        return y if was_torch else y.cpu().numpy()
+
+    def _phi_x(self, x):
+        """L^* x (x itself for the Euclidean kind) as a device tensor."""
+        t = D.torch()
+        if self.kind == "euclidean":
+            xd = x if D.is_torch(x) else t.from_numpy(np.ascontiguousarray(x))
+            return xd.to(f"cuda:{D.pick_device(xd)}")
+        dev = _dev_of(self, x)
+        return _phi(self, x, dev)
+
+    def gram(self, x, y):
+        """y^* B x -- oblique.py:66-68."""
+        from .core import gram as _gram
+        was_torch = D.is_torch(x) or D.is_torch(y)
+        g = _gram(y, self.apply(x))
+        return g if was_torch else g.cpu().numpy()
+
+    def col_norms(self, x):
+        """||L^* x_j||_2 per column -- oblique.py:70-73."""
+        from .core import gram as _gram
+        m = self._phi_x(x)
+        nr = _gram(m).diagonal().real.clamp_min(0).sqrt() if m.shape[1] else m.new_zeros(0).real
+        return nr if D.is_torch(x) else nr.cpu().numpy()
+
+    def norm(self, x):
+        """B-weighted spectral norm ||L^* x||_2 (vector 2-norm for 1-D x) --
+        oblique.py:75-81."""
+        from .core import spectral_norm
+        one_d = (x.dim() if D.is_torch(x) else np.ndim(x)) == 1
+        m = self._phi_x(x[:, None] if one_d else x)
+        return spectral_norm(m)
+
+    def defect(self, x):
+        """||x^* B x - I||_2 -- oblique.py:83-90."""
+        from .core import orthonormality_defect
+        if (x.numel() if D.is_torch(x) else np.size(x)) == 0:
+            return 0.0
+        return orthonormality_defect(self._phi_x(x))
+
+
+def _tcholesky(a):
+    """core.py:87-105 on a small device matrix: Hermitian to 1e-12 ||a||_2
+    (NotHermitian), symmetrised, lower Cholesky (NotPositiveDefinite)."""
+    t = D.torch()
+    if a.shape[0] != a.shape[1]:
+        raise E.DimensionError(f"cholesky needs a square matrix, got {tuple(a.shape)}")
+    if a.shape[0] == 0:
+        return a.clone()
+    nrm = float(t.linalg.matrix_norm(a, ord=2).item())
+    if float(t.linalg.matrix_norm(a - a.mH, ord=2).item()) > 1e-12 * nrm:
+        raise E.NotHermitian("matrix is not Hermitian to 1e-12 * ||a||_2")
+    h = (a + a.mH) / 2.0
+    l, info = t.linalg.cholesky_ex(h)
+    if int(info.item()) != 0 or not bool(t.isfinite(l).all().item()):
+        raise E.NotPositiveDefinite(f"{int(info.item())}-th leading minor not positive definite")
+    return l
+
 
 def _dense_basis(inner, m):
     """[L_m^{-T}; 0] = L^{-T} [I_m; 0] on the device (oblique.py:93-108)."""

@@ -122,18 +122,30 @@ def build_reflector(v, choice="qr", p=None, orth_tol=1e-8, allow_defect=False):
         raise E.DimensionError("v must have at least one column")
     if is_complex(v):
         raise NotImplementedError("complex build_reflector: not in this build")
+
+    def deferred(exc):   # the defect check (reflector.py:220-223) precedes the seed's checks
+        if not allow_defect:
+            from .core import orthonormality_defect
+            defect = orthonormality_defect(v)
+            if defect > orth_tol:
+                raise E.OrthonormalityError(f"||v^* v - I||_2 = {defect:.3e} exceeds {orth_tol:.1e}")
+        raise exc
+
     if choice not in CHOICES:
-        raise E.ParameterError(f"unknown choice {choice!r}; expected one of {CHOICES}")
+        deferred(E.ParameterError(f"unknown choice {choice!r}; expected one of {CHOICES}"))
     dev = D.pick_device(v)
     ctx = D.ctx(dev)
     V = D.to_device(v, dev)
     P = None
     if choice == "explicit":
         if p is None:
-            raise E.ParameterError("choice='explicit' requires a seed matrix p")
-        p = as_matrix(p, "p")
+            deferred(E.ParameterError("choice='explicit' requires a seed matrix p"))
+        try:
+            p = as_matrix(p, "p")
+        except E.DimensionError as exc:
+            deferred(exc)
         if tuple(p.shape) != (k0, k0):
-            raise E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}")
+            deferred(E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}"))
         P = D.to_device(p, dev)
     h = C.c_void_p()
     defect = C.c_double()

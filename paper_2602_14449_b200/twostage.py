@@ -62,12 +62,41 @@ def _zeros_like(was_torch, shape, ref=None):
     return np.zeros(shape, dtype=np.complex128 if cplx else np.float64)
 
 
+def _defect_then(v, exc, orth_tol=1e-8):
+    """The reference validates the orthonormality of v (reflector.py:220-223)
+    before the seed's choice / p checks (reflector.py:178-204) and before the
+    intra dispatch (twostage.py:54): raise OrthonormalityError if the device
+    defect exceeds orth_tol, else the deferred error `exc`."""
+    from .core import orthonormality_defect
+    defect = orthonormality_defect(v)
+    if defect > orth_tol:
+        raise E.OrthonormalityError(f"||v^* v - I||_2 = {defect:.3e} exceeds {orth_tol:.1e}")
+    raise exc
+
+
+def _run_two_stage(dev, V, A, Q, R, S, choice, intra, P, cplx):
+    """One C-ABI call on device matrices (DMat); returns the diagnostics."""
+    ctx = D.ctx(dev)
+    diag = (C.c_double * 3)()
+    fn = lib().ots_two_stage_c128 if cplx else lib().ots_two_stage_f64
+    rc = fn(
+        ctx, A.rows, V.cols, A.cols, V.ptr, V.ld, A.ptr, A.ld, CHOICES[choice],
+        INTRA[intra], P.ptr if P is not None else None, P.ld if P is not None else 0,
+        1e-8, 0, Q.ptr, Q.ld, R.ptr, R.ld, S.ptr, S.ld, diag, D.stream_ptr(dev))
+    check(rc, ctx)   # OrthonormalityError before the non-finite ValueError (device-side order)
+    return ReflectorDiagnostics(float(diag[0]), float(diag[1]))
+
+
 def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
     """Orthogonalize a against orthonormal v in two stages (Algorithm 1).
 
     Returns TwoStageResult(q, r, s, diagnostics) with
     [v, a] = [v, q] [[I, s], [0, r]] and [v, q]^* [v, q] = I.
     numpy in -> numpy out; CUDA tensors in -> CUDA tensors out (zero-copy).
+    Validation order of the reference: DimensionError (twostage.py:77-80),
+    OrthonormalityError (reflector.py:220-223), seed / choice / p errors
+    (reflector.py:178-204), non-finite ValueError (core.py:72-73), unknown
+    intra (twostage.py:54).
     """
     was_torch = D.is_torch(v) or D.is_torch(a)
     v = as_matrix(v, "v")
@@ -88,48 +117,46 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         return TwoStageResult(_zeros_like(was_torch, (n, 0), ref), _zeros_like(was_torch, (0, 0), ref),
                               _zeros_like(was_torch, (k0, 0), ref), ReflectorDiagnostics(1.0, 0.0))
     if choice not in CHOICES:
-        raise E.ParameterError(f"unknown choice {choice!r}; expected one of "
-                               f"('mlu', 'qr', 'polar', 'explicit')")
+        _defect_then(v, E.ParameterError(f"unknown choice {choice!r}; expected one of "
+                                         f"('mlu', 'qr', 'polar', 'explicit')"))
+    if choice == "explicit":
+        if p is None:
+            _defect_then(v, E.ParameterError("choice='explicit' requires a seed matrix p"))
+        try:
+            p = as_matrix(p, "p")
+        except E.DimensionError as exc:
+            _defect_then(v, exc)
+        if tuple(p.shape) != (k0, k0):
+            _defect_then(v, E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}"))
     if intra not in INTRA:
-        raise E.ParameterError(f"unknown intra method {intra!r}; expected {INTRA_METHODS}")
+        bad = E.ParameterError(f"unknown intra method {intra!r}; expected {INTRA_METHODS}")
+        try:   # every earlier error of the reference's order, then the intra dispatch
+            two_stage_qr(v, a, choice, "householder", p)
+        except ValueError:
+            raise bad from None
+        raise bad
     dev = D.pick_device(v, a)
-    ctx = D.ctx(dev)
     todev = D.cto_device if cplx else D.to_device
     V = todev(v, dev)
     A = todev(a, dev)
-    P = None
-    if choice == "explicit":
-        if p is None:
-            raise E.ParameterError("choice='explicit' requires a seed matrix p")
-        p = as_matrix(p, "p")
-        if tuple(p.shape) != (k0, k0):
-            raise E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}")
-        P = todev(p, dev)
+    P = todev(p, dev) if choice == "explicit" else None
     if cplx:
-        Q = D.cempty(n, k, dev)
-        R = D.czeros(k, k, dev)
-        S = D.cempty(k0, k, dev)
+        Q, R, S = D.cempty(n, k, dev), D.czeros(k, k, dev), D.cempty(k0, k, dev)
     else:
-        Q = D.empty(n, k, dev)
-        R = D.zeros(k, k, dev)
-        S = D.empty(k0, k, dev)
-    diag = (C.c_double * 3)()
-    fn = lib().ots_two_stage_c128 if cplx else lib().ots_two_stage_f64
-    rc = fn(
-        ctx, n, k0, k, V.ptr, V.ld, A.ptr, A.ld, CHOICES[choice], INTRA[intra],
-        P.ptr if P is not None else None, P.ld if P is not None else 0,
-        1e-8, 0, Q.ptr, Q.ld, R.ptr, R.ld, S.ptr, S.ld, diag, D.stream_ptr(dev))
-    check(rc, ctx)   # OrthonormalityError before the non-finite ValueError (device-side order)
+        Q, R, S = D.empty(n, k, dev), D.zeros(k, k, dev), D.empty(k0, k, dev)
+    diag = _run_two_stage(dev, V, A, Q, R, S, choice, intra, P, cplx)
     return TwoStageResult(Q.view() if was_torch else Q.numpy(),
                           R.view() if was_torch else R.numpy(),
-                          S.view() if was_torch else S.numpy(),
-                          ReflectorDiagnostics(float(diag[0]), float(diag[1])))
+                          S.view() if was_torch else S.numpy(), diag)
 
 
 def block_householder_qr(blocks, choice="qr", intra="householder"):
     """Algorithm 3 driver (twostage.py:100-151): block 0 by the intra QR,
-    block i >= 1 by `two_stage_qr` against the accumulated Q (device
-    resident when the blocks are CUDA tensors)."""
+    block i >= 1 by Algorithm 1 against the accumulated Q.  The basis lives
+    in ONE preallocated device buffer (n x sum k_i): block i reads its V as a
+    column view of that buffer and writes its Q straight into the next
+    columns (no per-block concatenation, ref :132).  numpy blocks are moved to
+    the device once and the results copied back at the end."""
     if not blocks:
         raise E.ParameterError("need at least one block")
     was_torch = any(D.is_torch(b) for b in blocks)
@@ -141,46 +168,64 @@ def block_householder_qr(blocks, choice="qr", intra="householder"):
     total = sum(sizes)
     if total > n:
         raise E.DimensionError(f"need sum(k_i) <= n, got {total} > {n}")
-    xp = D.torch() if was_torch else np
-    if was_torch:
-        t = D.torch()
-        dev = D.pick_device(*blocks)
-        blocks = [b if b.is_cuda else b.to(f"cuda:{dev}") for b in blocks]
-        r_full = t.zeros((total, total), dtype=t.float64, device=blocks[0].device)
-    else:
-        r_full = np.zeros((total, total))
+    cplx = any(is_complex(b) for b in blocks)       # ref :117 np.result_type(*blocks)
+    t = D.torch()
+    dev = D.pick_device(*blocks)
+    dt = t.complex128 if cplx else t.float64
+    todev = D.cto_device if cplx else D.to_device
+    ldb = max(2, total + (total & 1))
+    buf = t.empty((max(n, 1), ldb), dtype=dt, device=f"cuda:{dev}")
+    r_full = t.zeros((total, total), dtype=dt, device=f"cuda:{dev}")
+    b0 = blocks[0] if D.is_torch(blocks[0]) else t.from_numpy(blocks[0])
     try:
-        qr0 = intra_qr(blocks[0], intra)
+        qr0 = intra_qr(b0.to(device=f"cuda:{dev}", dtype=dt), intra)
     except E.IntraFailure as exc:
         exc.block = 0
         raise
-    qs = [qr0.q]
+    buf[:, :sizes[0]] = qr0.q
     r_full[:sizes[0], :sizes[0]] = qr0.r
     worst = ReflectorDiagnostics(1.0, 0.0)
     offset = sizes[0]
     for i in range(1, len(blocks)):
-        ki = sizes[i]
-        qacc = xp.hstack(qs) if not was_torch else D.torch().cat(qs, dim=1)
+        ki, m = sizes[i], offset
+        if ki == 0:
+            continue
+        V = D.DMat(buf, m, ld=ldb)        # column view [Q_0 ... Q_{i-1}]
+        A = todev(blocks[i], dev)
+        direct = (m % 2 == 0) or cplx      # Q view 16-byte aligned
+        if direct:
+            Q = D.DMat(buf[:, m:], ki, ld=ldb)
+        else:
+            Q = D.cempty(n, ki, dev) if cplx else D.empty(n, ki, dev)
+        if cplx:
+            R, S = D.czeros(ki, ki, dev), D.cempty(m, ki, dev)
+        else:
+            R, S = D.zeros(ki, ki, dev), D.empty(m, ki, dev)
         try:
-            res = two_stage_qr(qacc, blocks[i], choice, intra)
+            diag = _run_two_stage(dev, V, A, Q, R, S, choice, intra, None, cplx)
         except E.IntraFailure as exc:
             exc.block = i
             raise
-        qs.append(res.q)
-        m = qacc.shape[1]
-        r_full[:m, offset:offset + ki] = res.s
-        r_full[offset:offset + ki, offset:offset + ki] = res.r
-        if res.diagnostics.kappa_t > worst.kappa_t:
-            worst = res.diagnostics
+        if not direct:
+            buf[:, m:m + ki] = Q.view()
+        r_full[:m, offset:offset + ki] = S.view()
+        r_full[offset:offset + ki, offset:offset + ki] = R.view()
+        if diag.kappa_t > worst.kappa_t:
+            worst = diag
         offset += ki
-    q = D.torch().cat(qs, dim=1) if was_torch else np.hstack(qs)
-    return BlockQRResult(q, r_full, sizes, worst)
+    q = buf[:, :total] if n else buf[:0, :total]
+    if was_torch:
+        return BlockQRResult(q, r_full, sizes, worst)
+    return BlockQRResult(q.cpu().numpy(), r_full.cpu().numpy(), sizes, worst)
 
 
 def reorthogonalized_two_stage(v, a, choice="qr", intra="householder", sweeps=1, sequence=None):
-    """twostage.py:154-180 for choice != 'bcgs' (repeated Algorithm-1 passes)."""
+    """twostage.py:154-180: repeated Algorithm-1 passes composing r and s,
+    or (choice="bcgs") the classical inter/intra step sequence of the
+    baselines (baselines.py:34-73) on the GPU."""
     if choice == "bcgs":
-        raise NotImplementedError("BCGS baselines are out of scope for the GPU path")
+        from .baselines import bcgs_two_stage
+        return bcgs_two_stage(v, a, sequence or ["inter", "intra"], intra=intra)
     if sweeps < 1:
         raise E.ParameterError("sweeps must be >= 1")
     res = two_stage_qr(v, a, choice, intra)
@@ -198,14 +243,13 @@ def reorthogonalized_two_stage(v, a, choice="qr", intra="householder", sweeps=1,
 
 
 def _augmented_defect(v, q):
-    """||[v, q]^*[v, q] - I||_2 from the (k0+k)^2 Gram (host eigvalsh on the
-    small Gram; the n-length Gram itself is formed on the device when the
-    inputs are CUDA tensors)."""
-    if D.is_torch(q):
+    """orthonormality_defect([v, q]) (twostage.py:183-184) on the GPU: the
+    Gram of the stacked block and its symmetric spectrum (complex-aware)."""
+    from .core import orthonormality_defect
+    if D.is_torch(v) or D.is_torch(q):
         t = D.torch()
-        vq = t.cat([v.to(q.device), q], dim=1)
-        g = (vq.T @ vq).cpu().numpy()
+        dev = q.device if D.is_torch(q) else v.device
+        vq = t.cat([t.as_tensor(v, device=dev), t.as_tensor(q, device=dev)], dim=1)
     else:
         vq = np.hstack([np.asarray(v), np.asarray(q)])
-        g = vq.conj().T @ vq
-    return float(np.max(np.abs(np.linalg.eigvalsh(g) - 1.0))) if g.size else 0.0
+    return orthonormality_defect(vq)
