@@ -76,6 +76,7 @@ def to_device(x, device):
     if is_torch(x):
         if x.dtype != t.float64:
             x = x.to(t.float64)
+        x = x.resolve_neg()
         if x.is_cuda and x.device.index == device and x.dim() == 2 and x.stride(1) == 1 \
                 and x.stride(0) % 2 == 0 and x.data_ptr() % 16 == 0 and x.stride(0) >= x.shape[1]:
             return DMat(x, x.shape[1], ld=x.stride(0))
@@ -107,6 +108,9 @@ def cto_device(x, device):
     if is_torch(x):
         if x.dtype != t.complex128:
             x = x.to(t.complex128)
+        # lazy conjugate / negative views (e.g. .mH) keep unconjugated data
+        # behind the bit: materialise before handing out a raw pointer
+        x = x.resolve_conj().resolve_neg()
         if x.is_cuda and x.device.index == device and x.dim() == 2 and x.stride(1) == 1 \
                 and x.data_ptr() % 16 == 0 and x.stride(0) >= x.shape[1]:
             return DMat(x, x.shape[1], ld=x.stride(0))

@@ -712,6 +712,62 @@ __device__ __forceinline__ void t_store(const double* Tpv, const double* Tw, dou
   }
 }
 
+// Fused inter-block update: the tile's X rows [gr0, gr0+nb) = A_b + V_b Z1
+// formed straight into the register tile (quad layout, X^T as the DMMA
+// accumulator: x^T[col][row] += Z1^T[col][k] V^T[k][row]).  V_b's 128 x k0
+// row block and the matching rows of Z1 stream through shared memory in
+// VC-row chunks of k (cp.async, double-buffered in the Xs region, which is
+// free between tiles; one barrier per chunk).  Replaces the separate
+// tsgemm_nn launch of round 1 (X written to and re-read from HBM).
+template <int KT>
+struct FusedCfg {
+  static constexpr int VC = 16;                              // k-rows (V columns) per chunk
+  static constexpr int VCH = BlkCfg<KT>::B * VC;             // V chunk (128 x VC, swizzled)
+  static constexpr int ZCH = VC * KT;                        // Z1 chunk (VC x KT, swizzled)
+  static constexpr int CH = VCH + ZCH;                       // doubles per buffer
+};
+static_assert(2 * FusedCfg<64>::CH <= BlkCfg<64>::XS && 2 * FusedCfg<32>::CH <= BlkCfg<32>::XS &&
+                  2 * FusedCfg<16>::CH <= BlkCfg<16>::XS,
+              "fused V / Z1 chunks must fit the Xs region");
+
+template <int KT>
+__device__ __forceinline__ void fused_chunk_load(double* buf, const FactorArgs& a, long gr0, long rhi, int c,
+                                                 int tid) {
+  using F = FusedCfg<KT>;
+  load_tile_async(buf, F::VC, a.Vb, a.ldv, gr0, BlkCfg<KT>::B, gr0, rhi, c * F::VC, F::VC, a.kdim, tid, 256);
+  load_tile_async(buf + F::VCH, KT, a.Z1, a.ldz, (long)c * F::VC, F::VC, 0, a.kdim, 0, KT, a.ncols, tid, 256);
+  cp_async_commit();
+}
+
+template <int KT>
+__device__ __forceinline__ void fused_x(double (&x)[16][2], const FactorArgs& a, long gr0, int nb, double* Vs,
+                                        bool owner, int mycol) {
+  using F = FusedCfg<KT>;
+  constexpr int VC = F::VC;
+  const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int nch = (a.kdim + VC - 1) / VC;
+  const long rhi = gr0 + nb;
+  fused_chunk_load<KT>(Vs, a, gr0, rhi, 0, tid);
+  if (owner) tile_regs_load(x, a.Ab, a.lda, gr0, nb, mycol, a.ncols);
+  const int wc = mycol - g;                                  // warp's first column (8 w)
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<0>();
+    __syncthreads();                                         // chunk c landed; buffer (c+1)&1 free
+    if (c + 1 < nch) fused_chunk_load<KT>(Vs + ((c + 1) & 1) * F::CH, a, gr0, rhi, c + 1, tid);
+    if (owner) {
+      const double* Vc = Vs + (c & 1) * F::CH;
+      const double* Zc = Vc + F::VCH;
+#pragma unroll
+      for (int kk = 0; kk < VC / 4; ++kk) {
+        const double za = Zc[swz(4 * kk + t, wc + g, KT)];
+#pragma unroll
+        for (int f = 0; f < 16; ++f) dmma(x[f], za, Vc[swz(8 * f + g, 4 * kk + t, VC)]);
+      }
+    }
+  }
+  __syncthreads();                                           // Xs is reused by the panels
+}
+
 template <int KT>
 __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   using C = BlkCfg<KT>;
@@ -729,10 +785,26 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   double* Tbase = a.U + (long)chain * (a.G.L + 1) * KT * KT;
   const int b = a.G.b;
 
+  const bool fused = a.Vb != nullptr;
+  const bool owner = warp < NP;
+  const int mycol = 8 * warp + ((tid & 31) >> 2);
+  double x[16][2];
   // ---- head: plain QR of rows [r0, r0+KT) (unblocked smem sweep, once per chain)
-  load_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
-  cp_async_commit();
-  cp_async_wait<0>();
+  if (fused) {
+    const long remh = a.G.nrows - r0;
+    fused_x<KT>(x, a, r0, (int)(remh < KT ? remh : KT), Xs, owner, mycol);
+    if (owner) {
+      const int t4 = tid & 3;
+#pragma unroll
+      for (int f = 0; f < KT / 8; ++f)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) S[(8 * f + 2 * t4 + h) * KT + mycol] = x[f][h];
+    }
+  } else {
+    load_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
+    cp_async_commit();
+    cp_async_wait<0>();
+  }
   __syncthreads();
   if (a.head_tri) {
     // Tree levels: the head is an R factor (exact zeros below the diagonal),
@@ -748,14 +820,15 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   }
 
   // ---- structured tiles (register-resident, see BlkCfg)
-  const bool owner = warp < NP;
-  const int mycol = 8 * warp + ((tid & 31) >> 2);
   double* Ys = Xs;                                  // NSLOT panel slots of Y
-  double x[16][2];
-  if (owner && ntiles > 0) {
+  if (ntiles > 0) {
     const long g0 = r0 + KT;
     const long rem0 = a.G.nrows - g0;
-    tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
+    if (fused) {
+      fused_x<KT>(x, a, g0, (int)(rem0 < b ? rem0 : b), Xs, owner, mycol);
+    } else if (owner) {
+      tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
+    }
   }
   for (int t = 1; t <= ntiles; ++t) {
     double* Tpc = Tp + (t & 1) * NP * 64;           // this tile's T_pp
@@ -769,10 +842,20 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
       const long rem1 = a.G.nrows - g1;
       const int nb1 = (int)(rem1 < b ? rem1 : b);
       const int lpr = (a.ncols * 8 + 127) / 128;          // 128-byte lines per row
+      const double* src = fused ? a.Ab : a.D;
+      const long lds_ = fused ? a.lda : a.ldd;
       for (int i = tid; i < nb1 * lpr; i += 256) {
         const int r = i / lpr, l = i - r * lpr;
-        const double* ptr = a.D + (g1 + r) * a.ldd + l * 16;
+        const double* ptr = src + (g1 + r) * lds_ + l * 16;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+      }
+      if (fused) {     // and the tile's V_b rows
+        const int lpv = (a.kdim * 8 + 127) / 128;
+        for (int i = tid; i < nb1 * lpv; i += 256) {
+          const int r = i / lpv, l = i - r * lpv;
+          const double* ptr = a.Vb + (g1 + r) * a.ldv + l * 16;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+        }
       }
     }
     // The owner of the next panel (p+1) shares its SM sub-partition with warp
@@ -815,7 +898,7 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     // Y (in place of the tile) -> global; next tile -> registers
     if (owner) {
       tile_regs_store(x, a.D, a.ldd, gr0, nb, mycol, a.ncols);
-      if (t < ntiles) {
+      if (t < ntiles && !fused) {
         const long g1 = gr0 + b;
         const long rem1 = a.G.nrows - g1;
         tile_regs_load(x, a.D, a.ldd, g1, (int)(rem1 < b ? rem1 : b), mycol, a.ncols);
@@ -826,6 +909,14 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
     if (t > 1) {                    // previous tile's T is complete (phase NP-1 ran in panel NP-1)
       t_store<KT>(Tpp, Tw, Tbase + (long)(t - 1) * KT * KT);
       __syncthreads();              // Tpp is this parity's buffer for tile t+1
+    }
+    if (fused && t < ntiles) {      // X of the next tile (Xs: Y slots and Tw are free here)
+      const long g1 = gr0 + b;
+      const long rem1 = a.G.nrows - g1;
+      TSTAMP(f0);
+      fused_x<KT>(x, a, g1, (int)(rem1 < b ? rem1 : b), Xs, owner, mycol);
+      TSTAMP(f1);
+      TACC(13, f0, f1);
     }
     TSTAMP(t4);
     TACC(3, t3, t4);

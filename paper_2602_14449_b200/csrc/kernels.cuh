@@ -39,7 +39,15 @@ struct FactorArgs {
   ChainGeom G;
   double* U;             // per tile KT*KT, tile id = chain*(L+1) + t
   double* Rout;          // stacked chain R's: chain*KT rows, ld KT
-  int head_tri;          // input rows are stacked upper-triangular R's (tree levels)
+  int head_tri = 0;      // input rows are stacked upper-triangular R's (tree levels)
+  // Fused inter-block update (level 0 only; Vb == nullptr: D already holds X).
+  // The kernel forms each tile of X = A_b + V_b Z1 (twostage.py:91-93,
+  // reflector.py:238) on the fly -- A_b and V_b rows of the tile, Z1 k0 x k --
+  // instead of reading an X written by a separate apply kernel; Y still goes
+  // to D (same row numbering as X).
+  const double* Vb = nullptr; long ldv = 0; int kdim = 0;
+  const double* Z1 = nullptr; long ldz = 0;
+  const double* Ab = nullptr; long lda = 0;
 };
 
 struct QformArgs {

@@ -298,13 +298,30 @@ int ensure_ws(ots_ctx* ctx, size_t bytes) {
 
 // tri_first: level 0's rows are already stacked R factors (the global tree);
 // levels >= 1 always are.
-int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st, bool tri_first = false) {
+// fuse0 (optional): level 0 forms X = A_b + V_b Z1 tile by tile inside the
+// factor (FactorArgs fused fields) instead of reading an X in L.D.
+int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st, bool tri_first = false,
+                      const FactorArgs* fuse0 = nullptr) {
   for (size_t l = 0; l < lv.size(); ++l) {
     Level& L = lv[l];
     FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, (l > 0 || tri_first) ? 1 : 0};
+    if (l == 0 && fuse0) {
+      fa.Vb = fuse0->Vb; fa.ldv = fuse0->ldv; fa.kdim = fuse0->kdim;
+      fa.Z1 = fuse0->Z1; fa.ldz = fuse0->ldz; fa.Ab = fuse0->Ab; fa.lda = fuse0->lda;
+    }
     CK(launch_chain_factor(fa, KT, st));
   }
   return OTS_OK;
+}
+
+// level-0 fused-update arguments of a job (X rows start at V/A row qrow0)
+FactorArgs fused_args(const Job& j) {
+  const JobCfg& c = j.c;
+  FactorArgs f{};
+  f.Vb = c.V + (long)j.qrow0 * c.ldv; f.ldv = c.ldv; f.kdim = (int)c.k0;
+  f.Z1 = j.s.Z1; f.ldz = j.ld;
+  f.Ab = c.A + (long)j.qrow0 * c.lda; f.lda = c.lda;
+  return f;
 }
 
 // Q-form from the top level (whose single chain gets C = Ctop) down to level 0.
@@ -725,11 +742,22 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // an event a little later) fill the rest; apply1 hands out its tiles
   // dynamically, so those 3 SMs simply take fewer.  The factor then starts on
   // an idle GPU instead of waiting for the diagnostics' SMs.
+  // Optional (OTS_FUSE=1): the update X = A_b + V_b Z1 fused into the
+  // factor's level 0 (no apply1 launch, X never goes through HBM; the
+  // diagnostics then run beside apply2).  Measured slower at the headline
+  // (factor 32.4 ms vs factor 20.1 + apply1 9.9): the fused update's 4096
+  // DMMAs per tile compete with the other resident CTA's latency-bound panel
+  // chain for the FP64 pipe, so it is off by default.
+  static const bool want_fuse = getenv("OTS_FUSE") != nullptr && getenv("OTS_FUSE")[0] == '1';
+  const bool fuse = want_fuse && (intra == OTS_INTRA_HOUSEHOLDER) && c.k0 > 0;
+  const FactorArgs fa0 = fused_args(j);
   if (diag_side) {
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
     CK(launch_diag(j.s, ctx->side));
     CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // waited for before the status read
-    if ((rc = phase_apply1(ctx, j))) return rc;
+    if (!fuse && (rc = phase_apply1(ctx, j))) return rc;
+  } else if (fuse) {
+    // diagnostics deferred (beside apply2)
   } else {
     CK(launch_diag(j.s, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
@@ -741,9 +769,9 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply1 done
     CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   }
-  prof_mark(ctx, st, "apply1");
+  if (!fuse) prof_mark(ctx, st, "apply1");
   if (intra == OTS_INTRA_HOUSEHOLDER) {
-    if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
+    if ((rc = run_factor_levels(ctx, j.lv, KT, st, false, fuse ? &fa0 : nullptr))) return rc;
     prof_mark(ctx, st, "factor");
     set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
     if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st, diag_side ? j.nsm_use : 0))) return rc;
@@ -759,7 +787,22 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
   CK(launch_z2(j.s, st));
   prof_mark(ctx, st, "z2");
-  if ((rc = phase_apply2(ctx, j))) return rc;
+  if (fuse && !diag_side) {
+    // diagnostics (3 CTAs, ~2 ms) on the main stream first so they own their
+    // SMs before apply2's CTAs (side stream, dynamic tiles) fill the rest
+    CK(cudaEventRecord(ctx->ev_seedA, st));
+    CK(launch_diag(j.s, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
+    JobCfg c1 = j.c;
+    j.c.st = ctx->side;
+    rc = phase_apply2(ctx, j);
+    j.c = c1;
+    if (rc) return rc;
+    CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply2 done
+    CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
+  } else if ((rc = phase_apply2(ctx, j))) {
+    return rc;
+  }
   prof_mark(ctx, st, "apply2");
   CK(launch_qtop(j.s, Q, ldq, st));
   if (bh) {
@@ -776,7 +819,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   prof_mark(ctx, st, "tail");
   // gram, reduce, seed(B), diag, apply1, identity, sign, gram2, reduce, copy_y2,
   // z2, apply2, qtop + a factor and a qform launch per level (+ seedA, B epilogue)
-  ctx->launches = 13 + 2 * (int)j.lv.size() + (bh ? 2 : 0) + (split_seed ? 1 : 0);
+  ctx->launches = 13 + 2 * (int)j.lv.size() + (bh ? 2 : 0) + (split_seed ? 1 : 0) - (fuse ? 1 : 0);
   rc = read_status(ctx, j, diag_host);
   prof_end(ctx);
   return rc;
