@@ -29,6 +29,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 N_HEAD, K0_HEAD, K_HEAD = 1 << 24, 128, 64
+SHARE = os.environ.get("OTS_BENCH_SHARE_DEVICE") == "1"
 REF_SAMPLE_N = 1 << 18          # bounded CPU sample (same k0, k)
 
 
@@ -203,7 +204,7 @@ def run_gpu(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # OTS_BENCH_SHARE_DEVICE=1: every rank on cuda:0 with gloo collectives --
     # a plumbing check of the N>1 leg on a one-GPU box, never a measurement
-    share = os.environ.get("OTS_BENCH_SHARE_DEVICE") == "1"
+    share = SHARE
     torch.cuda.set_device(0 if share else local)
     if world > 1:
         dist.init_process_group("gloo" if share else "nccl")
@@ -384,8 +385,10 @@ def run_sharded(args, n, k0, k, rank, world, local):
             "data": "synthetic",
             "config": {"workload": "headline two_stage_qr(V, A) choice=qr intra=householder, row-sharded",
                        "n": n, "k0": k0, "k": k,
-                       "parallelism": f"row-sharded x{world} (NCCL allreduce/allgather/broadcast of the "
-                                      f"k0x(k0+k), KTxKT, k0xk blocks)",
+                       "parallelism": (f"row-sharded x{world} (NCCL allreduce/allgather/broadcast of the "
+                                       f"k0x(k0+k), KTxKT, k0xk blocks)") if not SHARE else
+                                      (f"row-sharded x{world} ranks SHARING ONE GPU, gloo host-staged "
+                                       f"collectives: plumbing check of the N>1 leg, not a scaling number"),
                        "l2": "inputs >> L2 on every rank (no flush needed)"},
             "roofline": {"bound": "tensor", "kernel": "whole step", "achieved": round(F / (ms * 1e-3) / 1e12, 3),
                          "peak": round(world * 37.0, 1), "unit": "TFLOP/s",

@@ -270,3 +270,27 @@ def test_householder_nonfinite_cabi():
         P.householder_qr(x.astype(np.complex128))
     with pytest.raises(ValueError):
         P.two_stage_qr(np.zeros((5000, 0)), x)
+
+
+def test_fused_update_factor_parity():
+    """OTS_FUSE=1 (update X = A_b + V_b Z1 formed inside the chain factor):
+    same results as the oracle (run in a subprocess: the switch is read once)."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "import paper_2602_14449_b200 as P; from oracle import twostage_oracle as O;"
+        "from paper_2602_14449_b200 import workloads as W\n"
+        "for n, k0, k in ((1 << 16, 128, 64), (40000, 13, 7), (30000, 100, 33)):\n"
+        "    rng = W.make_rng(n + k0); v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0));"
+        " a = W.normal_matrix(rng, n, k)\n"
+        "    ref = O.two_stage(v, a, 'qr', diagnostics=False); res = P.two_stage_qr(v, a)\n"
+        "    for key in 'qrs':\n"
+        "        x, y = getattr(res, key), ref[key]\n"
+        "        e = float((np.abs(x - y) / (np.abs(y) + 1e-4 * np.abs(y).max())).max())\n"
+        "        assert e < 1e-10, (n, k0, k, key, e)\n"
+        "print('fused ok')\n")
+    env = dict(os.environ, OTS_FUSE="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(ROOT), env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "fused ok" in out.stdout, out.stdout + out.stderr
