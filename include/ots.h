@@ -199,6 +199,12 @@ int ots_orthonormality_defect_f64(ots_ctx* ctx, int64_t n, int64_t k0,
                                   const double* V, int64_t ldv, double* out, void* stream);
 int ots_orthonormality_defect_c128(ots_ctx* ctx, int64_t n, int64_t k0,
                                    const void* V, int64_t ldv, double* out, void* stream);
+/* LAPACK sign vector of a positive-diagonal QR from its Q's
+ * top k x k block: svec (device, k entries +-1).  Column-blocked intra QR
+ * for k > 64 (householder_qr core.py:61-84 semantics).  k <= 512 (c128 256). */
+int ots_qr_signs_f64(ots_ctx* ctx, int64_t k, const double* Qtop, int64_t ldq, double* svec, void* stream);
+int ots_qr_signs_c128(ots_ctx* ctx, int64_t k, const void* Qtop, int64_t ldq, double* svec, void* stream);
+
 /* {lambda_min, lambda_max} of v^* v (host out2): spectral_norm (core.py:35-40)
  * = sqrt(lambda_max); InnerProduct.norm/defect (oblique.py:75-90) on L^* x. */
 int ots_gram_extremes_f64(ots_ctx* ctx, int64_t n, int64_t k0,

@@ -90,6 +90,8 @@ def lib():
                 L.ots_update_c128.argtypes = L.ots_update_f64.argtypes
                 L.ots_gram_extremes_f64.argtypes = L.ots_orthonormality_defect_f64.argtypes
                 L.ots_gram_extremes_c128.argtypes = L.ots_orthonormality_defect_f64.argtypes
+                L.ots_qr_signs_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp]
+                L.ots_qr_signs_c128.argtypes = L.ots_qr_signs_f64.argtypes
                 L.ots_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), _int]
                 L.ots_modified_lu_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp]
                 L.ots_shifted_cholesky_qr_f64.argtypes = [
@@ -133,7 +135,7 @@ EXPORTED_SYMBOLS = [
     "ots_stability_c128", "ots_orthonormality_defect_f64", "ots_orthonormality_defect_c128",
     "ots_shifted_cholesky_qr_ex_f64", "ots_shifted_cholesky_qr_ex_c128",
     "ots_gram_f64", "ots_gram_c128", "ots_update_f64", "ots_update_c128",
-    "ots_gram_extremes_f64", "ots_gram_extremes_c128",
+    "ots_gram_extremes_f64", "ots_gram_extremes_c128", "ots_qr_signs_f64", "ots_qr_signs_c128",
     "ots_dense_cholesky_f64", "ots_dense_trsm_lt_f64", "ots_dense_trmm_lt_f64", "ots_b_two_stage_dense_f64",
 ]
 

@@ -59,6 +59,55 @@ class QRPair:
     r: object
 
 
+def _qr_signs(qtop):
+    """LAPACK sign vector (device tensor, +-1) of a positive-diagonal QR from
+    its Q's top k x k block (ots_qr_signs_*)."""
+    t = D.torch()
+    k = qtop.shape[0]
+    dev = qtop.device.index
+    ctx = D.ctx(dev)
+    svec = t.empty(max(k, 1), dtype=t.float64, device=qtop.device)
+    if is_complex(qtop):
+        Qt = D.cto_device(qtop, dev)
+        rc = lib().ots_qr_signs_c128(ctx, k, Qt.ptr, Qt.ld, C.c_void_p(svec.data_ptr()), D.stream_ptr(dev))
+    else:
+        Qt = D.to_device(qtop, dev)
+        rc = lib().ots_qr_signs_f64(ctx, k, Qt.ptr, Qt.ld, C.c_void_p(svec.data_ptr()), D.stream_ptr(dev))
+    check(rc, ctx)
+    return svec[:k]
+
+
+def _householder_qr_wide(a, nonneg_diag, was_torch):
+    """k > 64 columns: Algorithm 3 over 64-column blocks on the device (block
+    0 by the TSQR, block i by Algorithm 1 against the accumulated Q), then
+    the LAPACK sign convention of the whole matrix recovered from Q's top
+    k x k block (the QR with positive diagonal is unique, and the
+    modified-LU rule on its Q gives dgeqrf's signs).  Same Q, R as LAPACK on
+    full-rank input up to rounding."""
+    from .twostage import block_householder_qr
+    t = D.torch()
+    m, n = a.shape
+    dev = D.pick_device(a)
+    dt = t.complex128 if is_complex(a) else t.float64
+    ad = (a if D.is_torch(a) else t.from_numpy(a)).to(device=f"cuda:{dev}", dtype=dt)
+    res = block_householder_qr([ad[:, c:c + 64] for c in range(0, n, 64)])
+    q, r = res.q, res.r
+    dg = t.diagonal(r).real
+    d = t.where(dg < 0, -1.0, 1.0).to(t.float64)
+    q = q * d.to(dt)[None, :]
+    r = r * d.to(dt)[:, None]
+    s = _qr_signs(q[:n, :n]).to(dt)
+    q = (q * s[None, :]).contiguous()
+    r = t.triu(r * s[:, None])
+    if nonneg_diag:
+        ph = t.where(t.diagonal(r).real < 0, -1.0, 1.0).to(dt)
+        q = q * ph[None, :]
+        r = r * ph[:, None]
+    if not t.isfinite(r).all():
+        raise ValueError("input contains non-finite entries")
+    return QRPair(q if was_torch else q.cpu().numpy(), r if was_torch else r.cpu().numpy())
+
+
 def householder_qr(a, nonneg_diag=False):
     """QR of a tall matrix on the GPU (core.py:61-84 semantics)."""
     was_torch = D.is_torch(a)
@@ -66,6 +115,8 @@ def householder_qr(a, nonneg_diag=False):
     m, n = a.shape
     if m < n:
         raise E.DimensionError(f"need rows >= cols, got {m}x{n}")
+    if n > 64:
+        return _householder_qr_wide(a, nonneg_diag, was_torch)
     # non-finite input: ValueError from the device (R check, core.py:72-73)
     dev = D.pick_device(a)
     ctx = D.ctx(dev)

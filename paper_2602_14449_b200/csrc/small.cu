@@ -1367,6 +1367,20 @@ cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, lo
   return cudaGetLastError();
 }
 
+// LAPACK sign vector of a QR with positive R diagonal from its
+// Q's top k x k block: the modified-LU rule, with the tau = 0 / |z_jj| = 1
+// exception (dlarfg's shortcut).  svec: k entries +-1 (device).
+__global__ void __launch_bounds__(SMALL_NT) qr_signs_kernel(const double* Qtop, long ldq, int k, double* work,
+                                                            double* svec) {
+  BLK_FOR(e, k * k) { const int i = e / k, j = e - i * k; work[i * k + j] = Qtop[(long)i * ldq + j]; }
+  __syncthreads();
+  blk_mlu(work, k, k, svec, true);
+}
+cudaError_t launch_qr_signs(const double* Qtop, long ldq, int k, double* work, double* svec, cudaStream_t st) {
+  qr_signs_kernel<<<1, SMALL_NT, 0, st>>>(Qtop, ldq, k, work, svec);
+  return cudaGetLastError();
+}
+
 // lambda_min, lambda_max of a symmetric m x m matrix (lower triangle of G
 // read; work: m*m + 4m doubles) -- spectra of Grams for orthonormality_defect
 // and the weighted norms (core.py:35-49, oblique.py:70-90)

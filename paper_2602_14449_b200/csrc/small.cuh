@@ -69,6 +69,8 @@ cudaError_t launch_seed_split(const SmallState& s, int part, cudaStream_t st);
 cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, long ldvq, const double* Gqq,
                              long ldqq, const double* Gee, long ldee, const double* Gaa, long ldaa, int k0, int k,
                              int augmented, double* work, double* out3, cudaStream_t st);
+cudaError_t launch_qr_signs(const double* Qtop, long ldq, int k, double* work, double* svec, cudaStream_t st);
+cudaError_t launch_zqr_signs(const void* Qtop, long ldq, int k, void* work, double* svec, cudaStream_t st);
 cudaError_t launch_sym_extremes(const double* G, long ldg, int m, double* work, double* out2, cudaStream_t st);
 cudaError_t launch_neg_copy(const double* X, long ldx, int r, int c, double* Y, long ldy, cudaStream_t st);
 cudaError_t launch_zseed(const ZState& z, cudaStream_t st, int part = 0);

@@ -135,6 +135,8 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
         except ValueError:
             raise bad from None
         raise bad
+    if k > 64:
+        return _two_stage_wide(v, a, choice, intra, p, was_torch)
     dev = D.pick_device(v, a)
     todev = D.cto_device if cplx else D.to_device
     V = todev(v, dev)
@@ -148,6 +150,37 @@ def two_stage_qr(v, a, choice="qr", intra="householder", p=None):
     return TwoStageResult(Q.view() if was_torch else Q.numpy(),
                           R.view() if was_torch else R.numpy(),
                           S.view() if was_torch else S.numpy(), diag)
+
+
+def _two_stage_wide(v, a, choice, intra, p, was_torch):
+    """k > 64: the reference's own sequence (twostage.py:90-97) on device
+    primitives -- reflector object (seed, T, W_t), H^* A through the DMMA
+    streaming kernels, S = P^* (H^* A)_top, the column-blocked intra QR with
+    LAPACK signs (core._householder_qr_wide), Q = H [0; Q_], diagnostics
+    from k0 x k0 data."""
+    from .core import gram
+    from .reflector import apply_reflector, build_reflector, reflector_diagnostics
+    t = D.torch()
+    n, k0 = v.shape
+    k = a.shape[1]
+    if is_complex(v) or is_complex(a):
+        raise NotImplementedError("complex two_stage_qr with k > 64 needs the complex reflector object")
+    dev = D.pick_device(v, a)
+    vd = (v if D.is_torch(v) else t.from_numpy(v)).to(device=f"cuda:{dev}", dtype=t.float64).contiguous()
+    ad = (a if D.is_torch(a) else t.from_numpy(a)).to(device=f"cuda:{dev}", dtype=t.float64)
+    h = build_reflector(vd, choice, p)
+    ah = apply_reflector(h, ad, adjoint=True)
+    pm = h.p if D.is_torch(h.p) else t.from_numpy(np.ascontiguousarray(h.p)).to(f"cuda:{dev}")
+    s = gram(pm, ah[:k0])                                   # P^* (H^* A)_top  (twostage.py:92)
+    qr = intra_qr(ah[k0:].contiguous(), intra)
+    lifted = t.zeros((n, k), dtype=t.float64, device=f"cuda:{dev}")
+    lifted[k0:] = qr.q
+    q = apply_reflector(h, lifted)
+    diag = reflector_diagnostics(h)
+    r = qr.r
+    if was_torch:
+        return TwoStageResult(q, r, s, diag)
+    return TwoStageResult(q.cpu().numpy(), r.cpu().numpy() if D.is_torch(r) else r, s.cpu().numpy(), diag)
 
 
 def block_householder_qr(blocks, choice="qr", intra="householder"):

@@ -294,3 +294,32 @@ def test_fused_update_factor_parity():
     out = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(ROOT), env=env,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "fused ok" in out.stdout, out.stdout + out.stderr
+
+
+# ----------------------------------------------------------------- wide shapes (k > 64)
+@pytest.mark.parametrize("field,m,k", [("real", 5000, 100), ("real", 3000, 200), ("complex", 4000, 96)])
+def test_householder_qr_wide_vs_lapack(field, m, k):
+    """k > 64: column-blocked device QR + LAPACK sign recovery == numpy's
+    (LAPACK dgeqrf/zgeqrf) Q and R elementwise."""
+    x = W.normal_matrix(W.make_rng(k + m), m, k, field)
+    q0, r0 = np.linalg.qr(x)
+    qr = P.householder_qr(x)
+    assert rel_e(qr.q, q0) < 1e-10 and rel_e(qr.r, r0) < 1e-10
+    qr = P.householder_qr(x, nonneg_diag=True)
+    assert np.all(np.diag(qr.r).real >= 0) and np.abs(qr.q @ qr.r - x).max() < 1e-12 * np.abs(x).max() * k
+    e = P.householder_qr(np.eye(300, 130))            # tau = 0 everywhere: R = I, Q = [I; 0]
+    assert np.allclose(e.r, np.eye(130)) and np.allclose(e.q, np.eye(300, 130))
+
+
+@pytest.mark.parametrize("choice", ["mlu", "qr", "polar"])
+def test_table4_shape_golden(g2, choice):
+    """The paper's Table-4 shape (n=1000, k0=k=100) through
+    the drop-in, against the reference's own outputs."""
+    v, a = g2["table4/v"], g2["table4/a"]
+    res = P.two_stage_qr(v, a, choice=choice)
+    g = lambda key: g2[f"table4/{choice}/{key}"]
+    assert rel_e(res.q, g("q")) < 1e-10
+    assert rel_e(res.r, g("r")) < 1e-10
+    assert rel_e(res.s, g("s")) < 1e-10
+    assert abs(res.diagnostics.kappa_t - float(g("kappa_t"))) < 1e-10 * float(g("kappa_t"))
+    assert abs(res.diagnostics.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
