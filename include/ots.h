@@ -257,6 +257,20 @@ int ots_reflector_tsolve_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, double*
 int ots_reflector_get_f64(ots_ctx* ctx, const ots_refl* r, int which, double* out, int64_t ldo,
                           void* stream);
 
+/* complex128 reflector objects (same semantics, interleaved data, ld in
+ * complex elements; k0 <= 256, m <= 64 per apply) -- reflector.py:156-247 */
+typedef struct ots_zrefl ots_zrefl;
+int ots_build_reflector_c128(ots_ctx* ctx, int64_t n, int64_t k0, const void* V, int64_t ldv,
+                             int choice, const void* P, int64_t ldp, double orth_tol,
+                             int allow_defect, ots_zrefl** out, double* defect_host, void* stream);
+void ots_zreflector_destroy(ots_zrefl* r);
+int ots_apply_reflector_c128(ots_ctx* ctx, ots_zrefl* r, int64_t m, const void* X, int64_t ldx,
+                             void* Y, int64_t ldy, int adjoint, void* stream);
+int ots_reflector_diagnostics_c128(ots_ctx* ctx, ots_zrefl* r, double* diag_host, void* stream);
+int ots_reflector_tsolve_c128(ots_ctx* ctx, ots_zrefl* r, int64_t m, void* B, int64_t ldb,
+                              int adjoint, void* stream);
+int ots_reflector_get_c128(ots_ctx* ctx, ots_zrefl* r, int which, void* out, int64_t ldo, void* stream);
+
 /* Per-phase device timings of the last call (CUDA events on the launching
  * stream), enabled with ots_set_profiling(ctx, 1).  names: '\n'-separated. */
 int ots_set_profiling(ots_ctx* ctx, int enable);

@@ -92,6 +92,12 @@ def lib():
                 L.ots_gram_extremes_c128.argtypes = L.ots_orthonormality_defect_f64.argtypes
                 L.ots_qr_signs_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp]
                 L.ots_qr_signs_c128.argtypes = L.ots_qr_signs_f64.argtypes
+                L.ots_build_reflector_c128.argtypes = L.ots_build_reflector_f64.argtypes
+                L.ots_zreflector_destroy.argtypes = [_vp]
+                L.ots_apply_reflector_c128.argtypes = L.ots_apply_reflector_f64.argtypes
+                L.ots_reflector_diagnostics_c128.argtypes = L.ots_reflector_diagnostics_f64.argtypes
+                L.ots_reflector_tsolve_c128.argtypes = L.ots_reflector_tsolve_f64.argtypes
+                L.ots_reflector_get_c128.argtypes = L.ots_reflector_get_f64.argtypes
                 L.ots_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), _int]
                 L.ots_modified_lu_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp]
                 L.ots_shifted_cholesky_qr_f64.argtypes = [
@@ -136,6 +142,8 @@ EXPORTED_SYMBOLS = [
     "ots_shifted_cholesky_qr_ex_f64", "ots_shifted_cholesky_qr_ex_c128",
     "ots_gram_f64", "ots_gram_c128", "ots_update_f64", "ots_update_c128",
     "ots_gram_extremes_f64", "ots_gram_extremes_c128", "ots_qr_signs_f64", "ots_qr_signs_c128",
+    "ots_build_reflector_c128", "ots_zreflector_destroy", "ots_apply_reflector_c128",
+    "ots_reflector_diagnostics_c128", "ots_reflector_tsolve_c128", "ots_reflector_get_c128",
     "ots_dense_cholesky_f64", "ots_dense_trsm_lt_f64", "ots_dense_trmm_lt_f64", "ots_b_two_stage_dense_f64",
 ]
 

@@ -79,6 +79,9 @@ cudaError_t launch_zcholqr_step(const double* Gr, long ldg, int k, long m, int s
 cudaError_t launch_zmlu(const void* Z, int ldz, int n, void* LU, double* p, double* work, int* status,
                         cudaStream_t st);
 cudaError_t launch_zidentity(void* D, int n, int ld, cudaStream_t st);
+cudaError_t launch_zrefl_apply(const ZState& z, const double* VhXr, long ldy, int m, int adjoint, const void* X,
+                               long ldx, void* Ytop, long ldyt, cudaStream_t st);
+cudaError_t launch_ztsolve(const ZState& z, void* B, long ldb, int m, int adjoint, cudaStream_t st);
 cudaError_t launch_zz2(const ZState& z, const double* Y2r, long ldy, void* Qtop, long ldq, cudaStream_t st);
 cudaError_t launch_zsign(const ZState& z, const void* Qtop, long ldq, const void* Rfin, int ldr, void* Rout,
                          long ldro, cudaStream_t st);

@@ -8,6 +8,7 @@ record types."""
 
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import numpy as np
@@ -46,6 +47,16 @@ class _DeviceTSolver:
 
     def solve(self, b, adjoint=False):
         was_torch = D.is_torch(b)
+        if self._h.cplx:    # complex T: pivoted LU of phi(T) on the device
+            bb = as_matrix(b if (was_torch or np.ndim(b) == 2) else np.asarray(b)[:, None], "b")
+            vec = (not was_torch) and np.ndim(b) == 1
+            out = D.cto_device(bb, self._dev)
+            out = D.DMat(out.buf.clone(), out.cols, ld=out.ld) if was_torch else out
+            ctx = D.ctx(self._dev)
+            check(lib().ots_reflector_tsolve_c128(ctx, self._h.ptr, out.cols, out.ptr, out.ld, int(bool(adjoint)),
+                                                  D.stream_ptr(self._dev)), ctx)
+            res = out.view() if was_torch else out.numpy()
+            return res[:, 0] if vec else res
         if is_complex(b):   # T is real: real and imaginary parts separately
             re = self.solve(b.real.contiguous() if was_torch else np.ascontiguousarray(np.real(b)), adjoint)
             im = self.solve(b.imag.contiguous() if was_torch else np.ascontiguousarray(np.imag(b)), adjoint)
@@ -66,19 +77,20 @@ class _DeviceTSolver:
 
 
 class _Handle:
-    def __init__(self, ptr, dev):
+    def __init__(self, ptr, dev, cplx=False):
         import weakref
         self.ptr = ptr
         self.dev = dev
-        self._fin = weakref.finalize(self, lib().ots_reflector_destroy, ptr)
+        self.cplx = cplx
+        destroy = lib().ots_zreflector_destroy if cplx else lib().ots_reflector_destroy
+        self._fin = weakref.finalize(self, destroy, ptr)
 
     def get(self, which, as_torch):
-        import ctypes as C
-        t = D.torch()
         ctx = D.ctx(self.dev)
         k0 = self.k0
-        out = D.empty(k0, k0, self.dev)
-        check(lib().ots_reflector_get_f64(ctx, self.ptr, which, out.ptr, out.ld, D.stream_ptr(self.dev)), ctx)
+        out = (D.cempty if self.cplx else D.empty)(k0, k0, self.dev)
+        fn = lib().ots_reflector_get_c128 if self.cplx else lib().ots_reflector_get_f64
+        check(fn(ctx, self.ptr, which, out.ptr, out.ld, D.stream_ptr(self.dev)), ctx)
         return out.view().clone() if as_torch else out.numpy()
 
 
@@ -105,6 +117,7 @@ class GenHouseholder:
             V = self._V.view()
             w = -V.clone()
             p = t.as_tensor(self.p, device=V.device) if not self._torch else self.p
+            p = p.to(w.dtype)
             w[:self.k0] = p - V[:self.k0]
             self._w = w if self._torch else w.cpu().numpy()
         return self._w
@@ -120,8 +133,7 @@ def build_reflector(v, choice="qr", p=None, orth_tol=1e-8, allow_defect=False):
         raise E.DimensionError(f"v must be tall, got {tuple(v.shape)}")
     if k0 == 0:
         raise E.DimensionError("v must have at least one column")
-    if is_complex(v):
-        raise NotImplementedError("complex build_reflector: not in this build")
+    cplx = is_complex(v)
 
     def deferred(exc):   # the defect check (reflector.py:220-223) precedes the seed's checks
         if not allow_defect:
@@ -135,7 +147,8 @@ def build_reflector(v, choice="qr", p=None, orth_tol=1e-8, allow_defect=False):
         deferred(E.ParameterError(f"unknown choice {choice!r}; expected one of {CHOICES}"))
     dev = D.pick_device(v)
     ctx = D.ctx(dev)
-    V = D.to_device(v, dev)
+    todev = D.cto_device if cplx else D.to_device
+    V = todev(v, dev)
     P = None
     if choice == "explicit":
         if p is None:
@@ -146,16 +159,15 @@ def build_reflector(v, choice="qr", p=None, orth_tol=1e-8, allow_defect=False):
             deferred(exc)
         if tuple(p.shape) != (k0, k0):
             deferred(E.DimensionError(f"seed p must be {k0}x{k0}, got {tuple(p.shape)}"))
-        P = D.to_device(p, dev)
+        P = todev(p, dev)
     h = C.c_void_p()
     defect = C.c_double()
     from ._native import CHOICES as _CH
-    rc = lib().ots_build_reflector_f64(ctx, n, k0, V.ptr, V.ld, _CH[choice],
-                                       P.ptr if P is not None else None, P.ld if P is not None else 0,
-                                       orth_tol, int(bool(allow_defect)), C.byref(h), C.byref(defect),
-                                       D.stream_ptr(dev))
+    fn = lib().ots_build_reflector_c128 if cplx else lib().ots_build_reflector_f64
+    rc = fn(ctx, n, k0, V.ptr, V.ld, _CH[choice], P.ptr if P is not None else None, P.ld if P is not None else 0,
+            orth_tol, int(bool(allow_defect)), C.byref(h), C.byref(defect), D.stream_ptr(dev))
     check(rc, ctx)
-    return GenHouseholder(_Handle(h, dev), V, choice, n, k0, was_torch)
+    return GenHouseholder(_Handle(h, dev, cplx), V, choice, n, k0, was_torch)
 
 
 def apply_reflector(h, x, adjoint=False):
@@ -164,22 +176,24 @@ def apply_reflector(h, x, adjoint=False):
     x = as_matrix(x, "x")
     if x.shape[0] != h.n:
         raise E.DimensionError(f"x has {x.shape[0]} rows, reflector expects {h.n}")
-    if is_complex(x):   # a real reflector acts on the real and imaginary parts separately
+    cplx = h._h.cplx
+    if is_complex(x) and not cplx:   # a real reflector acts on the real and imaginary parts separately
         re = apply_reflector(h, x.real.contiguous() if was_torch else np.ascontiguousarray(x.real), adjoint)
         im = apply_reflector(h, x.imag.contiguous() if was_torch else np.ascontiguousarray(x.imag), adjoint)
         return D.torch().complex(re, im) if was_torch else re + 1j * im
     dev = h._h.dev
     ctx = D.ctx(dev)
-    X = D.to_device(x, dev)
+    todev, mk = (D.cto_device, D.cempty) if cplx else (D.to_device, D.empty)
+    fn = lib().ots_apply_reflector_c128 if cplx else lib().ots_apply_reflector_f64
+    X = todev(x, dev)
     m = X.cols
-    Y = D.empty(h.n, m, dev)
-    for c0 in range(0, m, 64):
+    Y = mk(h.n, m, dev)
+    esz = 16 if cplx else 8
+    for c0 in range(0, m, 64):      # 64 columns per call; column views, no copies
         c1 = min(m, c0 + 64)
-        Xc = D.to_device(X.view()[:, c0:c1], dev)
-        Yc = D.empty(h.n, c1 - c0, dev)
-        check(lib().ots_apply_reflector_f64(ctx, h._h.ptr, c1 - c0, Xc.ptr, Xc.ld, Yc.ptr, Yc.ld,
-                                            int(bool(adjoint)), D.stream_ptr(dev)), ctx)
-        Y.buf[:, c0:c1].copy_(Yc.view())
+        xp = C.c_void_p(X.buf.data_ptr() + c0 * esz)
+        yp = C.c_void_p(Y.buf.data_ptr() + c0 * esz)
+        check(fn(ctx, h._h.ptr, c1 - c0, xp, X.ld, yp, Y.ld, int(bool(adjoint)), D.stream_ptr(dev)), ctx)
     return Y.view() if was_torch else Y.numpy()
 
 
@@ -188,7 +202,8 @@ def reflector_diagnostics(h):
     import ctypes as C
     ctx = D.ctx(h._h.dev)
     d = (C.c_double * 2)()
-    check(lib().ots_reflector_diagnostics_f64(ctx, h._h.ptr, d, D.stream_ptr(h._h.dev)), ctx)
+    fn = lib().ots_reflector_diagnostics_c128 if h._h.cplx else lib().ots_reflector_diagnostics_f64
+    check(fn(ctx, h._h.ptr, d, D.stream_ptr(h._h.dev)), ctx)
     return ReflectorDiagnostics(float(d[0]), float(d[1]))
 
 

@@ -163,17 +163,16 @@ def _two_stage_wide(v, a, choice, intra, p, was_torch):
     t = D.torch()
     n, k0 = v.shape
     k = a.shape[1]
-    if is_complex(v) or is_complex(a):
-        raise NotImplementedError("complex two_stage_qr with k > 64 needs the complex reflector object")
+    dt = t.complex128 if (is_complex(v) or is_complex(a)) else t.float64
     dev = D.pick_device(v, a)
-    vd = (v if D.is_torch(v) else t.from_numpy(v)).to(device=f"cuda:{dev}", dtype=t.float64).contiguous()
-    ad = (a if D.is_torch(a) else t.from_numpy(a)).to(device=f"cuda:{dev}", dtype=t.float64)
+    vd = (v if D.is_torch(v) else t.from_numpy(v)).to(device=f"cuda:{dev}", dtype=dt).contiguous()
+    ad = (a if D.is_torch(a) else t.from_numpy(a)).to(device=f"cuda:{dev}", dtype=dt)
     h = build_reflector(vd, choice, p)
     ah = apply_reflector(h, ad, adjoint=True)
-    pm = h.p if D.is_torch(h.p) else t.from_numpy(np.ascontiguousarray(h.p)).to(f"cuda:{dev}")
+    pm = (h.p if D.is_torch(h.p) else t.from_numpy(np.ascontiguousarray(h.p))).to(device=f"cuda:{dev}", dtype=dt)
     s = gram(pm, ah[:k0])                                   # P^* (H^* A)_top  (twostage.py:92)
     qr = intra_qr(ah[k0:].contiguous(), intra)
-    lifted = t.zeros((n, k), dtype=t.float64, device=f"cuda:{dev}")
+    lifted = t.zeros((n, k), dtype=dt, device=f"cuda:{dev}")
     lifted[k0:] = qr.q
     q = apply_reflector(h, lifted)
     diag = reflector_diagnostics(h)

@@ -138,6 +138,25 @@ def main():
             wt_inv_norm=res.diagnostics.wt_inv_norm)
     put("table4", v=v, a=a)
 
+    # --- complex reflector objects (reflector.py:156-247)
+    v = R.gen_random_orthonormal(300, 9, 61, "complex")
+    x = nm(rng(62), 300, 5, "complex")
+    b = nm(rng(63), 9, 4, "complex")
+    put("zrefl", v=v, x=x, b=b)
+    for ch in ("mlu", "qr", "polar"):
+        h = R.build_reflector(v, ch)
+        d = R.reflector_diagnostics(h)
+        put(f"zrefl/{ch}", p=h.p, t=h.t_solver.reconstruct(), w=h.w, hx=R.apply_reflector(h, x),
+            hhx=R.apply_reflector(h, x, adjoint=True), sol=h.t_solver.solve(b),
+            sola=h.t_solver.solve(b, adjoint=True), kappa_t=d.kappa_t, wt_inv_norm=d.wt_inv_norm)
+
+    # --- wide complex two_stage (k > 64)
+    v = R.gen_random_orthonormal(700, 20, 71, "complex")
+    a = nm(rng(72), 700, 80, "complex")
+    res = R.two_stage_qr(v, a)
+    put("zwide", v=v, a=a, q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
+        wt_inv_norm=res.diagnostics.wt_inv_norm)
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 

@@ -323,3 +323,29 @@ def test_table4_shape_golden(g2, choice):
     assert rel_e(res.s, g("s")) < 1e-10
     assert abs(res.diagnostics.kappa_t - float(g("kappa_t"))) < 1e-10 * float(g("kappa_t"))
     assert abs(res.diagnostics.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
+
+
+# ----------------------------------------------------------------- complex reflector objects
+@pytest.mark.parametrize("choice", ["mlu", "qr", "polar"])
+def test_complex_reflector_golden(g2, choice):
+    v, x, b = g2["zrefl/v"], g2["zrefl/x"], g2["zrefl/b"]
+    g = lambda key: g2[f"zrefl/{choice}/{key}"]
+    h = P.build_reflector(v, choice)
+    assert rel_e(h.p, g("p")) < 1e-10
+    assert rel_e(h.t_solver.reconstruct(), g("t")) < 1e-10
+    assert rel_e(h.w, g("w")) < 1e-10
+    assert rel_e(P.apply_reflector(h, x), g("hx")) < 1e-10
+    assert rel_e(P.apply_reflector(h, x, adjoint=True), g("hhx")) < 1e-10
+    assert rel_e(h.t_solver.solve(b), g("sol")) < 1e-10
+    assert rel_e(h.t_solver.solve(b, adjoint=True), g("sola")) < 1e-10
+    d = P.reflector_diagnostics(h)
+    assert abs(d.kappa_t - float(g("kappa_t"))) < 1e-10 * float(g("kappa_t"))
+    assert abs(d.wt_inv_norm - float(g("wt_inv_norm"))) < 1e-10 * float(g("wt_inv_norm"))
+
+
+def test_complex_wide_two_stage_golden(g2):
+    res = P.two_stage_qr(g2["zwide/v"], g2["zwide/a"])
+    assert rel_e(res.q, g2["zwide/q"]) < 1e-10
+    assert rel_e(res.r, g2["zwide/r"]) < 1e-10
+    assert rel_e(res.s, g2["zwide/s"]) < 1e-10
+    assert abs(res.diagnostics.kappa_t - float(g2["zwide/kappa_t"])) < 1e-10 * float(g2["zwide/kappa_t"])
