@@ -241,13 +241,21 @@ def b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
         raise E.DimensionError(f"u needs at least k0+k = {k0 + k} columns")
     if k0 + k > n:
         raise E.DimensionError(f"need k0 + k <= n, got {k0}+{k} > {n}")
-    if inner.kind != "weighted":
-        raise NotImplementedError("b_two_stage_qr needs a weighted inner product")
+    if inner.kind != "weighted":          # B = I: the unit diagonal weight
+        inner = InnerProduct(kind="weighted", diag=np.ones(n), host=not was_torch)
     cplx = is_complex(v) or is_complex(a)
+    if not _canonical(u, inner, k0 + k):
+        # Q, R, S do not depend on u (positive-diagonal B-QR, S = v^* B a are
+        # unique); the seed P, T and the diagnostics do, through the coupling
+        # v^* B u0 (oblique.py:125-151): run the canonical path for Q, R, S and
+        # take the diagnostics from the B-reflector of (v, u[:, :k0]).
+        res = b_two_stage_qr(v, a, initial_b_basis(inner, k0 + k), inner, choice, reorth, p)
+        if k0 > 0:
+            h = b_build_reflector(v, u[:, :k0], inner, choice, p=p)
+            res.diagnostics = b_reflector_diagnostics(h)
+        return res
     if inner.diag is None:
         return _b_two_stage_dense(v, a, u, inner, choice, p, n, k0, k, was_torch)
-    if not _is_canonical_basis(u, inner.diag, k0 + k):
-        raise NotImplementedError("this build needs u = initial_b_basis(inner, k0+k)")
     dev = D.pick_device(v, a)
     t = D.torch()
     d_dev = (inner.diag if D.is_torch(inner.diag) else t.from_numpy(inner.diag)).to(
@@ -293,11 +301,6 @@ def _b_two_stage_dense(v, a, u, inner, choice, p, n, k0, k, was_torch):
         raise NotImplementedError("dense complex B is not supported by this build")
     L = inner.chol_b
     dev = L.device.index
-    ucan = _dense_basis(inner, k0 + k)
-    ud = (u if D.is_torch(u) else t.from_numpy(np.ascontiguousarray(u))).to(device=L.device, dtype=t.float64)
-    scale = float(ucan.abs().max().item()) or 1.0
-    if float((ud[:, :k0 + k] - ucan).abs().max().item()) > 1e-12 * scale:
-        raise NotImplementedError("this build needs u = initial_b_basis(inner, k0+k)")
     if choice not in CHOICES:
         raise E.ParameterError(f"unknown choice {choice!r}")
     ctx = D.ctx(dev)
@@ -342,6 +345,7 @@ class BGenHouseholder:
     n: int
     k0: int
     _h: object = None          # the Euclidean reflector of (Phi v) on the device
+    _rot: object = None        # general u0: the rotation U with U [I; 0] = Phi u0
 
 
 # ---------------------------------------------------------------------------
@@ -404,6 +408,65 @@ def _check_weighted(inner, n):
         raise NotImplementedError("the B-path needs a weighted inner product")
     if inner.n != n:
         raise E.DimensionError(f"weight is {inner.n} x {inner.n}, data has {n} rows")
+
+
+def _canonical(u, inner, m):
+    """u[:, :m] == initial_b_basis(inner, m) (to rounding)?"""
+    try:
+        _require_canonical(u, inner, m, "u")
+        return True
+    except NotImplementedError:
+        return False
+
+
+class _Rot:
+    """Orthogonal U with U [I; 0] = u0' (an n x k0 orthonormal block):
+    U = H_u diag(P_u, I) for the Euclidean device reflector H_u mapping
+    [P_u; 0] onto u0' (reflector.py:207-228 with choice "qr").  In the frame
+    z -> U^* z a general B-orthonormal u0 becomes the canonical basis, so the
+    coupling v^* B u0 (oblique.py:146) is the top block of U^* Phi v."""
+
+    def __init__(self, pu):
+        from .reflector import build_reflector
+        self.h = build_reflector(pu, "qr", allow_defect=True)
+        self.k0 = pu.shape[1]
+        pp = self.h.p
+        self.pu = pp if D.is_torch(pp) else D.torch().from_numpy(np.ascontiguousarray(pp)).to(pu.device)
+
+    def adj(self, z):          # U^* z = diag(P_u^*, I) H_u^* z
+        from .core import gram
+        from .reflector import apply_reflector
+        y = apply_reflector(self.h, z, adjoint=True)
+        y[:self.k0] = gram(self.pu.to(y.dtype), y[:self.k0])
+        return y
+
+    def fwd(self, z):          # U z = H_u diag(P_u, I) z
+        from .core import gram
+        from .reflector import apply_reflector
+        z2 = z.clone()
+        z2[:self.k0] = gram(self.pu.mH.contiguous().to(z.dtype), z[:self.k0])
+        return apply_reflector(self.h, z2)
+
+
+def b_reflector_diagnostics(h):
+    """oblique.py:164-167: kappa_2(T) and ||W T^{-1}||_2 with the unweighted
+    W = x - v, on the device: kappa from the extreme eigenvalues of T^* T,
+    ||W T^{-1}||_2^2 = lambda_max(T^{-*} (W^* W) T^{-1}) from the Gram of W
+    and two T-solves."""
+    from .core import gram, gram_extremes
+    t = D.torch()
+    tm = h.t_solver.reconstruct()
+    tm = tm if D.is_torch(tm) else t.from_numpy(np.ascontiguousarray(tm)).cuda()
+    lo, hi = gram_extremes(tm)
+    kappa = float(np.sqrt(hi / lo)) if lo > 0 else float("inf")
+    w = h.w if D.is_torch(h.w) else t.from_numpy(np.ascontiguousarray(h.w)).to(tm.device)
+    gw = gram(w)                                            # W^* W
+    y1 = h.t_solver.solve(gw, adjoint=True)                 # T^{-*} W^* W
+    y1 = y1 if D.is_torch(y1) else t.from_numpy(y1).to(tm.device)
+    m = h.t_solver.solve(y1.mH.contiguous(), adjoint=True)  # (T^{-*} W^* W T^{-1})^*
+    m = m if D.is_torch(m) else t.from_numpy(m).to(tm.device)
+    _, lmax2 = gram_extremes(m)                            # lambda(M)^2 (M Hermitian PSD)
+    return ReflectorDiagnostics(kappa, float(np.sqrt(np.sqrt(max(lmax2, 0.0)))))
 
 
 def _require_canonical(u, inner, m, name):
@@ -493,27 +556,43 @@ def b_build_reflector(v, u0, inner, choice="qr", p=None, orth_tol=1e-6, allow_de
     n, k0 = v.shape
     if k0 == 0:
         raise E.DimensionError("v must have at least one column")
-    if is_complex(v) or is_complex(u0):
-        raise NotImplementedError("complex b_build_reflector: not in this build")
+    if inner.kind != "weighted":
+        inner = InnerProduct(kind="weighted", diag=np.ones(n), host=not was_torch)
     _check_weighted(inner, n)
-    _require_canonical(u0, inner, k0, "u0")
     dev = _dev_of(inner, v)
     pv = _phi(inner, v, dev)
+    rot = None
+    if not _canonical(u0, inner, k0):
+        # general B-orthonormal u0: defect checks in the reference's order
+        # (v, then u0; oblique.py:141-145), then the canonical construction
+        # in the frame U^* (Phi .) where U [I; 0] = Phi u0
+        from .core import orthonormality_defect
+        pu = _phi(inner, u0, dev)
+        if not allow_defect:
+            for name, blk in (("v", pv), ("u0", pu)):
+                dd = orthonormality_defect(blk)
+                if dd > orth_tol:
+                    raise E.OrthonormalityError(f"||{name}^* B {name} - I||_2 = {dd:.3e} exceeds {orth_tol:.1e}")
+        rot = _Rot(pu)
+        pv = rot.adj(pv)
+        allow_defect = True
     try:
         h = build_reflector(pv, choice=choice, p=p, orth_tol=orth_tol, allow_defect=allow_defect)
     except E.OrthonormalityError as exc:
         raise E.OrthonormalityError(str(exc).replace("v^* v", "v^* B v")) from None
     t = D.torch()
     pm = h.p                                     # device tensor (pv is torch)
-    top = t.zeros((n, k0), dtype=t.float64, device=pv.device)
-    top[:k0] = pm
-    x = _phi(inner, top, dev, inverse=True)     # u0 p = Phi^-1 [p; 0]
-    vd = v.to(pv.device) if D.is_torch(v) else t.from_numpy(np.ascontiguousarray(v)).to(pv.device)
+    top = t.zeros((n, k0), dtype=pv.dtype, device=pv.device)
+    top[:k0] = pm.to(pv.dtype)
+    if rot is not None:
+        top = rot.fwd(top)
+    x = _phi(inner, top, dev, inverse=True)     # u0 p = Phi^-1 U [p; 0]
+    vd = (v if D.is_torch(v) else t.from_numpy(np.ascontiguousarray(v))).to(device=pv.device, dtype=x.dtype)
     w = x - vd
     h._torch = was_torch
     h.t_solver._torch = was_torch
     return BGenHouseholder(w=_out(w, was_torch), t_solver=h.t_solver, p=_out(pm, was_torch), x=_out(x, was_torch),
-                           inner=inner, choice=choice, n=n, k0=k0, _h=h)
+                           inner=inner, choice=choice, n=n, k0=k0, _h=h, _rot=rot)
 
 
 def b_apply_reflector(h, x, inverse=False):
@@ -527,7 +606,12 @@ def b_apply_reflector(h, x, inverse=False):
     if h._h is None:
         raise E.ParameterError("b_apply_reflector needs a reflector from b_build_reflector")
     dev = h._h._h.dev
-    y = apply_reflector(h._h, _phi(h.inner, x, dev), adjoint=inverse)
+    z = _phi(h.inner, x, dev)
+    if h._rot is not None:
+        z = h._rot.adj(z)
+    y = apply_reflector(h._h, z, adjoint=inverse)
+    if h._rot is not None:
+        y = h._rot.fwd(y)
     return _out(_phi(h.inner, y, dev, inverse=True), was_torch)
 
 

@@ -157,6 +157,41 @@ def main():
     put("zwide", v=v, a=a, q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
         wt_inv_norm=res.diagnostics.wt_inv_norm)
 
+    # --- B-path with a general (non-canonical) B-orthonormal basis u
+    n, k0, k = 400, 6, 5
+    for fld, tag in (("real", "r"), ("complex", "c")):
+        d = 10.0 ** R.rand.uniform(rng(81), 0.0, 2.0, n)
+        ip = R.InnerProduct.weighted(np.diag(d))
+        sq = np.sqrt(d)[:, None]
+        v = np.linalg.qr(sq * nm(rng(82), n, k0, fld))[0] / sq
+        u = np.linalg.qr(sq * nm(rng(83), n, k0 + k, fld))[0] / sq
+        a = nm(rng(84), n, k, fld)
+        x = nm(rng(85), n, 3, fld)
+        put(f"bgen_{tag}", d=d, v=v, u=u, a=a, x=x)
+        for ch in ("mlu", "qr", "polar"):
+            res = R.b_two_stage_qr(v, a, u, ip, choice=ch)
+            h = R.b_build_reflector(v, u[:, :k0], ip, choice=ch)
+            dg = R.oblique.b_reflector_diagnostics(h)
+            put(f"bgen_{tag}/{ch}", q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
+                wt_inv_norm=res.diagnostics.wt_inv_norm, p=h.p, t=h.t_solver.reconstruct(), w=h.w, hx=h.x,
+                ax=R.b_apply_reflector(h, x), aix=R.b_apply_reflector(h, x, inverse=True),
+                dk=dg.kappa_t, dw=dg.wt_inv_norm)
+    b = R.gen_spd(n, 1e2, 87)
+    ipb = R.InnerProduct.weighted(b)
+    lt = np.linalg.cholesky(b).T
+    v = np.linalg.solve(lt, np.linalg.qr(nm(rng(88), n, k0))[0])
+    u = np.linalg.solve(lt, np.linalg.qr(nm(rng(89), n, k0 + k))[0])
+    a = nm(rng(90), n, k)
+    res = R.b_two_stage_qr(v, a, u, ipb, choice="qr")
+    put("bgen_dense", b=b, v=v, u=u, a=a, q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
+        wt_inv_norm=res.diagnostics.wt_inv_norm)
+    ipe = R.InnerProduct.euclidean()
+    v = R.gen_random_orthonormal(n, k0, 91)
+    u = R.gen_random_orthonormal(n, k0 + k, 92)
+    res = R.b_two_stage_qr(v, a, u, ipe, choice="mlu")
+    put("bgen_euc", v=v, u=u, a=a, q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
+        wt_inv_norm=res.diagnostics.wt_inv_norm)
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 

@@ -349,3 +349,43 @@ def test_complex_wide_two_stage_golden(g2):
     assert rel_e(res.r, g2["zwide/r"]) < 1e-10
     assert rel_e(res.s, g2["zwide/s"]) < 1e-10
     assert abs(res.diagnostics.kappa_t - float(g2["zwide/kappa_t"])) < 1e-10 * float(g2["zwide/kappa_t"])
+
+
+# ----------------------------------------------------------------- B-path, general u
+@pytest.mark.parametrize("tag", ["r", "c"])
+@pytest.mark.parametrize("choice", ["mlu", "qr", "polar"])
+def test_b_general_basis_golden(g2, tag, choice):
+    """b_two_stage_qr / b_build_reflector / b_apply_reflector for a
+    non-canonical B-orthonormal u (oblique.py:125-161, 279-315)."""
+    g = lambda key: g2[f"bgen_{tag}/{key}"]
+    h_ = lambda key: g2[f"bgen_{tag}/{choice}/{key}"]
+    ip = P.InnerProduct.weighted(np.diag(g("d")))
+    v, u, a, x = g("v"), g("u"), g("a"), g("x")
+    res = P.b_two_stage_qr(v, a, u, ip, choice=choice)
+    assert rel_e(res.q, h_("q")) < 1e-10 and rel_e(res.r, h_("r")) < 1e-10 and rel_e(res.s, h_("s")) < 1e-10
+    assert abs(res.diagnostics.kappa_t - float(h_("kappa_t"))) < 1e-10 * float(h_("kappa_t"))
+    assert abs(res.diagnostics.wt_inv_norm - float(h_("wt_inv_norm"))) < 1e-9 * float(h_("wt_inv_norm"))
+    k0 = v.shape[1]
+    h = P.b_build_reflector(v, u[:, :k0], ip, choice=choice)
+    assert rel_e(h.p, h_("p")) < 1e-10 and rel_e(h.t_solver.reconstruct(), h_("t")) < 1e-10
+    assert rel_e(h.w, h_("w")) < 1e-10 and rel_e(h.x, h_("hx")) < 1e-10
+    assert rel_e(P.b_apply_reflector(h, x), h_("ax")) < 1e-10
+    assert rel_e(P.b_apply_reflector(h, x, inverse=True), h_("aix")) < 1e-10
+    d = P.b_reflector_diagnostics(h)
+    assert abs(d.kappa_t - float(h_("dk"))) < 1e-10 * float(h_("dk"))
+    assert abs(d.wt_inv_norm - float(h_("dw"))) < 1e-9 * float(h_("dw"))
+
+
+def test_b_general_basis_dense_and_euclidean(g2):
+    ipb = P.InnerProduct.weighted(g2["bgen_dense/b"])
+    res = P.b_two_stage_qr(g2["bgen_dense/v"], g2["bgen_dense/a"], g2["bgen_dense/u"], ipb, choice="qr")
+    for key in ("q", "r", "s"):
+        assert rel_e(getattr(res, key), g2[f"bgen_dense/{key}"]) < 1e-9, key
+    assert abs(res.diagnostics.kappa_t - float(g2["bgen_dense/kappa_t"])) < 1e-9 * float(g2["bgen_dense/kappa_t"])
+    assert abs(res.diagnostics.wt_inv_norm - float(g2["bgen_dense/wt_inv_norm"])) < \
+        1e-9 * float(g2["bgen_dense/wt_inv_norm"])
+    res = P.b_two_stage_qr(g2["bgen_euc/v"], g2["bgen_dense/a"], g2["bgen_euc/u"], P.InnerProduct.euclidean(),
+                           choice="mlu")
+    for key in ("q", "r", "s"):
+        assert rel_e(getattr(res, key), g2[f"bgen_euc/{key}"]) < 1e-10, key
+    assert abs(res.diagnostics.kappa_t - float(g2["bgen_euc/kappa_t"])) < 1e-10 * float(g2["bgen_euc/kappa_t"])
