@@ -78,6 +78,18 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
                       double* Q, int64_t ldq, double* R, int64_t ldr,
                       double* S, int64_t lds, double* diag_host, void* stream);
 
+/* two_stage_qr with the Gram V^T V supplied by the caller (device, k0 x k0,
+ * ld ldg, full symmetric): the defect check, seed and diagnostics use it and
+ * only V_b^T A_b streams over V.  For the Alg. 3 / Krylov driver
+ * (twostage.py:100-151), which assembles the Gram of its growing basis
+ * block by block (block_householder_qr(..., incremental_gram=True)). */
+int ots_two_stage_gram_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k,
+                           const double* V, int64_t ldv, const double* A, int64_t lda,
+                           int choice, int intra, const double* P, int64_t ldp,
+                           double orth_tol, int allow_defect, const double* gram, int64_t ldg,
+                           double* Q, int64_t ldq, double* R, int64_t ldr,
+                           double* S, int64_t lds, double* diag_host, void* stream);
+
 /* InnerProduct.weighted(b) for a dense SPD b      -- oblique.py:48-56
  * the reference's chol_b = cholesky(b) (core.py:87-105): lower L (strict
  * upper stored as zeros); OTS_E_NOT_PD when a pivot is not positive. */

@@ -98,6 +98,9 @@ def lib():
                 L.ots_reflector_diagnostics_c128.argtypes = L.ots_reflector_diagnostics_f64.argtypes
                 L.ots_reflector_tsolve_c128.argtypes = L.ots_reflector_tsolve_f64.argtypes
                 L.ots_reflector_get_c128.argtypes = L.ots_reflector_get_f64.argtypes
+                L.ots_two_stage_gram_f64.argtypes = [
+                    _vp, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _int, _int, _vp, _i64,
+                    _dbl, _int, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, C.POINTER(_dbl), _vp]
                 L.ots_debug_counters.argtypes = [C.POINTER(C.c_ulonglong), _int]
                 L.ots_modified_lu_f64.argtypes = [_vp, _i64, _vp, _i64, _vp, _vp, _vp]
                 L.ots_shifted_cholesky_qr_f64.argtypes = [
@@ -144,6 +147,7 @@ EXPORTED_SYMBOLS = [
     "ots_gram_extremes_f64", "ots_gram_extremes_c128", "ots_qr_signs_f64", "ots_qr_signs_c128",
     "ots_build_reflector_c128", "ots_zreflector_destroy", "ots_apply_reflector_c128",
     "ots_reflector_diagnostics_c128", "ots_reflector_tsolve_c128", "ots_reflector_get_c128",
+    "ots_two_stage_gram_f64",
     "ots_dense_cholesky_f64", "ots_dense_trsm_lt_f64", "ots_dense_trmm_lt_f64", "ots_b_two_stage_dense_f64",
 ]
 

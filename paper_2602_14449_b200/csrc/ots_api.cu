@@ -192,6 +192,7 @@ struct JobCfg {
   cudaStream_t st;
   bool distributed;
   int nsm_avail = 0;     // SMs the row-parallel phases may plan for (0: all)
+  const double* gram_in = nullptr; long ldgi = 0;   // caller's V^T V (incremental Gram), or null
 };
 
 }  // namespace
@@ -432,6 +433,25 @@ int phase_gram(ots_ctx* ctx, Job& j) {
   const JobCfg& c = j.c;
   const int k0 = (int)c.k0, k = (int)c.k;
   const int gnsm = j.gram_nsm > 0 ? j.gram_nsm : ctx->nsm;   // SMs the Gram kernels may use
+  if (c.gram_in) {
+    // V^T V supplied by the caller (assembled incrementally by the Alg. 3
+    // driver from earlier blocks): only V_b^T A_b streams over V here
+    CK(cudaMemcpy2DAsync(j.Gfull, (size_t)j.NTOT1 * 8, c.gram_in, (size_t)c.ldgi * 8, (size_t)k0 * 8, k0,
+                         cudaMemcpyDeviceToDevice, c.st));
+    for (int a0 = 0; a0 < k0; a0 += 128) {
+      const int aw = std::min(128, k0 - a0), PWa = pad32(aw);
+      TnArgs a{};
+      a.P = c.V; a.ldp = c.ldv; a.pc0 = a0; a.pcols = aw;
+      a.B = c.A; a.ldb = c.lda; a.bc0 = 0; a.bcols = k;
+      a.row_begin = 0; a.row_end = c.n_local; a.b_row_begin = j.qrow0; a.p_row_begin = 0;
+      a.partial = j.partial;
+      const int grid = grid_for_tn(PWa, j.BWa, false, false, gnsm);
+      CK(launch_tsgemm_tn(a, PWa, j.BWa, false, false, grid, c.st));
+      CK(launch_reduce_strided(j.partial, grid, aw, k, j.BWa, j.Gfull + (long)a0 * j.NTOT1 + j.PW, j.NTOT1, 1.0,
+                               c.st));
+    }
+    return OTS_OK;
+  }
   if (k0 <= 128) {
     TnArgs a{};
     a.P = c.V; a.ldp = c.ldv; a.pc0 = 0; a.pcols = k0;
@@ -909,6 +929,15 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
                       const double* A, int64_t lda, int choice, int intra, const double* P, int64_t ldp,
                       double orth_tol, int allow_defect, double* Q, int64_t ldq, double* R, int64_t ldr,
                       double* S, int64_t lds, double* diag_host, void* stream) {
+  return ots_two_stage_gram_f64(ctx, n, k0, k, V, ldv, A, lda, choice, intra, P, ldp, orth_tol, allow_defect,
+                                nullptr, 0, Q, ldq, R, ldr, S, lds, diag_host, stream);
+}
+
+int ots_two_stage_gram_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const double* V, int64_t ldv,
+                           const double* A, int64_t lda, int choice, int intra, const double* P, int64_t ldp,
+                           double orth_tol, int allow_defect, const double* gram, int64_t ldg, double* Q,
+                           int64_t ldq, double* R, int64_t ldr, double* S, int64_t lds, double* diag_host,
+                           void* stream) {
   if (!ctx) return OTS_E_VALUE;
   cudaSetDevice(ctx->device);
   (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
@@ -936,6 +965,7 @@ int ots_two_stage_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const doub
     return rc;
   }
   JobCfg c{n, 0, k0, k, V, ldv, A, lda, Q, ldq, choice, P, ldp, orth_tol, allow_defect, st, false};
+  c.gram_in = gram; c.ldgi = ldg;
   return two_stage_pipeline(ctx, c, intra, Q, ldq, R, ldr, S, lds, diag_host, nullptr);
 }
 

@@ -320,6 +320,157 @@ __device__ void blk_org2r_cm(double* A, int lda, int m, int n, const double* tau
   }
 }
 
+// ---------------------------------------------------------------------------
+// Blocked Householder QR / Q formation of a square n x n column-major matrix
+// in global memory (k0 x k0 seeds too large for shared memory, k0 > ~158):
+// QNB-column panels factored by the unblocked sweep above, compact-WY T per
+// panel (dlarft, forward), and the trailing columns updated a - V T^T V^T a
+// (geqrf) / a - V T V^T a (orgqr, backward) one column per warp with the
+// panel's V staged in shared memory -- one pass over the trailing matrix per
+// panel instead of one per column.  Same reflectors (v, tau) as the
+// unblocked sweep, so R and Q match it to rounding.
+// ---------------------------------------------------------------------------
+constexpr int QNB = 32;
+
+// lane l ends with the warp-wide sum of v[l] (31 shuffles)
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[QNB]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) {
+    const bool up = (lane & s) != 0;
+#pragma unroll
+    for (int i = 0; i < s; ++i) {
+      const double send = up ? v[i] : v[i + s];
+      const double keep = up ? v[i + s] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, s);
+    }
+  }
+  return v[0];
+}
+
+// Vs (QNB x mp, column-major in smem, unit lower, zero columns >= nb) <- panel
+__device__ void qr_stage_panel(const double* A, int lda, int j0, int nb, int mp, double* Vs) {
+  BLK_FOR(e, QNB * mp) {
+    const int i = e / mp, r = e - i * mp;
+    Vs[e] = (i >= nb || r < i) ? 0.0 : (r == i ? 1.0 : A[(long)(j0 + i) * lda + j0 + r]);
+  }
+}
+
+// a <- a - V M (V^T a) for the trailing columns c in [c0, n) (rows j0..n),
+// M = T^T (geqrf) or T (orgqr); one warp per column.
+__device__ void qr_trailing(double* A, int lda, int j0, int mp, int c0, int n, const double* Vs, const double* Ts,
+                            bool transT, double* Wbuf) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* w2 = Wbuf + warp * QNB;
+  for (int c = c0 + warp; c < n; c += nw) {
+    double* Ac = A + (long)c * lda + j0;
+    double acc[QNB];
+#pragma unroll
+    for (int i = 0; i < QNB; ++i) acc[i] = 0.0;
+    for (int r = lane; r < mp; r += 32) {
+      const double a = Ac[r];
+#pragma unroll
+      for (int i = 0; i < QNB; ++i) acc[i] = fma(Vs[i * mp + r], a, acc[i]);
+    }
+    const double wl = warp_reduce_scatter32(acc);            // (V^T a)_lane
+    double m = 0.0;                                          // (M w)_lane
+#pragma unroll
+    for (int i = 0; i < QNB; ++i) {
+      const double wi = __shfl_sync(0xffffffffu, wl, i);
+      m = fma(transT ? Ts[i * QNB + lane] : Ts[lane * QNB + i], wi, m);
+    }
+    w2[lane] = m;
+    __syncwarp();
+    for (int r = lane; r < mp; r += 32) {
+      double a = Ac[r];
+#pragma unroll
+      for (int i = 0; i < QNB; ++i) a = fma(-Vs[i * mp + r], w2[i], a);
+      Ac[r] = a;
+    }
+    __syncwarp();
+  }
+}
+
+// T (QNB x QNB upper, zero beyond nb) of the staged panel: G = V^T V, then
+// T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]  (dlarft forward)
+__device__ void qr_panel_t(const double* Vs, int mp, int nb, const double* tau, double* Gs, double* Ts) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int j = warp; j < QNB; j += nw) {
+    double acc[QNB];
+#pragma unroll
+    for (int i = 0; i < QNB; ++i) acc[i] = 0.0;
+    for (int r = lane; r < mp; r += 32) {
+      const double vj = Vs[j * mp + r];
+#pragma unroll
+      for (int i = 0; i < QNB; ++i) acc[i] = fma(Vs[i * mp + r], vj, acc[i]);
+    }
+    Gs[lane * QNB + j] = warp_reduce_scatter32(acc);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int i = threadIdx.x;
+    for (int e = 0; e < QNB; ++e) Ts[i * QNB + e] = 0.0;
+    __syncwarp();
+    for (int j = 0; j < nb; ++j) {
+      double sacc = 0.0;
+      if (i < j)
+        for (int l = i; l < j; ++l) sacc = fma(Ts[i * QNB + l], Gs[l * QNB + j], sacc);
+      __syncwarp();
+      if (i < j) Ts[i * QNB + j] = -tau[j] * sacc;
+      if (i == j) Ts[j * QNB + j] = tau[j];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+}
+
+// geqrf: A (n x n column-major) -> reflectors below the diagonal, R on and
+// above, tau[n]; the panels' T kept in Tg (n/QNB+1 blocks of QNB x QNB).
+// sm: >= QNB*n + 2*QNB*QNB + 16*QNB doubles of shared memory.
+__device__ void blk_geqrf_cm(double* A, int lda, int n, double* tau, double* Tg, double* red, double* sm) {
+  double* Vs = sm;
+  double* Ts = sm + QNB * n;
+  double* Gs = Ts + QNB * QNB;
+  double* Wb = Gs + QNB * QNB;
+  for (int j0 = 0; j0 < n; j0 += QNB) {
+    const int nb = min(QNB, n - j0), mp = n - j0;
+    blk_geqr2_cm(A + (long)j0 * lda + j0, lda, mp, nb, tau + j0, red);
+    __syncthreads();
+    qr_stage_panel(A, lda, j0, nb, mp, Vs);
+    __syncthreads();
+    qr_panel_t(Vs, mp, nb, tau + j0, Gs, Ts);
+    BLK_FOR(e, QNB * QNB) Tg[(j0 / QNB) * QNB * QNB + e] = Ts[e];
+    if (j0 + nb < n) qr_trailing(A, lda, j0, mp, j0 + nb, n, Vs, Ts, true, Wb);
+    __syncthreads();
+  }
+}
+
+// orgqr: Q (n x n) in place from the reflectors of blk_geqrf_cm (R entries
+// above the diagonal are overwritten), backward over the panels.
+__device__ void blk_orgqr_cm(double* A, int lda, int n, const double* tau, const double* Tg, double* red,
+                             double* sm) {
+  double* Vs = sm;
+  double* Ts = sm + QNB * n;
+  double* Wb = Ts + 2 * QNB * QNB;
+  const int last = ((n - 1) / QNB) * QNB;
+  for (int j0 = last; j0 >= 0; j0 -= QNB) {
+    const int nb = min(QNB, n - j0), mp = n - j0;
+    qr_stage_panel(A, lda, j0, nb, mp, Vs);
+    BLK_FOR(e, QNB * QNB) Ts[e] = Tg[(j0 / QNB) * QNB * QNB + e];
+    // trailing Q columns: rows j0 .. j0+nb-1 are zero before H_p is applied
+    const int nt = n - j0 - nb;
+    BLK_FOR(e, nb * nt) { const int c = j0 + nb + e / nb, r = j0 + e % nb; A[(long)c * lda + r] = 0.0; }
+    __syncthreads();
+    if (nt > 0) qr_trailing(A, lda, j0, mp, j0 + nb, n, Vs, Ts, false, Wb);
+    __syncthreads();
+    // panel columns: rows above the panel are zero, then the unblocked dorg2r
+    BLK_FOR(e, j0 * nb) { const int c = j0 + e / j0, r = e % j0; A[(long)c * lda + r] = 0.0; }
+    __syncthreads();
+    blk_org2r_cm(A + (long)j0 * lda + j0, lda, mp, nb, tau + j0, red);
+    __syncthreads();
+  }
+}
+
 // Modified LU (reflector.py:53-77 / paper Alg. 2) in place:
 // Z -> L (strict lower, unit diag implied) and U (upper), p[n].
 // signrec=true applies the LAPACK-sign-recovery variant: a pivot
@@ -889,10 +1040,10 @@ __device__ int seed_build(SmallState& s, double* red, int* ired) {
       } else {                                    // global memory: column-major (coalesced)
         BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[j * ld + i] = s.Vt[i * ld + j]; }
         __syncthreads();
-        blk_geqr2_cm(s.X1, ld, n, n, s.tau, red);
+        blk_geqrf_cm(s.X1, ld, n, s.tau, s.Z2, red, dsm);      // panel T's in Z2 (free during the seed)
         BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? s.X1[j * ld + i] : 0.0; }
         __syncthreads();
-        blk_org2r_cm(s.X1, ld, n, n, s.tau, red);  // Q1, column-major
+        blk_orgqr_cm(s.X1, ld, n, s.tau, s.Z2, red, dsm);       // Q1, column-major
         BLK_FOR(e, n * n) {                        // -> row-major in place
           int i = e / n, j = e - i * n;
           if (i < j) { const double a = s.X1[i * ld + j]; s.X1[i * ld + j] = s.X1[j * ld + i]; s.X1[j * ld + i] = a; }

@@ -74,10 +74,19 @@ def _defect_then(v, exc, orth_tol=1e-8):
     raise exc
 
 
-def _run_two_stage(dev, V, A, Q, R, S, choice, intra, P, cplx):
-    """One C-ABI call on device matrices (DMat); returns the diagnostics."""
+def _run_two_stage(dev, V, A, Q, R, S, choice, intra, P, cplx, gram=None):
+    """One C-ABI call on device matrices (DMat); returns the diagnostics.
+    gram: optional device tensor holding V^T V (real only)."""
     ctx = D.ctx(dev)
     diag = (C.c_double * 3)()
+    if gram is not None:
+        rc = lib().ots_two_stage_gram_f64(
+            ctx, A.rows, V.cols, A.cols, V.ptr, V.ld, A.ptr, A.ld, CHOICES[choice],
+            INTRA[intra], P.ptr if P is not None else None, P.ld if P is not None else 0,
+            1e-8, 0, C.c_void_p(gram.data_ptr()), gram.stride(0), Q.ptr, Q.ld, R.ptr, R.ld, S.ptr, S.ld, diag,
+            D.stream_ptr(dev))
+        check(rc, ctx)
+        return ReflectorDiagnostics(float(diag[0]), float(diag[1]))
     fn = lib().ots_two_stage_c128 if cplx else lib().ots_two_stage_f64
     rc = fn(
         ctx, A.rows, V.cols, A.cols, V.ptr, V.ld, A.ptr, A.ld, CHOICES[choice],
@@ -182,13 +191,95 @@ def _two_stage_wide(v, a, choice, intra, p, was_torch):
     return TwoStageResult(q.cpu().numpy(), r.cpu().numpy() if D.is_torch(r) else r, s.cpu().numpy(), diag)
 
 
-def block_householder_qr(blocks, choice="qr", intra="householder"):
+class KrylovBasis:
+    """Device-resident growing orthonormal basis [Q_0 ... Q_i] -- the state of
+    the Alg. 3 / block-Krylov driver (twostage.py:100-151, BASELINE configs[4]).
+    One preallocated n x capacity buffer: `append(a)` orthogonalises the
+    block a against the current basis with Algorithm 1, reading V as a
+    column view of the buffer and writing Q straight into the next columns
+    (no per-block concatenation, ref :132); it returns the block's (q, r, s,
+    diagnostics).  incremental_gram (real data): the Gram of the basis is
+    kept on the device and extended per block by [Q_acc, Q_i]^T Q_i (one pass
+    with k_i output columns) instead of the full V^T V in every call; the
+    orthonormality check, seed and diagnostics read it (V does not change
+    between blocks, so the values agree up to rounding)."""
+
+    def __init__(self, n, capacity, dtype="float64", device=None, choice="qr", intra="householder",
+                 incremental_gram=False):
+        t = D.torch()
+        self.cplx = str(dtype).endswith("complex128")
+        self.dt = t.complex128 if self.cplx else t.float64
+        self.dev = D.pick_device() if device is None else int(device)
+        self.n, self.cap, self.m = n, capacity, 0
+        self.choice, self.intra = choice, intra
+        self.ldb = max(2, capacity + (capacity & 1))
+        self.buf = t.empty((max(n, 1), self.ldb), dtype=self.dt, device=f"cuda:{self.dev}")
+        self.inc = incremental_gram and not self.cplx
+        self.G = t.zeros((capacity, capacity + (capacity & 1)), dtype=t.float64,
+                         device=f"cuda:{self.dev}") if self.inc else None
+
+    @property
+    def q(self):
+        return self.buf[:, :self.m] if self.n else self.buf[:0, :self.m]
+
+    def _grow_gram(self, m, ki):
+        from .core import gram as _gram
+        if not self.inc:
+            return
+        if m == 0:
+            self.G[:ki, :ki] = _gram(self.buf[:, :ki])
+            return
+        cross = _gram(self.buf[:, :m + ki], self.buf[:, m:m + ki])       # [Q_acc, Q_i]^T Q_i
+        self.G[:m + ki, m:m + ki] = cross
+        self.G[m:m + ki, :m] = cross[:m].T
+
+    def append(self, a):
+        t = D.torch()
+        a = a if D.is_torch(a) else t.from_numpy(np.ascontiguousarray(a))
+        a = a.to(device=f"cuda:{self.dev}", dtype=self.dt)
+        ki, m = a.shape[1], self.m
+        if a.shape[0] != self.n:
+            raise E.DimensionError("all blocks must have the same row count")
+        if m + ki > self.cap:
+            raise E.DimensionError(f"basis capacity {self.cap} exceeded")
+        if m == 0:
+            qr = intra_qr(a, self.intra)
+            self.buf[:, :ki] = qr.q
+            self.m = ki
+            self._grow_gram(0, ki)
+            z = t.zeros((0, ki), dtype=self.dt, device=a.device)
+            return TwoStageResult(self.buf[:, :ki], qr.r, z, ReflectorDiagnostics(1.0, 0.0))
+        if ki == 0:
+            z = t.zeros((0, 0), dtype=self.dt, device=a.device)
+            return TwoStageResult(self.buf[:, m:m], z, t.zeros((m, 0), dtype=self.dt, device=a.device),
+                                  ReflectorDiagnostics(1.0, 0.0))
+        todev = D.cto_device if self.cplx else D.to_device
+        V = D.DMat(self.buf, m, ld=self.ldb)         # column view [Q_0 ... Q_{i-1}]
+        A = todev(a, self.dev)
+        direct = (m % 2 == 0) or self.cplx           # Q view 16-byte aligned
+        if direct:
+            Q = D.DMat(self.buf[:, m:], ki, ld=self.ldb)
+        else:
+            Q = (D.cempty if self.cplx else D.empty)(self.n, ki, self.dev)
+        if self.cplx:
+            R, S = D.czeros(ki, ki, self.dev), D.cempty(m, ki, self.dev)
+        else:
+            R, S = D.zeros(ki, ki, self.dev), D.empty(m, ki, self.dev)
+        diag = _run_two_stage(self.dev, V, A, Q, R, S, self.choice, self.intra, None, self.cplx,
+                              gram=self.G[:m, :m] if self.inc else None)
+        if not direct:
+            self.buf[:, m:m + ki] = Q.view()
+        self.m = m + ki
+        self._grow_gram(m, ki)
+        return TwoStageResult(self.buf[:, m:m + ki], R.view(), S.view(), diag)
+
+
+def block_householder_qr(blocks, choice="qr", intra="householder", incremental_gram=False):
     """Algorithm 3 driver (twostage.py:100-151): block 0 by the intra QR,
-    block i >= 1 by Algorithm 1 against the accumulated Q.  The basis lives
-    in ONE preallocated device buffer (n x sum k_i): block i reads its V as a
-    column view of that buffer and writes its Q straight into the next
-    columns (no per-block concatenation, ref :132).  numpy blocks are moved to
-    the device once and the results copied back at the end."""
+    block i >= 1 by Algorithm 1 against the accumulated Q, on a
+    device-resident `KrylovBasis` (see there; incremental_gram is its
+    extension).  numpy blocks are moved to the device once and the results
+    copied back at the end."""
     if not blocks:
         raise E.ParameterError("need at least one block")
     was_torch = any(D.is_torch(b) for b in blocks)
@@ -203,49 +294,24 @@ def block_householder_qr(blocks, choice="qr", intra="householder"):
     cplx = any(is_complex(b) for b in blocks)       # ref :117 np.result_type(*blocks)
     t = D.torch()
     dev = D.pick_device(*blocks)
-    dt = t.complex128 if cplx else t.float64
-    todev = D.cto_device if cplx else D.to_device
-    ldb = max(2, total + (total & 1))
-    buf = t.empty((max(n, 1), ldb), dtype=dt, device=f"cuda:{dev}")
-    r_full = t.zeros((total, total), dtype=dt, device=f"cuda:{dev}")
-    b0 = blocks[0] if D.is_torch(blocks[0]) else t.from_numpy(blocks[0])
-    try:
-        qr0 = intra_qr(b0.to(device=f"cuda:{dev}", dtype=dt), intra)
-    except E.IntraFailure as exc:
-        exc.block = 0
-        raise
-    buf[:, :sizes[0]] = qr0.q
-    r_full[:sizes[0], :sizes[0]] = qr0.r
+    kb = KrylovBasis(n, total, "complex128" if cplx else "float64", dev, choice, intra, incremental_gram)
+    r_full = t.zeros((total, total), dtype=kb.dt, device=f"cuda:{dev}")
     worst = ReflectorDiagnostics(1.0, 0.0)
-    offset = sizes[0]
-    for i in range(1, len(blocks)):
-        ki, m = sizes[i], offset
-        if ki == 0:
-            continue
-        V = D.DMat(buf, m, ld=ldb)        # column view [Q_0 ... Q_{i-1}]
-        A = todev(blocks[i], dev)
-        direct = (m % 2 == 0) or cplx      # Q view 16-byte aligned
-        if direct:
-            Q = D.DMat(buf[:, m:], ki, ld=ldb)
-        else:
-            Q = D.cempty(n, ki, dev) if cplx else D.empty(n, ki, dev)
-        if cplx:
-            R, S = D.czeros(ki, ki, dev), D.cempty(m, ki, dev)
-        else:
-            R, S = D.zeros(ki, ki, dev), D.empty(m, ki, dev)
+    offset = 0
+    for i, blk in enumerate(blocks):
+        ki = sizes[i]
         try:
-            diag = _run_two_stage(dev, V, A, Q, R, S, choice, intra, None, cplx)
+            res = kb.append(blk)
         except E.IntraFailure as exc:
             exc.block = i
             raise
-        if not direct:
-            buf[:, m:m + ki] = Q.view()
-        r_full[:m, offset:offset + ki] = S.view()
-        r_full[offset:offset + ki, offset:offset + ki] = R.view()
-        if diag.kappa_t > worst.kappa_t:
-            worst = diag
+        if offset:
+            r_full[:offset, offset:offset + ki] = res.s
+        r_full[offset:offset + ki, offset:offset + ki] = res.r
+        if i and res.diagnostics.kappa_t > worst.kappa_t:
+            worst = res.diagnostics
         offset += ki
-    q = buf[:, :total] if n else buf[:0, :total]
+    q = kb.q
     if was_torch:
         return BlockQRResult(q, r_full, sizes, worst)
     return BlockQRResult(q.cpu().numpy(), r_full.cpu().numpy(), sizes, worst)

@@ -389,3 +389,41 @@ def test_b_general_basis_dense_and_euclidean(g2):
     for key in ("q", "r", "s"):
         assert rel_e(getattr(res, key), g2[f"bgen_euc/{key}"]) < 1e-10, key
     assert abs(res.diagnostics.kappa_t - float(g2["bgen_euc/kappa_t"])) < 1e-10 * float(g2["bgen_euc/kappa_t"])
+
+
+def test_krylov_basis_incremental_gram():
+    """KrylovBasis / block_householder_qr(incremental_gram=True): same Q, R as
+    the oracle's Alg. 3 (the Gram of the basis is assembled per block)."""
+    rng = W.make_rng(78)
+    sizes = [32, 32, 16, 32, 64]
+    blocks = [W.normal_matrix(rng, 1 << 15, s) for s in sizes]
+    rq, rr = O.block_qr(blocks, "qr")
+    res = P.block_householder_qr(blocks, incremental_gram=True)
+    assert rel_e(res.q, rq) < 1e-10 and rel_e(res.r, rr) < 1e-10
+    import torch
+    kb = P.KrylovBasis(1 << 15, 200, device=0, incremental_gram=True)
+    for b in blocks:
+        kb.append(torch.from_numpy(b).cuda())
+    assert rel_e(kb.q.cpu().numpy(), rq) < 1e-10
+    g = kb.G[:176, :176].cpu().numpy()
+    q = kb.q.cpu().numpy()
+    assert np.abs(g - q.T @ q).max() < 1e-13
+    with pytest.raises(P.OrthonormalityError):    # the assembled Gram still guards the check
+        kb.G[3, 3] += 1e-6
+        kb.append(torch.from_numpy(blocks[0][:, :8]).cuda())
+
+
+@pytest.mark.parametrize("k0,choice", [(192, "qr"), (256, "qr"), (448, "qr"), (320, "mlu"), (256, "polar")])
+def test_large_k0_seed_vs_oracle(k0, choice):
+    """k0 > 158: the k0 x k0 seed in global memory (blocked Householder QR /
+    Q formation for the 'qr' choice) -- Q, R, S and the diagnostics vs the
+    oracle."""
+    n, k = 1 << 15, 32
+    rng = W.make_rng(500 + k0)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    a = W.normal_matrix(rng, n, k)
+    ref = O.two_stage(v, a, choice)
+    res = P.two_stage_qr(v, a, choice=choice)
+    assert rel_e(res.q, ref["q"]) < 1e-10 and rel_e(res.r, ref["r"]) < 1e-10 and rel_e(res.s, ref["s"]) < 1e-10
+    assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
+    assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
