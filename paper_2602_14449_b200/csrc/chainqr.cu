@@ -731,29 +731,29 @@ static_assert(2 * FusedCfg<64>::CH <= BlkCfg<64>::XS && 2 * FusedCfg<32>::CH <= 
               "fused V / Z1 chunks must fit the Xs region");
 
 template <int KT>
-__device__ __forceinline__ void fused_chunk_load(double* buf, const FactorArgs& a, long gr0, long rhi, int c,
-                                                 int tid) {
+__device__ __forceinline__ void fused_chunk_load(double* buf, const FusedArgs& a, int ncols, long gr0, long rhi,
+                                                 int c, int tid) {
   using F = FusedCfg<KT>;
   load_tile_async(buf, F::VC, a.Vb, a.ldv, gr0, BlkCfg<KT>::B, gr0, rhi, c * F::VC, F::VC, a.kdim, tid, 256);
-  load_tile_async(buf + F::VCH, KT, a.Z1, a.ldz, (long)c * F::VC, F::VC, 0, a.kdim, 0, KT, a.ncols, tid, 256);
+  load_tile_async(buf + F::VCH, KT, a.Z1, a.ldz, (long)c * F::VC, F::VC, 0, a.kdim, 0, KT, ncols, tid, 256);
   cp_async_commit();
 }
 
 template <int KT>
-__device__ __forceinline__ void fused_x(double (&x)[16][2], const FactorArgs& a, long gr0, int nb, double* Vs,
-                                        bool owner, int mycol) {
+__device__ __forceinline__ void fused_x(double (&x)[16][2], const FusedArgs& a, int ncols, long gr0, int nb,
+                                        double* Vs, bool owner, int mycol) {
   using F = FusedCfg<KT>;
   constexpr int VC = F::VC;
   const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int nch = (a.kdim + VC - 1) / VC;
   const long rhi = gr0 + nb;
-  fused_chunk_load<KT>(Vs, a, gr0, rhi, 0, tid);
-  if (owner) tile_regs_load(x, a.Ab, a.lda, gr0, nb, mycol, a.ncols);
+  fused_chunk_load<KT>(Vs, a, ncols, gr0, rhi, 0, tid);
+  if (owner) tile_regs_load(x, a.Ab, a.lda, gr0, nb, mycol, ncols);
   const int wc = mycol - g;                                  // warp's first column (8 w)
   for (int c = 0; c < nch; ++c) {
     cp_async_wait<0>();
     __syncthreads();                                         // chunk c landed; buffer (c+1)&1 free
-    if (c + 1 < nch) fused_chunk_load<KT>(Vs + ((c + 1) & 1) * F::CH, a, gr0, rhi, c + 1, tid);
+    if (c + 1 < nch) fused_chunk_load<KT>(Vs + ((c + 1) & 1) * F::CH, a, ncols, gr0, rhi, c + 1, tid);
     if (owner) {
       const double* Vc = Vs + (c & 1) * F::CH;
       const double* Zc = Vc + F::VCH;
@@ -785,20 +785,160 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   double* Tbase = a.U + (long)chain * (a.G.L + 1) * KT * KT;
   const int b = a.G.b;
 
-  const bool fused = a.Vb != nullptr;
+  // ---- head: plain QR of rows [r0, r0+KT) (unblocked smem sweep, once per chain)
+  load_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  if (a.head_tri) {
+    // Tree levels: the head is an R factor (exact zeros below the diagonal),
+    // so every dlarfg sees |x| = 0: tau = 0, beta = alpha (LAPACK's shortcut),
+    // R = head, Y = 0, T = 0 -- the unblocked sweep would compute exactly that.
+    for (int e = tid; e < KT * KT; e += 256) Tbase[e] = 0.0;
+  } else {
+    householder_sweep<KT, true, KT>(S, 0, Xs, tau_s);   // U -> Xs (ld KT+1)
+    store_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
+    __syncthreads();
+    u_to_t_block<KT>(Xs, Xs + KT * (KT + 1), Tbase);
+    __syncthreads();
+  }
+
+  // ---- structured tiles (register-resident, see BlkCfg)
   const bool owner = warp < NP;
   const int mycol = 8 * warp + ((tid & 31) >> 2);
+  double* Ys = Xs;                                  // NSLOT panel slots of Y
   double x[16][2];
-  // ---- head: plain QR of rows [r0, r0+KT) (unblocked smem sweep, once per chain)
-  if (fused) {
-    const long remh = a.G.nrows - r0;
-    fused_x<KT>(x, a, r0, (int)(remh < KT ? remh : KT), Xs, owner, mycol);
+  if (owner && ntiles > 0) {
+    const long g0 = r0 + KT;
+    const long rem0 = a.G.nrows - g0;
+    tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
+  }
+  for (int t = 1; t <= ntiles; ++t) {
+    double* Tpc = Tp + (t & 1) * NP * 64;           // this tile's T_pp
+    const double* Tpp = Tp + ((t - 1) & 1) * NP * 64;   // previous tile's (its T is built now)
+    const long gr0 = r0 + KT + (long)(t - 1) * b;
+    const long rem = a.G.nrows - gr0;
+    const int nb = (int)(rem < b ? rem : b);
+    TSTAMP(t1);
+    if (t < ntiles) {   // next tile -> L2 while this one is factored (its load is on the chain)
+      const long g1 = gr0 + b;
+      const long rem1 = a.G.nrows - g1;
+      const int nb1 = (int)(rem1 < b ? rem1 : b);
+      const int lpr = (a.ncols * 8 + 127) / 128;          // 128-byte lines per row
+      for (int i = tid; i < nb1 * lpr; i += 256) {
+        const int r = i / lpr, l = i - r * lpr;
+        const double* ptr = a.D + (g1 + r) * a.ldd + l * 16;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+      }
+    }
+    // The owner of the next panel (p+1) shares its SM sub-partition with warp
+    // (p+1)^4; that warp defers its DMMA apply of panel p by one iteration so
+    // the latency-bound panel factorisation does not queue behind its DMMAs
+    // on the shared FP64 pipe.  A 3-slot Y ring keeps Y_p alive for it.
+    int pending = -1;
+    for (int p = 0; p < NP; ++p) {
+#ifdef OTS_TIMING
+      long long q0 = clock64();
+#endif
+      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tpc, tau_s, scr + warp * 64,
+                                      Xs + C::NSLOT * C::YSLOT + warp * 64);
+      else if (t > 1 && warp < p) t_block<KT>(warp, p, S, Tpp, Tw, scr + warp * 64);
+#ifdef OTS_TIMING
+      if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
+#endif
+      __syncthreads();
+#ifdef OTS_TIMING
+      long long q1 = clock64();
+#endif
+      if (owner && warp != p) {
+        const int defer_w = (p + 1 < NP) ? ((p + 1) ^ 4) : -1;
+        if (pending >= 0) {
+          panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tpc);
+          pending = -1;
+        }
+        if (warp == defer_w) pending = p;
+        else panel_apply<KT>(p, warp, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tpc);
+      }
+#ifdef OTS_TIMING
+      if (warp == p + 1 && (tid & 31) == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - q1));
+      if (tid == 0) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - q0));
+#endif
+    }
+    if (pending >= 0) panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tpc);
+    __syncthreads();
+    TSTAMP(t2);
+    TACC(1, t1, t2);
+    // Y (in place of the tile) -> global; next tile -> registers
     if (owner) {
+      tile_regs_store(x, a.D, a.ldd, gr0, nb, mycol, a.ncols);
+      if (t < ntiles) {
+        const long g1 = gr0 + b;
+        const long rem1 = a.G.nrows - g1;
+        tile_regs_load(x, a.D, a.ldd, g1, (int)(rem1 < b ? rem1 : b), mycol, a.ncols);
+      }
+    }
+    TSTAMP(t3);
+    TACC(2, t2, t3);
+    if (t > 1) {                    // previous tile's T is complete (phase NP-1 ran in panel NP-1)
+      t_store<KT>(Tpp, Tw, Tbase + (long)(t - 1) * KT * KT);
+      __syncthreads();              // Tpp is this parity's buffer for tile t+1
+    }
+    TSTAMP(t4);
+    TACC(3, t3, t4);
+    if (threadIdx.x == 0) TACC(4, 0, 1);
+  }
+  if (ntiles > 0) {                 // last tile: its T phases in sequence
+    const double* Tpl = Tp + (ntiles & 1) * NP * 64;
+    for (int p = 1; p < NP; ++p) {
+      if (warp < p) t_block<KT>(warp, p, S, Tpl, Tw, scr + warp * 64);
+      __syncthreads();
+    }
+    t_store<KT>(Tpl, Tw, Tbase + (long)ntiles * KT * KT);
+  }
+
+  // ---- chain R (upper triangle, exact zeros below)
+  double* R = a.Rout + (long)chain * KT * KT;
+  for (int i = tid; i < KT * KT; i += 256) {
+    int r = i / KT, cc = i - r * KT;
+    R[i] = (cc >= r) ? S[r * KT + cc] : 0.0;
+  }
+}
+
+// The fused variant (OTS_FUSE=1, see DESIGN 6b): the unfused kernel above is
+// kept verbatim -- any change to its code or argument record moves ptxas's
+// register allocation of the panel loop (measured +1 ms).
+template <int KT>
+__global__ void __launch_bounds__(256, 2) chain_factor_fused_kernel(FactorArgs a, FusedArgs fz) {
+  constexpr bool FUSED = true;
+  using C = BlkCfg<KT>;
+  constexpr int NP = C::NP;
+  extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
+  double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
+  double* Tp = Xs + C::XS;                        // 2 x NP x 64: panel T_pp, by tile parity
+  double* scr = Tp + 2 * NP * 64;                 // 8 warps x 64
+  double* Tw = Xs + C::TWOFF;                     // packed off-diagonal T blocks (previous tile)
+  __shared__ double tau_s[KT];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int chain = blockIdx.x;
+  const long r0 = (long)chain * a.G.rpc;
+  const int ntiles = chain_real_tiles(a.G, chain, KT);
+  double* Tbase = a.U + (long)chain * (a.G.L + 1) * KT * KT;
+  const int b = a.G.b;
+
+  constexpr bool fused = FUSED;      // compile-time: the unfused kernel carries no fused code
+  // ---- head: plain QR of rows [r0, r0+KT) (unblocked smem sweep, once per chain)
+  if constexpr (FUSED) {
+    double xh[16][2];
+    const bool own = warp < NP;
+    const int col = 8 * warp + ((tid & 31) >> 2);
+    const long remh = a.G.nrows - r0;
+    fused_x<KT>(xh, fz, a.ncols, r0, (int)(remh < KT ? remh : KT), Xs, own, col);
+    if (own) {
       const int t4 = tid & 3;
 #pragma unroll
       for (int f = 0; f < KT / 8; ++f)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) S[(8 * f + 2 * t4 + h) * KT + mycol] = x[f][h];
+        for (int h = 0; h < 2; ++h) S[(8 * f + 2 * t4 + h) * KT + col] = xh[f][h];
     }
   } else {
     load_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
@@ -820,15 +960,20 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   }
 
   // ---- structured tiles (register-resident, see BlkCfg)
+  const bool owner = warp < NP;
+  const int mycol = 8 * warp + ((tid & 31) >> 2);
   double* Ys = Xs;                                  // NSLOT panel slots of Y
-  if (ntiles > 0) {
+  double x[16][2];
+  if constexpr (FUSED) {
+    if (ntiles > 0) {
+      const long g0 = r0 + KT;
+      const long rem0 = a.G.nrows - g0;
+      fused_x<KT>(x, fz, a.ncols, g0, (int)(rem0 < b ? rem0 : b), Xs, owner, mycol);
+    }
+  } else if (owner && ntiles > 0) {
     const long g0 = r0 + KT;
     const long rem0 = a.G.nrows - g0;
-    if (fused) {
-      fused_x<KT>(x, a, g0, (int)(rem0 < b ? rem0 : b), Xs, owner, mycol);
-    } else if (owner) {
-      tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
-    }
+    tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
   }
   for (int t = 1; t <= ntiles; ++t) {
     double* Tpc = Tp + (t & 1) * NP * 64;           // this tile's T_pp
@@ -842,18 +987,18 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
       const long rem1 = a.G.nrows - g1;
       const int nb1 = (int)(rem1 < b ? rem1 : b);
       const int lpr = (a.ncols * 8 + 127) / 128;          // 128-byte lines per row
-      const double* src = fused ? a.Ab : a.D;
-      const long lds_ = fused ? a.lda : a.ldd;
+      const double* src = fused ? fz.Ab : a.D;
+      const long lds_ = fused ? fz.lda : a.ldd;
       for (int i = tid; i < nb1 * lpr; i += 256) {
         const int r = i / lpr, l = i - r * lpr;
         const double* ptr = src + (g1 + r) * lds_ + l * 16;
         asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
       }
       if (fused) {     // and the tile's V_b rows
-        const int lpv = (a.kdim * 8 + 127) / 128;
+        const int lpv = (fz.kdim * 8 + 127) / 128;
         for (int i = tid; i < nb1 * lpv; i += 256) {
           const int r = i / lpv, l = i - r * lpv;
-          const double* ptr = a.Vb + (g1 + r) * a.ldv + l * 16;
+          const double* ptr = fz.Vb + (g1 + r) * fz.ldv + l * 16;
           asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
         }
       }
@@ -914,7 +1059,7 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
       const long g1 = gr0 + b;
       const long rem1 = a.G.nrows - g1;
       TSTAMP(f0);
-      fused_x<KT>(x, a, g1, (int)(rem1 < b ? rem1 : b), Xs, owner, mycol);
+      fused_x<KT>(x, fz, a.ncols, g1, (int)(rem1 < b ? rem1 : b), Xs, owner, mycol);
       TSTAMP(f1);
       TACC(13, f0, f1);
     }
@@ -1113,19 +1258,25 @@ __global__ void __launch_bounds__(256, 2) chain_qform_kernel(QformArgs a) {
 
 // ---------------------------------------------------------------------------
 template <int KT>
-static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st) {
+static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st, const FusedArgs* fz) {
   using C = BlkCfg<KT>;
   if (a.G.b > C::B || a.G.nchains <= 0) return cudaErrorInvalidValue;
-  auto k = chain_factor_kernel<KT>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  k<<<a.G.nchains, 256, C::SMEM, st>>>(a);
+  if (fz && fz->Vb) {
+    auto k = chain_factor_fused_kernel<KT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    k<<<a.G.nchains, 256, C::SMEM, st>>>(a, *fz);
+  } else {
+    auto k = chain_factor_kernel<KT>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    k<<<a.G.nchains, 256, C::SMEM, st>>>(a);
+  }
   return cudaGetLastError();
 }
 
-cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st) {
-  if (KT == 16) return factor_t<16>(a, st);
-  if (KT == 32) return factor_t<32>(a, st);
-  if (KT == 64) return factor_t<64>(a, st);
+cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st, const FusedArgs* fz) {
+  if (KT == 16) return factor_t<16>(a, st, fz);
+  if (KT == 32) return factor_t<32>(a, st, fz);
+  if (KT == 64) return factor_t<64>(a, st, fz);
   return cudaErrorInvalidValue;
 }
 

@@ -39,12 +39,16 @@ struct FactorArgs {
   ChainGeom G;
   double* U;             // per tile KT*KT, tile id = chain*(L+1) + t
   double* Rout;          // stacked chain R's: chain*KT rows, ld KT
-  int head_tri = 0;      // input rows are stacked upper-triangular R's (tree levels)
-  // Fused inter-block update (level 0 only; Vb == nullptr: D already holds X).
-  // The kernel forms each tile of X = A_b + V_b Z1 (twostage.py:91-93,
-  // reflector.py:238) on the fly -- A_b and V_b rows of the tile, Z1 k0 x k --
-  // instead of reading an X written by a separate apply kernel; Y still goes
-  // to D (same row numbering as X).
+  int head_tri;          // input rows are stacked upper-triangular R's (tree levels)
+};
+
+// Fused inter-block update for the chain factor's level 0 (opt-in): the
+// kernel forms each tile of X = A_b + V_b Z1 (twostage.py:91-93,
+// reflector.py:238) on the fly -- A_b and V_b rows of the tile, Z1 k0 x k --
+// instead of reading an X written by a separate apply kernel; Y still goes to
+// FactorArgs::D (same row numbering as X).  A separate record: a larger
+// FactorArgs alone costs the unfused kernel register spills.
+struct FusedArgs {
   const double* Vb = nullptr; long ldv = 0; int kdim = 0;
   const double* Z1 = nullptr; long ldz = 0;
   const double* Ab = nullptr; long lda = 0;
@@ -63,7 +67,7 @@ cudaError_t launch_reduce(const double* partial, int nparts, long count, double*
 cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, int cols, int ldp, double* out,
                                   long ldo, double alpha, cudaStream_t st);
 cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
-cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
+cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st, const FusedArgs* fz = nullptr);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
 // complex128 TSQR (zchain.cu): same argument records, pointers to interleaved
 // (re, im) data, leading dimensions in complex units

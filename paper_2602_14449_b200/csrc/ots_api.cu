@@ -302,23 +302,19 @@ int ensure_ws(ots_ctx* ctx, size_t bytes) {
 // fuse0 (optional): level 0 forms X = A_b + V_b Z1 tile by tile inside the
 // factor (FactorArgs fused fields) instead of reading an X in L.D.
 int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st, bool tri_first = false,
-                      const FactorArgs* fuse0 = nullptr) {
+                      const FusedArgs* fuse0 = nullptr) {
   for (size_t l = 0; l < lv.size(); ++l) {
     Level& L = lv[l];
     FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, (l > 0 || tri_first) ? 1 : 0};
-    if (l == 0 && fuse0) {
-      fa.Vb = fuse0->Vb; fa.ldv = fuse0->ldv; fa.kdim = fuse0->kdim;
-      fa.Z1 = fuse0->Z1; fa.ldz = fuse0->ldz; fa.Ab = fuse0->Ab; fa.lda = fuse0->lda;
-    }
-    CK(launch_chain_factor(fa, KT, st));
+    CK(launch_chain_factor(fa, KT, st, l == 0 ? fuse0 : nullptr));
   }
   return OTS_OK;
 }
 
 // level-0 fused-update arguments of a job (X rows start at V/A row qrow0)
-FactorArgs fused_args(const Job& j) {
+FusedArgs fused_args(const Job& j) {
   const JobCfg& c = j.c;
-  FactorArgs f{};
+  FusedArgs f{};
   f.Vb = c.V + (long)j.qrow0 * c.ldv; f.ldv = c.ldv; f.kdim = (int)c.k0;
   f.Z1 = j.s.Z1; f.ldz = j.ld;
   f.Ab = c.A + (long)j.qrow0 * c.lda; f.lda = c.lda;
@@ -770,7 +766,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // chain for the FP64 pipe, so it is off by default.
   static const bool want_fuse = getenv("OTS_FUSE") != nullptr && getenv("OTS_FUSE")[0] == '1';
   const bool fuse = want_fuse && (intra == OTS_INTRA_HOUSEHOLDER) && c.k0 > 0;
-  const FactorArgs fa0 = fused_args(j);
+  const FusedArgs fa0 = fused_args(j);
   if (diag_side) {
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
     CK(launch_diag(j.s, ctx->side));

@@ -228,7 +228,19 @@ def _is_canonical_basis(u, d, m):
 
 
 def b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
-    """Algorithm 4 (oblique.py:279-315) for M = diag(d) on the GPU."""
+    """Algorithm 4 (oblique.py:279-315) on the GPU (diagonal or dense B, any
+    B-orthonormal basis u); OrthonormalityError names the B-defect as the
+    reference's b_build_reflector does (oblique.py:141-145)."""
+    try:
+        return _b_two_stage_qr(v, a, u, inner, choice, reorth, p)
+    except E.OrthonormalityError as exc:
+        msg = str(exc)
+        if "B v" not in msg and "B u" not in msg:
+            msg = msg.replace("v^* v", "v^* B v")
+        raise E.OrthonormalityError(msg) from None
+
+
+def _b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
     was_torch = D.is_torch(v) or D.is_torch(a)
     v = as_matrix(v, "v")
     a = as_matrix(a, "a")
@@ -249,7 +261,7 @@ def b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
         # unique); the seed P, T and the diagnostics do, through the coupling
         # v^* B u0 (oblique.py:125-151): run the canonical path for Q, R, S and
         # take the diagnostics from the B-reflector of (v, u[:, :k0]).
-        res = b_two_stage_qr(v, a, initial_b_basis(inner, k0 + k), inner, choice, reorth, p)
+        res = _b_two_stage_qr(v, a, initial_b_basis(inner, k0 + k), inner, choice, reorth, p)
         if k0 > 0:
             h = b_build_reflector(v, u[:, :k0], inner, choice, p=p)
             res.diagnostics = b_reflector_diagnostics(h)

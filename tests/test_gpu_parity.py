@@ -17,11 +17,20 @@ pytestmark = pytest.mark.gpu
 U = 2.0 ** -53
 
 
-def rel(x, y):
+def rel(x, y, floor=1e-4):
+    """Elementwise relative difference with an absolute floor of
+    floor * max|y| for entries at the roundoff scale of the block."""
     x, y = np.asarray(x), np.asarray(y)
     if y.size == 0:
         return 0.0
-    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300))
+    scale = max(float(np.abs(y).max()), 1e-300)
+    return float((np.abs(x - y) / (np.abs(y) + floor * scale)).max())
+
+
+def nrel(x, y):
+    """normwise max|x - y| / max|y| (for residual checks)"""
+    x, y = np.asarray(x), np.asarray(y)
+    return float(np.abs(x - y).max() / max(np.abs(y).max(), 1e-300)) if y.size else 0.0
 
 
 def golden_cases(golden, prefix):
@@ -233,8 +242,9 @@ def test_binner_dense_errors():
     ip = P.InnerProduct.weighted(b)
     v = np.zeros((n, 2)); v[0, 0] = v[1, 1] = 1.0
     u = np.eye(n)[:, :5]                              # not the canonical basis of this B
-    with pytest.raises(NotImplementedError):
+    with pytest.raises(P.OrthonormalityError) as ei:  # v is not B-orthonormal (oblique.py:141-145)
         P.b_two_stage_qr(v, np.ones((n, 3)), u, ip)
+    assert "v^* B v" in str(ei.value)
 
 
 def test_binner_diag_vs_oracle_large():
@@ -278,21 +288,21 @@ def test_block_krylov_sweep_small():
         out[:-1] -= q[1:]
         return out
 
-    blocks_gpu = [a0]
     qs = [P.two_stage_qr(np.zeros((n, 0)), a0).q]
-    ref_qs = [O.two_stage(np.zeros((n, 0)), a0)["q"]]
+    assert rel(qs[0], O.two_stage(np.zeros((n, 0)), a0)["q"]) < 1e-10
     for i in range(steps):
         vq = np.hstack(qs)
         ai = lap(qs[-1])
         res = P.two_stage_qr(vq, ai)
+        # every step elementwise against the oracle on the same inputs (the
+        # sweep itself amplifies earlier roundoff through L, so the blocks of
+        # two independent sweeps are not compared)
+        rr = O.two_stage(vq, ai, diagnostics=False)
+        assert rel(res.q, rr["q"]) < 1e-10 and rel(res.r, rr["r"]) < 1e-10 and rel(res.s, rr["s"]) < 1e-10, i
         qs.append(res.q)
-        vr = np.hstack(ref_qs)
-        rr = O.two_stage(vr, lap(ref_qs[-1]), diagnostics=False)
-        ref_qs.append(rr["q"])
     Qg = np.hstack(qs)
     loss = np.abs(np.linalg.eigvalsh(Qg.T @ Qg) - 1).max()
     assert loss <= 10 * n * U
-    assert rel(Qg, np.hstack(ref_qs)) < 1e-8
 
 
 @pytest.mark.parametrize("ch", ["mlu", "qr", "polar"])
@@ -325,8 +335,8 @@ def test_apply_reflector_vs_oracle(ch):
     # t_solver.solve round trip
     b = W.normal_matrix(rng, k0, 5)
     tt = h.t_solver.reconstruct()
-    assert rel(tt @ h.t_solver.solve(b), b) < 1e-12
-    assert rel(tt.T @ h.t_solver.solve(b, adjoint=True), b) < 1e-12
+    assert nrel(tt @ h.t_solver.solve(b), b) < 1e-12
+    assert nrel(tt.T @ h.t_solver.solve(b, adjoint=True), b) < 1e-12
 
 
 def test_stream_front_end_matches_calls():
@@ -459,7 +469,7 @@ def test_b_block_householder_qr_vs_oracle(kind):
         off += sizes[i]
     assert rel(res.q, np.hstack(qs)) < 1e-10 and rel(res.r, rf) < 1e-10
     assert res.block_sizes == sizes
-    assert rel(res.q @ res.r, a) < 1e-12
+    assert nrel(res.q @ res.r, a) < 1e-12
     bad = [b.copy() for b in blocks]
     bad[0][:, 3] = 0.0
     with pytest.raises(P.IntraFailure) as ei:
