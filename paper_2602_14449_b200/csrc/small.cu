@@ -651,7 +651,11 @@ __device__ void blk_jacobi_rows_core(double* W, int ldw, double* Jt, int ldj, in
               W[p * ldw + e] = cs * x - sn * y;
               W[q * ldw + e] = sn * x + cs * y;
             }
+#ifndef OTS_JACOBI_NOJT
             if (Jt)
+#else
+            if (false)
+#endif
               for (int e = gl; e < n; e += gs) {
                 double x = Jt[p * ldj + e], y = Jt[q * ldj + e];
                 Jt[p * ldj + e] = cs * x - sn * y;
