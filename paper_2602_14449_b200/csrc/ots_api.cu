@@ -740,7 +740,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
     CK(launch_seed_split(j.s, 0, ctx->side));
     CK(cudaEventRecord(ctx->ev_seedA, ctx->side));
-    j.gram_nsm = ctx->nsm - 1;
+    j.gram_nsm = ctx->nsm - (seed_uses_cluster(j.s) ? 2 : 1);
     j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, j.gram_nsm);
   }
   if ((rc = phase_gram(ctx, j))) return rc;
@@ -1419,7 +1419,7 @@ int ots_dist_seed_early(ots_ctx* ctx, const double* top_rows) {
   CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
   CK(launch_seed_split(j.s, 0, ctx->side));
   CK(cudaEventRecord(ctx->ev_seedA, ctx->side));
-  j.gram_nsm = ctx->nsm - 1;
+  j.gram_nsm = ctx->nsm - (seed_uses_cluster(j.s) ? 2 : 1);
   j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, j.gram_nsm);
   j.seeded_early = true;
   return OTS_OK;

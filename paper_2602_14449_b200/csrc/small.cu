@@ -10,6 +10,7 @@
 // shared or global (L2-resident) memory (generic addressing).
 #include "common.cuh"
 #include "small.cuh"
+#include <cstdlib>
 
 namespace ots {
 
@@ -671,6 +672,9 @@ __device__ void blk_jacobi_rows_core(double* W, int ldw, double* Jt, int ldj, in
     __syncthreads();
     int any = rotated;
     __syncthreads();
+#ifdef OTS_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_dbg_small[15], 1ull);   // Jacobi sweeps
+#endif
     if (!any) break;
   }
   // row norms
@@ -897,6 +901,238 @@ __device__ void t_solve_core(const SmallState& s, const double* F, int ld, doubl
 }
 
 // ---------------------------------------------------------------------------
+// Polar seed on a 2-CTA cluster (k0 <= JC_NMAX): the one-sided Jacobi sweeps
+// rotate the rows of W = V_t^T in CTA 0's shared memory and send each round's
+// rotations (cs, sn per pair) through distributed shared memory to CTA 1,
+// which applies them to the accumulated J^T held in ITS shared memory -- so
+// neither matrix lives in global memory (the single-CTA version kept J^T in
+// global memory: 10.5 ms of long-scoreboard stalls at k0 = 128, and W and J^T
+// together exceed one CTA's 227 KB).  A ring of JC_NR rounds with
+// full (CTA 1) / empty (CTA 0) mbarriers lets CTA 0 run ahead.
+// ---------------------------------------------------------------------------
+constexpr int JC_NR = 4, JC_NMAX = 152, JC_PAIRS = (JC_NMAX + 2) / 2;   // 152 x jc_ls(152) <= SMALL_SMEM_DOUBLES
+struct JacobiLink {
+  double rot[JC_NR][2 * JC_PAIRS];
+  int cmd[JC_NR];                 // 0: apply round rd[slot]; 1: stop
+  int rd[JC_NR];
+  unsigned long long full[JC_NR];  // on CTA 1 (one remote arrival per round)
+  unsigned long long empty[JC_NR]; // on CTA 0 (one remote arrival per round)
+  int done;                        // CTA 0: stop already sent
+};
+__shared__ JacobiLink g_jlink;
+
+__device__ __forceinline__ unsigned cl_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ unsigned cl_size() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cl_map(const void* p, unsigned rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(p), r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cl_st_f64(uint32_t addr, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ void cl_st_s32(uint32_t addr, int v) {
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void cl_arrive_remote(uint32_t bar) {
+  asm volatile("fence.acq_rel.cluster;\n\tmbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void cl_wait(unsigned long long* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nJW_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra JW_%=;\n}\n" ::"r"(a), "r"(parity)
+      : "memory");
+}
+
+// both CTAs of a 2-CTA seed cluster, at kernel start
+__device__ void jacobi_link_init() {
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < JC_NR; ++i) {
+      mbar_init(&g_jlink.full[i], 1);
+      mbar_init(&g_jlink.empty[i], 1);
+    }
+    g_jlink.done = 0;
+    fence_mbar_init();
+  }
+  __syncthreads();
+  cl_sync();
+}
+
+// CTA 0: send the stop command (once) and meet CTA 1 at the closing cluster
+// barrier (after which CTA 1 has written J^T to global memory)
+__device__ void jacobi_link_close(long long rounds) {
+  __syncthreads();
+  if (g_jlink.done) return;           // closed already (uniform across the CTA)
+  const int slot = (int)(rounds % JC_NR);
+  if (rounds >= JC_NR) cl_wait(&g_jlink.empty[slot], (unsigned)(((rounds / JC_NR) - 1) & 1));
+  if (threadIdx.x == 0) {
+    cl_st_s32(cl_map(&g_jlink.cmd[slot], 1), 1);
+    cl_arrive_remote(cl_map(&g_jlink.full[slot], 1));
+  }
+  __syncthreads();
+  cl_sync();
+  if (threadIdx.x == 0) g_jlink.done = 1;
+  __syncthreads();
+}
+
+__device__ __forceinline__ double rcp_nr(double x) {     // 1/x: MUFU seed + 2 Newton steps
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  return r * fma(-x, r, 2.0);
+}
+__device__ __forceinline__ double rsqrt_nr(double x) {   // 1/sqrt(x): MUFU seed + 2 Newton steps
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-0.5 * x * r, r, 1.5);
+  return r * fma(-0.5 * x * r, r, 1.5);
+}
+// row stride of the staged W / J^T: = 8 (mod 16) doubles, so the 4 pairs of
+// a warp (consecutive rows) read disjoint bank halves (2 wavefronts)
+__device__ __forceinline__ int jc_ls(int n) { return ((n + 15) / 16) * 16 + 8; }
+
+// CTA 0 side of the Jacobi (W already in shared memory); returns the number
+// of rounds sent.  Same rotations and order as blk_jacobi_rows_core.
+__device__ long long blk_jacobi_rows_cluster(double* W, int ldw, int n, double* sigma, double* red) {
+  const int ne = (n + 1) & ~1;
+  const int npairs = ne / 2;
+  int gs = 1;
+  while (gs * 2 * npairs <= (int)blockDim.x && gs < 32) gs *= 2;
+  const int grp = threadIdx.x / gs, gl = threadIdx.x % gs;
+  const unsigned gmask = (gs == 32) ? 0xffffffffu : (((1u << gs) - 1u) << ((threadIdx.x & 31) & ~(gs - 1)));
+  const double tol = 4.0 * 2.220446049250313e-16 * (n > 4 ? n : 4);
+  __shared__ int rotated;
+  long long r = 0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    int my_rot = 0;
+    for (int rd = 0; rd < ne - 1; ++rd, ++r) {
+      const int slot = (int)(r % JC_NR);
+      if (r >= JC_NR) cl_wait(&g_jlink.empty[slot], (unsigned)(((r / JC_NR) - 1) & 1));
+      if (grp < npairs) {
+        int p, q;
+        if (grp == 0) { p = ne - 1; q = rd; }
+        else { p = (rd + grp) % (ne - 1); q = (rd - grp + (ne - 1)) % (ne - 1); }
+        double cs = 1.0, sn = 0.0;
+        if (p < n && q < n) {
+          double a = 0, b = 0, c = 0;
+          for (int e = gl; e < n; e += gs) {
+            double x = W[p * ldw + e], y = W[q * ldw + e];
+            a = fma(x, x, a); b = fma(y, y, b); c = fma(x, y, c);
+          }
+          for (int o = gs / 2; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(gmask, a, o);
+            b += __shfl_xor_sync(gmask, b, o);
+            c += __shfl_xor_sync(gmask, c, o);
+          }
+          // same test and rotation as blk_jacobi_rows_core, with the divisions
+          // and square roots as MUFU seeds + Newton steps (~1 ulp; the
+          // rotation stays orthogonal to rounding: sn = cs tt)
+          if (c != 0.0 && c * c > (tol * tol) * a * b) {
+            const double zeta = (b - a) * rcp_nr(2.0 * c);
+            double tt;
+            if (fabs(zeta) > 1e150) tt = 0.5 * rcp_nr(zeta);
+            else {
+              const double h = fma(zeta, zeta, 1.0);
+              const double rs = rsqrt_nr(h);
+              tt = copysign(rcp_nr(fabs(zeta) + h * rs), zeta);
+            }
+            cs = rsqrt_nr(fma(tt, tt, 1.0));
+            sn = cs * tt;
+            for (int e = gl; e < n; e += gs) {
+              double x = W[p * ldw + e], y = W[q * ldw + e];
+              W[p * ldw + e] = cs * x - sn * y;
+              W[q * ldw + e] = sn * x + cs * y;
+            }
+            my_rot = 1;
+          }
+        }
+        if (gl == 0) {
+          const uint32_t rot = cl_map(&g_jlink.rot[slot][2 * grp], 1);
+          cl_st_f64(rot, cs);
+          cl_st_f64(rot + 8, sn);
+        }
+      }
+      if (threadIdx.x == 0) {
+        cl_st_s32(cl_map(&g_jlink.cmd[slot], 1), 0);
+        cl_st_s32(cl_map(&g_jlink.rd[slot], 1), rd);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) cl_arrive_remote(cl_map(&g_jlink.full[slot], 1));
+    }
+    if (my_rot) rotated = 1;
+    __syncthreads();
+    int any = rotated;
+    __syncthreads();
+#ifdef OTS_TIMING
+    if (threadIdx.x == 0) atomicAdd(&g_dbg_small[15], 1ull);
+#endif
+    if (!any) break;
+  }
+  for (int i = 0; i < n; ++i) {
+    double sacc = 0.0;
+    for (int e = threadIdx.x; e < n; e += blockDim.x) { double x = W[i * ldw + e]; sacc = fma(x, x, sacc); }
+    sacc = block_sum(sacc, red);
+    if (threadIdx.x == 0) sigma[i] = sqrt(sacc);
+  }
+  __syncthreads();
+  return r;
+}
+
+// CTA 1: J^T (starting at I) in shared memory, rotated as CTA 0 dictates,
+// then written to Jt (global, ldj); ends at the closing cluster barrier.
+__device__ void jacobi_jt_helper(double* Jt, int ldj, int n) {
+  const int ls = jc_ls(n);
+  double* Js = dsm;
+  BLK_FOR(e, n * n) { const int i = e / n, j = e - i * n; Js[i * ls + j] = (i == j) ? 1.0 : 0.0; }
+  const int ne = (n + 1) & ~1;
+  const int npairs = ne / 2;
+  int gs = 1;
+  while (gs * 2 * npairs <= (int)blockDim.x && gs < 32) gs *= 2;
+  const int grp = threadIdx.x / gs, gl = threadIdx.x % gs;
+  __syncthreads();
+  for (long long r = 0;; ++r) {
+    const int slot = (int)(r % JC_NR);
+    cl_wait(&g_jlink.full[slot], (unsigned)((r / JC_NR) & 1));
+    if (g_jlink.cmd[slot] == 1) break;
+    const int rd = g_jlink.rd[slot];
+    if (grp < npairs) {
+      int p, q;
+      if (grp == 0) { p = ne - 1; q = rd; }
+      else { p = (rd + grp) % (ne - 1); q = (rd - grp + (ne - 1)) % (ne - 1); }
+      const double cs = g_jlink.rot[slot][2 * grp], sn = g_jlink.rot[slot][2 * grp + 1];
+      if (p < n && q < n && !(cs == 1.0 && sn == 0.0))
+        for (int e = gl; e < n; e += gs) {
+          const double x = Js[p * ls + e], y = Js[q * ls + e];
+          Js[p * ls + e] = cs * x - sn * y;
+          Js[q * ls + e] = sn * x + cs * y;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) cl_arrive_remote(cl_map(&g_jlink.empty[slot], 0));
+  }
+  __syncthreads();
+  BLK_FOR(e, n * n) { const int i = e / n, j = e - i * n; Jt[(long)i * ldj + j] = Js[i * ls + j]; }
+  __syncthreads();
+  cl_sync();
+}
+
+// ---------------------------------------------------------------------------
 // Kernels
 // ---------------------------------------------------------------------------
 
@@ -906,11 +1142,23 @@ __device__ void t_solve_core(const SmallState& s, const double* F, int ld, doubl
 __device__ int seed_polar(const SmallState& s, double* red, int* ired) {
   const int n = s.k0, ld = s.ld;
   int st = 0;
+  long long tm0 = clock64();
   // rows of X1 := columns of V_t ; X2 := I (accumulates J^T)
-  BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = s.Vt[j * ld + i]; }
-  blk_identity(s.X2, ld, n);
-  __syncthreads();
-  blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
+  if (cl_size() == 2) {   // W in this CTA's shared memory, J^T in CTA 1's (see above)
+    const int ls = jc_ls(n);
+    double* Ws = dsm;
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; Ws[i * ls + j] = s.Vt[j * ld + i]; }
+    __syncthreads();
+    const long long rounds = blk_jacobi_rows_cluster(Ws, ls, n, s.sig, red);
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = Ws[i * ls + j]; }
+    jacobi_link_close(rounds);          // J^T now in s.X2
+  } else {
+    BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[i * ld + j] = s.Vt[j * ld + i]; }
+    blk_identity(s.X2, ld, n);
+    __syncthreads();
+    blk_jacobi_rows(s.X1, ld, s.X2, ld, n, s.sig, red, dsm, SMALL_SMEM_DOUBLES);
+  }
+  SMARK(10, tm0);
   // U columns u_j = X1 row j / sigma_j (null directions: v_j orthogonalised)
   // store U^T rows in X1 (normalised)
   BLK_FOR(e, n * n) {
@@ -939,6 +1187,7 @@ __device__ int seed_polar(const SmallState& s, double* red, int* ired) {
     BLK_FOR(c, n) s.X1[j * ld + c] /= nn;
     __syncthreads();
   }
+  SMARK(11, tm0);
   // Up = U V^T = sum_j u_j v_j^T ; H = V diag(sigma) V^T
   BLK_FOR(e, n * n) {
     int a = e / n, b = e - a * n;
@@ -968,7 +1217,9 @@ __device__ int seed_polar(const SmallState& s, double* red, int* ired) {
   __syncthreads();
   blk_copy(s.Tf, ld, s.Tdense, ld, n, n);
   __syncthreads();
+  SMARK(12, tm0);
   if (!blk_getrf(s.Tf, ld, n, s.piv, red, ired)) st = OTS_E_SINGULAR_T;
+  SMARK(13, tm0);
   return st;
 }
 
@@ -1136,9 +1387,7 @@ __device__ void seed_finish(SmallState& s) {
   blk_gemm(s.Sout, s.lds_out, s.P, ld, true, s.X1, ld, false, n, k, n, 1.0, 0.0);
 }
 
-__global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
-  __shared__ double red[64];
-  __shared__ int ired[64];
+__device__ void seed_body(SmallState& s, double* red, int* ired) {
   if (threadIdx.x == 0) { s.status[0] = 0; }
   if (!seed_checks(s, red)) return;
   const int st = seed_build(s, red, ired);
@@ -1149,11 +1398,31 @@ __global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
   seed_finish(s);
 }
 
+// A 2-CTA cluster launch (polar seed, k0 <= JC_NMAX): CTA 1 only serves the
+// Jacobi's J^T; CTA 0 runs the seed and closes the link on every exit path.
+__global__ void __launch_bounds__(SMALL_NT) seed_kernel(SmallState s) {
+  __shared__ double red[64];
+  __shared__ int ired[64];
+  const bool clu = cl_size() == 2;
+  if (clu) {
+    jacobi_link_init();
+    if (cl_rank() == 1) { jacobi_jt_helper(s.X2, s.ld, s.k0); return; }
+  }
+  seed_body(s, red, ired);
+  if (clu) jacobi_link_close(0);
+}
+
 __global__ void __launch_bounds__(SMALL_NT) seedA_kernel(SmallState s) {
   __shared__ double red[64];
   __shared__ int ired[64];
+  const bool clu = cl_size() == 2;
+  if (clu) {
+    jacobi_link_init();
+    if (cl_rank() == 1) { jacobi_jt_helper(s.X2, s.ld, s.k0); return; }
+  }
   const int st = seed_build(s, red, ired);
   if (threadIdx.x == 0) s.status[1] = st;
+  if (clu) jacobi_link_close(0);
 }
 
 __global__ void __launch_bounds__(SMALL_NT) seedB_kernel(SmallState s) {
@@ -1406,18 +1675,39 @@ cudaError_t launch_cholqr_step(const double* Gf, int ldg, int k, long m, int shi
   return cudaGetLastError();
 }
 
-cudaError_t launch_seed_split(const SmallState& s, int part, cudaStream_t st) {
-  auto k = part == 0 ? seedA_kernel : seedB_kernel;
+bool seed_uses_cluster(const SmallState& s) {
+  static const bool off = getenv("OTS_NO_SEED_CLUSTER") != nullptr;   // A/B switch
+  return !off && s.choice == CHOICE_POLAR && s.k0 >= 16 && s.k0 <= JC_NMAX;
+}
+
+// the polar seed as a 2-CTA cluster (seed_uses_cluster), else one CTA
+static cudaError_t launch_seed_kernel(void (*k)(SmallState), const SmallState& s, cudaStream_t st) {
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
-  k<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
+  if (!seed_uses_cluster(s)) {
+    k<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2, 1, 1);
+  cfg.blockDim = dim3(SMALL_NT, 1, 1);
+  cfg.dynamicSmemBytes = SMALL_SMEM_DOUBLES * 8;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, s);
+}
+
+cudaError_t launch_seed_split(const SmallState& s, int part, cudaStream_t st) {
+  if (part == 0) return launch_seed_kernel(seedA_kernel, s, st);
+  cudaFuncSetAttribute(seedB_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
+  seedB_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
   return cudaGetLastError();
 }
 
-cudaError_t launch_seed(const SmallState& s, cudaStream_t st) {
-  cudaFuncSetAttribute(seed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
-  seed_kernel<<<1, SMALL_NT, SMALL_SMEM_DOUBLES * 8, st>>>(s);
-  return cudaGetLastError();
-}
+cudaError_t launch_seed(const SmallState& s, cudaStream_t st) { return launch_seed_kernel(seed_kernel, s, st); }
 cudaError_t launch_diag(const SmallState& s, cudaStream_t st) {
   cudaFuncSetAttribute(diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMALL_SMEM_DOUBLES * 8);
   cudaMemsetAsync(s.dcount, 0, sizeof(int), st);

@@ -64,6 +64,7 @@ struct ZState {
 };
 
 cudaError_t launch_seed(const SmallState& s, cudaStream_t st);
+bool seed_uses_cluster(const SmallState& s);   // polar seed on a 2-CTA cluster
 // part 0: V_t-only seed construction (status[1]); part 1: Gram checks + Z1, S
 cudaError_t launch_seed_split(const SmallState& s, int part, cudaStream_t st);
 cudaError_t launch_stability(const double* Gvv, long ldvv, const double* Gvq, long ldvq, const double* Gqq,

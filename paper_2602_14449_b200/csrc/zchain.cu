@@ -269,7 +269,11 @@ __device__ void zsweep_tile(cplx* A, cplx* U, cplx* tau_s, cplx* slot, cplx* D, 
     }
     if (j >= 2) t_col(j - 1);
     if (crit) phase_a(j + 1, alpha_n);
+#ifndef OTS_Z_NOBAR        // timing probe only (wrong results): the per-step barrier's cost
     __syncthreads();
+#else
+    if ((j & 3) == 3) __syncthreads();
+#endif
   }
   t_col(KT - 1);
   __syncthreads();
