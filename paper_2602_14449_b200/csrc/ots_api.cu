@@ -941,7 +941,7 @@ int ots_two_stage_gram_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, const
   if (n < 0 || k0 < 0 || k < 0) return fail(ctx, OTS_E_DIMENSION, "negative dimension");
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
   if (k > 64) return fail(ctx, OTS_E_UNSUPPORTED, "k > 64 not supported by this build");
-  if (k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 512 not supported by this build");
+  if (k0 > 1024) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 1024 not supported by this build");
   if (intra != OTS_INTRA_HOUSEHOLDER && intra != OTS_INTRA_CHOLSHIFT)
     return fail(ctx, OTS_E_PARAMETER, "unknown intra method");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
@@ -1012,7 +1012,7 @@ int ots_build_reflector_f64(ots_ctx* ctx, int64_t n, int64_t k0, const double* V
   cudaStream_t st = (cudaStream_t)stream;
   if (k0 > n) return fail(ctx, OTS_E_DIMENSION, "v must be tall");
   if (k0 == 0) return fail(ctx, OTS_E_DIMENSION, "v must have at least one column");
-  if (k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 512 not supported by this build");
+  if (k0 > 1024) return fail(ctx, OTS_E_UNSUPPORTED, "k0 > 1024 not supported by this build");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
   int rc;
   if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
@@ -1212,7 +1212,7 @@ int ots_b_two_stage_dense_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, co
   (void)cudaGetLastError();
   cudaStream_t st = (cudaStream_t)stream;
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
-  if (k > 64 || k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
+  if (k > 64 || k0 > 1024) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
   if (k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "b_two_stage_dense needs k0, k >= 1");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
   int rc;
@@ -1258,7 +1258,7 @@ int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, con
   (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   if (k0 + k > n) return fail(ctx, OTS_E_DIMENSION, "need k0 + k <= n");
-  if (k > 64 || k0 > 512) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
+  if (k > 64 || k0 > 1024) return fail(ctx, OTS_E_UNSUPPORTED, "shape not supported by this build");
   if (k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "b_two_stage_diag needs k0, k >= 1");
   if (choice < 0 || choice > 3) return fail(ctx, OTS_E_PARAMETER, "unknown choice");
   int rc;
@@ -1351,7 +1351,7 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
                    const double* P, int64_t ldp, double orth_tol, void* stream) {
   cudaSetDevice(ctx->device);
   (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
-  if (k > 64 || k0 > 512 || k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "shape not in this build");
+  if (k > 64 || k0 > 1024 || k0 < 1 || k < 1) return fail(ctx, OTS_E_UNSUPPORTED, "shape not in this build");
   if (row0 == 0 && n_local < k0 + k) return fail(ctx, OTS_E_DIMENSION, "rank 0 must own >= k0+k rows");
   int rc;
   if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;

@@ -331,10 +331,9 @@ __device__ void blk_org2r_cm(double* A, int lda, int m, int n, const double* tau
 // panel instead of one per column.  Same reflectors (v, tau) as the
 // unblocked sweep, so R and Q match it to rounding.
 // ---------------------------------------------------------------------------
-constexpr int QNB = 32;
 
 // lane l ends with the warp-wide sum of v[l] (31 shuffles)
-__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[QNB]) {
+__device__ __forceinline__ double warp_reduce_scatter32(double (&v)[32]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int s = 16; s >= 1; s >>= 1) {
@@ -350,6 +349,7 @@ __device__ __forceinline__ double warp_reduce_scatter32(double (&v)[QNB]) {
 }
 
 // Vs (QNB x mp, column-major in smem, unit lower, zero columns >= nb) <- panel
+template <int QNB>
 __device__ void qr_stage_panel(const double* A, int lda, int j0, int nb, int mp, double* Vs) {
   BLK_FOR(e, QNB * mp) {
     const int i = e / mp, r = e - i * mp;
@@ -359,28 +359,29 @@ __device__ void qr_stage_panel(const double* A, int lda, int j0, int nb, int mp,
 
 // a <- a - V M (V^T a) for the trailing columns c in [c0, n) (rows j0..n),
 // M = T^T (geqrf) or T (orgqr); one warp per column.
+template <int QNB>
 __device__ void qr_trailing(double* A, int lda, int j0, int mp, int c0, int n, const double* Vs, const double* Ts,
                             bool transT, double* Wbuf) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   double* w2 = Wbuf + warp * QNB;
   for (int c = c0 + warp; c < n; c += nw) {
     double* Ac = A + (long)c * lda + j0;
-    double acc[QNB];
+    double acc[32];
 #pragma unroll
-    for (int i = 0; i < QNB; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 32; ++i) acc[i] = 0.0;
     for (int r = lane; r < mp; r += 32) {
       const double a = Ac[r];
 #pragma unroll
       for (int i = 0; i < QNB; ++i) acc[i] = fma(Vs[i * mp + r], a, acc[i]);
     }
-    const double wl = warp_reduce_scatter32(acc);            // (V^T a)_lane
+    const double wl = warp_reduce_scatter32(acc);            // (V^T a)_lane (lanes >= QNB: 0)
     double m = 0.0;                                          // (M w)_lane
 #pragma unroll
     for (int i = 0; i < QNB; ++i) {
       const double wi = __shfl_sync(0xffffffffu, wl, i);
-      m = fma(transT ? Ts[i * QNB + lane] : Ts[lane * QNB + i], wi, m);
+      if (lane < QNB) m = fma(transT ? Ts[i * QNB + lane] : Ts[lane * QNB + i], wi, m);
     }
-    w2[lane] = m;
+    if (lane < QNB) w2[lane] = m;
     __syncwarp();
     for (int r = lane; r < mp; r += 32) {
       double a = Ac[r];
@@ -394,32 +395,35 @@ __device__ void qr_trailing(double* A, int lda, int j0, int mp, int c0, int n, c
 
 // T (QNB x QNB upper, zero beyond nb) of the staged panel: G = V^T V, then
 // T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] G[0:j, j]  (dlarft forward)
+template <int QNB>
 __device__ void qr_panel_t(const double* Vs, int mp, int nb, const double* tau, double* Gs, double* Ts) {
+  constexpr unsigned PM = QNB >= 32 ? 0xffffffffu : ((1u << (QNB & 31)) - 1u);   // lanes < QNB
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int j = warp; j < QNB; j += nw) {
-    double acc[QNB];
+    double acc[32];
 #pragma unroll
-    for (int i = 0; i < QNB; ++i) acc[i] = 0.0;
+    for (int i = 0; i < 32; ++i) acc[i] = 0.0;
     for (int r = lane; r < mp; r += 32) {
       const double vj = Vs[j * mp + r];
 #pragma unroll
       for (int i = 0; i < QNB; ++i) acc[i] = fma(Vs[i * mp + r], vj, acc[i]);
     }
-    Gs[lane * QNB + j] = warp_reduce_scatter32(acc);
+    const double gl = warp_reduce_scatter32(acc);
+    if (lane < QNB) Gs[lane * QNB + j] = gl;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {
+  if (threadIdx.x < QNB) {
     const int i = threadIdx.x;
     for (int e = 0; e < QNB; ++e) Ts[i * QNB + e] = 0.0;
-    __syncwarp();
+    __syncwarp(PM);
     for (int j = 0; j < nb; ++j) {
       double sacc = 0.0;
       if (i < j)
         for (int l = i; l < j; ++l) sacc = fma(Ts[i * QNB + l], Gs[l * QNB + j], sacc);
-      __syncwarp();
+      __syncwarp(PM);
       if (i < j) Ts[i * QNB + j] = -tau[j] * sacc;
       if (i == j) Ts[j * QNB + j] = tau[j];
-      __syncwarp();
+      __syncwarp(PM);
     }
   }
   __syncthreads();
@@ -428,6 +432,7 @@ __device__ void qr_panel_t(const double* Vs, int mp, int nb, const double* tau, 
 // geqrf: A (n x n column-major) -> reflectors below the diagonal, R on and
 // above, tau[n]; the panels' T kept in Tg (n/QNB+1 blocks of QNB x QNB).
 // sm: >= QNB*n + 2*QNB*QNB + 16*QNB doubles of shared memory.
+template <int QNB>
 __device__ void blk_geqrf_cm(double* A, int lda, int n, double* tau, double* Tg, double* red, double* sm) {
   double* Vs = sm;
   double* Ts = sm + QNB * n;
@@ -437,17 +442,18 @@ __device__ void blk_geqrf_cm(double* A, int lda, int n, double* tau, double* Tg,
     const int nb = min(QNB, n - j0), mp = n - j0;
     blk_geqr2_cm(A + (long)j0 * lda + j0, lda, mp, nb, tau + j0, red);
     __syncthreads();
-    qr_stage_panel(A, lda, j0, nb, mp, Vs);
+    qr_stage_panel<QNB>(A, lda, j0, nb, mp, Vs);
     __syncthreads();
-    qr_panel_t(Vs, mp, nb, tau + j0, Gs, Ts);
+    qr_panel_t<QNB>(Vs, mp, nb, tau + j0, Gs, Ts);
     BLK_FOR(e, QNB * QNB) Tg[(j0 / QNB) * QNB * QNB + e] = Ts[e];
-    if (j0 + nb < n) qr_trailing(A, lda, j0, mp, j0 + nb, n, Vs, Ts, true, Wb);
+    if (j0 + nb < n) qr_trailing<QNB>(A, lda, j0, mp, j0 + nb, n, Vs, Ts, true, Wb);
     __syncthreads();
   }
 }
 
 // orgqr: Q (n x n) in place from the reflectors of blk_geqrf_cm (R entries
 // above the diagonal are overwritten), backward over the panels.
+template <int QNB>
 __device__ void blk_orgqr_cm(double* A, int lda, int n, const double* tau, const double* Tg, double* red,
                              double* sm) {
   double* Vs = sm;
@@ -456,13 +462,13 @@ __device__ void blk_orgqr_cm(double* A, int lda, int n, const double* tau, const
   const int last = ((n - 1) / QNB) * QNB;
   for (int j0 = last; j0 >= 0; j0 -= QNB) {
     const int nb = min(QNB, n - j0), mp = n - j0;
-    qr_stage_panel(A, lda, j0, nb, mp, Vs);
+    qr_stage_panel<QNB>(A, lda, j0, nb, mp, Vs);
     BLK_FOR(e, QNB * QNB) Ts[e] = Tg[(j0 / QNB) * QNB * QNB + e];
     // trailing Q columns: rows j0 .. j0+nb-1 are zero before H_p is applied
     const int nt = n - j0 - nb;
     BLK_FOR(e, nb * nt) { const int c = j0 + nb + e / nb, r = j0 + e % nb; A[(long)c * lda + r] = 0.0; }
     __syncthreads();
-    if (nt > 0) qr_trailing(A, lda, j0, mp, j0 + nb, n, Vs, Ts, false, Wb);
+    if (nt > 0) qr_trailing<QNB>(A, lda, j0, mp, j0 + nb, n, Vs, Ts, false, Wb);
     __syncthreads();
     // panel columns: rows above the panel are zero, then the unblocked dorg2r
     BLK_FOR(e, j0 * nb) { const int c = j0 + e / j0, r = e % j0; A[(long)c * lda + r] = 0.0; }
@@ -1295,10 +1301,14 @@ __device__ int seed_build(SmallState& s, double* red, int* ired) {
       } else {                                    // global memory: column-major (coalesced)
         BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X1[j * ld + i] = s.Vt[i * ld + j]; }
         __syncthreads();
-        blk_geqrf_cm(s.X1, ld, n, s.tau, s.Z2, red, dsm);      // panel T's in Z2 (free during the seed)
+        // panel width 32 while the staged panel fits the shared memory, else 16
+        const bool wide = 32 * n + 2 * 32 * 32 + 16 * 32 <= SMALL_SMEM_DOUBLES;
+        if (wide) blk_geqrf_cm<32>(s.X1, ld, n, s.tau, s.Z2, red, dsm);   // panel T's in Z2 (free here)
+        else blk_geqrf_cm<16>(s.X1, ld, n, s.tau, s.Z2, red, dsm);
         BLK_FOR(e, n * n) { int i = e / n, j = e - i * n; s.X2[i * ld + j] = (j >= i) ? s.X1[j * ld + i] : 0.0; }
         __syncthreads();
-        blk_orgqr_cm(s.X1, ld, n, s.tau, s.Z2, red, dsm);       // Q1, column-major
+        if (wide) blk_orgqr_cm<32>(s.X1, ld, n, s.tau, s.Z2, red, dsm);   // Q1, column-major
+        else blk_orgqr_cm<16>(s.X1, ld, n, s.tau, s.Z2, red, dsm);
         BLK_FOR(e, n * n) {                        // -> row-major in place
           int i = e / n, j = e - i * n;
           if (i < j) { const double a = s.X1[i * ld + j]; s.X1[i * ld + j] = s.X1[j * ld + i]; s.X1[j * ld + i] = a; }
@@ -1445,12 +1455,15 @@ __global__ void __launch_bounds__(SMALL_NT) seedB_kernel(SmallState s) {
 // last CTA to finish combines them.
 __global__ void __launch_bounds__(SMALL_NT) diag_kernel(SmallState s) {
   __shared__ double red[64];
-  __shared__ double vec[4 * 512];
+  __shared__ double vec_s[4 * 512];
   __shared__ int last;
   if (s.status[0] != 0) return;
   const int n = s.k0, ld = s.ld;
   long long tm0 = clock64();
   const bool fit = n * (n + 1) <= SMALL_SMEM_DOUBLES;
+  // k0 > 512: the tridiagonal scratch moves to the dynamic shared memory (the
+  // matrices then live in global memory, so dsm is otherwise unused)
+  double* vec = (n <= 512) ? vec_s : dsm;
   const int lss = fit ? n + 1 : ld;
   double lam;
   if (blockIdx.x == 0) {  // T^T T

@@ -427,3 +427,18 @@ def test_large_k0_seed_vs_oracle(k0, choice):
     assert rel_e(res.q, ref["q"]) < 1e-10 and rel_e(res.r, ref["r"]) < 1e-10 and rel_e(res.s, ref["s"]) < 1e-10
     assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
     assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
+
+
+@pytest.mark.parametrize("k0,field", [(640, "real"), (1000, "real"), (256, "complex")])
+def test_k0_above_512_vs_oracle(k0, field):
+    """k0 up to 1024 (complex 256): single-CTA k0 x k0 seeds / diagnostics
+    in global memory -- elementwise vs the oracle."""
+    n, k = 1 << 14, 16
+    rng = W.make_rng(900 + k0)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0, field))
+    a = W.normal_matrix(rng, n, k, field)
+    ref = O.two_stage(v, a, "qr")
+    res = P.two_stage_qr(v, a)
+    assert rel_e(res.q, ref["q"]) < 1e-10 and rel_e(res.r, ref["r"]) < 1e-10 and rel_e(res.s, ref["s"]) < 1e-10
+    assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
+    assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
