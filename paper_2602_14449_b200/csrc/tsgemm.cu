@@ -343,6 +343,20 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
     if (ch == 0 && tid == 0)
       s_tile[(lt + 2) % 3] = dyn ? gridDim.x + atomicAdd(a.tile_counter, 1) : tile_of(lt + 1) + gridDim.x;
     issue(it + C::NSTAGE - 1);
+    if (ch == 1 && a.B != nullptr) {        // next tile's B rows -> L2 (acc_from_b reads them straight
+      const long lt1 = lt + 1;             // into registers at its chunk 0)
+      if (tile_of(lt1) < ntiles_total) {
+        const long r1 = tile_r0(lt1);
+        const int lpr = (a.ncols * 8 + 127) / 128;
+        for (int i = tid; i < C::RT * lpr; i += C::NT) {
+          const long r = r1 + i / lpr;
+          if (r < a.row_end) {
+            const double* ptr = a.B + r * a.ldb + (i % lpr) * 16;
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
+          }
+        }
+      }
+    }
     const int s = (int)(it % C::NSTAGE);
     const double* Ps = smem + s * C::STAGE;
     const double* Zs = Ps + C::RT * C::KC;
