@@ -135,8 +135,8 @@ def b_intra_qr(x, inner, intra="householder"):
             from .core import EPS
             g = gram(x, _b_apply(inner, x))
             g = (g + g.mH) / 2.0
-            lmax = float(t.linalg.eigvalsh(g).abs().max().item()) if n else 0.0
-            shift = 11.0 * (m * n + n * (n + 1)) * EPS * lmax
+            from .core import spectral_norm
+            shift = 11.0 * (m * n + n * (n + 1)) * EPS * spectral_norm(g)
             l = _tcholesky(g + shift * t.eye(n, dtype=g.dtype, device=g.device))
             q = update(x, _inv_h(l))
             r = l.mH

@@ -139,6 +139,36 @@ def householder_qr(a, nonneg_diag=False):
     return QRPair(out_like(was_torch, Q), out_like(was_torch, R))
 
 
+def _shifted_cholesky_qr_wide(a, refine_passes, was_torch):
+    """k > 64: the same algorithm (core.py:177-202) with the n-length Grams
+    and updates on the device kernels (ots_gram_* / ots_update_*) and the
+    k x k shift / Cholesky / triangular inverse as small device ops."""
+    from .oblique import _tcholesky
+    t = D.torch()
+    m, n = a.shape
+    dev = D.pick_device(a)
+    dt = t.complex128 if is_complex(a) else t.float64
+    x = (a if D.is_torch(a) else t.from_numpy(a)).to(device=f"cuda:{dev}", dtype=dt)
+
+    def inv_h(l):
+        return t.linalg.solve_triangular(l, t.eye(n, dtype=l.dtype, device=l.device), upper=False).mH
+
+    g = gram(x)
+    g = (g + g.mH) / 2.0
+    shift = 11.0 * (m * n + n * (n + 1)) * EPS * spectral_norm(g)     # ||g||_2 from the device spectrum
+    l = _tcholesky(g + shift * t.eye(n, dtype=g.dtype, device=g.device))
+    q = update(x, inv_h(l))
+    r = l.mH
+    for _ in range(refine_passes):
+        g2 = gram(q)
+        g2 = (g2 + g2.mH) / 2.0
+        l2 = _tcholesky(g2)
+        q = update(q, inv_h(l2))
+        r = l2.mH @ r
+    r = t.triu(r)
+    return QRPair(q if was_torch else q.cpu().numpy(), r if was_torch else r.cpu().numpy())
+
+
 def shifted_cholesky_qr(a, refine_passes=2):
     """Shifted Cholesky-QR + `refine_passes` unshifted refinements on the GPU
     (core.py:177-202).  Breakdown raises NotPositiveDefinite."""
@@ -148,6 +178,8 @@ def shifted_cholesky_qr(a, refine_passes=2):
     m, n = a.shape
     if m < n:
         raise E.DimensionError(f"need rows >= cols, got {m}x{n}")
+    if n > 64:
+        return _shifted_cholesky_qr_wide(a, refine_passes, was_torch)
     dev = D.pick_device(a)
     ctx = D.ctx(dev)
     if is_complex(a):

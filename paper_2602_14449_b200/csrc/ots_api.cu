@@ -193,6 +193,7 @@ struct JobCfg {
   bool distributed;
   int nsm_avail = 0;     // SMs the row-parallel phases may plan for (0: all)
   const double* gram_in = nullptr; long ldgi = 0;   // caller's V^T V (incremental Gram), or null
+  int ld_min = 0;        // small-state leading dimension at least this (reflector objects: fixed ld)
 };
 
 }  // namespace
@@ -358,7 +359,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   j.BWa = k <= 32 ? 32 : 64;
   j.KT = kt_for(k);
   j.NTOT1 = j.PW + j.BWa;
-  j.ld = std::max(j.PW, j.KT);
+  j.ld = std::max(std::max(j.PW, j.KT), c.ld_min);
   j.qrow0 = (c.row0 == 0) ? k0 : 0;
   j.m = c.n_local - j.qrow0;
   j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, ctx->nsm);
@@ -1018,6 +1019,7 @@ int ots_build_reflector_f64(ots_ctx* ctx, int64_t n, int64_t k0, const double* V
   if ((rc = validate_layout(ctx, V, ldv, "V"))) return rc;
   // a one-column job on A = V gives the Gram, the defect check and the seed
   JobCfg c{n, 0, k0, 1, V, ldv, V, ldv, nullptr, 0, choice, P, ldp, orth_tol, allow_defect, st, false};
+  c.ld_min = std::max(pad32(k0), 64);   // the ld every later job on this object uses (any m <= 64)
   Job j;
   if ((rc = job_setup(ctx, j, c))) return rc;
   if ((rc = phase_gram(ctx, j))) return rc;
@@ -1058,6 +1060,7 @@ int ots_apply_reflector_f64(ots_ctx* ctx, const ots_refl* r, int64_t m, const do
   if ((rc = validate_layout(ctx, X, ldx, "X"))) return rc;
   if ((rc = validate_layout(ctx, Y, ldy, "Y"))) return rc;
   JobCfg c{r->n, 0, r->k0, m, r->V, r->ldv, X, ldx, Y, ldy, r->choice, nullptr, 0, 1.0, 1, st, false};
+  c.ld_min = r->ld;   // the object's small matrices are stored at r->ld (refl_attach points at them)
   Job j;
   if ((rc = job_setup(ctx, j, c))) return rc;
   refl_attach(r, j);
@@ -1080,6 +1083,7 @@ int ots_reflector_diagnostics_f64(ots_ctx* ctx, const ots_refl* r, double* diag_
   (void)cudaGetLastError();   // a stale error from unrelated earlier work is not ours
   cudaStream_t st = (cudaStream_t)stream;
   JobCfg c{r->n, 0, r->k0, 1, r->V, r->ldv, r->V, r->ldv, nullptr, 0, r->choice, nullptr, 0, 1.0, 1, st, false};
+  c.ld_min = r->ld;
   Job j;
   int rc;
   if ((rc = job_setup(ctx, j, c))) return rc;

@@ -168,8 +168,9 @@ def _tcholesky(a):
         raise E.DimensionError(f"cholesky needs a square matrix, got {tuple(a.shape)}")
     if a.shape[0] == 0:
         return a.clone()
-    nrm = float(t.linalg.matrix_norm(a, ord=2).item())
-    if float(t.linalg.matrix_norm(a - a.mH, ord=2).item()) > 1e-12 * nrm:
+    from .core import spectral_norm                # device Gram spectrum (no cuSOLVER)
+    nrm = spectral_norm(a)
+    if spectral_norm((a - a.mH).contiguous()) > 1e-12 * nrm:
         raise E.NotHermitian("matrix is not Hermitian to 1e-12 * ||a||_2")
     h = (a + a.mH) / 2.0
     l, info = t.linalg.cholesky_ex(h)

@@ -442,3 +442,33 @@ def test_k0_above_512_vs_oracle(k0, field):
     assert rel_e(res.q, ref["q"]) < 1e-10 and rel_e(res.r, ref["r"]) < 1e-10 and rel_e(res.s, ref["s"]) < 1e-10
     assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
     assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
+
+
+@pytest.mark.parametrize("field", ["real", "complex"])
+def test_shifted_cholesky_qr_wide_vs_oracle(field):
+    """k > 64 shifted Cholesky-QR (device Grams / updates) vs the oracle's."""
+    x = W.normal_matrix(W.make_rng(17), 20000, 80, field)
+    qr = P.shifted_cholesky_qr(x)
+    q, r = O.cholqr_shifted(x)
+    assert rel_e(qr.q, q) < 1e-10 and rel_e(qr.r, r) < 1e-10
+    res = P.two_stage_qr(np.linalg.qr(W.normal_matrix(W.make_rng(18), 20000, 30, field))[0], x,
+                         intra="cholshift")
+    assert np.abs(res.q.conj().T @ res.q - np.eye(80)).max() < 1e-12   # k > 64 two_stage with cholshift
+
+
+@pytest.mark.parametrize("k0,k", [(30, 80), (9, 70), (70, 100)])
+def test_two_stage_wide_small_k0_vs_oracle(k0, k):
+    """k > 64 with k0 < 64: reflector jobs of 64 columns on an object built
+    with a smaller k0 (fixed small-state ld of the reflector object)."""
+    n = 6000
+    rng = W.make_rng(k0 * 1000 + k)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    a = W.normal_matrix(rng, n, k)
+    ref = O.two_stage(v, a, "qr")
+    res = P.two_stage_qr(v, a)
+    assert rel_e(res.q, ref["q"]) < 1e-10 and rel_e(res.r, ref["r"]) < 1e-10 and rel_e(res.s, ref["s"]) < 1e-10
+    assert abs(res.diagnostics.wt_inv_norm - ref["wt_inv_norm"]) <= 1e-10 * ref["wt_inv_norm"]
+    h = P.build_reflector(v, "mlu")
+    hx = P.apply_reflector(h, a, adjoint=True)
+    assert np.isfinite(hx).all()
+    assert np.abs(P.apply_reflector(h, hx) - a).max() < 1e-12 * np.abs(a).max() * 10
