@@ -45,6 +45,7 @@ class InnerProduct:
     chol_b: object = None
     diag: object = None
     host: bool = True          # weights given as numpy (results returned as numpy)
+    cplx: bool = False         # dense complex B: chol_b is the 2n x 2n real embedding phi(L)
 
     @staticmethod
     def euclidean():
@@ -53,22 +54,33 @@ class InnerProduct:
     @staticmethod
     def _dense(b, host):
         """oblique.py:48-56 for a dense b: Hermitian check (Frobenius form of
-        the reference's 1e-12 spectral test), symmetrise, Cholesky on the GPU."""
+        the reference's 1e-12 spectral test), symmetrise, Cholesky on the GPU.
+        A complex Hermitian b = L L^* is factored through its real embedding
+        phi(b) (2n x 2n, entry b_ij -> [[Re, -Im], [Im, Re]] with rows and
+        columns interleaved re/im): phi(b) is SPD and its real Cholesky factor
+        is exactly phi(L) (lower triangular, the diagonal blocks l_jj I), so
+        L^* x and L^-* x are the real dense kernels on the interleaved x."""
         t = D.torch()
-        if b.is_complex():
-            raise NotImplementedError("dense complex B is not supported by this build")
         n = b.shape[0]
         dev = b.device.index if b.is_cuda else t.cuda.current_device()
-        bd = b.to(device=f"cuda:{dev}", dtype=t.float64)
-        asym = t.linalg.matrix_norm(bd - bd.T).item()
+        cplx = b.is_complex()
+        bd = b.to(device=f"cuda:{dev}", dtype=t.complex128 if cplx else t.float64)
+        asym = t.linalg.matrix_norm(bd - bd.mH).item()
         if asym > 1e-12 * t.linalg.matrix_norm(bd).item():
             raise E.NotHermitian("weight matrix is not Hermitian to tolerance")
-        bs = ((bd + bd.T) * 0.5).contiguous()
-        L = t.empty_like(bs)
+        bs = ((bd + bd.mH) * 0.5).contiguous()
+        if cplx:
+            br, bi = bs.real, bs.imag
+            blk = t.stack([t.stack([br, -bi], -1), t.stack([bi, br], -1)], -2)   # [i, j, a, c]
+            bf = blk.permute(0, 2, 1, 3).reshape(2 * n, 2 * n).contiguous()
+        else:
+            bf = bs
+        nf = bf.shape[0]
+        L = t.empty_like(bf)
         ctx = D.ctx(dev)
-        check(lib().ots_dense_cholesky_f64(ctx, n, C.c_void_p(bs.data_ptr()), n, C.c_void_p(L.data_ptr()), n,
+        check(lib().ots_dense_cholesky_f64(ctx, nf, C.c_void_p(bf.data_ptr()), nf, C.c_void_p(L.data_ptr()), nf,
                                            D.stream_ptr(dev)), ctx)
-        return InnerProduct(kind="weighted", b=bs, chol_b=L, host=host)
+        return InnerProduct(kind="weighted", b=bs, chol_b=L, host=host, cplx=cplx)
 
     @staticmethod
     def weighted(b):
@@ -103,7 +115,9 @@ class InnerProduct:
     def n(self):
         if self.diag is not None:
             return int(self.diag.shape[0])
-        return None if self.chol_b is None else int(self.chol_b.shape[0])
+        if self.chol_b is None:
+            return None
+        return int(self.chol_b.shape[0]) // (2 if self.cplx else 1)
 
     # -- oblique.py:62-90 (n-length work on the device; numpy in -> numpy out)
     def apply(self, x):
@@ -118,7 +132,8 @@ class InnerProduct:
             d = _sqrt_d(self, dev) ** 2
             y = xd * (d[:, None] if xd.dim() == 2 else d)
         else:
-            y = self.b.to(xd.dtype) @ xd
+            dt = t.complex128 if (self.cplx or xd.is_complex()) else t.float64
+            y = self.b.to(dt) @ xd.to(dt)
         return y if was_torch else y.cpu().numpy()
 
     def _phi_x(self, x):
@@ -180,11 +195,15 @@ def _tcholesky(a):
 
 
 def _dense_basis(inner, m):
-    """[L_m^{-T}; 0] = L^{-T} [I_m; 0] on the device (oblique.py:93-108)."""
+    """[L_m^{-*}; 0] = L^{-*} [I_m; 0] on the device (oblique.py:93-108)."""
     t = D.torch()
     L = inner.chol_b
-    n = L.shape[0]
     dev = L.device.index
+    if inner.cplx:
+        e = t.zeros((inner.n, m), dtype=t.complex128, device=L.device)
+        e[:m, :m] = t.eye(m, dtype=t.complex128, device=L.device)
+        return _phi(inner, e, dev, inverse=True)
+    n = L.shape[0]
     u = t.zeros((n, m + (m & 1)), dtype=t.float64, device=L.device)
     u[:m, :m] = t.eye(m, dtype=t.float64, device=L.device)
     ctx = D.ctx(dev)
@@ -310,8 +329,8 @@ def _b_two_stage_qr(v, a, u, inner, choice="qr", reorth=True, p=None):
 def _b_two_stage_dense(v, a, u, inner, choice, p, n, k0, k, was_torch):
     """Dense SPD B = L L^T with the canonical basis (module docstring)."""
     t = D.torch()
-    if is_complex(v) or is_complex(a):
-        raise NotImplementedError("dense complex B is not supported by this build")
+    if inner.cplx or is_complex(v) or is_complex(a):
+        return _zb_two_stage_dense(v, a, inner, choice, p, k0, k, was_torch)
     L = inner.chol_b
     dev = L.device.index
     if choice not in CHOICES:
@@ -344,6 +363,40 @@ def _b_two_stage_dense(v, a, u, inner, choice, p, n, k0, k, was_torch):
     if was_torch:
         return TwoStageResult(Q.view(), R.view(), S.view(), ReflectorDiagnostics(diag[0], diag[1]))
     return TwoStageResult(Q.numpy(), R.numpy(), S.numpy(), ReflectorDiagnostics(diag[0], diag[1]))
+
+
+def _zb_two_stage_dense(v, a, inner, choice, p, k0, k, was_torch):
+    """Dense complex B, canonical basis: the Euclidean complex pipeline on
+    (L^* v, L^* a) gives S = v^* B a and the unique positive-diagonal B-QR
+    of the projected block after the phase fix Q = L^-* Q' d, R = d^* R'
+    (d = the phases of diag R'); the diagnostics are those of the canonical
+    B-reflector (oblique.py:125-167), as for the general-u path."""
+    from .twostage import two_stage_qr
+    t = D.torch()
+    dev = inner.chol_b.device.index
+    if choice not in CHOICES:
+        raise E.ParameterError(f"unknown choice {choice!r}")
+    pa = _phi(inner, a, dev)
+    if k0 == 0:
+        qr = householder_qr(pa, nonneg_diag=True)
+        q = _phi(inner, qr.q, dev, inverse=True)
+        z = t.zeros((0, k), dtype=t.complex128, device=q.device)
+        return TwoStageResult(_out(q, was_torch), _out(qr.r, was_torch), _out(z, was_torch),
+                              ReflectorDiagnostics(1.0, 0.0))
+    if choice == "explicit" and p is None:
+        raise E.ParameterError("choice='explicit' requires a seed matrix p")
+    pv = _phi(inner, v, dev)
+    pp = None if p is None else (p if D.is_torch(p) else t.from_numpy(np.ascontiguousarray(p))).to(
+        device=pv.device, dtype=t.complex128)
+    res = two_stage_qr(pv, pa, choice=choice, p=pp)
+    r = res.r
+    dg = t.diagonal(r)
+    ph = t.where(dg.abs() > 0, dg / dg.abs().clamp_min(1e-300), t.ones_like(dg))
+    r = t.triu(ph.conj()[:, None] * r)
+    q = _phi(inner, res.q * ph[None, :], dev, inverse=True)
+    h = b_build_reflector(v, initial_b_basis(inner, k0), inner, choice, p=p, allow_defect=True)
+    diag = b_reflector_diagnostics(h)
+    return TwoStageResult(_out(q, was_torch), _out(r, was_torch), _out(res.s, was_torch), diag)
 
 
 @dataclass
@@ -394,8 +447,11 @@ def _phi(inner, x, dev, inverse=False):
         xd = (x if D.is_torch(x) else t.from_numpy(np.ascontiguousarray(x))).to(f"cuda:{dev}")
         s = _sqrt_d(inner, dev)[:, None]
         return xd / s if inverse else xd * s
+    if inner.cplx:
+        return _zphi(inner, x, dev, inverse)
     if is_complex(x):
-        raise NotImplementedError("dense complex B is not supported by this build")
+        raise E.ParameterError("complex data needs a complex (or diagonal) weight; B is real dense here "
+                               "(pass B as a complex128 matrix)")
     L = inner.chol_b
     n = L.shape[0]
     ctx = D.ctx(dev)
@@ -410,6 +466,31 @@ def _phi(inner, x, dev, inverse=False):
         check(lib().ots_dense_trmm_lt_f64(ctx, n, X.cols, C.c_void_p(L.data_ptr()), n, X.ptr, X.ld, Y.ptr, Y.ld,
                                           D.stream_ptr(dev)), ctx)
     return Y.view()
+
+
+def _zphi(inner, x, dev, inverse):
+    """L^* x / L^-* x for a dense complex B through the real embedding: the
+    columns of x (n x m complex) become 2n-vectors with re/im interleaved
+    along the rows, multiplied by phi(L)^T (= phi(L^*)) or solved with it."""
+    t = D.torch()
+    xd = (x if D.is_torch(x) else t.from_numpy(np.ascontiguousarray(x))).to(device=f"cuda:{dev}",
+                                                                            dtype=t.complex128)
+    n, m = xd.shape
+    L = inner.chol_b
+    nf = 2 * n
+    ld = m + (m & 1) if m else 2
+    xr = t.zeros((nf, ld), dtype=t.float64, device=xd.device)
+    xr[:, :m] = t.view_as_real(xd.resolve_conj()).permute(0, 2, 1).reshape(nf, m)
+    ctx = D.ctx(dev)
+    if inverse:
+        check(lib().ots_dense_trsm_lt_f64(ctx, nf, m, C.c_void_p(L.data_ptr()), nf, C.c_void_p(xr.data_ptr()),
+                                          ld, D.stream_ptr(dev)), ctx)
+        yr = xr
+    else:
+        yr = t.empty_like(xr)
+        check(lib().ots_dense_trmm_lt_f64(ctx, nf, m, C.c_void_p(L.data_ptr()), nf, C.c_void_p(xr.data_ptr()),
+                                          ld, C.c_void_p(yr.data_ptr()), ld, D.stream_ptr(dev)), ctx)
+    return t.view_as_complex(yr[:, :m].reshape(n, 2, m).permute(0, 2, 1).contiguous())
 
 
 def _out(x, was_torch):
@@ -490,8 +571,8 @@ def _require_canonical(u, inner, m, name):
     else:
         t = D.torch()
         ucan = _dense_basis(inner, m)
-        ud = (u if D.is_torch(u) else t.from_numpy(np.ascontiguousarray(u))).to(
-            device=ucan.device, dtype=t.float64)
+        ud = (u if D.is_torch(u) else t.from_numpy(np.ascontiguousarray(u))).to(device=ucan.device)
+        ud = ud.to(t.complex128 if (ud.is_complex() or ucan.is_complex()) else t.float64)
         scale = float(ucan.abs().max().item()) if m else 1.0
         ok = float((ud[:, :m] - ucan).abs().max().item()) <= 1e-12 * (scale or 1.0) if m else True
     if not ok:
@@ -648,12 +729,13 @@ def b_block_householder_qr(blocks, inner, choice="qr", reorth=True):
     t = D.torch()
     u = initial_b_basis(inner, total)
     dev = _dev_of(inner, *blocks)
-    cplx = any(is_complex(b) for b in blocks)
+    cplx = any(is_complex(b) for b in blocks) or inner.cplx
     tdt = t.complex128 if cplx else t.float64
     todev = (lambda z: (z if D.is_torch(z) else t.from_numpy(np.ascontiguousarray(z))).to(
         device=f"cuda:{dev}", dtype=tdt))
     blocks = [todev(b) for b in blocks]
-    u = (u if D.is_torch(u) else t.from_numpy(u)).to(device=f"cuda:{dev}", dtype=t.float64)
+    u = (u if D.is_torch(u) else t.from_numpy(u)).to(device=f"cuda:{dev}",
+                                                       dtype=t.complex128 if inner.cplx else t.float64)
     r_full = t.zeros((total, total), dtype=tdt, device=f"cuda:{dev}")
     try:
         qr0 = b_householder_qr(blocks[0], u[:, :sizes[0]], inner, reorth=reorth)

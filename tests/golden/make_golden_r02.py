@@ -192,6 +192,34 @@ def main():
     put("bgen_euc", v=v, u=u, a=a, q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
         wt_inv_norm=res.diagnostics.wt_inv_norm)
 
+    # --- dense complex Hermitian B (oblique.py:36-361 with a complex weight)
+    n, k0, k = 240, 6, 5
+    uu = np.linalg.qr(nm(rng(101), n, n, "complex"))[0]
+    b = (uu * (10.0 ** np.linspace(0.0, 2.0, n))) @ uu.conj().T
+    ipz = R.InnerProduct.weighted(b)
+    lh = ipz.chol_b.conj().T
+    v = np.linalg.solve(lh, np.linalg.qr(nm(rng(102), n, k0, "complex"))[0])
+    ucan = R.initial_b_basis(ipz, k0 + k)
+    ugen = np.linalg.solve(lh, np.linalg.qr(nm(rng(103), n, k0 + k, "complex"))[0])
+    a = nm(rng(104), n, k, "complex")
+    x = nm(rng(105), n, 3, "complex")
+    xr = nm(rng(106), n, 2)
+    put("zdense", b=b, v=v, ucan=ucan, ugen=ugen, a=a, x=x, xr=xr, apply=ipz.apply(x), gram=ipz.gram(x, v),
+        col_norms=ipz.col_norms(x), norm=ipz.norm(x), defect=ipz.defect(v), apply_r=ipz.apply(xr))
+    for ch in ("mlu", "qr", "polar"):
+        for tag, u in (("can", ucan), ("gen", ugen)):
+            res = R.b_two_stage_qr(v, a, u, ipz, choice=ch)
+            h = R.b_build_reflector(v, u[:, :k0], ipz, choice=ch)
+            put(f"zdense/{ch}_{tag}", q=res.q, r=res.r, s=res.s, kappa_t=res.diagnostics.kappa_t,
+                wt_inv_norm=res.diagnostics.wt_inv_norm, p=h.p, w=h.w, ax=R.b_apply_reflector(h, x),
+                aix=R.b_apply_reflector(h, x, inverse=True))
+    qr = R.b_householder_qr(a, ucan[:, :k], ipz)
+    put("zdense/bhqr", q=qr.q, r=qr.r)
+    blocks = [nm(rng(107 + i), n, 4, "complex") for i in range(3)]
+    res = R.b_block_householder_qr(blocks, ipz, choice="qr")
+    put("zdense/bblock", b0=blocks[0], b1=blocks[1], b2=blocks[2], q=res.q, r=res.r,
+        kappa_t=res.diagnostics.kappa_t)
+
     np.savez_compressed(OUT, **store)
     print(f"wrote {OUT}: {len(store)} arrays, {os.path.getsize(OUT) / 1e6:.2f} MB")
 

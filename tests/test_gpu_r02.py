@@ -472,3 +472,43 @@ def test_two_stage_wide_small_k0_vs_oracle(k0, k):
     hx = P.apply_reflector(h, a, adjoint=True)
     assert np.isfinite(hx).all()
     assert np.abs(P.apply_reflector(h, hx) - a).max() < 1e-12 * np.abs(a).max() * 10
+
+
+def test_dense_complex_weight(g2):
+    """Dense complex Hermitian B (oblique.py:36-361 with a complex weight):
+    InnerProduct's methods, initial_b_basis, b_two_stage_qr for the canonical
+    and a general B-orthonormal basis, the B-reflector and its application,
+    b_householder_qr and b_block_householder_qr against the reference."""
+    z = lambda key: g2[f"zdense/{key}"]
+    ip = P.InnerProduct.weighted(z("b"))
+    assert ip.n == 240
+    assert rel_e(ip.apply(z("x")), z("apply")) < 1e-12
+    assert rel_e(ip.apply(z("xr")), z("apply_r")) < 1e-12
+    assert rel_e(ip.gram(z("x"), z("v")), z("gram")) < 1e-10
+    assert rel_e(ip.col_norms(z("x")), z("col_norms")) < 1e-12
+    assert abs(ip.norm(z("x")) - float(z("norm"))) < 1e-12 * float(z("norm"))
+    assert abs(ip.defect(z("v")) - float(z("defect"))) < 1e-12
+    assert rel_e(P.initial_b_basis(ip, 11), z("ucan")) < 1e-12
+    v, a, x = z("v"), z("a"), z("x")
+    for ch in ("mlu", "qr", "polar"):
+        for tag in ("can", "gen"):
+            key = f"{ch}_{tag}"
+            u = z("ucan") if tag == "can" else z("ugen")
+            res = P.b_two_stage_qr(v, a, u, ip, choice=ch)
+            for k in ("q", "r", "s"):
+                assert rel_e(getattr(res, k), z(f"{key}/{k}")) < 1e-9, (key, k)
+            assert abs(res.diagnostics.kappa_t - float(z(f"{key}/kappa_t"))) < 1e-9 * float(z(f"{key}/kappa_t"))
+            assert abs(res.diagnostics.wt_inv_norm - float(z(f"{key}/wt_inv_norm"))) < \
+                1e-9 * float(z(f"{key}/wt_inv_norm")), key
+            h = P.b_build_reflector(v, u[:, :6], ip, choice=ch)
+            assert rel_e(h.p, z(f"{key}/p")) < 1e-9, key
+            assert rel_e(h.w, z(f"{key}/w")) < 1e-9, key
+            assert rel_e(P.b_apply_reflector(h, x), z(f"{key}/ax")) < 1e-9, key
+            assert rel_e(P.b_apply_reflector(h, x, inverse=True), z(f"{key}/aix")) < 1e-9, key
+    qr = P.b_householder_qr(a, z("ucan")[:, :5], ip)
+    assert rel_e(qr.q, z("bhqr/q")) < 1e-10 and rel_e(qr.r, z("bhqr/r")) < 1e-10
+    res = P.b_block_householder_qr([z("bblock/b0"), z("bblock/b1"), z("bblock/b2")], ip, choice="qr")
+    assert rel_e(res.q, z("bblock/q")) < 1e-9 and rel_e(res.r, z("bblock/r")) < 1e-9
+    assert P.orthogonality_loss(res.q, ip) < 1e-13
+    rep = P.compute_metrics(v, a, P.b_two_stage_qr(v, a, z("ucan"), ip), inner=ip)
+    assert rep.loss_orth < 1e-13 and rep.rel_residual < 1e-13
