@@ -771,6 +771,7 @@ __device__ __forceinline__ void fused_x(double (&x)[16][2], const FusedArgs& a, 
 template <int KT>
 __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   using C = BlkCfg<KT>;
+  if (a.only && !a.only[blockIdx.x]) return;
   constexpr int NP = C::NP;
   extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
   double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
@@ -909,6 +910,7 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
 // register allocation of the panel loop (measured +1 ms).
 template <int KT>
 __global__ void __launch_bounds__(256, 2) chain_factor_fused_kernel(FactorArgs a, FusedArgs fz) {
+  if (a.only && !a.only[blockIdx.x]) return;
   constexpr bool FUSED = true;
   using C = BlkCfg<KT>;
   constexpr int NP = C::NP;
@@ -1255,6 +1257,8 @@ __global__ void __launch_bounds__(256, 2) chain_qform_kernel(QformArgs a) {
     }
   }
 }
+
+#include "gsweep.inc"
 
 // ---------------------------------------------------------------------------
 template <int KT>

@@ -40,6 +40,22 @@ struct FactorArgs {
   double* U;             // per tile KT*KT, tile id = chain*(L+1) + t
   double* Rout;          // stacked chain R's: chain*KT rows, ld KT
   int head_tri;          // input rows are stacked upper-triangular R's (tree levels)
+  const int* only = nullptr;   // non-null: factor only the chains with only[chain] != 0
+};
+
+// Gram-form tile factorization of level 0 (KT = 64; gsweep in chainqr.cu).
+// Pass 1 reads X (never writes it) and per tile produces T, the coefficient
+// matrix Cc with Y = X_tile Cc, and the running chain R; a chain whose tiles
+// fail the cancellation bound is flagged in `fail` and redone by the exact
+// register-tile kernel (FactorArgs::only).  Pass 2 forms Y = X Cc in place.
+struct GsweepArgs {
+  double* D; long ldd; int ncols;   // level-0 rows (X in, Y out after pass 2)
+  ChainGeom G;
+  double* U;             // T per tile (FactorArgs::U indexing)
+  double* Rout;          // chain R's
+  double* Cc;            // per tile KT*KT (same indexing as U; tile 0 unused)
+  double* Hs;            // head rows per chain (KT x KT): R upper, V strictly lower
+  int* fail;             // per chain: 0 = Gram-form result valid, 1 = redo exactly
 };
 
 // Fused inter-block update for the chain factor's level 0 (opt-in): the
@@ -69,6 +85,8 @@ cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, i
 cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
 cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st, const FusedArgs* fz = nullptr);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
+cudaError_t launch_chain_gsweep(const GsweepArgs& a, cudaStream_t st);
+cudaError_t launch_gs_apply(const GsweepArgs& a, int nsm, cudaStream_t st);
 // complex128 TSQR (zchain.cu): same argument records, pointers to interleaved
 // (re, im) data, leading dimensions in complex units
 using ZFactorArgs = FactorArgs;

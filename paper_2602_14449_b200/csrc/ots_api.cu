@@ -94,6 +94,9 @@ struct Level {
   ChainGeom G;
   double* UT;     // per-tile U -> T
   double* R;      // stacked chain R's (nchains * KT rows, ld KT)
+  double* CC = nullptr;   // level 0, KT = 64: per-tile Cc of the Gram-form factor
+  double* HS = nullptr;   //   head rows per chain
+  int* FAIL = nullptr;    //   per-chain fallback flags
 };
 
 }  // namespace
@@ -230,6 +233,16 @@ long chains_per_sm() {
   return v;
 }
 
+// The Gram-form level-0 factor (gsweep.inc) for KT = 64, opt-in with
+// OTS_GSWEEP=1 while it is slower than the register-tile kernel.
+bool gsweep_on(int KT, int b) {
+  static int v = [] {
+    const char* e = getenv("OTS_GSWEEP");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0 && KT == 64 && b == 128;
+}
+
 std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, long m, int KT, int nsm) {
   std::vector<Level> lv;
   // level 0
@@ -247,6 +260,11 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     L.G = ChainGeom{m, b, (int)Lt, rpc, (int)nch};
     L.UT = ar.take<double>((size_t)nch * (Lt + 1) * KT * KT);
     L.R = ar.take<double>((size_t)nch * KT * KT);
+    if (gsweep_on(KT, b)) {
+      L.CC = ar.take<double>((size_t)nch * (Lt + 1) * KT * KT);
+      L.HS = ar.take<double>((size_t)nch * KT * KT);
+      L.FAIL = ar.take<int>((size_t)nch);
+    }
     lv.push_back(L);
   }
   while (lv.back().G.nchains > 1) {
@@ -277,6 +295,7 @@ size_t plan_levels_bytes(long m, int KT, int nsm) {
   long nch = (m + rpc - 1) / rpc;
   if (nch < 1) nch = 1;
   tot += ((size_t)nch * (Lt + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + 512;
+  if (gsweep_on(KT, b)) tot += ((size_t)nch * (Lt + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + nch * 4 + 1536;
   while (nch > 1) {
     long nrows = nch * KT;
     long rpc2 = (long)KT * 4;
@@ -307,6 +326,18 @@ int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t
   for (size_t l = 0; l < lv.size(); ++l) {
     Level& L = lv[l];
     FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, (l > 0 || tri_first) ? 1 : 0};
+    if (l == 0 && !tri_first && !(fuse0 && fuse0->Vb) && L.CC) {
+      // Gram-form tiles; chains beyond the cancellation bound are redone by
+      // the register-tile kernel (X untouched until the Y pass)
+      GsweepArgs ga{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, L.CC, L.HS, L.FAIL};
+      CK(launch_chain_gsweep(ga, st));
+      prof_mark(ctx, st, "gs_sweep");
+      fa.only = L.FAIL;
+      CK(launch_chain_factor(fa, KT, st, nullptr));
+      prof_mark(ctx, st, "gs_redo");
+      CK(launch_gs_apply(ga, ctx->nsm, st));
+      continue;
+    }
     CK(launch_chain_factor(fa, KT, st, l == 0 ? fuse0 : nullptr));
   }
   return OTS_OK;

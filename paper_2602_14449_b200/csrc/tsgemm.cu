@@ -401,7 +401,7 @@ cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool s
 #define OTS_TN(pw, bw, al, sy)                                                   \
   if (PW == pw && BW == bw && alias == al && sym == sy)                          \
     return launch_tn_t<pw, bw, al, sy>(a, grid, st);
-  OTS_TN(32, 32, true, true) OTS_TN(64, 32, true, true) OTS_TN(64, 64, true, true)
+  OTS_TN(32, 32, true, true) OTS_TN(32, 64, true, true) OTS_TN(64, 32, true, true) OTS_TN(64, 64, true, true)
   OTS_TN(96, 32, true, true) OTS_TN(96, 64, true, true)
   OTS_TN(128, 32, true, true) OTS_TN(128, 64, true, true)
   OTS_TN(32, 0, true, true) OTS_TN(64, 0, true, true) OTS_TN(96, 0, true, true) OTS_TN(128, 0, true, true)
