@@ -512,3 +512,16 @@ def test_dense_complex_weight(g2):
     assert P.orthogonality_loss(res.q, ip) < 1e-13
     rep = P.compute_metrics(v, a, P.b_two_stage_qr(v, a, z("ucan"), ip), inner=ip)
     assert rep.loss_orth < 1e-13 and rep.rel_residual < 1e-13
+
+
+@pytest.mark.parametrize("n,k0,k", [(1 << 16, 32, 64), (100003, 32, 48), (3000, 16, 40), (20000, 8, 33)])
+def test_small_k0_with_k_above_32(n, k0, k):
+    """k0 <= 32 with 32 < k <= 64 (the V^T [V A] Gram at widths 32 | 64):
+    elementwise parity with the oracle."""
+    rng = W.make_rng(n + 31 * k0 + k)
+    v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))
+    a = W.normal_matrix(rng, n, k)
+    ref = O.two_stage(v, a, "qr")
+    res = P.two_stage_qr(v, a, choice="qr")
+    for key in ("q", "r", "s"):
+        assert rel_e(getattr(res, key), ref[key]) < 1e-10, key
