@@ -768,10 +768,15 @@ __device__ __forceinline__ void fused_x(double (&x)[16][2], const FusedArgs& a, 
   __syncthreads();                                           // Xs is reused by the panels
 }
 
-template <int KT>
+// REDO: level-0 redo of the chains the Gram-form factor flagged (gsweep.inc;
+// flag = Rout[chain][KT-1][0] != 0, an entry a chain R leaves 0).  A separate
+// instantiation: the default one is unchanged (ptxas allocation).
+template <int KT, bool REDO = false>
 __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   using C = BlkCfg<KT>;
-  if (a.only && !a.only[blockIdx.x]) return;
+  if constexpr (REDO) {
+    if (a.Rout[((long)blockIdx.x * KT + KT - 1) * KT] == 0.0) return;
+  }
   constexpr int NP = C::NP;
   extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
   double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
@@ -910,7 +915,6 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
 // register allocation of the panel loop (measured +1 ms).
 template <int KT>
 __global__ void __launch_bounds__(256, 2) chain_factor_fused_kernel(FactorArgs a, FusedArgs fz) {
-  if (a.only && !a.only[blockIdx.x]) return;
   constexpr bool FUSED = true;
   using C = BlkCfg<KT>;
   constexpr int NP = C::NP;
@@ -1269,6 +1273,16 @@ static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st, const FusedArg
     auto k = chain_factor_fused_kernel<KT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     k<<<a.G.nchains, 256, C::SMEM, st>>>(a, *fz);
+  } else if (a.head_tri == 2) {
+    if constexpr (KT == 64) {
+      FactorArgs b = a;
+      b.head_tri = 0;
+      auto k = chain_factor_kernel<KT, true>;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+      k<<<a.G.nchains, 256, C::SMEM, st>>>(b);
+    } else {
+      return cudaErrorInvalidValue;
+    }
   } else {
     auto k = chain_factor_kernel<KT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);

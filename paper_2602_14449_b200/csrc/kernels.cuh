@@ -39,15 +39,17 @@ struct FactorArgs {
   ChainGeom G;
   double* U;             // per tile KT*KT, tile id = chain*(L+1) + t
   double* Rout;          // stacked chain R's: chain*KT rows, ld KT
-  int head_tri;          // input rows are stacked upper-triangular R's (tree levels)
-  const int* only = nullptr;   // non-null: factor only the chains with only[chain] != 0
+  int head_tri;          // input rows are stacked upper-triangular R's (tree levels);
+                         // 2 at launch: level-0 redo of the chains the Gram-form
+                         // factor flagged (chain_factor_kernel<KT, true>)
 };
 
 // Gram-form tile factorization of level 0 (KT = 64; gsweep in chainqr.cu).
 // Pass 1 reads X (never writes it) and per tile produces T, the coefficient
 // matrix Cc with Y = X_tile Cc, and the running chain R; a chain whose tiles
-// fail the cancellation bound is flagged in `fail` and redone by the exact
-// register-tile kernel (FactorArgs::only).  Pass 2 forms Y = X Cc in place.
+// fail the cancellation bound is flagged (Rout[chain][KT-1][0] = 1) and redone
+// by the exact register-tile kernel (FactorArgs::head_tri = 2) after pass 2
+// (Y = X Cc in place) has skipped it.
 struct GsweepArgs {
   double* D; long ldd; int ncols;   // level-0 rows (X in, Y out after pass 2)
   ChainGeom G;
@@ -55,7 +57,6 @@ struct GsweepArgs {
   double* Rout;          // chain R's
   double* Cc;            // per tile KT*KT (same indexing as U; tile 0 unused)
   double* Hs;            // head rows per chain (KT x KT): R upper, V strictly lower
-  int* fail;             // per chain: 0 = Gram-form result valid, 1 = redo exactly
 };
 
 // Fused inter-block update for the chain factor's level 0 (opt-in): the

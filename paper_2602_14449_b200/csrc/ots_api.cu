@@ -96,7 +96,6 @@ struct Level {
   double* R;      // stacked chain R's (nchains * KT rows, ld KT)
   double* CC = nullptr;   // level 0, KT = 64: per-tile Cc of the Gram-form factor
   double* HS = nullptr;   //   head rows per chain
-  int* FAIL = nullptr;    //   per-chain fallback flags
 };
 
 }  // namespace
@@ -220,6 +219,7 @@ struct Job {
   double* Rfinal = nullptr;
 };
 
+namespace ots { void gs_event_log(long long* out); }
 namespace {
 
 // level-0 chains per SM (2 = the two CTAs an SM holds); OTS_CHAINS_PER_SM
@@ -263,7 +263,6 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     if (gsweep_on(KT, b)) {
       L.CC = ar.take<double>((size_t)nch * (Lt + 1) * KT * KT);
       L.HS = ar.take<double>((size_t)nch * KT * KT);
-      L.FAIL = ar.take<int>((size_t)nch);
     }
     lv.push_back(L);
   }
@@ -329,13 +328,13 @@ int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t
     if (l == 0 && !tri_first && !(fuse0 && fuse0->Vb) && L.CC) {
       // Gram-form tiles; chains beyond the cancellation bound are redone by
       // the register-tile kernel (X untouched until the Y pass)
-      GsweepArgs ga{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, L.CC, L.HS, L.FAIL};
+      GsweepArgs ga{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, L.CC, L.HS};
       CK(launch_chain_gsweep(ga, st));
       prof_mark(ctx, st, "gs_sweep");
-      fa.only = L.FAIL;
+      CK(launch_gs_apply(ga, ctx->nsm, st));          // skips the flagged chains
+      prof_mark(ctx, st, "gs_apply");
+      fa.head_tri = 2;                                 // redo the flagged chains exactly
       CK(launch_chain_factor(fa, KT, st, nullptr));
-      prof_mark(ctx, st, "gs_redo");
-      CK(launch_gs_apply(ga, ctx->nsm, st));
       continue;
     }
     CK(launch_chain_factor(fa, KT, st, l == 0 ? fuse0 : nullptr));
@@ -879,6 +878,8 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
 extern "C" {
 
 int ots_version(void) { return 1; }
+
+void ots_gs_event_log(long long* out) { ots::gs_event_log(out); }
 
 int ots_ctx_create(int device, ots_ctx** out) {
   if (!out) return OTS_E_VALUE;

@@ -296,6 +296,38 @@ def test_fused_update_factor_parity():
     assert out.returncode == 0 and "fused ok" in out.stdout, out.stdout + out.stderr
 
 
+def test_gram_form_factor_parity_and_redo():
+    """OTS_GSWEEP=1 (Gram-form level-0 tiles, gsweep.inc): oracle parity on
+    well-conditioned shapes (Gram path) and on configs[1]-like data whose
+    chains fail the cancellation bound and are redone by the exact kernel."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, sys; sys.path.insert(0, '.');"
+        "import paper_2602_14449_b200 as P; from oracle import twostage_oracle as O;"
+        "from paper_2602_14449_b200 import workloads as W\n"
+        "for n, k0, k in ((1 << 16, 128, 64), (100003, 32, 48), (3000, 16, 40)):\n"
+        "    rng = W.make_rng(n + k0); v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0));"
+        " a = W.normal_matrix(rng, n, k)\n"
+        "    ref = O.two_stage(v, a, 'qr', diagnostics=False); res = P.two_stage_qr(v, a)\n"
+        "    for key in 'qrs':\n"
+        "        x, y = getattr(res, key), ref[key]\n"
+        "        e = float((np.abs(x - y) / (np.abs(y) + 1e-4 * np.abs(y).max())).max())\n"
+        "        assert e < 1e-10, (n, k0, k, key, e)\n"
+        "rng = W.make_rng(7); n, k0, k = 1 << 16, 64, 64\n"
+        "v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0))\n"
+        "u, _ = np.linalg.qr(W.normal_matrix(rng, n, k) - v @ (v.T @ W.normal_matrix(rng, n, k)))\n"
+        "a = v @ W.normal_matrix(rng, k0, k) + (u * np.logspace(0, -15, k)) @ "
+        "np.linalg.qr(W.normal_matrix(rng, k, k))[0]\n"
+        "res = P.two_stage_qr(v, a); m = P.compute_metrics(v, a, res)\n"
+        "assert m.loss_orth < 10 * n * 2.0 ** -53 and m.rel_residual < 10 * n * 2.0 ** -53, m\n"
+        "print('gsweep ok')\n")
+    env = dict(os.environ, OTS_GSWEEP="1")
+    out = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(ROOT), env=env,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "gsweep ok" in out.stdout, out.stdout + out.stderr
+
+
 # ----------------------------------------------------------------- wide shapes (k > 64)
 @pytest.mark.parametrize("field,m,k", [("real", 5000, 100), ("real", 3000, 200), ("complex", 4000, 96)])
 def test_householder_qr_wide_vs_lapack(field, m, k):
