@@ -712,62 +712,6 @@ __device__ __forceinline__ void t_store(const double* Tpv, const double* Tw, dou
   }
 }
 
-// Fused inter-block update: the tile's X rows [gr0, gr0+nb) = A_b + V_b Z1
-// formed straight into the register tile (quad layout, X^T as the DMMA
-// accumulator: x^T[col][row] += Z1^T[col][k] V^T[k][row]).  V_b's 128 x k0
-// row block and the matching rows of Z1 stream through shared memory in
-// VC-row chunks of k (cp.async, double-buffered in the Xs region, which is
-// free between tiles; one barrier per chunk).  Replaces the separate
-// tsgemm_nn launch of round 1 (X written to and re-read from HBM).
-template <int KT>
-struct FusedCfg {
-  static constexpr int VC = 16;                              // k-rows (V columns) per chunk
-  static constexpr int VCH = BlkCfg<KT>::B * VC;             // V chunk (128 x VC, swizzled)
-  static constexpr int ZCH = VC * KT;                        // Z1 chunk (VC x KT, swizzled)
-  static constexpr int CH = VCH + ZCH;                       // doubles per buffer
-};
-static_assert(2 * FusedCfg<64>::CH <= BlkCfg<64>::XS && 2 * FusedCfg<32>::CH <= BlkCfg<32>::XS &&
-                  2 * FusedCfg<16>::CH <= BlkCfg<16>::XS,
-              "fused V / Z1 chunks must fit the Xs region");
-
-template <int KT>
-__device__ __forceinline__ void fused_chunk_load(double* buf, const FusedArgs& a, int ncols, long gr0, long rhi,
-                                                 int c, int tid) {
-  using F = FusedCfg<KT>;
-  load_tile_async(buf, F::VC, a.Vb, a.ldv, gr0, BlkCfg<KT>::B, gr0, rhi, c * F::VC, F::VC, a.kdim, tid, 256);
-  load_tile_async(buf + F::VCH, KT, a.Z1, a.ldz, (long)c * F::VC, F::VC, 0, a.kdim, 0, KT, ncols, tid, 256);
-  cp_async_commit();
-}
-
-template <int KT>
-__device__ __forceinline__ void fused_x(double (&x)[16][2], const FusedArgs& a, int ncols, long gr0, int nb,
-                                        double* Vs, bool owner, int mycol) {
-  using F = FusedCfg<KT>;
-  constexpr int VC = F::VC;
-  const int tid = threadIdx.x, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int nch = (a.kdim + VC - 1) / VC;
-  const long rhi = gr0 + nb;
-  fused_chunk_load<KT>(Vs, a, ncols, gr0, rhi, 0, tid);
-  if (owner) tile_regs_load(x, a.Ab, a.lda, gr0, nb, mycol, ncols);
-  const int wc = mycol - g;                                  // warp's first column (8 w)
-  for (int c = 0; c < nch; ++c) {
-    cp_async_wait<0>();
-    __syncthreads();                                         // chunk c landed; buffer (c+1)&1 free
-    if (c + 1 < nch) fused_chunk_load<KT>(Vs + ((c + 1) & 1) * F::CH, a, ncols, gr0, rhi, c + 1, tid);
-    if (owner) {
-      const double* Vc = Vs + (c & 1) * F::CH;
-      const double* Zc = Vc + F::VCH;
-#pragma unroll
-      for (int kk = 0; kk < VC / 4; ++kk) {
-        const double za = Zc[swz(4 * kk + t, wc + g, KT)];
-#pragma unroll
-        for (int f = 0; f < 16; ++f) dmma(x[f], za, Vc[swz(8 * f + g, 4 * kk + t, VC)]);
-      }
-    }
-  }
-  __syncthreads();                                           // Xs is reused by the panels
-}
-
 // REDO: level-0 redo of the chains the Gram-form factor flagged (gsweep.inc;
 // flag = Rout[chain][KT-1][0] != 0, an entry a chain R leaves 0).  A separate
 // instantiation: the default one is unchanged (ptxas allocation).
@@ -910,370 +854,18 @@ __global__ void __launch_bounds__(256, 2) chain_factor_kernel(FactorArgs a) {
   }
 }
 
-// The fused variant (OTS_FUSE=1, see DESIGN 6b): the unfused kernel above is
-// kept verbatim -- any change to its code or argument record moves ptxas's
-// register allocation of the panel loop (measured +1 ms).
-template <int KT>
-__global__ void __launch_bounds__(256, 2) chain_factor_fused_kernel(FactorArgs a, FusedArgs fz) {
-  constexpr bool FUSED = true;
-  using C = BlkCfg<KT>;
-  constexpr int NP = C::NP;
-  extern __shared__ __align__(128) double S[];   // R (KT x KT), G in its lower part
-  double* Xs = S + KT * KT;                       // tile (swizzled) | head U/T
-  double* Tp = Xs + C::XS;                        // 2 x NP x 64: panel T_pp, by tile parity
-  double* scr = Tp + 2 * NP * 64;                 // 8 warps x 64
-  double* Tw = Xs + C::TWOFF;                     // packed off-diagonal T blocks (previous tile)
-  __shared__ double tau_s[KT];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int chain = blockIdx.x;
-  const long r0 = (long)chain * a.G.rpc;
-  const int ntiles = chain_real_tiles(a.G, chain, KT);
-  double* Tbase = a.U + (long)chain * (a.G.L + 1) * KT * KT;
-  const int b = a.G.b;
-
-  constexpr bool fused = FUSED;      // compile-time: the unfused kernel carries no fused code
-  // ---- head: plain QR of rows [r0, r0+KT) (unblocked smem sweep, once per chain)
-  if constexpr (FUSED) {
-    double xh[16][2];
-    const bool own = warp < NP;
-    const int col = 8 * warp + ((tid & 31) >> 2);
-    const long remh = a.G.nrows - r0;
-    fused_x<KT>(xh, fz, a.ncols, r0, (int)(remh < KT ? remh : KT), Xs, own, col);
-    if (own) {
-      const int t4 = tid & 3;
-#pragma unroll
-      for (int f = 0; f < KT / 8; ++f)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) S[(8 * f + 2 * t4 + h) * KT + col] = xh[f][h];
-    }
-  } else {
-    load_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
-    cp_async_commit();
-    cp_async_wait<0>();
-  }
-  __syncthreads();
-  if (a.head_tri) {
-    // Tree levels: the head is an R factor (exact zeros below the diagonal),
-    // so every dlarfg sees |x| = 0: tau = 0, beta = alpha (LAPACK's shortcut),
-    // R = head, Y = 0, T = 0 -- the unblocked sweep would compute exactly that.
-    for (int e = tid; e < KT * KT; e += 256) Tbase[e] = 0.0;
-  } else {
-    householder_sweep<KT, true, KT>(S, 0, Xs, tau_s);   // U -> Xs (ld KT+1)
-    store_rows_plain<KT, KT>(S, 0, a.D, a.ldd, r0, KT, a.G.nrows, a.ncols, tid, 256);
-    __syncthreads();
-    u_to_t_block<KT>(Xs, Xs + KT * (KT + 1), Tbase);
-    __syncthreads();
-  }
-
-  // ---- structured tiles (register-resident, see BlkCfg)
-  const bool owner = warp < NP;
-  const int mycol = 8 * warp + ((tid & 31) >> 2);
-  double* Ys = Xs;                                  // NSLOT panel slots of Y
-  double x[16][2];
-  if constexpr (FUSED) {
-    if (ntiles > 0) {
-      const long g0 = r0 + KT;
-      const long rem0 = a.G.nrows - g0;
-      fused_x<KT>(x, fz, a.ncols, g0, (int)(rem0 < b ? rem0 : b), Xs, owner, mycol);
-    }
-  } else if (owner && ntiles > 0) {
-    const long g0 = r0 + KT;
-    const long rem0 = a.G.nrows - g0;
-    tile_regs_load(x, a.D, a.ldd, g0, (int)(rem0 < b ? rem0 : b), mycol, a.ncols);
-  }
-  for (int t = 1; t <= ntiles; ++t) {
-    double* Tpc = Tp + (t & 1) * NP * 64;           // this tile's T_pp
-    const double* Tpp = Tp + ((t - 1) & 1) * NP * 64;   // previous tile's (its T is built now)
-    const long gr0 = r0 + KT + (long)(t - 1) * b;
-    const long rem = a.G.nrows - gr0;
-    const int nb = (int)(rem < b ? rem : b);
-    TSTAMP(t1);
-    if (t < ntiles) {   // next tile -> L2 while this one is factored (its load is on the chain)
-      const long g1 = gr0 + b;
-      const long rem1 = a.G.nrows - g1;
-      const int nb1 = (int)(rem1 < b ? rem1 : b);
-      const int lpr = (a.ncols * 8 + 127) / 128;          // 128-byte lines per row
-      const double* src = fused ? fz.Ab : a.D;
-      const long lds_ = fused ? fz.lda : a.ldd;
-      for (int i = tid; i < nb1 * lpr; i += 256) {
-        const int r = i / lpr, l = i - r * lpr;
-        const double* ptr = src + (g1 + r) * lds_ + l * 16;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
-      }
-      if (fused) {     // and the tile's V_b rows
-        const int lpv = (fz.kdim * 8 + 127) / 128;
-        for (int i = tid; i < nb1 * lpv; i += 256) {
-          const int r = i / lpv, l = i - r * lpv;
-          const double* ptr = fz.Vb + (g1 + r) * fz.ldv + l * 16;
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr));
-        }
-      }
-    }
-    // The owner of the next panel (p+1) shares its SM sub-partition with warp
-    // (p+1)^4; that warp defers its DMMA apply of panel p by one iteration so
-    // the latency-bound panel factorisation does not queue behind its DMMAs
-    // on the shared FP64 pipe.  A 3-slot Y ring keeps Y_p alive for it.
-    int pending = -1;
-    for (int p = 0; p < NP; ++p) {
-#ifdef OTS_TIMING
-      long long q0 = clock64();
-#endif
-      if (warp == p) panel_factor<KT>(p, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tpc, tau_s, scr + warp * 64,
-                                      Xs + C::NSLOT * C::YSLOT + warp * 64);
-      else if (t > 1 && warp < p) t_block<KT>(warp, p, S, Tpp, Tw, scr + warp * 64);
-#ifdef OTS_TIMING
-      if (warp == p && (tid & 31) == 0) atomicAdd(&g_dbg[5], (unsigned long long)(clock64() - q0));
-#endif
-      __syncthreads();
-#ifdef OTS_TIMING
-      long long q1 = clock64();
-#endif
-      if (owner && warp != p) {
-        const int defer_w = (p + 1 < NP) ? ((p + 1) ^ 4) : -1;
-        if (pending >= 0) {
-          panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tpc);
-          pending = -1;
-        }
-        if (warp == defer_w) pending = p;
-        else panel_apply<KT>(p, warp, x, S, Ys + (p % C::NSLOT) * C::YSLOT, Tpc);
-      }
-#ifdef OTS_TIMING
-      if (warp == p + 1 && (tid & 31) == 0) atomicAdd(&g_dbg[6], (unsigned long long)(clock64() - q1));
-      if (tid == 0) atomicAdd(&g_dbg[7], (unsigned long long)(clock64() - q0));
-#endif
-    }
-    if (pending >= 0) panel_apply<KT>(pending, warp, x, S, Ys + (pending % C::NSLOT) * C::YSLOT, Tpc);
-    __syncthreads();
-    TSTAMP(t2);
-    TACC(1, t1, t2);
-    // Y (in place of the tile) -> global; next tile -> registers
-    if (owner) {
-      tile_regs_store(x, a.D, a.ldd, gr0, nb, mycol, a.ncols);
-      if (t < ntiles && !fused) {
-        const long g1 = gr0 + b;
-        const long rem1 = a.G.nrows - g1;
-        tile_regs_load(x, a.D, a.ldd, g1, (int)(rem1 < b ? rem1 : b), mycol, a.ncols);
-      }
-    }
-    TSTAMP(t3);
-    TACC(2, t2, t3);
-    if (t > 1) {                    // previous tile's T is complete (phase NP-1 ran in panel NP-1)
-      t_store<KT>(Tpp, Tw, Tbase + (long)(t - 1) * KT * KT);
-      __syncthreads();              // Tpp is this parity's buffer for tile t+1
-    }
-    if (fused && t < ntiles) {      // X of the next tile (Xs: Y slots and Tw are free here)
-      const long g1 = gr0 + b;
-      const long rem1 = a.G.nrows - g1;
-      TSTAMP(f0);
-      fused_x<KT>(x, fz, a.ncols, g1, (int)(rem1 < b ? rem1 : b), Xs, owner, mycol);
-      TSTAMP(f1);
-      TACC(13, f0, f1);
-    }
-    TSTAMP(t4);
-    TACC(3, t3, t4);
-    if (threadIdx.x == 0) TACC(4, 0, 1);
-  }
-  if (ntiles > 0) {                 // last tile: its T phases in sequence
-    const double* Tpl = Tp + (ntiles & 1) * NP * 64;
-    for (int p = 1; p < NP; ++p) {
-      if (warp < p) t_block<KT>(warp, p, S, Tpl, Tw, scr + warp * 64);
-      __syncthreads();
-    }
-    t_store<KT>(Tpl, Tw, Tbase + (long)ntiles * KT * KT);
-  }
-
-  // ---- chain R (upper triangle, exact zeros below)
-  double* R = a.Rout + (long)chain * KT * KT;
-  for (int i = tid; i < KT * KT; i += 256) {
-    int r = i / KT, cc = i - r * KT;
-    R[i] = (cc >= r) ? S[r * KT + cc] : 0.0;
-  }
-}
-
-// head T from U (ld KT+1): T via dlarft recurrence (once per chain)
 // ---------------------------------------------------------------------------
 // Q formation (reverse chain walk).  Per structured tile (reverse order):
 //   M = T C ; out_rows = -Y M ; C <- C - M
 // Head:  W1 = Yt^T C ; M = T W1 ; out_rows(head) = C - Yt M   (Yt unit lower)
 // ---------------------------------------------------------------------------
-template <int KT>
-struct QformCfg {
-  static constexpr int NT = 256;
-  static constexpr int BMAX = FactorCfg<KT>::BMAX;
-  static constexpr int YH = 64;                              // Y rows per half-step
-  static constexpr int SMEM = (2 * KT * KT + YH * KT) * 8;   // C, T|M, Y half
-};
-
-template <int KT, bool TA, bool UPPER_A, bool TB = false>
-__device__ __forceinline__ void kt_gemm(const double* A, const double* B, double (&acc)[KT / 8][2]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-#pragma unroll
-  for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-  if (warp >= KT / 8) return;
-  const int kk0 = UPPER_A ? (2 * warp) : 0;  // A upper triangular: rows 8w.. need k >= 8w
-#pragma unroll 4
-  for (int kk = kk0; kk < KT / 4; ++kk) {
-    double av = TA ? A[swz(4 * kk + t, 8 * warp + g, KT)] : A[swz(8 * warp + g, 4 * kk + t, KT)];
-#pragma unroll
-    for (int j = 0; j < KT / 8; ++j)
-      dmma(acc[j], av, TB ? B[swz(8 * j + g, 4 * kk + t, KT)] : B[swz(4 * kk + t, 8 * j + g, KT)]);
-  }
-}
-
-template <int KT>
-__device__ __forceinline__ void kt_store(double* O, const double (&acc)[KT / 8][2]) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  if (warp >= KT / 8) return;
-#pragma unroll
-  for (int j = 0; j < KT / 8; ++j) {
-    O[swz(8 * warp + g, 8 * j + 2 * t, KT)] = acc[j][0];
-    O[swz(8 * warp + g, 8 * j + 2 * t + 1, KT)] = acc[j][1];
-  }
-}
-
-
-// Tall product out = -Y M over rows [y0, y0+nr) of a tile half in smem
-// (YH x KT), warp tiles 16 x WN, written to global rows grow0.. (< rhi).
-template <int KT>
-__device__ __forceinline__ void qform_half(const double* Ys, const double* Ms, double* D, long ldd, int ncols,
-                                           long grow0, long rhi) {
-  constexpr int YH = QformCfg<KT>::YH;
-  constexpr int WN = KT < 32 ? KT : 32;
-  constexpr int NJ = WN / 8;
-  constexpr int NWN = KT / WN;
-  constexpr int NWT = (YH / 16) * NWN;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  for (int wt = warp; wt < NWT; wt += 8) {
-    const int wm0 = (wt / NWN) * 16, wn0 = (wt % NWN) * WN;
-    double o[2][NJ][2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) o[i][j][0] = o[i][j][1] = 0.0;
-#pragma unroll 4
-    for (int kk = 0; kk < KT / 4; ++kk) {
-      double af[2], bf[NJ];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) af[i] = Ys[swz(wm0 + 8 * i + g, 4 * kk + t4, KT)];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = Ms[swz(4 * kk + t4, wn0 + 8 * j + g, KT)];
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma(o[i][j], af[i], bf[j]);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i)
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) {
-        const long r = grow0 + wm0 + 8 * i + g;
-        const int cc = wn0 + 8 * j + 2 * t4;
-        if (r >= rhi) continue;
-        double* p = D + r * ldd + cc;
-        if (cc + 1 < ncols) *reinterpret_cast<double2*>(p) = make_double2(-o[i][j][0], -o[i][j][1]);
-        else if (cc < ncols) p[0] = -o[i][j][0];
-      }
-  }
-}
-
-template <int KT>
-__global__ void __launch_bounds__(256, 2) chain_qform_kernel(QformArgs a) {
-  using C = QformCfg<KT>;
-  constexpr int YH = C::YH;
-  extern __shared__ __align__(128) double sm[];
-  double* Cs = sm;
-  double* Ts = Cs + KT * KT;    // T, then M = T C in place
-  double* Ys = Ts + KT * KT;    // YH rows of Y
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  const int chain = blockIdx.x;
-  const long r0 = (long)chain * a.G.rpc;
-  const int ntiles = chain_real_tiles(a.G, chain, KT);
-  const double* Tbase = a.T + (long)chain * (a.G.L + 1) * KT * KT;
-
-  load_tile_async(Cs, KT, a.Cin + (long)chain * KT * KT, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
-  cp_async_commit();
-
-  for (int tt = ntiles; tt >= 1; --tt) {
-    const long gr0 = r0 + KT + (long)(tt - 1) * a.G.b;
-    const long rhi = gr0 + a.G.b < a.G.nrows ? gr0 + a.G.b : a.G.nrows;   // this tile only
-    load_tile_async(Ts, KT, Tbase + (long)tt * KT * KT, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
-    load_tile_async(Ys, KT, a.D, a.ldd, gr0, YH, gr0, rhi, 0, KT, a.ncols, tid, C::NT);
-    cp_async_commit();
-    cp_async_wait<0>();
-    __syncthreads();
-    double acc[KT / 8][2];
-    kt_gemm<KT, false, true>(Ts, Cs, acc);  // M = T C
-    __syncthreads();
-    kt_store<KT>(Ts, acc);                  // M over T
-    __syncthreads();
-    for (int e = tid; e < KT * KT; e += C::NT) Cs[e] -= Ts[e];   // C <- C - M (same swizzle)
-    for (int h = 0; h * YH < a.G.b; ++h) {
-      const long y0 = gr0 + (long)h * YH;
-      if (y0 >= rhi) break;
-      if (h > 0) {
-        __syncthreads();
-        load_tile_async(Ys, KT, a.D, a.ldd, y0, YH, y0, rhi, 0, KT, a.ncols, tid, C::NT);
-        cp_async_commit();
-        cp_async_wait<0>();
-        __syncthreads();
-      }
-      qform_half<KT>(Ys, Ts, a.D, a.ldd, a.ncols, y0, rhi);
-    }
-    __syncthreads();
-  }
-
-  // ---- head (Yt unit lower, from the stored head block): rows [r0, r0+KT)
-  double* Yt = Ys;   // KT <= YH rows
-  load_tile_async(Ts, KT, Tbase, KT, 0, KT, 0, KT, 0, KT, KT, tid, C::NT);
-  load_tile_async(Yt, KT, a.D, a.ldd, r0, KT, r0, (r0 + KT < a.G.nrows ? r0 + KT : a.G.nrows), 0, KT,
-                  a.ncols, tid, C::NT);
-  cp_async_commit();
-  cp_async_wait<0>();
-  __syncthreads();
-  for (int e = tid; e < KT * KT; e += C::NT) {  // Yt: unit lower
-    int r = e / KT, cc = e - r * KT;
-    if (cc >= r) Yt[swz(r, cc, KT)] = (cc == r) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  // out = C - Yt T Yt^T C = C - Yt M,  M = (T Yt^T) C  (all in smem)
-  double acc[KT / 8][2];
-  kt_gemm<KT, false, true, true>(Ts, Yt, acc);   // N = T Yt^T
-  __syncthreads();
-  kt_store<KT>(Ts, acc);
-  __syncthreads();
-  kt_gemm<KT, false, false>(Ts, Cs, acc);        // M = N C
-  __syncthreads();
-  kt_store<KT>(Ts, acc);
-  __syncthreads();
-  kt_gemm<KT, false, false>(Yt, Ts, acc);        // Yt M
-  if (warp < KT / 8) {
-#pragma unroll
-    for (int j = 0; j < KT / 8; ++j) {
-      int r = 8 * warp + g;
-      int cc = 8 * j + 2 * t4;
-      long gr = r0 + r;
-      if (gr >= a.G.nrows) continue;
-      double y0 = Cs[swz(r, cc, KT)] - acc[j][0];
-      double y1 = Cs[swz(r, cc + 1, KT)] - acc[j][1];
-      double* p = a.D + gr * a.ldd + cc;
-      if (cc + 1 < a.ncols) *reinterpret_cast<double2*>(p) = make_double2(y0, y1);
-      else if (cc < a.ncols) p[0] = y0;
-    }
-  }
-}
-
-#include "gsweep.inc"
 
 // ---------------------------------------------------------------------------
 template <int KT>
-static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st, const FusedArgs* fz) {
+static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st) {
   using C = BlkCfg<KT>;
   if (a.G.b > C::B || a.G.nchains <= 0) return cudaErrorInvalidValue;
-  if (fz && fz->Vb) {
-    auto k = chain_factor_fused_kernel<KT>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    k<<<a.G.nchains, 256, C::SMEM, st>>>(a, *fz);
-  } else if (a.head_tri == 2) {
+  if (a.head_tri == 2) {
     if constexpr (KT == 64) {
       FactorArgs b = a;
       b.head_tri = 0;
@@ -1291,10 +883,10 @@ static cudaError_t factor_t(const FactorArgs& a, cudaStream_t st, const FusedArg
   return cudaGetLastError();
 }
 
-cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st, const FusedArgs* fz) {
-  if (KT == 16) return factor_t<16>(a, st, fz);
-  if (KT == 32) return factor_t<32>(a, st, fz);
-  if (KT == 64) return factor_t<64>(a, st, fz);
+cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st) {
+  if (KT == 16) return factor_t<16>(a, st);
+  if (KT == 32) return factor_t<32>(a, st);
+  if (KT == 64) return factor_t<64>(a, st);
   return cudaErrorInvalidValue;
 }
 
@@ -1391,6 +983,78 @@ __device__ __forceinline__ void q2_ym(const double* Ys, const double* Ms, double
     }
 }
 
+// Head rows [r0, r0 + KT) of a chain: out = C - Yt (T Yt^T) C with Yt the
+// head's unit lower Householder block (smem, swizzled; its upper part is
+// overwritten here), T in Ts; Ms is scratch.  Called by all threads.
+template <int KT>
+__device__ __forceinline__ void q2_head(double* Ts, double* Yt, double* Ms, const double* Cs, double* D, long ldd,
+                                        int ncols, long r0, long nrows) {
+  constexpr int NT = Qform2Cfg<KT>::NT;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  for (int e = tid; e < KT * KT; e += NT) {
+    const int r = e / KT, cc = e - r * KT;
+    if (cc >= r) Yt[swz(r, cc, KT)] = (cc == r) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  // N = T Yt^T -> Ms (first 8 warps, row blocks), then M = N C -> Ts
+  if (warp < KT / 8) {
+    double acc[KT / 8][2];
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 2 * warp; kk < KT / 4; ++kk) {
+      const double av = Ts[swz(8 * warp + g, 4 * kk + t4, KT)];
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Yt[swz(8 * j + g, 4 * kk + t4, KT)]);
+    }
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) {
+      Ms[swz(8 * warp + g, 8 * j + 2 * t4, KT)] = acc[j][0];
+      Ms[swz(8 * warp + g, 8 * j + 2 * t4 + 1, KT)] = acc[j][1];
+    }
+  }
+  __syncthreads();
+  if (warp < KT / 8) {
+    double acc[KT / 8][2];
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < KT / 4; ++kk) {
+      const double av = Ms[swz(8 * warp + g, 4 * kk + t4, KT)];
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Cs[swz(4 * kk + t4, 8 * j + g, KT)]);
+    }
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) {
+      Ts[swz(8 * warp + g, 8 * j + 2 * t4, KT)] = acc[j][0];
+      Ts[swz(8 * warp + g, 8 * j + 2 * t4 + 1, KT)] = acc[j][1];
+    }
+  }
+  __syncthreads();
+  if (warp < KT / 8) {
+    double acc[KT / 8][2];
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < KT / 4; ++kk) {
+      const double av = Yt[swz(8 * warp + g, 4 * kk + t4, KT)];
+#pragma unroll
+      for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Ts[swz(4 * kk + t4, 8 * j + g, KT)]);
+    }
+#pragma unroll
+    for (int j = 0; j < KT / 8; ++j) {
+      const int r = 8 * warp + g, cc = 8 * j + 2 * t4;
+      const long gr = r0 + r;
+      if (gr >= nrows) continue;
+      const double y0 = Cs[swz(r, cc, KT)] - acc[j][0];
+      const double y1 = Cs[swz(r, cc + 1, KT)] - acc[j][1];
+      double* p = D + gr * ldd + cc;
+      if (cc + 1 < ncols) *reinterpret_cast<double2*>(p) = make_double2(y0, y1);
+      else if (cc < ncols) p[0] = y0;
+    }
+  }
+}
+
 template <int KT>
 __global__ void __launch_bounds__(512, 1) chain_qform2_kernel(QformArgs a) {
   using C = Qform2Cfg<KT>;
@@ -1400,11 +1064,12 @@ __global__ void __launch_bounds__(512, 1) chain_qform2_kernel(QformArgs a) {
   double* Ts = Cs + KT * KT;
   double* Ms = Ts + KT * KT;
   double* Yb = Ms + KT * KT;          // 2 x (B x KT)
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int tid = threadIdx.x;
   for (int chain = blockIdx.x; chain < a.G.nchains; chain += gridDim.x) {
+    if (a.mode == 1 && !a.flags[chain]) continue;   // Gram-form level 0: accepted chain
     const long r0 = (long)chain * a.G.rpc;
     const int ntiles = chain_real_tiles(a.G, chain, KT);
-    const double* Tbase = a.T + (long)chain * (a.G.L + 1) * KT * KT;
+    const double* Tbase = a.T + (long)chain * (a.tslots ? a.tslots : a.G.L + 1) * KT * KT;
     auto tile_rows = [&](int tt, long& gr0, long& rhi) {
       gr0 = r0 + KT + (long)(tt - 1) * a.G.b;
       rhi = gr0 + a.G.b < a.G.nrows ? gr0 + a.G.b : a.G.nrows;
@@ -1441,71 +1106,11 @@ __global__ void __launch_bounds__(512, 1) chain_qform2_kernel(QformArgs a) {
     // ---- head: out = C - Yt (T Yt^T) C  (Yt unit lower)
     cp_async_wait<0>();
     __syncthreads();
-    double* Yt = Yb + buf * B * KT;
-    for (int e = tid; e < KT * KT; e += C::NT) {
-      const int r = e / KT, cc = e - r * KT;
-      if (cc >= r) Yt[swz(r, cc, KT)] = (cc == r) ? 1.0 : 0.0;
-    }
-    __syncthreads();
-    // N = T Yt^T -> Ms (first 8 warps, row blocks), then M = N C -> Ts
-    if (warp < KT / 8) {
-      double acc[KT / 8][2];
-#pragma unroll
-      for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll 4
-      for (int kk = 2 * warp; kk < KT / 4; ++kk) {
-        const double av = Ts[swz(8 * warp + g, 4 * kk + t4, KT)];
-#pragma unroll
-        for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Yt[swz(8 * j + g, 4 * kk + t4, KT)]);
-      }
-#pragma unroll
-      for (int j = 0; j < KT / 8; ++j) {
-        Ms[swz(8 * warp + g, 8 * j + 2 * t4, KT)] = acc[j][0];
-        Ms[swz(8 * warp + g, 8 * j + 2 * t4 + 1, KT)] = acc[j][1];
-      }
-    }
-    __syncthreads();
-    if (warp < KT / 8) {
-      double acc[KT / 8][2];
-#pragma unroll
-      for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll 4
-      for (int kk = 0; kk < KT / 4; ++kk) {
-        const double av = Ms[swz(8 * warp + g, 4 * kk + t4, KT)];
-#pragma unroll
-        for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Cs[swz(4 * kk + t4, 8 * j + g, KT)]);
-      }
-#pragma unroll
-      for (int j = 0; j < KT / 8; ++j) {
-        Ts[swz(8 * warp + g, 8 * j + 2 * t4, KT)] = acc[j][0];
-        Ts[swz(8 * warp + g, 8 * j + 2 * t4 + 1, KT)] = acc[j][1];
-      }
-    }
-    __syncthreads();
-    if (warp < KT / 8) {
-      double acc[KT / 8][2];
-#pragma unroll
-      for (int j = 0; j < KT / 8; ++j) acc[j][0] = acc[j][1] = 0.0;
-#pragma unroll 4
-      for (int kk = 0; kk < KT / 4; ++kk) {
-        const double av = Yt[swz(8 * warp + g, 4 * kk + t4, KT)];
-#pragma unroll
-        for (int j = 0; j < KT / 8; ++j) dmma(acc[j], av, Ts[swz(4 * kk + t4, 8 * j + g, KT)]);
-      }
-#pragma unroll
-      for (int j = 0; j < KT / 8; ++j) {
-        const int r = 8 * warp + g, cc = 8 * j + 2 * t4;
-        const long gr = r0 + r;
-        if (gr >= a.G.nrows) continue;
-        const double y0 = Cs[swz(r, cc, KT)] - acc[j][0];
-        const double y1 = Cs[swz(r, cc + 1, KT)] - acc[j][1];
-        double* p = a.D + gr * a.ldd + cc;
-        if (cc + 1 < a.ncols) *reinterpret_cast<double2*>(p) = make_double2(y0, y1);
-        else if (cc < a.ncols) p[0] = y0;
-      }
-    }
+    q2_head<KT>(Ts, Yb + buf * B * KT, Ms, Cs, a.D, a.ldd, a.ncols, r0, a.G.nrows);
   }
 }
+
+#include "gsweep.inc"
 
 template <int KT>
 static cudaError_t qform_t(const QformArgs& a, cudaStream_t st) {

@@ -44,31 +44,23 @@ struct FactorArgs {
                          // factor flagged (chain_factor_kernel<KT, true>)
 };
 
-// Gram-form tile factorization of level 0 (KT = 64; gsweep in chainqr.cu).
-// Pass 1 reads X (never writes it) and per tile produces T, the coefficient
-// matrix Cc with Y = X_tile Cc, and the running chain R; a chain whose tiles
-// fail the cancellation bound is flagged (Rout[chain][KT-1][0] = 1) and redone
-// by the exact register-tile kernel (FactorArgs::head_tri = 2) after pass 2
-// (Y = X Cc in place) has skipped it.
+// Gram-form tile factorization of level 0 (KT = 64; gsweep.inc).  Pass 1
+// reads X (never writes it) and per tall tile (G.b rows, a multiple of 128)
+// produces T, the coefficient matrix Cc with Y = X_tile Cc, and the running
+// chain R; a chain whose tiles fail the cancellation bound is flagged
+// (flags[chain] = 1 and Rout[chain][KT-1][0] = 1) and redone by the exact
+// register-tile kernel on 128-row tiles of the same chain rows
+// (FactorArgs::head_tri = 2).  Y is never formed: the Q formation of an
+// accepted chain computes Q_tile = -X_tile (Cc T C) directly.
 struct GsweepArgs {
-  double* D; long ldd; int ncols;   // level-0 rows (X in, Y out after pass 2)
-  ChainGeom G;
-  double* U;             // T per tile (FactorArgs::U indexing)
+  double* D; long ldd; int ncols;   // level-0 rows (X in, untouched)
+  ChainGeom G;           // tall-tile geometry
+  double* U;             // T per tile: chain * tslots + t
   double* Rout;          // chain R's
-  double* Cc;            // per tile KT*KT (same indexing as U; tile 0 unused)
+  double* Cc;            // per tile KT*KT (chain * (G.L+1) + t; tile 0 unused)
   double* Hs;            // head rows per chain (KT x KT): R upper, V strictly lower
-};
-
-// Fused inter-block update for the chain factor's level 0 (opt-in): the
-// kernel forms each tile of X = A_b + V_b Z1 (twostage.py:91-93,
-// reflector.py:238) on the fly -- A_b and V_b rows of the tile, Z1 k0 x k --
-// instead of reading an X written by a separate apply kernel; Y still goes to
-// FactorArgs::D (same row numbering as X).  A separate record: a larger
-// FactorArgs alone costs the unfused kernel register spills.
-struct FusedArgs {
-  const double* Vb = nullptr; long ldv = 0; int kdim = 0;
-  const double* Z1 = nullptr; long ldz = 0;
-  const double* Ab = nullptr; long lda = 0;
+  int* flags;            // per chain: 1 = redo exactly (128-row tiles)
+  long tslots;           // T slots per chain (the 128-row geometry's L + 1)
 };
 
 struct QformArgs {
@@ -77,6 +69,14 @@ struct QformArgs {
   const double* T;       // per tile KT*KT
   const double* Cin;     // stacked chain C's (chain*KT rows, ld KT)
   int grid_max = 0;      // CTAs at most (0: one per SM)
+  // level 0 of the Gram-form factor (GsweepArgs): mode 1 forms only the
+  // flagged chains (128-row geometry G, Y in D), mode 2 only the accepted
+  // ones (tall geometry G, X in D, Cc / Hs); mode 0 every chain
+  int mode = 0;
+  const double* Cc = nullptr;
+  const double* Hs = nullptr;
+  const int* flags = nullptr;
+  long tslots = 0;       // T slots per chain (0: G.L + 1)
 };
 
 cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid, cudaStream_t st);
@@ -84,10 +84,10 @@ cudaError_t launch_reduce(const double* partial, int nparts, long count, double*
 cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, int cols, int ldp, double* out,
                                   long ldo, double alpha, cudaStream_t st);
 cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
-cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st, const FusedArgs* fz = nullptr);
+cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_chain_gsweep(const GsweepArgs& a, cudaStream_t st);
-cudaError_t launch_gs_apply(const GsweepArgs& a, int nsm, cudaStream_t st);
+cudaError_t launch_gs_qform(const QformArgs& a, cudaStream_t st);
 // complex128 TSQR (zchain.cu): same argument records, pointers to interleaved
 // (re, im) data, leading dimensions in complex units
 using ZFactorArgs = FactorArgs;

@@ -96,6 +96,8 @@ struct Level {
   double* R;      // stacked chain R's (nchains * KT rows, ld KT)
   double* CC = nullptr;   // level 0, KT = 64: per-tile Cc of the Gram-form factor
   double* HS = nullptr;   //   head rows per chain
+  int* FL = nullptr;      //   per-chain redo flags
+  ChainGeom G128{};       //   the same chains on 128-row tiles (exact redo)
 };
 
 }  // namespace
@@ -233,14 +235,35 @@ long chains_per_sm() {
   return v;
 }
 
-// The Gram-form level-0 factor (gsweep.inc) for KT = 64, opt-in with
-// OTS_GSWEEP=1 while it is slower than the register-tile kernel.
+// The Gram-form level-0 factor (gsweep.inc) for KT = 64 on tall tiles of
+// gs_tile_rows() rows (default 2048; OTS_GS_B overrides, a multiple of 128);
+// OTS_GSWEEP=0 selects the register-tile kernel for every chain.
 bool gsweep_on(int KT, int b) {
   static int v = [] {
     const char* e = getenv("OTS_GSWEEP");
-    return e ? atoi(e) : 0;
+    return e ? atoi(e) : 1;
   }();
   return v != 0 && KT == 64 && b == 128;
+}
+
+int gs_tile_rows() {
+  static int v = [] {
+    const char* e = getenv("OTS_GS_B");
+    int x = e ? atoi(e) : 2048;
+    return (x >= 128 && x % 128 == 0) ? x : 2048;
+  }();
+  return v;
+}
+
+// level-0 chain geometry: tiles of b rows, rows split over chains_per_sm * nsm chains
+ChainGeom level0_geom(long m, int KT, int b, int nsm) {
+  long target = chains_per_sm() * nsm;
+  long per = (m + target - 1) / target;
+  long Lt = per > KT ? (per - KT + b - 1) / b : 0;
+  long rpc = KT + Lt * b;
+  long nch = (m + rpc - 1) / rpc;
+  if (nch < 1) nch = 1;
+  return ChainGeom{m, b, (int)Lt, rpc, (int)nch};
 }
 
 std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, long m, int KT, int nsm) {
@@ -251,19 +274,20 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     L.D = D0; L.ldd = ldd0; L.ncols = ncols0;
     int b = chain_bmax(KT);
     if (b > 128 && KT == 64) b = 128;
-    long target = chains_per_sm() * nsm;
-    long per = (m + target - 1) / target;
-    long Lt = per > KT ? (per - KT + b - 1) / b : 0;
-    long rpc = KT + Lt * b;
-    long nch = (m + rpc - 1) / rpc;
-    if (nch < 1) nch = 1;
-    L.G = ChainGeom{m, b, (int)Lt, rpc, (int)nch};
-    L.UT = ar.take<double>((size_t)nch * (Lt + 1) * KT * KT);
-    L.R = ar.take<double>((size_t)nch * KT * KT);
-    if (gsweep_on(KT, b)) {
-      L.CC = ar.take<double>((size_t)nch * (Lt + 1) * KT * KT);
+    const bool gs = gsweep_on(KT, b);
+    L.G = level0_geom(m, KT, gs ? gs_tile_rows() : b, nsm);
+    const long nch = L.G.nchains;
+    if (gs) {
+      const int f = L.G.b / b;
+      L.G128 = ChainGeom{m, b, L.G.L * f, L.G.rpc, L.G.nchains};
+      L.UT = ar.take<double>((size_t)nch * (L.G128.L + 1) * KT * KT);
+      L.CC = ar.take<double>((size_t)nch * (L.G.L + 1) * KT * KT);
       L.HS = ar.take<double>((size_t)nch * KT * KT);
+      L.FL = ar.take<int>((size_t)nch);
+    } else {
+      L.UT = ar.take<double>((size_t)nch * (L.G.L + 1) * KT * KT);
     }
+    L.R = ar.take<double>((size_t)nch * KT * KT);
     lv.push_back(L);
   }
   while (lv.back().G.nchains > 1) {
@@ -287,14 +311,12 @@ size_t plan_levels_bytes(long m, int KT, int nsm) {
   size_t tot = 0;
   int b = chain_bmax(KT);
   if (b > 128 && KT == 64) b = 128;
-  long target = chains_per_sm() * nsm;
-  long per = (m + target - 1) / target;
-  long Lt = per > KT ? (per - KT + b - 1) / b : 0;
-  long rpc = KT + Lt * b;
-  long nch = (m + rpc - 1) / rpc;
-  if (nch < 1) nch = 1;
-  tot += ((size_t)nch * (Lt + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + 512;
-  if (gsweep_on(KT, b)) tot += ((size_t)nch * (Lt + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + nch * 4 + 1536;
+  const bool gs = gsweep_on(KT, b);
+  const ChainGeom G = level0_geom(m, KT, gs ? gs_tile_rows() : b, nsm);
+  long nch = G.nchains;
+  const long tslots = gs ? (long)G.L * (G.b / b) + 1 : G.L + 1;
+  tot += ((size_t)nch * tslots * KT * KT + (size_t)nch * KT * KT) * 8 + 512;
+  if (gs) tot += ((size_t)nch * (G.L + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + nch * 4 + 1536;
   while (nch > 1) {
     long nrows = nch * KT;
     long rpc2 = (long)KT * 4;
@@ -318,38 +340,24 @@ int ensure_ws(ots_ctx* ctx, size_t bytes) {
 
 // tri_first: level 0's rows are already stacked R factors (the global tree);
 // levels >= 1 always are.
-// fuse0 (optional): level 0 forms X = A_b + V_b Z1 tile by tile inside the
-// factor (FactorArgs fused fields) instead of reading an X in L.D.
-int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st, bool tri_first = false,
-                      const FusedArgs* fuse0 = nullptr) {
+int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t st, bool tri_first = false) {
   for (size_t l = 0; l < lv.size(); ++l) {
     Level& L = lv[l];
     FactorArgs fa{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, (l > 0 || tri_first) ? 1 : 0};
-    if (l == 0 && !tri_first && !(fuse0 && fuse0->Vb) && L.CC) {
-      // Gram-form tiles; chains beyond the cancellation bound are redone by
-      // the register-tile kernel (X untouched until the Y pass)
-      GsweepArgs ga{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, L.CC, L.HS};
+    if (l == 0 && !tri_first && L.CC) {
+      // Gram-form tall tiles (X untouched); chains beyond the cancellation
+      // bound are redone by the register-tile kernel on 128-row tiles
+      GsweepArgs ga{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, L.CC, L.HS, L.FL, (long)L.G128.L + 1};
       CK(launch_chain_gsweep(ga, st));
       prof_mark(ctx, st, "gs_sweep");
-      CK(launch_gs_apply(ga, ctx->nsm, st));          // skips the flagged chains
-      prof_mark(ctx, st, "gs_apply");
+      fa.G = L.G128;
       fa.head_tri = 2;                                 // redo the flagged chains exactly
-      CK(launch_chain_factor(fa, KT, st, nullptr));
+      CK(launch_chain_factor(fa, KT, st));
       continue;
     }
-    CK(launch_chain_factor(fa, KT, st, l == 0 ? fuse0 : nullptr));
+    CK(launch_chain_factor(fa, KT, st));
   }
   return OTS_OK;
-}
-
-// level-0 fused-update arguments of a job (X rows start at V/A row qrow0)
-FusedArgs fused_args(const Job& j) {
-  const JobCfg& c = j.c;
-  FusedArgs f{};
-  f.Vb = c.V + (long)j.qrow0 * c.ldv; f.ldv = c.ldv; f.kdim = (int)c.k0;
-  f.Z1 = j.s.Z1; f.ldz = j.ld;
-  f.Ab = c.A + (long)j.qrow0 * c.lda; f.lda = c.lda;
-  return f;
 }
 
 // Q-form from the top level (whose single chain gets C = Ctop) down to level 0.
@@ -359,7 +367,22 @@ int run_qform_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, const double*
   for (int l = (int)lv.size() - 1; l >= 0; --l) {
     Level& L = lv[l];
     QformArgs qa{L.D, L.ldd, L.ncols, L.G, L.UT, Cin, grid_max};
-    CK(launch_chain_qform(qa, KT, st));
+    if (L.CC) {
+      // Gram-form level 0: flagged chains from Y (128-row tiles), accepted
+      // ones from X and Cc (tall tiles)
+      qa.G = L.G128;
+      qa.mode = 1;
+      qa.flags = L.FL;
+      qa.tslots = (long)L.G128.L + 1;
+      CK(launch_chain_qform(qa, KT, st));
+      qa.G = L.G;
+      qa.mode = 2;
+      qa.Cc = L.CC;
+      qa.Hs = L.HS;
+      CK(launch_gs_qform(qa, st));
+    } else {
+      CK(launch_chain_qform(qa, KT, st));
+    }
     Cin = L.D;  // output rows of level l are the C's of level l-1's chains
   }
   return OTS_OK;
@@ -789,22 +812,11 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // an event a little later) fill the rest; apply1 hands out its tiles
   // dynamically, so those 3 SMs simply take fewer.  The factor then starts on
   // an idle GPU instead of waiting for the diagnostics' SMs.
-  // Optional (OTS_FUSE=1): the update X = A_b + V_b Z1 fused into the
-  // factor's level 0 (no apply1 launch, X never goes through HBM; the
-  // diagnostics then run beside apply2).  Measured slower at the headline
-  // (factor 32.4 ms vs factor 20.1 + apply1 9.9): the fused update's 4096
-  // DMMAs per tile compete with the other resident CTA's latency-bound panel
-  // chain for the FP64 pipe, so it is off by default.
-  static const bool want_fuse = getenv("OTS_FUSE") != nullptr && getenv("OTS_FUSE")[0] == '1';
-  const bool fuse = want_fuse && (intra == OTS_INTRA_HOUSEHOLDER) && c.k0 > 0;
-  const FusedArgs fa0 = fused_args(j);
   if (diag_side) {
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
     CK(launch_diag(j.s, ctx->side));
     CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // waited for before the status read
-    if (!fuse && (rc = phase_apply1(ctx, j))) return rc;
-  } else if (fuse) {
-    // diagnostics deferred (beside apply2)
+    if ((rc = phase_apply1(ctx, j))) return rc;
   } else {
     CK(launch_diag(j.s, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
@@ -816,9 +828,9 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply1 done
     CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   }
-  if (!fuse) prof_mark(ctx, st, "apply1");
+  prof_mark(ctx, st, "apply1");
   if (intra == OTS_INTRA_HOUSEHOLDER) {
-    if ((rc = run_factor_levels(ctx, j.lv, KT, st, false, fuse ? &fa0 : nullptr))) return rc;
+    if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
     prof_mark(ctx, st, "factor");
     set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
     if ((rc = run_qform_levels(ctx, j.lv, KT, j.ident, st, diag_side ? j.nsm_use : 0))) return rc;
@@ -834,20 +846,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
   CK(launch_z2(j.s, st));
   prof_mark(ctx, st, "z2");
-  if (fuse && !diag_side) {
-    // diagnostics (3 CTAs, ~2 ms) on the main stream first so they own their
-    // SMs before apply2's CTAs (side stream, dynamic tiles) fill the rest
-    CK(cudaEventRecord(ctx->ev_seedA, st));
-    CK(launch_diag(j.s, st));
-    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seedA, 0));
-    JobCfg c1 = j.c;
-    j.c.st = ctx->side;
-    rc = phase_apply2(ctx, j);
-    j.c = c1;
-    if (rc) return rc;
-    CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply2 done
-    CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
-  } else if ((rc = phase_apply2(ctx, j))) {
+  if ((rc = phase_apply2(ctx, j))) {
     return rc;
   }
   prof_mark(ctx, st, "apply2");
@@ -866,7 +865,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   prof_mark(ctx, st, "tail");
   // gram, reduce, seed(B), diag, apply1, identity, sign, gram2, reduce, copy_y2,
   // z2, apply2, qtop + a factor and a qform launch per level (+ seedA, B epilogue)
-  ctx->launches = 13 + 2 * (int)j.lv.size() + (bh ? 2 : 0) + (split_seed ? 1 : 0) - (fuse ? 1 : 0);
+  ctx->launches = 13 + 2 * (int)j.lv.size() + (bh ? 2 : 0) + (split_seed ? 1 : 0);
   rc = read_status(ctx, j, diag_host);
   prof_end(ctx);
   return rc;

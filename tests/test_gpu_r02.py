@@ -272,41 +272,20 @@ def test_householder_nonfinite_cabi():
         P.two_stage_qr(np.zeros((5000, 0)), x)
 
 
-def test_fused_update_factor_parity():
-    """OTS_FUSE=1 (update X = A_b + V_b Z1 formed inside the chain factor):
-    same results as the oracle (run in a subprocess: the switch is read once)."""
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, sys; sys.path.insert(0, '.');"
-        "import paper_2602_14449_b200 as P; from oracle import twostage_oracle as O;"
-        "from paper_2602_14449_b200 import workloads as W\n"
-        "for n, k0, k in ((1 << 16, 128, 64), (40000, 13, 7), (30000, 100, 33)):\n"
-        "    rng = W.make_rng(n + k0); v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0));"
-        " a = W.normal_matrix(rng, n, k)\n"
-        "    ref = O.two_stage(v, a, 'qr', diagnostics=False); res = P.two_stage_qr(v, a)\n"
-        "    for key in 'qrs':\n"
-        "        x, y = getattr(res, key), ref[key]\n"
-        "        e = float((np.abs(x - y) / (np.abs(y) + 1e-4 * np.abs(y).max())).max())\n"
-        "        assert e < 1e-10, (n, k0, k, key, e)\n"
-        "print('fused ok')\n")
-    env = dict(os.environ, OTS_FUSE="1")
-    out = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(ROOT), env=env,
-                         capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "fused ok" in out.stdout, out.stdout + out.stderr
-
-
 def test_gram_form_factor_parity_and_redo():
-    """OTS_GSWEEP=1 (Gram-form level-0 tiles, gsweep.inc): oracle parity on
-    well-conditioned shapes (Gram path) and on configs[1]-like data whose
-    chains fail the cancellation bound and are redone by the exact kernel."""
+    """Level-0 factor variants, each in a fresh process (the switches are read
+    once): the register-tile kernel for every chain (OTS_GSWEEP=0) and the
+    Gram-form tall tiles at 128 / 1024 / 4096 rows (default 2048 runs in every
+    other test).  Oracle parity on well-conditioned shapes and, on
+    configs[1]-like data whose chains fail the cancellation bound and are
+    redone by the exact kernel, the 10 n u stability bounds."""
     import subprocess
     import sys
     code = (
         "import numpy as np, sys; sys.path.insert(0, '.');"
         "import paper_2602_14449_b200 as P; from oracle import twostage_oracle as O;"
         "from paper_2602_14449_b200 import workloads as W\n"
-        "for n, k0, k in ((1 << 16, 128, 64), (100003, 32, 48), (3000, 16, 40)):\n"
+        "for n, k0, k in ((1 << 16, 128, 64), (100003, 32, 48), (3000, 16, 40), (300000, 64, 64), (5000, 8, 64)):\n"
         "    rng = W.make_rng(n + k0); v, _ = np.linalg.qr(W.normal_matrix(rng, n, k0));"
         " a = W.normal_matrix(rng, n, k)\n"
         "    ref = O.two_stage(v, a, 'qr', diagnostics=False); res = P.two_stage_qr(v, a)\n"
@@ -322,10 +301,11 @@ def test_gram_form_factor_parity_and_redo():
         "res = P.two_stage_qr(v, a); m = P.compute_metrics(v, a, res)\n"
         "assert m.loss_orth < 10 * n * 2.0 ** -53 and m.rel_residual < 10 * n * 2.0 ** -53, m\n"
         "print('gsweep ok')\n")
-    env = dict(os.environ, OTS_GSWEEP="1")
-    out = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(ROOT), env=env,
-                         capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "gsweep ok" in out.stdout, out.stdout + out.stderr
+    for extra in ({"OTS_GSWEEP": "0"}, {"OTS_GS_B": "128"}, {"OTS_GS_B": "1024"}, {"OTS_GS_B": "4096"}):
+        env = dict(os.environ, **extra)
+        out = subprocess.run([sys.executable, "-c", code], cwd=os.path.dirname(ROOT), env=env,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0 and "gsweep ok" in out.stdout, (extra, out.stdout + out.stderr)
 
 
 # ----------------------------------------------------------------- wide shapes (k > 64)

@@ -1,7 +1,7 @@
 """Gram-form level-0 factor (gsweep) vs the register-tile kernel and the
 oracle: parity on assorted shapes, fallback on ill-conditioned inputs, and
-timing of the headline call with OTS_GSWEEP=1/0 (run each mode in a fresh
-process: the switch is read once per process)."""
+timing of the headline call with OTS_GSWEEP=0 and per tall-tile height
+OTS_GS_B (argv; each mode in a fresh process: the switches are read once)."""
 import json
 import os
 import subprocess
@@ -82,10 +82,14 @@ if __name__ == "__main__":
         print(json.dumps(timing()))
     else:
         res = {}
-        for mode in ("1", "0"):
-            env = dict(os.environ, OTS_GSWEEP=mode)
-            for what in ("parity", "time"):
+        modes = [("gs0", {"OTS_GSWEEP": "0"}, ("parity", "time"))]
+        for b in sys.argv[1:] or ["1024"]:
+            modes.append((f"b{b}", {"OTS_GSWEEP": "1", "OTS_GS_B": b}, ("parity", "time")))
+        for tag, extra, whats in modes:
+            env = dict(os.environ, **extra)
+            for what in whats:
                 r = subprocess.run([sys.executable, __file__, "child-" + what], env=env, capture_output=True, text=True)
-                res[f"{what}_gs{mode}"] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else \
+                res[f"{what}_{tag}"] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else \
                     {"rc": r.returncode, "err": r.stderr[-2000:]}
+                print(tag, what, json.dumps(res[f"{what}_{tag}"]), flush=True)
         print(json.dumps(res, indent=1))
