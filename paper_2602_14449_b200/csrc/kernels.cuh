@@ -86,6 +86,7 @@ cudaError_t launch_reduce_strided(const double* partial, int nparts, int rows, i
 cudaError_t launch_tsgemm_nn(const NnArgs& a, int KT, int nsm, cudaStream_t st);
 cudaError_t launch_chain_factor(const FactorArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
+cudaError_t launch_gs_gram(const GsweepArgs& a, cudaStream_t st);
 cudaError_t launch_chain_gsweep(const GsweepArgs& a, cudaStream_t st);
 cudaError_t launch_gs_qform(const QformArgs& a, cudaStream_t st);
 // complex128 TSQR (zchain.cu): same argument records, pointers to interleaved

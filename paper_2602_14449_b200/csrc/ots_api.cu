@@ -348,6 +348,8 @@ int run_factor_levels(ots_ctx* ctx, std::vector<Level>& lv, int KT, cudaStream_t
       // Gram-form tall tiles (X untouched); chains beyond the cancellation
       // bound are redone by the register-tile kernel on 128-row tiles
       GsweepArgs ga{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, L.CC, L.HS, L.FL, (long)L.G128.L + 1};
+      CK(launch_gs_gram(ga, st));
+      prof_mark(ctx, st, "gs_gram");
       CK(launch_chain_gsweep(ga, st));
       prof_mark(ctx, st, "gs_sweep");
       fa.G = L.G128;
