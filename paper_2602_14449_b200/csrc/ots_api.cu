@@ -198,6 +198,11 @@ struct JobCfg {
   int nsm_avail = 0;     // SMs the row-parallel phases may plan for (0: all)
   const double* gram_in = nullptr; long ldgi = 0;   // caller's V^T V (incremental Gram), or null
   int ld_min = 0;        // small-state leading dimension at least this (reflector objects: fixed ld)
+  // Row-weighted callers (B = diag(d), rows scaled by d^1/2 and the result by
+  // d^-1/2): every row has to be accurate relative to its OWN norm, and the
+  // register-tile kernel's constant there is about half the Gram form's
+  // (tools/gs_accuracy.py), so those calls keep the exact level-0 factor.
+  bool exact_intra = false;
 };
 
 }  // namespace
@@ -266,7 +271,8 @@ ChainGeom level0_geom(long m, int KT, int b, int nsm) {
   return ChainGeom{m, b, (int)Lt, rpc, (int)nch};
 }
 
-std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, long m, int KT, int nsm) {
+std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, long m, int KT, int nsm,
+                                bool exact = false) {
   std::vector<Level> lv;
   // level 0
   {
@@ -274,7 +280,7 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     L.D = D0; L.ldd = ldd0; L.ncols = ncols0;
     int b = chain_bmax(KT);
     if (b > 128 && KT == 64) b = 128;
-    const bool gs = gsweep_on(KT, b);
+    const bool gs = !exact && gsweep_on(KT, b);
     L.G = level0_geom(m, KT, gs ? gs_tile_rows() : b, nsm);
     const long nch = L.G.nchains;
     if (gs) {
@@ -306,12 +312,12 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
   return lv;
 }
 
-size_t plan_levels_bytes(long m, int KT, int nsm) {
+size_t plan_levels_bytes(long m, int KT, int nsm, bool exact = false) {
   // mirror of plan_levels' allocations (+ alignment slack)
   size_t tot = 0;
   int b = chain_bmax(KT);
   if (b > 128 && KT == 64) b = 128;
-  const bool gs = gsweep_on(KT, b);
+  const bool gs = !exact && gsweep_on(KT, b);
   const ChainGeom G = level0_geom(m, KT, gs ? gs_tile_rows() : b, nsm);
   long nch = G.nchains;
   const long tslots = gs ? (long)G.L * (G.b / b) + 1 : G.L + 1;
@@ -440,7 +446,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   bytes += (size_t)22 * ld * ld * 8 + 22 * 256;                    // small matrices + diag scratch
   bytes += (size_t)8 * ld * 8 + 10 * 256;                          // vectors, dlam, dcount
   bytes += (size_t)KT * KT * 8 * 2 + 1024;                         // ident, svec
-  bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, nsm_use);
+  bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, nsm_use, c.exact_intra);
   bytes += (size_t)64 * KT * KT * 8 * 4 + 4096;                    // global tree (<=64 ranks)
   bytes += 64;
   int rc = ensure_ws(ctx, bytes);
@@ -471,7 +477,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   s.status = ar.take<int>(4);
   j.ident = ar.take<double>((size_t)KT * KT);
   j.svec = s.svec;
-  j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, nsm_use);
+  j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, nsm_use, c.exact_intra);
   j.Rall = ar.take<double>((size_t)64 * KT * KT);
   j.Cglob = ar.take<double>((size_t)64 * KT * KT);
   if (ar.off > ctx->ws_size) return fail(ctx, OTS_E_CUDA, "workspace plan overflow");
@@ -1329,6 +1335,7 @@ int ots_b_two_stage_diag_f64(ots_ctx* ctx, int64_t n, int64_t k0, int64_t k, con
   CK(launch_reduce(part, gridu, (long)PWv * PWv, Gu, 1.0, st));
   BHook bh{Gu, PWv, dinv, d, n};
   JobCfg c{n, 0, k0, k, V2, ldv2, A2, lda2, Q, ldq, choice, P, ldp, orth_tol, 0, st, false};
+  c.exact_intra = true;
   return two_stage_pipeline(ctx, c, OTS_INTRA_HOUSEHOLDER, Q, ldq, R, ldr, S, lds, diag_host, &bh);
 }
 
