@@ -63,6 +63,11 @@ int ots_ctx_create(int device, ots_ctx** out);
 void ots_ctx_destroy(ots_ctx* ctx);
 const char* ots_last_error(const ots_ctx* ctx);
 int ots_sm_count(const ots_ctx* ctx);
+/* 1 when the last ots_two_stage_f64 call on ctx ran the direct-Q pipeline
+ * (tile Grams of [V | A], no materialised X), 0 when it ran the
+ * materialised-X pipeline (ineligible shape, or the cancellation test sent
+ * it there); both compute twostage.py:57-97. */
+int ots_last_fast(const ots_ctx* ctx);
 int ots_version(void);
 
 /* two_stage_qr(v, a, choice, intra, p)          -- twostage.py:57-97

@@ -44,6 +44,7 @@ def lib():
                 L.ots_last_error.argtypes = [_vp]
                 L.ots_last_error.restype = C.c_char_p
                 L.ots_sm_count.argtypes = [_vp]
+                L.ots_last_fast.argtypes = [_vp]
                 L.ots_version.restype = _int
                 L.ots_set_profiling.argtypes = [_vp, _int]
                 L.ots_last_launch_count.argtypes = [_vp]
@@ -130,7 +131,7 @@ def lib():
 _NO_ARGS = {"ots_version"}
 
 EXPORTED_SYMBOLS = [
-    "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_version",
+    "ots_ctx_create", "ots_ctx_destroy", "ots_last_error", "ots_sm_count", "ots_last_fast", "ots_version",
     "ots_two_stage_f64", "ots_householder_qr_f64", "ots_modified_lu_f64",
     "ots_two_stage_c128", "ots_householder_qr_c128", "ots_b_two_stage_diag_c128", "ots_stability_f64",
     "ots_shifted_cholesky_qr_c128", "ots_modified_lu_c128",

@@ -61,6 +61,7 @@ struct GsweepArgs {
   double* Hs;            // head rows per chain (KT x KT): R upper, V strictly lower
   int* flags;            // per chain: 1 = redo exactly (128-row tiles)
   long tslots;           // T slots per chain (the 128-row geometry's L + 1)
+  const int* abort_flag = nullptr;   // nonzero at kernel start: do nothing
 };
 
 struct QformArgs {
@@ -77,7 +78,38 @@ struct QformArgs {
   const double* Hs = nullptr;
   const int* flags = nullptr;
   long tslots = 0;       // T slots per chain (0: G.L + 1)
+  // gs_coef (direct-Q pipeline): K_t of tall tile (chain, t) goes to
+  // Kout + (chain * G.L + t - 1) * kstride + koff instead of being applied
+  double* Kout = nullptr;
+  long kstride = 0, koff = 0;
 };
+
+// Direct-Q pipeline (fastpath.cu): every pointer is offset to the first chain
+// row (the QR rows), geometry G = the Gram-form factor's tall tiles.
+struct FastArgs {
+  const double* V; long ldv;
+  const double* A; long lda;
+  double* D; long ldd;       // Q rows (heads only: X, then Q_, then Q)
+  int k0, k, PW;             // PW = k0 padded to 32
+  ChainGeom G;
+  double* TG; long tg_stride;   // per tall tile (chain * L + t - 1): [VV | VA] PW x (PW + 64), then AA 64 x 64
+  double* part;              // per-CTA totals of [VV | VA]
+  const double* Z1; int ldz;
+  double* M;                 // the factor's Cc slots (tile Gram of X in, Cc out)
+  double* Coef;              // per tall tile: (PW + 64) x 64 = [Z1 K + Z2; K]
+  int* flags;                // [0]: bit 0 cancellation, bit 1 a chain flagged by the sweep
+  int* ticket;               // dynamic tile counter
+};
+cudaError_t launch_tgram(const FastArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_tgram_reduce(const FastArgs& a, int nparts, const double* Vtop, int ntop, double* out, int ldg,
+                                cudaStream_t st);
+cudaError_t launch_head_rows(const FastArgs& a, int mode, const double* Z, int ldz, const double* colscale,
+                             double* part, int grid, cudaStream_t st);
+cudaError_t launch_tile_alg(const FastArgs& a, cudaStream_t st);
+cudaError_t launch_coef_b(const FastArgs& a, double* ypart, int grid, cudaStream_t st);
+cudaError_t launch_coef_add_z2(const FastArgs& a, const double* Z2, int ldz, cudaStream_t st);
+cudaError_t launch_final_nn(const FastArgs& a, const double* colscale, double* X, long ldx, cudaStream_t st);
+cudaError_t launch_fast_flags(const int* chain_flags, int nch, int* flags, cudaStream_t st);
 
 cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid, cudaStream_t st);
 cudaError_t launch_reduce(const double* partial, int nparts, long count, double* out, double alpha, cudaStream_t st);
@@ -89,6 +121,7 @@ cudaError_t launch_chain_qform(const QformArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_gs_gram(const GsweepArgs& a, cudaStream_t st);
 cudaError_t launch_chain_gsweep(const GsweepArgs& a, cudaStream_t st);
 cudaError_t launch_gs_qform(const QformArgs& a, cudaStream_t st);
+cudaError_t launch_gs_coef(const QformArgs& a, cudaStream_t st);
 // complex128 TSQR (zchain.cu): same argument records, pointers to interleaved
 // (re, im) data, leading dimensions in complex units
 using ZFactorArgs = FactorArgs;

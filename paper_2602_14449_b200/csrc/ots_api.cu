@@ -107,7 +107,8 @@ struct ots_ctx {
   int nsm = 148;
   cudaStream_t side = nullptr;   // highest priority: its few CTAs go first, the
                                  // dynamically scheduled apply1 tiles fill around them
-  cudaEvent_t ev_seed = nullptr, ev_diag = nullptr, ev_seedA = nullptr;
+  cudaEvent_t ev_seed = nullptr, ev_diag = nullptr, ev_seedA = nullptr, ev_fast = nullptr;
+  int fast_taken = 0;            // last two_stage call went through the direct-Q pipeline
   int* nn_counter = nullptr;     // tile tickets of the NN updates
   char* ws = nullptr;
   size_t ws_size = 0;
@@ -203,6 +204,7 @@ struct JobCfg {
   // register-tile kernel's constant there is about half the Gram form's
   // (tools/gs_accuracy.py), so those calls keep the exact level-0 factor.
   bool exact_intra = false;
+  bool fast_try = false;   // caller allows the direct-Q pipeline (fastpath.cu) when the shape qualifies
 };
 
 }  // namespace
@@ -224,6 +226,11 @@ struct Job {
   double* Rall = nullptr;       // gathered R's copy (nranks*KT x KT)
   double* chol_ws = nullptr;    // 3 ld x ld scratch of the cholshift step
   double* Rfinal = nullptr;
+  // direct-Q pipeline (fastpath.cu)
+  bool fast = false;
+  double *fTG = nullptr, *fCoef = nullptr, *fpart = nullptr;
+  long ftg_stride = 0;
+  int* fflags = nullptr;        // [0] flags, [1] ticket
 };
 
 namespace ots { void gs_event_log(long long* out); }
@@ -249,6 +256,25 @@ bool gsweep_on(int KT, int b) {
     return e ? atoi(e) : 1;
   }();
   return v != 0 && KT == 64 && b == 128;
+}
+
+// The direct-Q pipeline (fastpath.cu): OTS_FAST=0 turns it off; calls with
+// fewer QR rows than OTS_FAST_MIN_ROWS (default 2^19) keep the materialised-X
+// pipeline (the extra small kernels and the host hand-off do not pay there).
+bool fast_on() {
+  static int v = [] {
+    const char* e = getenv("OTS_FAST");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+long fast_min_rows() {
+  static long v = [] {
+    const char* e = getenv("OTS_FAST_MIN_ROWS");
+    long x = e ? atol(e) : (1L << 19);
+    return x > 0 ? x : (1L << 19);
+  }();
+  return v;
 }
 
 int gs_tile_rows() {
@@ -447,6 +473,22 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   bytes += (size_t)8 * ld * 8 + 10 * 256;                          // vectors, dlam, dcount
   bytes += (size_t)KT * KT * 8 * 2 + 1024;                         // ident, svec
   bytes += plan_levels_bytes(std::max<long>(j.m, 1), KT, nsm_use, c.exact_intra);
+  // direct-Q pipeline: per-tall-tile Grams of [V | A] and coefficients
+  j.fast = false;
+  size_t f_tg = 0, f_coef = 0, f_part = 0;
+  if (c.fast_try && fast_on() && !c.distributed && c.row0 == 0 && !c.gram_in && !c.exact_intra && c.ld_min == 0 &&
+      k0 > 96 && k0 <= 128 && KT == 64 && gsweep_on(KT, 128) && j.m >= fast_min_rows()) {
+    const ChainGeom G = level0_geom(j.m, KT, gs_tile_rows(), nsm_use);
+    if (G.L >= 1) {
+      j.fast = true;
+      const size_t ntl = (size_t)G.nchains * G.L;
+      j.ftg_stride = (long)j.PW * (j.PW + 64) + 64 * 64;
+      f_tg = ntl * (size_t)j.ftg_stride;
+      f_coef = ntl * (size_t)(j.PW + 64) * 64;
+      f_part = (size_t)2 * ctx->nsm * j.PW * (j.PW + 64);
+      bytes += (f_tg + f_coef + f_part) * 8 + 1024 + 64;
+    }
+  }
   bytes += (size_t)64 * KT * KT * 8 * 4 + 4096;                    // global tree (<=64 ranks)
   bytes += 64;
   int rc = ensure_ws(ctx, bytes);
@@ -480,6 +522,12 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, nsm_use, c.exact_intra);
   j.Rall = ar.take<double>((size_t)64 * KT * KT);
   j.Cglob = ar.take<double>((size_t)64 * KT * KT);
+  if (j.fast) {
+    j.fTG = ar.take<double>(f_tg);
+    j.fCoef = ar.take<double>(f_coef);
+    j.fpart = ar.take<double>(f_part);
+    j.fflags = ar.take<int>(16);
+  }
   if (ar.off > ctx->ws_size) return fail(ctx, OTS_E_CUDA, "workspace plan overflow");
   return OTS_OK;
 }
@@ -768,6 +816,115 @@ __global__ void inv_top_kernel(const double* d, int k0, double* out) {
   for (int i = threadIdx.x; i < k0; i += blockDim.x) out[i] = 1.0 / d[i];
 }
 
+// ---------------------------------------------------------------------------
+// Direct-Q pipeline (fastpath.cu) between the seed and qtop.  Returns 1 when
+// the cancellation test or the sweep flagged the input (nothing the caller
+// keeps was written: the materialised-X pipeline then runs from apply1), 0
+// when Q's bottom rows, R and Z2 are done, < 0 on errors.
+// ---------------------------------------------------------------------------
+FastArgs fast_args(ots_ctx* ctx, Job& j) {
+  const JobCfg& c = j.c;
+  const Level& L0 = j.lv[0];
+  FastArgs fa{};
+  fa.V = c.V + j.qrow0 * c.ldv; fa.ldv = c.ldv;
+  fa.A = c.A + j.qrow0 * c.lda; fa.lda = c.lda;
+  fa.D = L0.D; fa.ldd = L0.ldd;
+  fa.k0 = (int)c.k0; fa.k = (int)c.k; fa.PW = j.PW;
+  fa.G = L0.G;
+  fa.TG = j.fTG; fa.tg_stride = j.ftg_stride;
+  fa.part = j.fpart;
+  fa.Z1 = j.s.Z1; fa.ldz = j.ld;
+  fa.M = L0.CC;
+  fa.Coef = j.fCoef;
+  fa.flags = j.fflags;
+  fa.ticket = j.fflags + 1;
+  (void)ctx;
+  return fa;
+}
+
+int fast_gram(ots_ctx* ctx, Job& j) {
+  const JobCfg& c = j.c;
+  FastArgs fa = fast_args(ctx, j);
+  const int grid = j.gram_nsm > 0 ? j.gram_nsm : ctx->nsm;
+  CK(cudaMemsetAsync(j.fflags, 0, 16 * sizeof(int), c.st));
+  CK(launch_tgram(fa, grid, c.st));
+  CK(launch_tgram_reduce(fa, grid, c.V, (int)j.qrow0, j.Gfull, j.NTOT1, c.st));
+  return OTS_OK;
+}
+
+int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr, bool diag_side) {
+  const JobCfg& c = j.c;
+  cudaStream_t st = c.st;
+  const int KT = j.KT;
+  const long k0 = c.k0, k = c.k;
+  FastArgs fa = fast_args(ctx, j);
+  Level& L0 = j.lv[0];
+  const int nch = L0.G.nchains;
+  const int ghead = std::min(nch, 2 * ctx->nsm);
+  CK(launch_head_rows(fa, 0, j.s.Z1, j.ld, nullptr, nullptr, ghead, st));     // X rows of the heads
+  CK(launch_tile_alg(fa, st));
+  prof_mark(ctx, st, "tile_alg");
+  GsweepArgs ga{L0.D, L0.ldd, L0.ncols, L0.G, L0.UT, L0.R, L0.CC, L0.HS, L0.FL, (long)L0.G128.L + 1};
+  ga.abort_flag = j.fflags;
+  CK(launch_chain_gsweep(ga, st));
+  CK(launch_fast_flags(L0.FL, nch, j.fflags, st));
+  CK(cudaMemcpyAsync(ctx->h_status + 8, j.fflags, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(ctx->ev_fast, st));
+  prof_mark(ctx, st, "gs_sweep");
+  for (size_t l = 1; l < j.lv.size(); ++l) {          // tree over the chain R's (speculative)
+    Level& L = j.lv[l];
+    FactorArgs fl{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, 1};
+    CK(launch_chain_factor(fl, KT, st));
+  }
+  CK(cudaEventSynchronize(ctx->ev_fast));
+  if (ctx->h_status[8] != 0) return 1;
+  prof_mark(ctx, st, "factor");
+  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
+  const double* Cin = j.ident;
+  for (int l = (int)j.lv.size() - 1; l >= 1; --l) {
+    Level& L = j.lv[l];
+    QformArgs qa{L.D, L.ldd, L.ncols, L.G, L.UT, Cin, 0};
+    CK(launch_chain_qform(qa, KT, st));
+    Cin = L.D;
+  }
+  {
+    QformArgs qa{L0.D, L0.ldd, L0.ncols, L0.G, L0.UT, Cin, 0};
+    qa.mode = 2;
+    qa.Cc = L0.CC; qa.Hs = L0.HS; qa.flags = L0.FL;
+    qa.tslots = (long)L0.G128.L + 1;
+    qa.Kout = j.fCoef; qa.kstride = (long)(j.PW + 64) * 64; qa.koff = (long)j.PW * 64;
+    qa.grid_max = j.nsm_use;
+    CK(launch_gs_coef(qa, st));
+  }
+  CK(launch_sign(j.s, Q + k0 * ldq, ldq, j.lv.back().R, KT, R, (int)ldr, st));
+  // Y2 = -V_b^T Q_ = -(sum_t Cx_t K_t + sum_heads V_h^T Q_h)
+  const int gb = j.nsm_use, gh = std::min(nch, j.nsm_use);
+  CK(launch_coef_b(fa, j.fpart, gb, st));
+  CK(launch_head_rows(fa, 2, nullptr, 0, nullptr, j.fpart + (size_t)gb * j.PW * 64, gh, st));
+  CK(launch_reduce_strided(j.fpart, gb + gh, (int)k0, (int)k, 64, j.Y2full, j.BWa, -1.0, st));
+  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
+  CK(launch_z2(j.s, st));
+  CK(launch_coef_add_z2(fa, j.s.Z2, j.ld, st));
+  prof_mark(ctx, st, "coef");
+  if (diag_side) {
+    // the diagnostics already run on the side stream (launched behind the seed)
+    CK(launch_final_nn(fa, j.svec, L0.D, L0.ldd, st));
+    CK(launch_head_rows(fa, 1, j.s.Z2, j.ld, j.svec, nullptr, ghead, st));
+  } else {
+    // diagnostics (3 CTAs) on the main stream ahead of the final pass on the
+    // side stream (dynamic sub-tiles: the SMs they hold take fewer), as apply1
+    CK(cudaEventRecord(ctx->ev_seed, st));
+    CK(launch_diag(j.s, st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
+    CK(launch_final_nn(fa, j.svec, L0.D, L0.ldd, ctx->side));
+    CK(launch_head_rows(fa, 1, j.s.Z2, j.ld, j.svec, nullptr, ghead, ctx->side));
+    CK(cudaEventRecord(ctx->ev_diag, ctx->side));
+    CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
+  }
+  prof_mark(ctx, st, "final");
+  return 0;
+}
+
 int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long ldq, double* R, long ldr,
                        double* S, long lds, double* diag_host, const BHook* bh) {
   const long n = c.n_local, k0 = c.k0, k = c.k;
@@ -784,6 +941,8 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   const bool diag_side = (k0 > 128 || small_call) && ctx->nsm > 16;
   JobCfg c2 = c;
   if (diag_side) c2.nsm_avail = ctx->nsm - 3;
+  c2.fast_try = intra == OTS_INTRA_HOUSEHOLDER && bh == nullptr;
+  ctx->fast_taken = 0;
   if ((rc = job_setup(ctx, j, c2))) return rc;
   const int KT = j.KT;
   if (bh) {
@@ -805,7 +964,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     j.gram_nsm = ctx->nsm - (seed_uses_cluster(j.s) ? 2 : 1);
     j.grid_tn = grid_for_tn(j.PW, j.BWa, true, true, j.gram_nsm);
   }
-  if ((rc = phase_gram(ctx, j))) return rc;
+  if ((rc = j.fast ? fast_gram(ctx, j) : phase_gram(ctx, j))) return rc;
   prof_mark(ctx, st, "gram");
   if (split_seed) {
     CK(cudaStreamWaitEvent(st, ctx->ev_seedA, 0));
@@ -820,10 +979,21 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // an event a little later) fill the rest; apply1 hands out its tiles
   // dynamically, so those 3 SMs simply take fewer.  The factor then starts on
   // an idle GPU instead of waiting for the diagnostics' SMs.
+  bool fast_done = false;
   if (diag_side) {
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
     CK(launch_diag(j.s, ctx->side));
     CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // waited for before the status read
+  }
+  if (j.fast) {
+    rc = fast_pipeline(ctx, j, Q, ldq, R, ldr, diag_side);
+    if (rc < 0) return rc;
+    fast_done = rc == 0;
+    ctx->fast_taken = fast_done ? 1 : 0;
+  }
+  if (fast_done) {
+    // Q's bottom rows, R, Z2 done
+  } else if (diag_side) {
     if ((rc = phase_apply1(ctx, j))) return rc;
   } else {
     CK(launch_diag(j.s, st));
@@ -836,6 +1006,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     CK(cudaEventRecord(ctx->ev_diag, ctx->side));   // apply1 done
     CK(cudaStreamWaitEvent(st, ctx->ev_diag, 0));
   }
+  if (!fast_done) {
   prof_mark(ctx, st, "apply1");
   if (intra == OTS_INTRA_HOUSEHOLDER) {
     if ((rc = run_factor_levels(ctx, j.lv, KT, st))) return rc;
@@ -858,6 +1029,7 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
     return rc;
   }
   prof_mark(ctx, st, "apply2");
+  }  // !fast_done
   CK(launch_qtop(j.s, Q, ldq, st));
   if (bh) {
     if (bh->L != nullptr) {       // dense B: Q = L^{-T} Q' sgn
@@ -874,6 +1046,9 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   // gram, reduce, seed(B), diag, apply1, identity, sign, gram2, reduce, copy_y2,
   // z2, apply2, qtop + a factor and a qform launch per level (+ seedA, B epilogue)
   ctx->launches = 13 + 2 * (int)j.lv.size() + (bh ? 2 : 0) + (split_seed ? 1 : 0);
+  // direct-Q: tgram, reduce, seed(B), head x3, tile_alg, gsweep, flags, identity, gs_coef, sign, coef_b,
+  // reduce, copy_y2, z2, add_z2, diag, final, qtop + a factor and a qform launch per tree level (+ seedA)
+  if (fast_done) ctx->launches = 20 + 2 * ((int)j.lv.size() - 1) + (split_seed ? 1 : 0);
   rc = read_status(ctx, j, diag_host);
   prof_end(ctx);
   return rc;
@@ -904,6 +1079,7 @@ int ots_ctx_create(int device, ots_ctx** out) {
   cudaEventCreateWithFlags(&c->ev_seed, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_diag, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_seedA, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_fast, cudaEventDisableTiming);
   cudaMallocHost(&c->h_status, 64);
   cudaMallocHost(&c->h_diag, 64);
   *out = c;
@@ -923,6 +1099,7 @@ void ots_ctx_destroy(ots_ctx* c) {
   if (c->ev_seed) cudaEventDestroy(c->ev_seed);
   if (c->ev_diag) cudaEventDestroy(c->ev_diag);
   if (c->ev_seedA) cudaEventDestroy(c->ev_seedA);
+  if (c->ev_fast) cudaEventDestroy(c->ev_fast);
   if (c->h_status) cudaFreeHost(c->h_status);
   if (c->h_diag) cudaFreeHost(c->h_diag);
   for (auto e : c->pev) cudaEventDestroy(e);
@@ -932,6 +1109,7 @@ void ots_ctx_destroy(ots_ctx* c) {
 
 const char* ots_last_error(const ots_ctx* c) { return c ? c->err.c_str() : "null context"; }
 int ots_sm_count(const ots_ctx* c) { return c ? c->nsm : 0; }
+int ots_last_fast(const ots_ctx* c) { return c ? c->fast_taken : 0; }
 
 int ots_set_profiling(ots_ctx* c, int enable) { c->profile = enable != 0; return OTS_OK; }
 
