@@ -266,8 +266,14 @@ def run_gpu(args):
 
     # dominant kernel: the phase with the largest share of the step
     dom = max(phase_ms, key=phase_ms.get)
+    # flops the dominant launch EXECUTES (its own algorithmic count).  Direct-Q
+    # pipeline (ots_last_fast = 1): "gram" is the tile-Gram pass over [V | A]
+    # (V^T V, V^T A and A^T A per tall tile), "final" the pass Q = [V | A] Coef.
+    w = k0 + k
+    fast = NT.last_fast(ctx) == 1
     dom_flops = {
-        "gram": gram_flops(n, k0, k),
+        "gram": (n - k0) * w * (w + 1.0) if fast else gram_flops(n, k0, k),
+        "final": 2.0 * (n - k0) * w * k,
         "apply1": 2.0 * (n - k0) * k0 * k,
         "gram2": 2.0 * (n - k0) * k0 * k,
         "apply2": 2.0 * (n - k0) * k0 * k,
@@ -278,11 +284,13 @@ def run_gpu(args):
     roofline = {"bound": "tensor", "kernel": dom, "achieved": round(dom_tf, 3),
                 "peak": round(fp64_peak, 3), "unit": "TFLOP/s",
                 "frac": round(dom_tf / fp64_peak, 4) if fp64_peak else None,
-                "traffic": load_traffic(dom),
+                "traffic": load_traffic(dom + "_direct" if fast else dom),
                 "peak_source": "FP64 DMMA loop measured in this run (ots_fp64_peak); "
                                "MEASURED_PEAKS.json has no FP64 figure",
                 "phase_ms": {kk: round(vv, 3) for kk, vv in phase_ms.items()},
                 "step_frac_of_roofline": round(t_roof / (step_ms * 1e-3), 4),
+                "pipeline": "direct-Q (tile Grams of [V | A]; executes fewer flops than F_alg)" if fast
+                            else "materialised X",
                 "step_hbm_gbs": round(gbs, 1), "step_hbm_frac": round(gbs / hbm, 4)}
 
     # e2e: public API with host buffers (pinned), H2D of V, A and D2H of Q, R, S

@@ -200,6 +200,12 @@ def check(rc, ctx, block=None):
     raise exc(msg)
 
 
+def last_fast(ctx):
+    """1 when the last two_stage call on ctx took the direct-Q pipeline
+    (csrc/fastpath.cu), 0 when it took the materialised-X pipeline."""
+    return int(lib().ots_last_fast(ctx))
+
+
 def profile(ctx):
     """[(phase, ms)] of the last call (when profiling is enabled)."""
     L = lib()

@@ -43,52 +43,52 @@ namespace ots {
 // The A^T A fragments sit in the accumulator entries the role leaves unused
 // (D: the strict upper triangle of the 4 x 4 fragment grid, H: column 2).
 // ============================================================================
+#ifndef TG_UNROLL
+#define TG_UNROLL 16
+#endif
+#ifndef TG_RT
+#define TG_RT 64
+#endif
+#ifndef TG_NSTAGE
+#define TG_NSTAGE 2
+#endif
+#ifndef TG_LA
+#define TG_LA 1
+#endif
 struct TgCfg {
-  static constexpr int PW = 128, NTASK = 20, NT = NTASK * 32, RT = 64;
+  static constexpr int PW = 128, NTASK = 20, NT = NTASK * 32, RT = TG_RT;
   static constexpr int STAGE = RT * (PW + 64);
-  static constexpr int NSTAGE = 2;
+  static constexpr int NSTAGE = TG_NSTAGE;
+  static constexpr int LA = TG_LA;               // stages issued ahead; NSTAGE - 1 - LA stages of slack between warps
   static constexpr int SMEM = NSTAGE * STAGE * 8;
   static constexpr int NT1 = PW + 64;
+  static constexpr int UNR = TG_UNROLL;          // 4-row steps unrolled in the stage loop
 };
 
 // A^T A lower-triangle fragments (i, j) of the 8 x 8 fragment grid, packed 8 i + j:
-// groups 0..3 (6 fragments, D warps), 4..7 (3 fragments, H warps)
-__host__ __device__ constexpr int tg_aa(int grp, int q) {
-  constexpr int T[8][6] = {
-      {40, 41, 42, 43, 44, 45},       // row 5
-      {0, 8, 9, 16, 17, 18},          // rows 0..2
-      {24, 25, 26, 27, 32, 33},       // row 3, (4,0), (4,1)
-      {48, 49, 50, 51, 52, 53},       // row 6, columns 0..5
-      {34, 35, 36, 0, 0, 0},          // (4,2..4)
-      {56, 57, 58, 0, 0, 0},          // (7,0..2)
-      {59, 60, 61, 0, 0, 0},          // (7,3..5)
-      {62, 63, 54, 0, 0, 0}};         // (7,6), (7,7), (6,6)
-  return T[grp][q];
-}
+// groups 0..3 (6 fragments, D warps), 4..7 (3 fragments, H warps).  The lists
+// are data (constant memory), not code: one body per role keeps the kernel's
+// hot loops inside the instruction cache (nine specialised bodies measured
+// 23.0 ms at 2-step unrolling and 29.4 ms at 16).
+__constant__ unsigned char c_tg_aa[8][6] = {
+    {40, 41, 42, 43, 44, 45},       // row 5
+    {0, 8, 9, 16, 17, 18},          // rows 0..2
+    {24, 25, 26, 27, 32, 33},       // row 3, (4,0), (4,1)
+    {48, 49, 50, 51, 52, 53},       // row 6, columns 0..5
+    {34, 35, 36, 0, 0, 0},          // (4,2..4)
+    {56, 57, 58, 0, 0, 0},          // (7,0..2)
+    {59, 60, 61, 0, 0, 0},          // (7,3..5)
+    {62, 63, 54, 0, 0, 0}};         // (7,6), (7,7), (6,6)
 // accumulator entry of extra fragment q: D -> strict upper triangle, H -> column 2
 __host__ __device__ constexpr int tg_ex_i(bool isD, int q) { return isD ? (q < 3 ? 0 : (q < 5 ? 1 : 2)) : q; }
 __host__ __device__ constexpr int tg_ex_j(bool isD, int q) { return isD ? (q < 3 ? q + 1 : (q < 5 ? q - 1 : 3)) : 2; }
 
-template <int GRP>
-__device__ __forceinline__ void tg_aa_step(double (&acc)[4][4][2], const double* As, int r, int g) {
-  constexpr bool isD = GRP < 4;
+template <bool isD>
+__device__ __forceinline__ void tg_aa_flush(double (&acc)[4][4][2], int grp, double* AA, bool store, int g, int t) {
   constexpr int N = isD ? 6 : 3;
 #pragma unroll
   for (int q = 0; q < N; ++q) {
-    constexpr int dummy = 0;
-    (void)dummy;
-    const int fi = tg_aa(GRP, q) >> 3, fj = tg_aa(GRP, q) & 7;
-    dmma(acc[tg_ex_i(isD, q)][tg_ex_j(isD, q)], As[swz(r, 8 * fi + g, 64)], As[swz(r, 8 * fj + g, 64)]);
-  }
-}
-
-template <int GRP>
-__device__ __forceinline__ void tg_aa_flush(double (&acc)[4][4][2], double* AA, bool store, int g, int t) {
-  constexpr bool isD = GRP < 4;
-  constexpr int N = isD ? 6 : 3;
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-    const int fi = tg_aa(GRP, q) >> 3, fj = tg_aa(GRP, q) & 7;
+    const int fi = c_tg_aa[grp][q] >> 3, fj = c_tg_aa[grp][q] & 7;
     double (&e)[2] = acc[tg_ex_i(isD, q)][tg_ex_j(isD, q)];
     if (store) {
       const int r = 8 * fi + g, c = 8 * fj + 2 * t;
@@ -102,85 +102,34 @@ __device__ __forceinline__ void tg_aa_flush(double (&acc)[4][4][2], double* AA, 
   }
 }
 
-#define TG_AA_DISPATCH(fn, ...)                      \
-  switch (aagrp) {                                   \
-    case 0: fn<0>(__VA_ARGS__); break;               \
-    case 1: fn<1>(__VA_ARGS__); break;               \
-    case 2: fn<2>(__VA_ARGS__); break;               \
-    case 3: fn<3>(__VA_ARGS__); break;               \
-    case 4: fn<4>(__VA_ARGS__); break;               \
-    case 5: fn<5>(__VA_ARGS__); break;               \
-    case 6: fn<6>(__VA_ARGS__); break;               \
-    default: fn<7>(__VA_ARGS__); break;              \
-  }
-
-// one 64-row stage of a D warp (diagonal block `blk` + A^T A group GRP)
-template <int GRP>
-__device__ __forceinline__ void tg_stage_d(double (&acc)[4][4][2], const double* Vs, const double* As, int blk, int g,
-                                           int t) {
-#pragma unroll
-  for (int kk = 0; kk < TgCfg::RT / 4; ++kk) {
-    const int r = 4 * kk + t;
-    double af[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 32 * blk + 8 * i + g, 128)];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j <= i; ++j) dmma(acc[i][j], af[i], af[j]);
-    tg_aa_step<GRP>(acc, As, r, g);
-  }
-}
-// one stage of an H warp (half `hc` (16 columns at column hc of A) of V_3^T A + group GRP)
-template <int GRP>
-__device__ __forceinline__ void tg_stage_h(double (&acc)[4][4][2], const double* Vs, const double* As, int hc, int g,
-                                           int t) {
-#pragma unroll
-  for (int kk = 0; kk < TgCfg::RT / 4; ++kk) {
-    const int r = 4 * kk + t;
-    double af[4], bf[2];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 96 + 8 * i + g, 128)];
-#pragma unroll
-    for (int j = 0; j < 2; ++j) bf[j] = As[swz(r, hc + 8 * j + g, 64)];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[i], bf[j]);
-    tg_aa_step<GRP>(acc, As, r, g);
-  }
-}
-
-__global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
+// ROLE 0: D warp (diagonal block idx of V^T V + A^T A group idx), 1: H warp
+// (half idx of V_3^T A + group 4 + idx), 2: F warp (block (ra, rb)).
+template <int ROLE>
+__device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigned long long* full_bar,
+                                        unsigned long long* empty_bar, int idx, int ra, int rb) {
   using C = TgCfg;
   constexpr int PW = C::PW, NT1 = C::NT1, RT = C::RT;
-  extern __shared__ __align__(128) double smem[];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int NX = ROLE == 0 ? 6 : (ROLE == 1 ? 3 : 0);
+  const int grp = ROLE == 0 ? idx : 4 + idx;
+  const int tid = threadIdx.x, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-
-  // roles
-  const int role = warp < 4 ? 0 : (warp < 8 ? 1 : 2);       // D, H, F
-  const int aagrp = warp;                                    // D: 0..3, H: 4..7
-  int ra = 0, rb = 0;                                        // F: block (ra, rb) of S^T S, S = [V | A]
-  if (role == 2) {
-    const int f = warp - 8;
-    if (f < 6) {                                             // off-diagonal V^T V
-      const int fa[6] = {1, 2, 2, 3, 3, 3}, fb[6] = {0, 0, 1, 0, 1, 2};
-      ra = fa[f];
-      rb = fb[f];
-    } else {                                                 // V_b^T A, b = 0..2
-      ra = (f - 6) >> 1;
-      rb = 4 + ((f - 6) & 1);
-    }
+  // swizzled in-row offsets (row r = 4 kk + t, so r & 3 = t) of the two operand
+  // fragments of every extra A^T A fragment
+  int xa[NX > 0 ? NX : 1], xb[NX > 0 ? NX : 1];
+#pragma unroll
+  for (int q = 0; q < NX; ++q) {
+    const int fi = c_tg_aa[grp][q] >> 3, fj = c_tg_aa[grp][q] & 7;
+    xa[q] = swz(t, 8 * fi + g, 64) - t * 64;
+    xb[q] = swz(t, 8 * fj + g, 64) - t * 64;
   }
   const bool b_isV = rb < 4;
   const int boff = b_isV ? 0 : RT * PW, bW = b_isV ? PW : 64, bcol = b_isV ? 32 * rb : 32 * (rb - 4);
-  const int hc = 16 * (warp - 4);                            // H: column of A (0, 16, 32, 48)
 
   // this CTA's items: tall tiles first (tile index ti = chain * L + t - 1),
   // then chain heads
   const int L = a.G.L, nch = a.G.nchains;
   const int ntl = nch * L;
+  const int nitems_end = ntl + nch;
   auto item_rows = [&](int it, long& r0, long& rhi) {      // it < ntl: tile, else head it - ntl
     if (it < ntl) {
       const int chain = it / L, tt = it - chain * L;
@@ -201,49 +150,69 @@ __global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
     return it + (int)gridDim.x;
   };
   auto item_chunks = [&](int it) {
-    if (it >= ntl + nch) return 0;
+    if (it >= nitems_end) return 0;
     long r0, rhi;
     item_rows(it, r0, rhi);
     if (rhi <= r0) return 0;
     return (int)((rhi - r0 + RT - 1) / RT);
   };
-  const int nitems_end = ntl + nch;
   auto skip_empty = [&](int it) {
     while (it < nitems_end && item_chunks(it) == 0) it = next_item(it);
     return it;
   };
 
-  __shared__ __align__(8) unsigned long long full_bar[C::NSTAGE], empty_bar[C::NSTAGE];
-  if (tid == 0) {
-    for (int s = 0; s < C::NSTAGE; ++s) {
-      mbar_init(&full_bar[s], C::NT);
-      mbar_init(&empty_bar[s], C::NTASK);
-    }
-    fence_mbar_init();
-  }
-  __syncthreads();
-
   const int it0 = skip_empty(blockIdx.x < ntl ? (int)blockIdx.x : ntl + (int)blockIdx.x);
-  int p_it = it0, p_ch = 0, p_j = 0;
+  // producer: this thread's fixed share of a stage -- 16-byte unit uv of rows
+  // rv0, rv0 + 10, ... of the V part (640 threads = 10 rows of 64 units) and unit
+  // ua of rows ra0, ra0 + 20, ... of the A part (20 rows of 32 units); the
+  // item's row range is worked out once per item, not per stage
+  const int uv = tid & 63, rv0 = tid >> 6, ua = tid & 31, ra0 = tid >> 5;
+  const int vbytes = 2 * uv + 1 < a.k0 ? 16 : (2 * uv < a.k0 ? 8 : 0);
+  const int abytes = 2 * ua + 1 < a.k ? 16 : (2 * ua < a.k ? 8 : 0);
+  const double* vsrc = a.V + (vbytes ? 2 * uv : 0);
+  const double* asrc = a.A + (abytes ? 2 * ua : 0);
+  int p_it = it0, p_ch = 0, p_j = 0, p_n = 0;
+  long p_r0 = 0, p_rhi = 0;
+  if (p_it < nitems_end) {
+    item_rows(p_it, p_r0, p_rhi);
+    p_n = (int)((p_rhi - p_r0 + RT - 1) / RT);
+  }
   auto produce = [&]() {
     if (p_it >= nitems_end) return;
     const int s = p_j % C::NSTAGE, rnd = p_j / C::NSTAGE;
     if (rnd >= 1) mbar_wait(&empty_bar[s], (rnd - 1) & 1);
-    long r0, rhi;
-    item_rows(p_it, r0, rhi);
-    const long rr = r0 + (long)p_ch * RT;
+    const long rr = p_r0 + (long)p_ch * RT;
+    const int nr = (int)(p_rhi - rr < RT ? p_rhi - rr : RT);           // rows of this stage inside the item
     double* Ps = smem + s * C::STAGE;
-    load_tile_async(Ps, PW, a.V, a.ldv, rr, RT, r0, rhi, 0, PW, a.k0, tid, C::NT);
-    load_tile_async(Ps + RT * PW, 64, a.A, a.lda, rr, RT, r0, rhi, 0, 64, a.k, tid, C::NT);
+    double* Bs = Ps + RT * PW;
+#pragma unroll
+    for (int q = 0; q < (RT + 9) / 10; ++q) {
+      const int r = rv0 + 10 * q;
+      if (r < RT) {
+        const bool in = r < nr;
+        cp_async16(Ps + swz(r, 2 * uv, PW), in ? vsrc + (rr + r) * a.ldv : a.V, in ? vbytes : 0);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < (RT + 19) / 20; ++q) {
+      const int r = ra0 + 20 * q;
+      if (r < RT) {
+        const bool in = r < nr;
+        cp_async16(Bs + swz(r, 2 * ua, 64), in ? asrc + (rr + r) * a.lda : a.A, in ? abytes : 0);
+      }
+    }
     cp_async_mbar_arrive(&full_bar[s]);
     ++p_j;
-    if (++p_ch >= item_chunks(p_it)) {
+    if (++p_ch >= p_n) {
       p_ch = 0;
       p_it = skip_empty(next_item(p_it));
+      if (p_it < nitems_end) {
+        item_rows(p_it, p_r0, p_rhi);
+        p_n = (int)((p_rhi - p_r0 + RT - 1) / RT);
+      }
     }
   };
-  constexpr int LA = C::NSTAGE - 1;
-  for (int j = 0; j < LA; ++j) produce();
+  for (int j = 0; j < C::LA; ++j) produce();
 
   double acc[4][4][2];
 #pragma unroll
@@ -254,19 +223,48 @@ __global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
   double* tot = a.part + (long)blockIdx.x * PW * NT1;       // CTA totals [PW][NT1]
   bool tot_first = true;
   int c_it = it0, c_ch = 0, c_j = 0;
+  int c_n = item_chunks(c_it);
   while (c_it < nitems_end) {
     produce();
     const int s = c_j % C::NSTAGE;
     mbar_wait(&full_bar[s], (c_j / C::NSTAGE) & 1);
     const double* Vs = smem + s * C::STAGE;
     const double* As = Vs + RT * PW;
-    if (role == 0) {
-      TG_AA_DISPATCH(tg_stage_d, acc, Vs, As, warp, g, t)
-    } else if (role == 1) {
-      TG_AA_DISPATCH(tg_stage_h, acc, Vs, As, hc, g, t)
+    if (ROLE == 0) {
+#pragma unroll(TgCfg::UNR)
+      for (int kk = 0; kk < RT / 4; ++kk) {
+        const int r = 4 * kk + t;
+        double af[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 32 * idx + 8 * i + g, PW)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j <= i; ++j) dmma(acc[i][j], af[i], af[j]);
+#pragma unroll
+        for (int q = 0; q < NX; ++q)
+          dmma(acc[tg_ex_i(true, q)][tg_ex_j(true, q)], As[r * 64 + xa[q]], As[r * 64 + xb[q]]);
+      }
+    } else if (ROLE == 1) {
+#pragma unroll(TgCfg::UNR)
+      for (int kk = 0; kk < RT / 4; ++kk) {
+        const int r = 4 * kk + t;
+        double af[4], bf[2];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 96 + 8 * i + g, PW)];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) bf[j] = As[swz(r, 16 * idx + 8 * j + g, 64)];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[i], bf[j]);
+#pragma unroll
+        for (int q = 0; q < NX; ++q)
+          dmma(acc[tg_ex_i(false, q)][tg_ex_j(false, q)], As[r * 64 + xa[q]], As[r * 64 + xb[q]]);
+      }
     } else {
       const double* Bs = smem + s * C::STAGE + boff;
-#pragma unroll
+#pragma unroll(TgCfg::UNR)
       for (int kk = 0; kk < RT / 4; ++kk) {
         const int r = 4 * kk + t;
         double af[4], bf[4];
@@ -283,28 +281,25 @@ __global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty_bar[s]);
     ++c_j;
-    if (++c_ch >= item_chunks(c_it)) {
+    if (++c_ch >= c_n) {
       // ---- flush the item: tile slot (mirrored) and the CTA totals
       const bool is_tile = c_it < ntl;
       double* slot = a.TG + (long)c_it * a.tg_stride;
-      if (role != 2) {
-        double* AA = slot + (long)PW * NT1;
-        TG_AA_DISPATCH(tg_aa_flush, acc, AA, is_tile, g, t)
-      }
+      if (ROLE != 2) tg_aa_flush<ROLE == 0>(acc, grp, slot + (long)PW * NT1, is_tile, g, t);
       // main block: rows 32 ra_.., cols c0_.. of [V^T V | V^T A]; D: lower fragments, H: 2 fragment columns
-      const int ra_ = role == 0 ? warp : (role == 1 ? 3 : ra);
-      const int c0_ = role == 0 ? 32 * warp : (role == 1 ? PW + hc : (b_isV ? 32 * rb : PW + 32 * (rb - 4)));
-      const bool mirror = role == 0 || (role == 2 && b_isV);
+      const int ra_ = ROLE == 0 ? idx : (ROLE == 1 ? 3 : ra);
+      const int c0_ = ROLE == 0 ? 32 * idx : (ROLE == 1 ? PW + 16 * idx : (b_isV ? 32 * rb : PW + 32 * (rb - 4)));
+      const bool mirror = ROLE == 0 || (ROLE == 2 && b_isV);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          if (role == 0 && j > i) continue;
-          if (role == 1 && j >= 2) continue;
+          if (ROLE == 0 && j > i) continue;
+          if (ROLE == 1 && j >= 2) continue;
           const int r = 32 * ra_ + 8 * i + g, c = c0_ + 8 * j + 2 * t;
           if (is_tile) {
             *reinterpret_cast<double2*>(slot + (long)r * NT1 + c) = make_double2(acc[i][j][0], acc[i][j][1]);
-            if (mirror && !(role == 0 && i == j)) {
+            if (mirror && !(ROLE == 0 && i == j)) {
               slot[(long)c * NT1 + r] = acc[i][j][0];
               slot[(long)(c + 1) * NT1 + r] = acc[i][j][1];
             }
@@ -322,21 +317,54 @@ __global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
       tot_first = false;
       c_ch = 0;
       c_it = skip_empty(next_item(c_it));
+      c_n = item_chunks(c_it);
     }
   }
   cp_async_wait<0>();
   if (tot_first) {                                           // a CTA without items: zero totals
-    const int ra_ = role == 0 ? warp : (role == 1 ? 3 : ra);
-    const int c0_ = role == 0 ? 32 * warp : (role == 1 ? PW + hc : (b_isV ? 32 * rb : PW + 32 * (rb - 4)));
+    const int ra_ = ROLE == 0 ? idx : (ROLE == 1 ? 3 : ra);
+    const int c0_ = ROLE == 0 ? 32 * idx : (ROLE == 1 ? PW + 16 * idx : (b_isV ? 32 * rb : PW + 32 * (rb - 4)));
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (role == 0 && j > i) continue;
-        if (role == 1 && j >= 2) continue;
+        if (ROLE == 0 && j > i) continue;
+        if (ROLE == 1 && j >= 2) continue;
         const int r = 32 * ra_ + 8 * i + g, c = c0_ + 8 * j + 2 * t;
         *reinterpret_cast<double2*>(tot + (long)r * NT1 + c) = make_double2(0.0, 0.0);
       }
+  }
+}
+
+__global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
+  using C = TgCfg;
+  extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) unsigned long long full_bar[C::NSTAGE], empty_bar[C::NSTAGE];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < C::NSTAGE; ++s) {
+      mbar_init(&full_bar[s], C::NT);
+      mbar_init(&empty_bar[s], C::NTASK);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (warp < 4) {
+    tg_body<0>(a, smem, full_bar, empty_bar, warp, 0, 0);
+  } else if (warp < 8) {
+    tg_body<1>(a, smem, full_bar, empty_bar, warp - 4, 0, 0);
+  } else {
+    // F: 6 off-diagonal blocks of V^T V, then V_b^T A for b = 0..2
+    const int f = warp - 8;
+    int ra, rb;
+    if (f < 6) {
+      ra = f < 1 ? 1 : (f < 3 ? 2 : 3);
+      rb = f - (ra == 1 ? 0 : (ra == 2 ? 1 : 3));
+    } else {
+      ra = (f - 6) >> 1;
+      rb = 4 + ((f - 6) & 1);
+    }
+    tg_body<2>(a, smem, full_bar, empty_bar, 0, ra, rb);
   }
 }
 
@@ -823,7 +851,7 @@ static int fast_nsm() {
 }
 
 cudaError_t launch_tgram(const FastArgs& a, int grid, cudaStream_t st) {
-  if (a.G.b % 64 || a.G.L < 1 || a.PW != 128) return cudaErrorInvalidValue;
+  if (a.G.L < 1 || a.PW != 128) return cudaErrorInvalidValue;
   cudaFuncSetAttribute(tgram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TgCfg::SMEM);
   tgram_kernel<<<grid, TgCfg::NT, TgCfg::SMEM, st>>>(a);
   return cudaGetLastError();

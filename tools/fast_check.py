@@ -59,7 +59,7 @@ def timing():
     import paper_2602_14449_b200 as P
     from paper_2602_14449_b200 import _native as NT
     from bench import make_inputs
-    n, k0, k = 1 << 24, 128, 64
+    n, k0, k = int(os.environ.get("FC_N", 1 << 24)), 128, 64
     v, a = make_inputs(n, k0, k, 0)
     for _ in range(3):
         res = P.two_stage_qr(v, a, choice="qr")
