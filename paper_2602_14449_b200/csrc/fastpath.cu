@@ -403,14 +403,16 @@ __global__ void __launch_bounds__(256) head_rows_kernel(FastArgs a, int mode, co
     // out (k0 x k) accumulated over this CTA's chains; thread -> row i, 8 cols per pass
     for (int i0 = 0; i0 < a.PW; i0 += 32) {
       double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      const int i = i0 + (tid >> 3), c0 = (tid & 7) * 8;     // row i (V column), cols c0..c0+7
+      const int i = i0 + (tid >> 3), c0 = tid & 7;           // row i (V column), cols c0, c0 + 8, ... (bank-spread)
       for (int chain = blockIdx.x; chain < a.G.nchains; chain += gridDim.x) {
         const long r0 = (long)chain * a.G.rpc;
         __syncthreads();
-        for (int e = tid; e < 64 * 64; e += 256) {
+#pragma unroll
+        for (int e = tid; e < 64 * 64; e += 256) {             // independent loads, issued together
           const int r = e >> 6, c = e & 63;
           Ds[r][c] = (r0 + r < a.G.nrows && c < a.k) ? a.D[(r0 + r) * a.ldd + c] : 0.0;
         }
+#pragma unroll
         for (int e = tid; e < 64 * 32; e += 256) {
           const int r = e >> 5, c = e & 31;
           Vs[r][c] = (r0 + r < a.G.nrows && i0 + c < a.k0) ? a.V[(r0 + r) * a.ldv + i0 + c] : 0.0;
@@ -419,27 +421,29 @@ __global__ void __launch_bounds__(256) head_rows_kernel(FastArgs a, int mode, co
         for (int r = 0; r < 64; ++r) {
           const double v = Vs[r][tid >> 3];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) acc[c] = fma(v, Ds[r][c0 + c], acc[c]);
+          for (int c = 0; c < 8; ++c) acc[c] = fma(v, Ds[r][c0 + 8 * c], acc[c]);
         }
       }
       double* out = part + (long)blockIdx.x * a.PW * 64;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) out[(long)i * 64 + c0 + c] = acc[c];
+      for (int c = 0; c < 8; ++c) out[(long)i * 64 + c0 + 8 * c] = acc[c];
     }
     return;
   }
   for (int chain = blockIdx.x; chain < a.G.nchains; chain += gridDim.x) {
     const long r0 = (long)chain * a.G.rpc;
-    const int r = tid >> 2, c0 = (tid & 3) * 16;             // row r, cols c0..c0+15
+    const int r = tid >> 2, c0 = tid & 3;                    // row r, cols c0, c0 + 4, ... (bank-spread)
     double acc[16];
 #pragma unroll
     for (int c = 0; c < 16; ++c) acc[c] = 0.0;
     for (int kc = 0; kc < a.k0; kc += 32) {
       __syncthreads();
+#pragma unroll
       for (int e = tid; e < 64 * 32; e += 256) {
         const int rr = e >> 5, c = e & 31;
         Vs[rr][c] = (r0 + rr < a.G.nrows && kc + c < a.k0) ? a.V[(r0 + rr) * a.ldv + kc + c] : 0.0;
       }
+#pragma unroll
       for (int e = tid; e < 32 * 64; e += 256) {
         const int rr = e >> 6, c = e & 63;
         Zs[rr][c] = (kc + rr < a.k0 && c < a.k) ? Z[(long)(kc + rr) * ldz + c] : 0.0;
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(256) head_rows_kernel(FastArgs a, int mode, co
       for (int kk = 0; kk < 32; ++kk) {
         const double v = Vs[r][kk];
 #pragma unroll
-        for (int c = 0; c < 16; ++c) acc[c] = fma(v, Zs[kk][c0 + c], acc[c]);
+        for (int c = 0; c < 16; ++c) acc[c] = fma(v, Zs[kk][c0 + 4 * c], acc[c]);
       }
     }
     if (r0 + r < a.G.nrows) {
@@ -456,10 +460,11 @@ __global__ void __launch_bounds__(256) head_rows_kernel(FastArgs a, int mode, co
       double* dst = a.D + (r0 + r) * a.ldd;
 #pragma unroll
       for (int c = 0; c < 16; ++c) {
-        if (c0 + c >= a.k) continue;
-        double v = src[c0 + c] + acc[c];
-        if (mode == 1 && colscale && colscale[c0 + c] < 0.0) v = -v;
-        dst[c0 + c] = v;
+        const int cc = c0 + 4 * c;
+        if (cc >= a.k) continue;
+        double v = src[cc] + acc[c];
+        if (mode == 1 && colscale && colscale[cc] < 0.0) v = -v;
+        dst[cc] = v;
       }
     }
   }

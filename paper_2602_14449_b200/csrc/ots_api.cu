@@ -248,7 +248,7 @@ long chains_per_sm() {
 }
 
 // The Gram-form level-0 factor (gsweep.inc) for KT = 64 on tall tiles of
-// gs_tile_rows() rows (default 2048; OTS_GS_B overrides, a multiple of 128);
+// gs_tile_rows() rows (2048 .. 8192 by size; OTS_GS_B overrides, a multiple of 128);
 // OTS_GSWEEP=0 selects the register-tile kernel for every chain.
 bool gsweep_on(int KT, int b) {
   static int v = [] {
@@ -277,16 +277,34 @@ long fast_min_rows() {
   return v;
 }
 
-int gs_tile_rows() {
-  static int v = [] {
+// Tall-tile height of the Gram-form factor.  The sweep, the per-tile algebra
+// and the coefficient kernels cost one unit per tile, so taller is cheaper
+// (headline: 2048 -> 42.0 ms, 4096 -> 39.8, 8192 -> 38.7, parity unchanged),
+// as long as every SM still gets a dozen tiles to balance over: 2048 rows,
+// doubled up to 8192 while m / b >= 12 nsm.  OTS_GS_B overrides it.
+int gs_tile_rows(long m, int nsm) {
+  static int env = [] {
     const char* e = getenv("OTS_GS_B");
-    int x = e ? atoi(e) : 2048;
-    return (x >= 128 && x % 128 == 0) ? x : 2048;
+    int x = e ? atoi(e) : 0;
+    return (x >= 128 && x % 128 == 0) ? x : 0;
+  }();
+  if (env) return env;
+  int b = 2048;
+  while (b < 8192 && m / (2 * b) >= 12L * nsm) b *= 2;
+  return b;
+}
+
+// level-0 chain geometry: tiles of b rows, rows split over chains_per_sm * nsm chains
+// fan-in of the reduction tree over the chain R's (OTS_TREE_G, default 4)
+int tree_fanin() {
+  static int v = [] {
+    const char* e = getenv("OTS_TREE_G");
+    int x = e ? atoi(e) : 4;
+    return (x >= 2 && x <= 4) ? x : 4;
   }();
   return v;
 }
 
-// level-0 chain geometry: tiles of b rows, rows split over chains_per_sm * nsm chains
 ChainGeom level0_geom(long m, int KT, int b, int nsm) {
   long target = chains_per_sm() * nsm;
   long per = (m + target - 1) / target;
@@ -307,7 +325,7 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     int b = chain_bmax(KT);
     if (b > 128 && KT == 64) b = 128;
     const bool gs = !exact && gsweep_on(KT, b);
-    L.G = level0_geom(m, KT, gs ? gs_tile_rows() : b, nsm);
+    L.G = level0_geom(m, KT, gs ? gs_tile_rows(m, nsm) : b, nsm);
     const long nch = L.G.nchains;
     if (gs) {
       const int f = L.G.b / b;
@@ -327,7 +345,7 @@ std::vector<Level> plan_levels(Arena& ar, double* D0, long ldd0, int ncols0, lon
     Level L{};
     L.D = P.R; L.ldd = KT; L.ncols = KT;
     long nrows = (long)P.G.nchains * KT;
-    int g = 4;
+    int g = tree_fanin();
     long rpc = (long)KT * g;
     long nch = (nrows + rpc - 1) / rpc;
     L.G = ChainGeom{nrows, KT, g - 1, rpc, (int)nch};
@@ -344,14 +362,14 @@ size_t plan_levels_bytes(long m, int KT, int nsm, bool exact = false) {
   int b = chain_bmax(KT);
   if (b > 128 && KT == 64) b = 128;
   const bool gs = !exact && gsweep_on(KT, b);
-  const ChainGeom G = level0_geom(m, KT, gs ? gs_tile_rows() : b, nsm);
+  const ChainGeom G = level0_geom(m, KT, gs ? gs_tile_rows(m, nsm) : b, nsm);
   long nch = G.nchains;
   const long tslots = gs ? (long)G.L * (G.b / b) + 1 : G.L + 1;
   tot += ((size_t)nch * tslots * KT * KT + (size_t)nch * KT * KT) * 8 + 512;
   if (gs) tot += ((size_t)nch * (G.L + 1) * KT * KT + (size_t)nch * KT * KT) * 8 + nch * 4 + 1536;
   while (nch > 1) {
     long nrows = nch * KT;
-    long rpc2 = (long)KT * 4;
+    long rpc2 = (long)KT * tree_fanin();
     long n2 = (nrows + rpc2 - 1) / rpc2;
     tot += ((size_t)n2 * 4 * KT * KT + (size_t)n2 * KT * KT) * 8 + 512;
     nch = n2;
@@ -478,7 +496,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   size_t f_tg = 0, f_coef = 0, f_part = 0;
   if (c.fast_try && fast_on() && !c.distributed && c.row0 == 0 && !c.gram_in && !c.exact_intra && c.ld_min == 0 &&
       k0 > 96 && k0 <= 128 && KT == 64 && gsweep_on(KT, 128) && j.m >= fast_min_rows()) {
-    const ChainGeom G = level0_geom(j.m, KT, gs_tile_rows(), nsm_use);
+    const ChainGeom G = level0_geom(j.m, KT, gs_tile_rows(j.m, nsm_use), nsm_use);
     if (G.L >= 1) {
       j.fast = true;
       const size_t ntl = (size_t)G.nchains * G.L;
