@@ -27,6 +27,20 @@ namespace ots {
 
 #define FAST_KEEP 0.25
 
+// cp.async.bulk global -> shared (SASS UBLKCP), completing on an mbarrier by bytes
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
 // ============================================================================
 // tgram (k0 padded to 128): per tall tile  [V^T V | V^T A]  (128 x 192)  and
 // A^T A  (64 x 64), both stored as full symmetric matrices (mirrored at the
@@ -57,7 +71,12 @@ namespace ots {
 #endif
 struct TgCfg {
   static constexpr int PW = 128, NTASK = 20, NT = NTASK * 32, RT = TG_RT;
-  static constexpr int STAGE = RT * (PW + 64);
+  // Stage rows are stored linearly with padded pitches (136 / 72 doubles: a
+  // row advances 64 bytes of bank space, so the 4 rows x 8 columns of a DMMA
+  // operand fragment take the 2-wavefront minimum) -- the layout a bulk
+  // global->shared copy (cp.async.bulk, one per row) can write.
+  static constexpr int PV = PW + 8, PA = 64 + 8;
+  static constexpr int STAGE = RT * (PV + PA);
   static constexpr int NSTAGE = TG_NSTAGE;
   static constexpr int LA = TG_LA;               // stages issued ahead; NSTAGE - 1 - LA stages of slack between warps
   static constexpr int SMEM = NSTAGE * STAGE * 8;
@@ -108,22 +127,21 @@ template <int ROLE>
 __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigned long long* full_bar,
                                         unsigned long long* empty_bar, int idx, int ra, int rb) {
   using C = TgCfg;
-  constexpr int PW = C::PW, NT1 = C::NT1, RT = C::RT;
+  constexpr int PW = C::PW, NT1 = C::NT1, RT = C::RT, PV = C::PV, PA = C::PA;
   constexpr int NX = ROLE == 0 ? 6 : (ROLE == 1 ? 3 : 0);
   const int grp = ROLE == 0 ? idx : 4 + idx;
   const int tid = threadIdx.x, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  // swizzled in-row offsets (row r = 4 kk + t, so r & 3 = t) of the two operand
-  // fragments of every extra A^T A fragment
+  // in-row offsets of the two operand fragments of every extra A^T A fragment
   int xa[NX > 0 ? NX : 1], xb[NX > 0 ? NX : 1];
 #pragma unroll
   for (int q = 0; q < NX; ++q) {
     const int fi = c_tg_aa[grp][q] >> 3, fj = c_tg_aa[grp][q] & 7;
-    xa[q] = swz(t, 8 * fi + g, 64) - t * 64;
-    xb[q] = swz(t, 8 * fj + g, 64) - t * 64;
+    xa[q] = 8 * fi + g;
+    xb[q] = 8 * fj + g;
   }
   const bool b_isV = rb < 4;
-  const int boff = b_isV ? 0 : RT * PW, bW = b_isV ? PW : 64, bcol = b_isV ? 32 * rb : 32 * (rb - 4);
+  const int boff = b_isV ? 0 : RT * PV, bW = b_isV ? PV : PA, bcol = b_isV ? 32 * rb : 32 * (rb - 4);
 
   // this CTA's items: tall tiles first (tile index ti = chain * L + t - 1),
   // then chain heads
@@ -162,10 +180,16 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
   };
 
   const int it0 = skip_empty(blockIdx.x < ntl ? (int)blockIdx.x : ntl + (int)blockIdx.x);
-  // producer: this thread's fixed share of a stage -- 16-byte unit uv of rows
-  // rv0, rv0 + 10, ... of the V part (640 threads = 10 rows of 64 units) and unit
-  // ua of rows ra0, ra0 + 20, ... of the A part (20 rows of 32 units); the
-  // item's row range is worked out once per item, not per stage
+  // producer.  Full stages (64 rows inside the item, even k0 and k): one bulk
+  // copy per row (threads 0..63 a V row, 64..127 an A row), completing on the
+  // stage's mbarrier by bytes; thread 0 posts the byte count with its arrival,
+  // everyone else just arrives.  Partial stages (the last tile of the last
+  // chain) and odd widths: this thread's fixed share of 16-byte cp.async units
+  // with zero fill -- unit uv of rows rv0, rv0 + 10, ... of the V part (640
+  // threads = 10 rows of 64 units) and unit ua of rows ra0, ra0 + 20, ... of
+  // the A part.  Columns beyond k0 / k are zeroed once (bulk copies never
+  // touch them).  The item's row range is worked out once per item.
+  const bool bulk_ok = !(a.k0 & 1) && !(a.k & 1);
   const int uv = tid & 63, rv0 = tid >> 6, ua = tid & 31, ra0 = tid >> 5;
   const int vbytes = 2 * uv + 1 < a.k0 ? 16 : (2 * uv < a.k0 ? 8 : 0);
   const int abytes = 2 * ua + 1 < a.k ? 16 : (2 * ua < a.k ? 8 : 0);
@@ -184,24 +208,31 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
     const long rr = p_r0 + (long)p_ch * RT;
     const int nr = (int)(p_rhi - rr < RT ? p_rhi - rr : RT);           // rows of this stage inside the item
     double* Ps = smem + s * C::STAGE;
-    double* Bs = Ps + RT * PW;
+    double* Bs = Ps + RT * PV;
+    if (bulk_ok && nr == RT) {
+      if (tid < RT) bulk_g2s(Ps + tid * PV, a.V + (rr + tid) * a.ldv, (unsigned)a.k0 * 8u, &full_bar[s]);
+      else if (tid < 2 * RT) bulk_g2s(Bs + (tid - RT) * PA, a.A + (rr + tid - RT) * a.lda, (unsigned)a.k * 8u, &full_bar[s]);
+      if (tid == 0) mbar_arrive_expect_tx(&full_bar[s], (unsigned)(RT * (a.k0 + a.k)) * 8u);
+      else mbar_arrive(&full_bar[s]);
+    } else {
 #pragma unroll
-    for (int q = 0; q < (RT + 9) / 10; ++q) {
-      const int r = rv0 + 10 * q;
-      if (r < RT) {
-        const bool in = r < nr;
-        cp_async16(Ps + swz(r, 2 * uv, PW), in ? vsrc + (rr + r) * a.ldv : a.V, in ? vbytes : 0);
+      for (int q = 0; q < (RT + 9) / 10; ++q) {
+        const int r = rv0 + 10 * q;
+        if (r < RT) {
+          const bool in = r < nr;
+          cp_async16(Ps + r * PV + 2 * uv, in ? vsrc + (rr + r) * a.ldv : a.V, in ? vbytes : 0);
+        }
       }
-    }
 #pragma unroll
-    for (int q = 0; q < (RT + 19) / 20; ++q) {
-      const int r = ra0 + 20 * q;
-      if (r < RT) {
-        const bool in = r < nr;
-        cp_async16(Bs + swz(r, 2 * ua, 64), in ? asrc + (rr + r) * a.lda : a.A, in ? abytes : 0);
+      for (int q = 0; q < (RT + 19) / 20; ++q) {
+        const int r = ra0 + 20 * q;
+        if (r < RT) {
+          const bool in = r < nr;
+          cp_async16(Bs + r * PA + 2 * ua, in ? asrc + (rr + r) * a.lda : a.A, in ? abytes : 0);
+        }
       }
+      cp_async_mbar_arrive(&full_bar[s]);
     }
-    cp_async_mbar_arrive(&full_bar[s]);
     ++p_j;
     if (++p_ch >= p_n) {
       p_ch = 0;
@@ -229,21 +260,21 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
     const int s = c_j % C::NSTAGE;
     mbar_wait(&full_bar[s], (c_j / C::NSTAGE) & 1);
     const double* Vs = smem + s * C::STAGE;
-    const double* As = Vs + RT * PW;
+    const double* As = Vs + RT * PV;
     if (ROLE == 0) {
 #pragma unroll(TgCfg::UNR)
       for (int kk = 0; kk < RT / 4; ++kk) {
         const int r = 4 * kk + t;
         double af[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 32 * idx + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Vs[r * PV + 32 * idx + 8 * i + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j <= i; ++j) dmma(acc[i][j], af[i], af[j]);
 #pragma unroll
         for (int q = 0; q < NX; ++q)
-          dmma(acc[tg_ex_i(true, q)][tg_ex_j(true, q)], As[r * 64 + xa[q]], As[r * 64 + xb[q]]);
+          dmma(acc[tg_ex_i(true, q)][tg_ex_j(true, q)], As[r * PA + xa[q]], As[r * PA + xb[q]]);
       }
     } else if (ROLE == 1) {
 #pragma unroll(TgCfg::UNR)
@@ -251,16 +282,16 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
         const int r = 4 * kk + t;
         double af[4], bf[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 96 + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Vs[r * PV + 96 + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) bf[j] = As[swz(r, 16 * idx + 8 * j + g, 64)];
+        for (int j = 0; j < 2; ++j) bf[j] = As[r * PA + 16 * idx + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[i], bf[j]);
 #pragma unroll
         for (int q = 0; q < NX; ++q)
-          dmma(acc[tg_ex_i(false, q)][tg_ex_j(false, q)], As[r * 64 + xa[q]], As[r * 64 + xb[q]]);
+          dmma(acc[tg_ex_i(false, q)][tg_ex_j(false, q)], As[r * PA + xa[q]], As[r * PA + xb[q]]);
       }
     } else {
       const double* Bs = smem + s * C::STAGE + boff;
@@ -269,9 +300,9 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
         const int r = 4 * kk + t;
         double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Vs[swz(r, 32 * ra + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Vs[r * PV + 32 * ra + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, bcol + 8 * j + g, bW)];
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[r * bW + bcol + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -348,6 +379,8 @@ __global__ void __launch_bounds__(TgCfg::NT, 1) tgram_kernel(FastArgs a) {
     }
     fence_mbar_init();
   }
+  for (int e = tid; e < C::NSTAGE * C::STAGE; e += C::NT) smem[e] = 0.0;   // columns beyond k0 / k stay zero
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
   if (warp < 4) {
     tg_body<0>(a, smem, full_bar, empty_bar, warp, 0, 0);

@@ -889,13 +889,15 @@ int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr
   CK(cudaMemcpyAsync(ctx->h_status + 8, j.fflags, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(ctx->ev_fast, st));
   prof_mark(ctx, st, "gs_sweep");
-  for (size_t l = 1; l < j.lv.size(); ++l) {          // tree over the chain R's (speculative)
+  // one int through pinned memory decides the route (a rejected attempt
+  // leaves nothing queued behind it)
+  CK(cudaEventSynchronize(ctx->ev_fast));
+  if (ctx->h_status[8] != 0) return 1;
+  for (size_t l = 1; l < j.lv.size(); ++l) {          // tree over the chain R's
     Level& L = j.lv[l];
     FactorArgs fl{L.D, L.ldd, L.ncols, L.G, L.UT, L.R, 1};
     CK(launch_chain_factor(fl, KT, st));
   }
-  CK(cudaEventSynchronize(ctx->ev_fast));
-  if (ctx->h_status[8] != 0) return 1;
   prof_mark(ctx, st, "factor");
   set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
   const double* Cin = j.ident;
@@ -1014,6 +1016,9 @@ int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long
   } else if (diag_side) {
     if ((rc = phase_apply1(ctx, j))) return rc;
   } else {
+    // (re-recorded: after a rejected direct-Q attempt the side stream must not
+    // run ahead of the diagnostics' launch)
+    CK(cudaEventRecord(ctx->ev_seed, st));
     CK(launch_diag(j.s, st));
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_seed, 0));
     JobCfg c1 = j.c;
