@@ -753,13 +753,19 @@ __global__ void coef_add_z2_kernel(FastArgs a, const double* Z2, int ldz) {
 // ============================================================================
 struct FnCfg {
   static constexpr int RT = 128, KC = 32, NT = 256, NSTAGE = 2;
-  static constexpr int STAGE = RT * KC + KC * 64;
+  // padded-linear stage rows (bulk-copy friendly, see TgCfg): the row-major A
+  // operand (8 rows x 4 columns per fragment) wants a pitch = 32 bytes mod 128,
+  // the B operand (4 rows x 8 columns) 64 bytes mod 128
+  static constexpr int PP = KC + 4, PZ = 64 + 8;
+  static constexpr int STAGE = RT * PP + KC * PZ;
   static constexpr int SMEM = NSTAGE * STAGE * 8;
 };
 
 __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const double* colscale, double* X, long ldx) {
   using C = FnCfg;
+  constexpr int PP = C::PP, PZ = C::PZ;
   extern __shared__ __align__(128) double smem[];
+  __shared__ __align__(8) unsigned long long full_bar[C::NSTAGE];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm0 = (warp >> 1) * 32, wn0 = (warp & 1) * 32;
@@ -768,10 +774,13 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
   const int spt = a.G.b / C::RT;                             // sub-tiles per tall tile
   const long nsub = (long)a.G.nchains * L * spt;
   const int nchV = a.PW / C::KC, nchunks = nchV + 2;
+  const bool bulk_ok = !(a.k0 & 1) && !(a.k & 1);
   __shared__ long s_tile[3];
   if (tid == 0) {
     s_tile[0] = blockIdx.x;
     s_tile[1] = gridDim.x + atomicAdd(a.ticket, 1);
+    for (int s = 0; s < C::NSTAGE; ++s) mbar_init(&full_bar[s], C::NT);
+    fence_mbar_init();
   }
   __syncthreads();
   auto tile_of = [&](long lt) { return s_tile[lt % 3]; };
@@ -783,24 +792,47 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
     rhi = g0 + a.G.b < a.G.nrows ? g0 + a.G.b : a.G.nrows;
     r0 = g0 + (long)sub * C::RT;
   };
+  // Stage it: rows of V (chunks < nchV) or A columns ch * 32 .. of one 128-row
+  // sub-tile and the matching 32 coefficient rows.  Full chunks: one bulk copy
+  // per row (threads 0..127 an operand row, 128..159 a coefficient row),
+  // completing on the stage's mbarrier by bytes; chunks cut by the sub-tile's
+  // last row or by k0 / k: 16-byte cp.async units with zero fill.
   auto issue = [&](long it) {
     const long lt = it / nchunks;
     const long st = tile_of(lt);
-    if (st < nsub) {
-      int ti;
-      long r0, rhi;
-      geom(st, ti, r0, rhi);
-      const int s = (int)(it % C::NSTAGE), ch = (int)(it - lt * nchunks);
-      double* Ps = smem + s * C::STAGE;
-      double* Zs = Ps + C::RT * C::KC;
-      if (ch < nchV)
-        load_tile_async(Ps, C::KC, a.V, a.ldv, r0, C::RT, r0, rhi, ch * C::KC, C::KC, a.k0, tid, C::NT);
-      else
-        load_tile_async(Ps, C::KC, a.A, a.lda, r0, C::RT, r0, rhi, (ch - nchV) * C::KC, C::KC, a.k, tid, C::NT);
-      load_tile_async(Zs, 64, a.Coef + (long)ti * NT1 * 64, 64, (long)ch * C::KC, C::KC, 0, NT1, 0, 64, 64, tid,
-                      C::NT);
+    const int s = (int)(it % C::NSTAGE);
+    if (st >= nsub) return;
+    int ti;
+    long r0, rhi;
+    geom(st, ti, r0, rhi);
+    const int ch = (int)(it - lt * nchunks);
+    double* Ps = smem + s * C::STAGE;
+    double* Zs = Ps + C::RT * PP;
+    const bool isV = ch < nchV;
+    const double* src = isV ? a.V : a.A;
+    const long lds = isV ? a.ldv : a.lda;
+    const int c0 = (isV ? ch : ch - nchV) * C::KC, cmax = isV ? a.k0 : a.k;
+    const double* coef = a.Coef + (long)ti * NT1 * 64 + (long)ch * C::KC * 64;
+    if (bulk_ok && r0 + C::RT <= rhi && c0 + C::KC <= cmax) {
+      if (tid < C::RT) bulk_g2s(Ps + tid * PP, src + (r0 + tid) * lds + c0, C::KC * 8, &full_bar[s]);
+      else if (tid < C::RT + C::KC) bulk_g2s(Zs + (tid - C::RT) * PZ, coef + (long)(tid - C::RT) * 64, 64 * 8, &full_bar[s]);
+      if (tid == 0) mbar_arrive_expect_tx(&full_bar[s], (C::RT * C::KC + C::KC * 64) * 8);
+      else mbar_arrive(&full_bar[s]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < C::RT * (C::KC / 2) / C::NT; ++q) {          // 2048 units: unit u of rows rb, rb + 16, ...
+        const int i = tid + q * C::NT, r = i >> 4, u = i & 15;
+        const int c = c0 + 2 * u;
+        const bool in = r0 + r < rhi && c < cmax;
+        cp_async16(Ps + r * PP + 2 * u, in ? src + (r0 + r) * lds + c : src, in ? (c + 1 < cmax ? 16 : 8) : 0);
+      }
+#pragma unroll
+      for (int q = 0; q < C::KC * 32 / C::NT; ++q) {                    // 1024 units of the coefficient rows
+        const int i = tid + q * C::NT, r = i >> 5, u = i & 31;
+        cp_async16(Zs + r * PZ + 2 * u, coef + (long)r * 64 + 2 * u, 16);
+      }
+      cp_async_mbar_arrive(&full_bar[s]);
     }
-    cp_async_commit();
   };
   unsigned negmask = 0;
   if (colscale) {
@@ -824,20 +856,20 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
-    cp_async_wait<0>();
-    __syncthreads();
+    __syncthreads();                                         // everyone is done with the other stage
     if (ch == 0 && tid == 0) s_tile[(lt + 2) % 3] = gridDim.x + atomicAdd(a.ticket, 1);
     issue(it + 1);
     const int s = (int)(it % C::NSTAGE);
+    mbar_wait(&full_bar[s], (unsigned)((it / C::NSTAGE) & 1));
     const double* Ps = smem + s * C::STAGE;
-    const double* Zs = Ps + C::RT * C::KC;
+    const double* Zs = Ps + C::RT * PP;
 #pragma unroll
     for (int kk = 0; kk < C::KC / 4; ++kk) {
       double af[4], bf[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = Ps[swz(wm0 + 8 * i + g, 4 * kk + t, C::KC)];
+      for (int i = 0; i < 4; ++i) af[i] = Ps[(wm0 + 8 * i + g) * PP + 4 * kk + t];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Zs[swz(4 * kk + t, wn0 + 8 * j + g, 64)];
+      for (int j = 0; j < 4; ++j) bf[j] = Zs[(4 * kk + t) * PZ + wn0 + 8 * j + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
