@@ -291,6 +291,9 @@ def run_gpu(args):
                 "step_frac_of_roofline": round(t_roof / (step_ms * 1e-3), 4),
                 "pipeline": "direct-Q (tile Grams of [V | A]; executes fewer flops than F_alg)" if fast
                             else "materialised X",
+                # flops the step EXECUTES on its two streaming passes (the per-tile algebra adds ~3%)
+                "step_executed_tflops": round(((n - k0) * w * (w + 1.0) + 2.0 * (n - k0) * w * k
+                                               if fast else F) / (step_ms * 1e-3) / 1e12, 3),
                 "step_hbm_gbs": round(gbs, 1), "step_hbm_frac": round(gbs / hbm, 4)}
 
     # e2e: public API with host buffers (pinned), H2D of V, A and D2H of Q, R, S
