@@ -113,3 +113,23 @@ def test_direct_q_shape_errors_and_non_finite():
     assert took_fast() == 1
     m = P.compute_metrics(v, a, res)
     assert m.loss_orth <= 10 * n * U and m.rel_residual <= 10 * n * U
+
+
+def test_direct_q_inside_the_block_driver():
+    """Alg. 3 driver (twostage.py:100-151) with the incremental Gram: the block
+    that meets a 128-column basis takes the direct-Q pipeline (the tile pass
+    forms V^T V itself, the caller's Gram is not needed); Q, R as the oracle's."""
+    import torch
+    n = 1 << 20
+    rng = W.make_rng(91)
+    blocks = [W.normal_matrix(rng, n, 64) for _ in range(3)]
+    rq, rr = O.block_qr(blocks, "qr")
+    kb = P.KrylovBasis(n, 192, device=0, incremental_gram=True)
+    took = []
+    for b in blocks:
+        kb.append(torch.from_numpy(b).cuda())
+        took.append(took_fast())
+    assert took[2] == 1
+    assert rel(kb.q.cpu().numpy(), rq) < 1e-10
+    res = P.block_householder_qr(blocks, incremental_gram=True)
+    assert rel(res.q, rq) < 1e-10 and rel(res.r, rr) < 1e-10
