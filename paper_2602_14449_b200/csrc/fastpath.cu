@@ -211,7 +211,7 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
     double* Bs = Ps + RT * PV;
     if (bulk_ok && nr == RT) {
       if (tid < RT) bulk_g2s(Ps + tid * PV, a.V + (rr + tid) * a.ldv, (unsigned)a.k0 * 8u, &full_bar[s]);
-      else if (tid < 2 * RT) bulk_g2s(Bs + (tid - RT) * PA, a.A + (rr + tid - RT) * a.lda, (unsigned)a.k * 8u, &full_bar[s]);
+      else if (tid < 2 * RT && a.k > 0) bulk_g2s(Bs + (tid - RT) * PA, a.A + (rr + tid - RT) * a.lda, (unsigned)a.k * 8u, &full_bar[s]);
       if (tid == 0) mbar_arrive_expect_tx(&full_bar[s], (unsigned)(RT * (a.k0 + a.k)) * 8u);
       else mbar_arrive(&full_bar[s]);
     } else {
@@ -751,29 +751,37 @@ __global__ void coef_add_z2_kernel(FastArgs a, const double* Z2, int ldz) {
 // (V chunks, then the two A chunks), the coefficient chunk beside it -- the
 // tsgemm_nn pipeline with a per-tile right operand.
 // ============================================================================
+// NOUT = 64: the real pipeline (K = PW + 64: V chunks, then two A chunks).
+// NOUT = 128: the complex Q formation on interleaved real views (zpath.inc):
+// Q_tile' = X_tile' E_t in place, K = 128 from the V operand only, 64-row sub-tiles.
+template <int NOUT>
 struct FnCfg {
-  static constexpr int RT = 128, KC = 32, NT = 256, NSTAGE = 2;
+  static constexpr int RT = NOUT == 64 ? 128 : 64, KC = 32, NT = 256, NSTAGE = 2;
   // padded-linear stage rows (bulk-copy friendly, see TgCfg): the row-major A
   // operand (8 rows x 4 columns per fragment) wants a pitch = 32 bytes mod 128,
   // the B operand (4 rows x 8 columns) 64 bytes mod 128
-  static constexpr int PP = KC + 4, PZ = 64 + 8;
+  static constexpr int PP = KC + 4, PZ = NOUT + 8;
   static constexpr int STAGE = RT * PP + KC * PZ;
   static constexpr int SMEM = NSTAGE * STAGE * 8;
 };
 
-__global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const double* colscale, double* X, long ldx) {
-  using C = FnCfg;
+template <int NOUT>
+__global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const double* colscale, double* X, long ldx,
+                                                          int ncols_out) {
+  using C = FnCfg<NOUT>;
   constexpr int PP = C::PP, PZ = C::PZ;
   extern __shared__ __align__(128) double smem[];
   __shared__ __align__(8) unsigned long long full_bar[C::NSTAGE];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm0 = (warp >> 1) * 32, wn0 = (warp & 1) * 32;
-  const int NT1 = a.PW + 64;
+  const int wm0 = NOUT == 64 ? (warp >> 1) * 32 : (warp >> 2) * 32;
+  const int wn0 = NOUT == 64 ? (warp & 1) * 32 : (warp & 3) * 32;
+  const int nchA = a.k > 0 ? 2 : 0;
+  const int NT1 = a.PW + 32 * nchA;
   const int L = a.G.L;
   const int spt = a.G.b / C::RT;                             // sub-tiles per tall tile
   const long nsub = (long)a.G.nchains * L * spt;
-  const int nchV = a.PW / C::KC, nchunks = nchV + 2;
+  const int nchV = a.PW / C::KC, nchunks = nchV + nchA;
   const bool bulk_ok = !(a.k0 & 1) && !(a.k & 1);
   __shared__ long s_tile[3];
   if (tid == 0) {
@@ -812,11 +820,11 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
     const double* src = isV ? a.V : a.A;
     const long lds = isV ? a.ldv : a.lda;
     const int c0 = (isV ? ch : ch - nchV) * C::KC, cmax = isV ? a.k0 : a.k;
-    const double* coef = a.Coef + (long)ti * NT1 * 64 + (long)ch * C::KC * 64;
+    const double* coef = a.Coef + (long)ti * NT1 * NOUT + (long)ch * C::KC * NOUT;
     if (bulk_ok && r0 + C::RT <= rhi && c0 + C::KC <= cmax) {
       if (tid < C::RT) bulk_g2s(Ps + tid * PP, src + (r0 + tid) * lds + c0, C::KC * 8, &full_bar[s]);
-      else if (tid < C::RT + C::KC) bulk_g2s(Zs + (tid - C::RT) * PZ, coef + (long)(tid - C::RT) * 64, 64 * 8, &full_bar[s]);
-      if (tid == 0) mbar_arrive_expect_tx(&full_bar[s], (C::RT * C::KC + C::KC * 64) * 8);
+      else if (tid < C::RT + C::KC) bulk_g2s(Zs + (tid - C::RT) * PZ, coef + (long)(tid - C::RT) * NOUT, NOUT * 8, &full_bar[s]);
+      if (tid == 0) mbar_arrive_expect_tx(&full_bar[s], (C::RT * C::KC + C::KC * NOUT) * 8);
       else mbar_arrive(&full_bar[s]);
     } else {
 #pragma unroll
@@ -827,9 +835,9 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
         cp_async16(Ps + r * PP + 2 * u, in ? src + (r0 + r) * lds + c : src, in ? (c + 1 < cmax ? 16 : 8) : 0);
       }
 #pragma unroll
-      for (int q = 0; q < C::KC * 32 / C::NT; ++q) {                    // 1024 units of the coefficient rows
-        const int i = tid + q * C::NT, r = i >> 5, u = i & 31;
-        cp_async16(Zs + r * PZ + 2 * u, coef + (long)r * 64 + 2 * u, 16);
+      for (int q = 0; q < C::KC * (NOUT / 2) / C::NT; ++q) {             // units of the coefficient rows
+        const int i = tid + q * C::NT, r = i / (NOUT / 2), u = i - r * (NOUT / 2);
+        cp_async16(Zs + r * PZ + 2 * u, coef + (long)r * NOUT + 2 * u, 16);
       }
       cp_async_mbar_arrive(&full_bar[s]);
     }
@@ -839,8 +847,8 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = wn0 + 8 * j + 2 * t;
-      if (c < a.k && colscale[c] < 0.0) negmask |= 1u << (2 * j);
-      if (c + 1 < a.k && colscale[c + 1] < 0.0) negmask |= 1u << (2 * j + 1);
+      if (c < ncols_out && colscale[c] < 0.0) negmask |= 1u << (2 * j);
+      if (c + 1 < ncols_out && colscale[c + 1] < 0.0) negmask |= 1u << (2 * j + 1);
     }
   }
   double acc[4][4][2];
@@ -894,8 +902,8 @@ __global__ void __launch_bounds__(256, 2) final_nn_kernel(FastArgs a, const doub
             y1 = __longlong_as_double(__double_as_longlong(y1) ^ f1);
           }
           double* p = X + r * ldx + c;
-          if (c + 1 < a.k) __stcs(reinterpret_cast<double2*>(p), make_double2(y0, y1));
-          else if (c < a.k) p[0] = y0;
+          if (c + 1 < ncols_out) __stcs(reinterpret_cast<double2*>(p), make_double2(y0, y1));
+          else if (c < ncols_out) p[0] = y0;
         }
     }
   }
@@ -989,16 +997,31 @@ cudaError_t launch_coef_add_z2(const FastArgs& a, const double* Z2, int ldz, cud
   return cudaGetLastError();
 }
 
-cudaError_t launch_final_nn(const FastArgs& a, const double* colscale, double* X, long ldx, cudaStream_t st) {
-  if (a.G.b % FnCfg::RT || !a.ticket) return cudaErrorInvalidValue;
-  cudaFuncSetAttribute(final_nn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FnCfg::SMEM);
-  const long nsub = (long)a.G.nchains * a.G.L * (a.G.b / FnCfg::RT);
+template <int NOUT>
+static cudaError_t launch_final_nn_t(const FastArgs& a, const double* colscale, double* X, long ldx, int ncols_out,
+                                     cudaStream_t st) {
+  using C = FnCfg<NOUT>;
+  if (a.G.b % C::RT || !a.ticket) return cudaErrorInvalidValue;
+  auto k = final_nn_kernel<NOUT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  const long nsub = (long)a.G.nchains * a.G.L * (a.G.b / C::RT);
   const int nsm = fast_nsm();
   const int grid = (int)(nsub < 2L * nsm ? nsub : 2L * nsm);
   cudaError_t e = cudaMemsetAsync(a.ticket, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
-  final_nn_kernel<<<grid, FnCfg::NT, FnCfg::SMEM, st>>>(a, colscale, X, ldx);
+  k<<<grid, C::NT, C::SMEM, st>>>(a, colscale, X, ldx, ncols_out);
   return cudaGetLastError();
+}
+
+cudaError_t launch_final_nn(const FastArgs& a, const double* colscale, double* X, long ldx, cudaStream_t st) {
+  return launch_final_nn_t<64>(a, colscale, X, ldx, a.k, st);
+}
+
+// complex Q formation on real views: X (rows x ncols_out, in place) <- X E_t per
+// tall tile, E_t = a.Coef + tile * 128 * 128 (a.V = X, a.k0 = a.PW = 128, a.k = 0)
+cudaError_t launch_final_nn128(const FastArgs& a, double* X, long ldx, int ncols_out, cudaStream_t st) {
+  if (a.PW != 128 || a.k != 0) return cudaErrorInvalidValue;
+  return launch_final_nn_t<128>(a, nullptr, X, ldx, ncols_out, st);
 }
 
 cudaError_t launch_fast_flags(const int* chain_flags, int nch, int* flags, cudaStream_t st) {

@@ -109,6 +109,7 @@ cudaError_t launch_tile_alg(const FastArgs& a, cudaStream_t st);
 cudaError_t launch_coef_b(const FastArgs& a, double* ypart, int grid, cudaStream_t st);
 cudaError_t launch_coef_add_z2(const FastArgs& a, const double* Z2, int ldz, cudaStream_t st);
 cudaError_t launch_final_nn(const FastArgs& a, const double* colscale, double* X, long ldx, cudaStream_t st);
+cudaError_t launch_final_nn128(const FastArgs& a, double* X, long ldx, int ncols_out, cudaStream_t st);
 cudaError_t launch_fast_flags(const int* chain_flags, int nch, int* flags, cudaStream_t st);
 
 cudaError_t launch_tsgemm_tn(const TnArgs& a, int PW, int BW, bool alias, bool sym, int grid, cudaStream_t st);
@@ -128,6 +129,26 @@ using ZFactorArgs = FactorArgs;
 using ZQformArgs = QformArgs;
 cudaError_t launch_zchain_factor(const ZFactorArgs& a, int KT, cudaStream_t st);
 cudaError_t launch_zchain_qform(const ZQformArgs& a, int KT, cudaStream_t st);
+// Gram-form complex level 0 on tall tiles (zchain.cu, zpath.inc): geometry G =
+// chains of a 64-row head + L tall tiles; all matrices complex (re, im) 64 x 64
+// row-major unless noted.
+struct ZgsArgs {
+  ChainGeom G;
+  const double* TG; long tg_stride;   // per tile (chain * L + t - 1): real Gram of the interleaved view, ld 192
+  const double* Rh;                   // head R per chain
+  double* T;                          // T per tile: chain * (L + 1) + t
+  double* Cc;                         // Cc per tile: chain * (L + 1) + t
+  double* Rout;                       // chain R's
+  int* flags;                         // per chain: 1 = cancellation, take the exact path
+  int ncols;                          // complex columns
+  const double* Cin = nullptr;        // coef: stacked chain C's
+  double* Kexp = nullptr;             // coef: per tile 128 x 128 real right-multiplier
+  double* Chead = nullptr;            // coef: per chain C for the head rows
+  double* Hsave = nullptr;            // heads: per chain 64 x 64 side buffer
+};
+cudaError_t launch_zgs_sweep(const ZgsArgs& a, cudaStream_t st);
+cudaError_t launch_zgs_coef(const ZgsArgs& a, cudaStream_t st);
+cudaError_t launch_zgs_heads(const ZgsArgs& a, double* D, long ldd, int mode, cudaStream_t st);
 int zchain_bmax();
 int chain_bmax(int KT);
 int debug_counters(unsigned long long* out, int reset);

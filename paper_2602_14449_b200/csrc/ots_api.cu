@@ -125,6 +125,8 @@ struct ots_ctx {
   char* b_ws = nullptr;      // B-inner scaled copies
   size_t b_size = 0;
   char* z_ws = nullptr;      // complex cholshift ping-pong buffer
+  char* zgs_ws = nullptr;    // complex Gram-form intra QR workspace (zpath.inc)
+  size_t zgs_size = 0;
   size_t z_size = 0;
   // distributed job state
   struct Job* job = nullptr;
@@ -1118,6 +1120,7 @@ void ots_ctx_destroy(ots_ctx* c) {
   if (c->ws) cudaFree(c->ws);
   if (c->b_ws) cudaFree(c->b_ws);
   if (c->z_ws) cudaFree(c->z_ws);
+  if (c->zgs_ws) cudaFree(c->zgs_ws);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->nn_counter) cudaFree(c->nn_counter);
   if (c->ev_seed) cudaEventDestroy(c->ev_seed);

@@ -590,7 +590,287 @@ cudaError_t zqform_t(const ZQformArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// Gram-form complex tile factorization on tall tiles (KT = 64): the complex
+// twin of gsweep.inc.  With alpha = R_jj real at every structured step (the
+// head's and every earlier tile's diagonal is a zlarfg beta), tau_j, scal_j
+// and beta_j are REAL, H_j is Hermitian, and the real identities carry over
+// with conjugates on the row factors:
+//   u_c = scal M[j][c],  w_c = tau (R[j][c] + u_c),  c_c = u_c - w_c yy/2,
+//   M[a][b] -= conj(w_a) c_b + conj(c_a) w_b                   (a, b > j)
+//   P[j][c] = u_c - w_c yy,  P[a][c] -= G[a][j] w_c,  G[a][j] = scal P[a][j]  (a < j)
+//   T = D_tau (I + striu(G) D_tau)^-1,   Cc = D (I + W D)^-1,   Y = X Cc,
+// where M = X^H X is recombined from the REAL Gram of the interleaved view
+// (tgram_kernel's V^T V block over the 128 real columns).  Unblocked: with
+// 4096-row tiles the sweep is a per-mille of the call.  A chain whose
+// cancellation factor exceeds ZGS_RHO is flagged; the caller then takes the
+// exact zchain_factor path for the whole call.
+// ===========================================================================
+#define ZGS_RHO 32.0
+
+struct ZgsCfg {
+  static constexpr int KT = 64, LDS = 65, NT = 256;
+  static constexpr int SMEM = 3 * KT * LDS * 16 + (4 * KT) * 8 + (3 * KT) * 16 + 64;
+};
+
+// out (upper triangular, ld LDS) = Dg (I + S Dg)^-1, Dg = diag(dv) real, S strictly
+// upper through an accessor:  out[i][j] = dv_j (delta_ij - sum_{l=i}^{j-1} out[i][l] S[l][j]).
+// 4 lanes per row i; called by all 256 threads.
+template <class SGet>
+__device__ __forceinline__ void zgs_tri(cplx* out, const double* dv, SGet S) {
+  constexpr int KT = ZgsCfg::KT, LDS = ZgsCfg::LDS;
+  const int i = threadIdx.x >> 2, part = threadIdx.x & 3;
+  for (int e = threadIdx.x; e < KT * KT; e += ZgsCfg::NT) out[(e >> 6) * LDS + (e & 63)] = cmk(0.0, 0.0);
+  __syncthreads();
+  for (int j = 0; j < KT; ++j) {
+    cplx s = cmk(0.0, 0.0);
+    if (i < j)
+      for (int l = i + part; l < j; l += 4) s = cfma(out[i * LDS + l], S(l, j), s);
+    s = gsumc<4>(s, 0xffffffffu);
+    __syncthreads();
+    if (part == 0) {
+      if (i < j) out[i * LDS + j] = cmk(-dv[j] * s.x, -dv[j] * s.y);
+      else if (i == j) out[i * LDS + j] = cmk(dv[j], 0.0);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) zgs_sweep_kernel(ZgsArgs a) {
+  using C = ZgsCfg;
+  constexpr int KT = C::KT, LDS = C::LDS;
+  extern __shared__ __align__(16) unsigned char zsm_raw[];
+  cplx* MP = reinterpret_cast<cplx*>(zsm_raw);      // M (unprocessed rows, upper) | P (processed rows) | G (processed cols)
+  cplx* RW = MP + KT * LDS;                           // R (upper, diag = beta) | W^T (strictly lower)
+  cplx* TB = RW + KT * LDS;                           // T, then Cc
+  double* tau_v = reinterpret_cast<double*>(TB + KT * LDS);
+  double* scal_v = tau_v + KT;
+  double* yy_v = scal_v + KT;
+  double* d0 = yy_v + KT;
+  cplx* wv = reinterpret_cast<cplx*>(d0 + KT);
+  cplx* cv = wv + KT;
+  cplx* gv = cv + KT;
+  int* flag = reinterpret_cast<int*>(gv + KT);
+  const int tid = threadIdx.x;
+  const int chain = blockIdx.x;
+  const long r0 = (long)chain * a.G.rpc;
+  long rem0 = a.G.nrows - (r0 + KT);
+  int ntiles = 0;
+  if (rem0 > 0) { long t = (rem0 + a.G.b - 1) / a.G.b; ntiles = (int)(t < a.G.L ? t : a.G.L); }
+  const long tstride = (long)KT * KT;
+  cplx* Tbase = reinterpret_cast<cplx*>(a.T) + (long)chain * (a.G.L + 1) * tstride;
+  cplx* Cbase = reinterpret_cast<cplx*>(a.Cc) + (long)chain * (a.G.L + 1) * tstride;
+  const cplx* Rh = reinterpret_cast<const cplx*>(a.Rh) + (long)chain * tstride;
+  for (int e = tid; e < KT * KT; e += C::NT) {
+    const int r = e >> 6, c = e & 63;
+    RW[r * LDS + c] = (c >= r) ? Rh[e] : cmk(0.0, 0.0);
+  }
+  if (tid == 0) flag[0] = 0;
+  __syncthreads();
+  for (int t = 1; t <= ntiles; ++t) {
+    // ---- M = X^H X from the real Gram of the interleaved view (ld 192)
+    const double* Gr = a.TG + ((long)chain * a.G.L + t - 1) * a.tg_stride;
+    for (int e = tid; e < KT * KT; e += C::NT) {
+      const int j = e >> 6, l = e & 63;
+      const double2 top = *reinterpret_cast<const double2*>(Gr + (long)(2 * j) * 192 + 2 * l);
+      const double2 bot = *reinterpret_cast<const double2*>(Gr + (long)(2 * j + 1) * 192 + 2 * l);
+      MP[j * LDS + l] = (l >= j) ? cmk(top.x + bot.y, top.y - bot.x) : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    if (tid < KT) d0[tid] = sqrt(fmax(MP[tid * LDS + tid].x, 0.0));
+    for (int j = 0; j < KT; ++j) {
+      __syncthreads();
+      // ---- step scalars (every thread, redundantly): real dlarfg on (alpha, s2)
+      const double alpha = RW[j * LDS + j].x;
+      const double s2 = fmax(MP[j * LDS + j].x, 0.0);
+      double beta = alpha, tj = 0.0, scal = 0.0;
+      if (s2 > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+        tj = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+      }
+      const double yy = scal * scal * s2;
+      __syncthreads();                                // everyone has read alpha before R_jj becomes beta
+      if (tid > j && tid < KT) {                      // trailing column c
+        const int c = tid;
+        const cplx m = MP[j * LDS + c];
+        const cplx u = cmk(scal * m.x, scal * m.y);
+        const cplx r = RW[j * LDS + c];
+        const cplx w = cmk(tj * (r.x + u.x), tj * (r.y + u.y));
+        RW[j * LDS + c] = csub(r, w);
+        RW[c * LDS + j] = w;                          // W[j][c]
+        wv[c] = w;
+        cv[c] = cmk(fma(-0.5 * yy, w.x, u.x), fma(-0.5 * yy, w.y, u.y));
+        MP[j * LDS + c] = cmk(fma(-yy, w.x, u.x), fma(-yy, w.y, u.y));   // P[j][c]
+      } else if (tid == j) {
+        RW[j * LDS + j] = cmk(beta, 0.0);
+        tau_v[j] = tj;
+        scal_v[j] = scal;
+        yy_v[j] = yy;
+      } else if (tid >= KT && tid < KT + j) {         // earlier row a: G[a][j]
+        const int r = tid - KT;
+        const cplx pj = MP[r * LDS + j];
+        const cplx gg = cmk(scal * pj.x, scal * pj.y);
+        MP[r * LDS + j] = gg;
+        gv[r] = gg;
+      }
+      __syncthreads();
+      // ---- rank-2 update of the trailing M and the processed rows' P
+      for (int e = tid; e < KT * KT; e += C::NT) {
+        const int r = e >> 6, c = e & 63;
+        if (c <= j) continue;
+        if (r > j) {
+          if (r > c) continue;
+          cplx m = MP[r * LDS + c];
+          m = csub(m, cmul(conjc(wv[r]), cv[c]));
+          m = csub(m, cmul(conjc(cv[r]), wv[c]));
+          MP[r * LDS + c] = m;
+        } else if (r < j) {
+          MP[r * LDS + c] = csub(MP[r * LDS + c], cmul(gv[r], wv[c]));
+        }
+      }
+    }
+    __syncthreads();
+    // ---- T = D_tau (I + striu(G) D_tau)^-1
+    zgs_tri(TB, tau_v, [&](int l, int j) { return MP[l * LDS + j]; });
+    {
+      cplx* Tg = Tbase + (long)t * tstride;
+      for (int e = tid; e < KT * KT; e += C::NT) Tg[e] = TB[(e >> 6) * LDS + (e & 63)];
+    }
+    __syncthreads();
+    // ---- Cc = D (I + W D)^-1,  W[l][j] in RW's lower part
+    zgs_tri(TB, scal_v, [&](int l, int j) { return RW[j * LDS + l]; });
+    {
+      cplx* Cg = Cbase + (long)t * tstride;
+      for (int e = tid; e < KT * KT; e += C::NT) Cg[e] = TB[(e >> 6) * LDS + (e & 63)];
+    }
+    // ---- cancellation factor rho_j = sum_l |Cc[l][j]| d0[l] against |y_j|
+    if (tid < KT) {
+      const int j = tid;
+      double rho = 0.0;
+      for (int l = 0; l <= j; ++l) {
+        const cplx x = TB[l * LDS + j];
+        rho = fma(sqrt(x.x * x.x + x.y * x.y), d0[l], rho);
+      }
+      const bool ok = (tau_v[j] == 0.0) || (rho <= ZGS_RHO * sqrt(yy_v[j]));
+      if (!ok) flag[0] = 1;
+    }
+    __syncthreads();
+    if (flag[0]) {
+      if (tid == 0) a.flags[chain] = 1;
+      return;
+    }
+    // strictly lower part of RW (this tile's W) is cleared for the next tile
+    for (int e = tid; e < KT * KT; e += C::NT) {
+      const int r = e >> 6, c = e & 63;
+      if (c < r) RW[r * LDS + c] = cmk(0.0, 0.0);
+    }
+    __syncthreads();
+  }
+  if (tid == 0) a.flags[chain] = 0;
+  cplx* R = reinterpret_cast<cplx*>(a.Rout) + (long)chain * tstride;
+  for (int e = tid; e < KT * KT; e += C::NT) {
+    const int r = e >> 6, c = e & 63;
+    R[e] = (c >= r) ? RW[r * LDS + c] : cmk(0.0, 0.0);
+  }
+}
+
+// Coefficients of the accepted chains, in reverse chain order: M = T C,
+// K = -Cc M, C <- C - M; K_t goes out as the 128 x 128 real right-multiplier
+// of the interleaved view ([re, im] K = [re kr - im ki, re ki + im kr]), the
+// chain's last C to Chead (the head rows' Q formation).
+__global__ void __launch_bounds__(256, 1) zgs_coef_kernel(ZgsArgs a) {
+  constexpr int KT = 64, LDS = ZCfg<64>::LDS, MT = KT / 16;
+  extern __shared__ __align__(16) unsigned char zsm_raw[];
+  cplx* Cs = reinterpret_cast<cplx*>(zsm_raw);
+  cplx* B1 = Cs + KT * LDS;
+  cplx* B2 = B1 + KT * LDS;
+  const int tid = threadIdx.x, tr = tid / 16, tc = tid % 16;
+  const int chain = blockIdx.x;
+  const long r0 = (long)chain * a.G.rpc;
+  long rem0 = a.G.nrows - (r0 + KT);
+  int ntiles = 0;
+  if (rem0 > 0) { long t = (rem0 + a.G.b - 1) / a.G.b; ntiles = (int)(t < a.G.L ? t : a.G.L); }
+  const long tstride = (long)KT * KT;
+  const cplx* Tbase = reinterpret_cast<const cplx*>(a.T) + (long)chain * (a.G.L + 1) * tstride;
+  const cplx* Cbase = reinterpret_cast<const cplx*>(a.Cc) + (long)chain * (a.G.L + 1) * tstride;
+  const cplx* Cin = reinterpret_cast<const cplx*>(a.Cin) + (long)chain * tstride;
+  for (int e = tid; e < KT * KT; e += 256) Cs[(e >> 6) * LDS + (e & 63)] = Cin[e];
+  for (int t = ntiles; t >= 1; --t) {
+    __syncthreads();
+    const cplx* Tt = Tbase + (long)t * tstride;
+    const cplx* Ct = Cbase + (long)t * tstride;
+    for (int e = tid; e < KT * KT; e += 256) {
+      B1[(e >> 6) * LDS + (e & 63)] = Tt[e];
+      B2[(e >> 6) * LDS + (e & 63)] = Ct[e];
+    }
+    __syncthreads();
+    cplx acc[MT][MT];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < MT; ++jj) acc[i][jj] = cmk(0.0, 0.0);
+    zmm<KT>(B1, Cs, acc, tr, tc);                     // M = T C
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < MT; ++jj) {
+        const int o = (tr + 16 * i) * LDS + tc + 16 * jj;
+        B1[o] = acc[i][jj];
+        Cs[o] = csub(Cs[o], acc[i][jj]);
+        acc[i][jj] = cmk(0.0, 0.0);
+      }
+    __syncthreads();
+    zmm<KT>(B2, B1, acc, tr, tc);                     // Cc M
+    double* E = a.Kexp + ((long)chain * a.G.L + t - 1) * (4 * tstride);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int jj = 0; jj < MT; ++jj) {
+        const int ra = tr + 16 * i, cb = tc + 16 * jj;
+        const double kr = -acc[i][jj].x, ki = -acc[i][jj].y;
+        *reinterpret_cast<double2*>(E + (long)(2 * ra) * 128 + 2 * cb) = make_double2(kr, ki);
+        *reinterpret_cast<double2*>(E + (long)(2 * ra + 1) * 128 + 2 * cb) = make_double2(-ki, kr);
+      }
+  }
+  __syncthreads();
+  cplx* Ch = reinterpret_cast<cplx*>(a.Chead) + (long)chain * tstride;
+  for (int e = tid; e < KT * KT; e += 256) Ch[e] = Cs[(e >> 6) * LDS + (e & 63)];
+}
+
+// head rows of every chain <-> a side buffer (mode 0: save, 1: restore)
+__global__ void zgs_heads_kernel(ZgsArgs a, double* D, long ldd, int mode) {
+  const int chain = blockIdx.x;
+  const long r0 = (long)chain * a.G.rpc;
+  cplx* Dc = reinterpret_cast<cplx*>(D);
+  cplx* S = reinterpret_cast<cplx*>(a.Hsave) + (long)chain * 64 * 64;
+  for (int e = threadIdx.x; e < 64 * 64; e += blockDim.x) {
+    const int r = e >> 6, c = e & 63;
+    if (r0 + r >= a.G.nrows || c >= a.ncols) continue;
+    if (mode == 0) S[e] = Dc[(r0 + r) * ldd + c];
+    else Dc[(r0 + r) * ldd + c] = S[e];
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_zgs_sweep(const ZgsArgs& a, cudaStream_t st) {
+  cudaFuncSetAttribute(zgs_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, ZgsCfg::SMEM);
+  zgs_sweep_kernel<<<a.G.nchains, ZgsCfg::NT, ZgsCfg::SMEM, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_zgs_coef(const ZgsArgs& a, cudaStream_t st) {
+  constexpr int SM = 3 * 64 * ZCfg<64>::LDS * 16;
+  cudaFuncSetAttribute(zgs_coef_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SM);
+  zgs_coef_kernel<<<a.G.nchains, 256, SM, st>>>(a);
+  return cudaGetLastError();
+}
+cudaError_t launch_zgs_heads(const ZgsArgs& a, double* D, long ldd, int mode, cudaStream_t st) {
+  zgs_heads_kernel<<<a.G.nchains, 256, 0, st>>>(a, D, ldd, mode);
+  return cudaGetLastError();
+}
 
 int zchain_bmax() { return ZCfg<64>::B; }
 
