@@ -130,6 +130,7 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
   constexpr int PW = C::PW, NT1 = C::NT1, RT = C::RT, PV = C::PV, PA = C::PA;
   constexpr int NX = ROLE == 0 ? 6 : (ROLE == 1 ? 3 : 0);
   const int grp = ROLE == 0 ? idx : 4 + idx;
+  const bool has_a = a.k > 0;      // k = 0 (the complex path's Gram of one 128-column view): A blocks are skipped
   const int tid = threadIdx.x, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   // in-row offsets of the two operand fragments of every extra A^T A fragment
@@ -272,11 +273,14 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
         for (int i = 0; i < 4; ++i)
 #pragma unroll
           for (int j = 0; j <= i; ++j) dmma(acc[i][j], af[i], af[j]);
+        if (has_a) {
 #pragma unroll
-        for (int q = 0; q < NX; ++q)
-          dmma(acc[tg_ex_i(true, q)][tg_ex_j(true, q)], As[r * PA + xa[q]], As[r * PA + xb[q]]);
+          for (int q = 0; q < NX; ++q)
+            dmma(acc[tg_ex_i(true, q)][tg_ex_j(true, q)], As[r * PA + xa[q]], As[r * PA + xb[q]]);
+        }
       }
     } else if (ROLE == 1) {
+      if (has_a)
 #pragma unroll(TgCfg::UNR)
       for (int kk = 0; kk < RT / 4; ++kk) {
         const int r = 4 * kk + t;
@@ -295,6 +299,7 @@ __device__ __forceinline__ void tg_body(const FastArgs& a, double* smem, unsigne
       }
     } else {
       const double* Bs = smem + s * C::STAGE + boff;
+      if (b_isV || has_a)
 #pragma unroll(TgCfg::UNR)
       for (int kk = 0; kk < RT / 4; ++kk) {
         const int r = 4 * kk + t;

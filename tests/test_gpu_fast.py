@@ -133,3 +133,66 @@ def test_direct_q_inside_the_block_driver():
     assert rel(kb.q.cpu().numpy(), rq) < 1e-10
     res = P.block_householder_qr(blocks, incremental_gram=True)
     assert rel(res.q, rq) < 1e-10 and rel(res.r, rr) < 1e-10
+
+
+# ---------------------------------------------------------------------------
+# complex128: Gram-form intra QR on tall tiles (zgs, csrc/zchain.cu + zpath.inc)
+# ---------------------------------------------------------------------------
+def _cgauss(rng, n, k):
+    return (W.normal_matrix(rng, n, k) + 1j * W.normal_matrix(rng, n, k)) * np.sqrt(0.5)
+
+
+@pytest.mark.parametrize("n,k0,k,choice", [(1 << 20, 64, 64, "qr"), (700001, 40, 48, "mlu"), (1 << 20, 24, 33, "polar")])
+def test_complex_gram_form_vs_oracle(n, k0, k, choice):
+    rng = W.make_rng(300 + k0 + k)
+    v, _ = np.linalg.qr(_cgauss(rng, n, k0))
+    a = _cgauss(rng, n, k)
+    ref = O.two_stage(v, a, choice, diagnostics=True)
+    res = P.two_stage_qr(v, a, choice=choice)
+    assert took_fast() == 1
+    assert rel(res.q, ref["q"]) < 1e-10
+    assert rel(res.r, ref["r"]) < 1e-10
+    assert rel(res.s, ref["s"]) < 1e-10
+    assert np.all(np.tril(res.r, -1) == 0.0) and np.abs(np.diag(res.r).imag).max() == 0.0
+    assert abs(res.diagnostics.kappa_t - ref["kappa_t"]) <= 1e-10 * ref["kappa_t"]
+
+
+def test_complex_gram_form_householder_qr():
+    n, k = 1 << 20, 64
+    a = _cgauss(W.make_rng(21), n, k)
+    q0, r0 = np.linalg.qr(a)
+    res = P.householder_qr(a)
+    assert took_fast() == 1
+    assert rel(res.q, q0) < 1e-10 and rel(res.r, r0) < 1e-10
+
+
+def test_complex_gram_form_falls_back():
+    # nearly dependent columns after the projection: the sweep's cancellation
+    # factor flags the chains and the call takes the exact zchain path
+    n, k0, k = 1 << 20, 32, 64
+    rng = W.make_rng(23)
+    v, _ = np.linalg.qr(_cgauss(rng, n, k0))
+    a = _cgauss(rng, n, k)
+    a[:, :16] = v @ _cgauss(rng, k0, 16)
+    a[:, 40:44] = a[:, 36:40] + 1e-30 * _cgauss(rng, n, 4)
+    ref = O.two_stage(v, a, "qr", diagnostics=False)
+    res = P.two_stage_qr(v, a)
+    assert took_fast() == 0
+    loss, _, resid = O.gram_stability(v, a, res.q, res.r, res.s)
+    rl, _, rr = O.gram_stability(v, a, ref["q"], ref["r"], ref["s"])
+    assert loss <= 10 * n * U and resid <= 10 * n * U
+    assert loss <= 10 * max(rl, 4 * U) and resid <= 10 * max(rr, 4 * U)
+
+
+def test_complex_weighted_rows_keep_the_exact_intra_qr():
+    n, k0, k = 1 << 20, 16, 48
+    rng = W.make_rng(29)
+    d = 10.0 ** W.uniform(W.make_rng(30), 0.0, 4.0, n)
+    sq = np.sqrt(d)
+    v = np.linalg.qr(sq[:, None] * _cgauss(rng, n, k0))[0] / sq[:, None]
+    a = _cgauss(rng, n, k)
+    ip = P.InnerProduct.weighted(d)
+    res = P.b_two_stage_qr(v, a, P.initial_b_basis(ip, k0 + k), ip)
+    assert took_fast() == 0
+    m = P.compute_metrics(v, a, res, inner=ip)
+    assert m.loss_orth <= 10 * n * U and m.rel_residual <= 10 * n * U
