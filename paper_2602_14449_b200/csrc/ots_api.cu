@@ -230,6 +230,7 @@ struct Job {
   double* Rfinal = nullptr;
   // direct-Q pipeline (fastpath.cu)
   bool fast = false;
+  bool fast_active = false;     // row-sharded phases: this rank's factor took the direct-Q route
   double *fTG = nullptr, *fCoef = nullptr, *fpart = nullptr;
   long ftg_stride = 0;
   int* fflags = nullptr;        // [0] flags, [1] ticket
@@ -497,7 +498,7 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   j.fast = false;
   size_t f_tg = 0, f_coef = 0, f_part = 0;
   // (a caller-supplied V^T V is not needed here: the tile pass forms V^T V per tile anyway)
-  if (c.fast_try && fast_on() && !c.distributed && c.row0 == 0 && !c.exact_intra && c.ld_min == 0 &&
+  if (c.fast_try && fast_on() && !c.exact_intra && c.ld_min == 0 &&
       k0 > 96 && k0 <= 128 && KT == 64 && gsweep_on(KT, 128) && j.m >= fast_min_rows()) {
     const ChainGeom G = level0_geom(j.m, KT, gs_tile_rows(j.m, nsm_use), nsm_use);
     if (G.L >= 1) {
@@ -541,14 +542,15 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   j.ident = ar.take<double>((size_t)KT * KT);
   j.svec = s.svec;
   j.lv = plan_levels(ar, c.Q + j.qrow0 * c.ldq, c.ldq, (int)k, std::max<long>(j.m, 1), KT, nsm_use, c.exact_intra);
-  j.Rall = ar.take<double>((size_t)64 * KT * KT);
-  j.Cglob = ar.take<double>((size_t)64 * KT * KT);
   if (j.fast) {
     j.fTG = ar.take<double>(f_tg);
     j.fCoef = ar.take<double>(f_coef);
     j.fpart = ar.take<double>(f_part);
     j.fflags = ar.take<int>(16);
   }
+  // (last: ots_dist_tree carves the global tree's levels from the workspace behind Cglob)
+  j.Rall = ar.take<double>((size_t)64 * KT * KT);
+  j.Cglob = ar.take<double>((size_t)64 * KT * KT);
   if (ar.off > ctx->ws_size) return fail(ctx, OTS_E_CUDA, "workspace plan overflow");
   return OTS_OK;
 }
@@ -873,11 +875,12 @@ int fast_gram(ots_ctx* ctx, Job& j) {
   return OTS_OK;
 }
 
-int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr, bool diag_side) {
+// stage 1: heads' X rows, X^T X / V^T X per tile, Gram-form sweep, route
+// decision (returns 1: rejected), local tree over the chain R's
+int fast_factor(ots_ctx* ctx, Job& j) {
   const JobCfg& c = j.c;
   cudaStream_t st = c.st;
   const int KT = j.KT;
-  const long k0 = c.k0, k = c.k;
   FastArgs fa = fast_args(ctx, j);
   Level& L0 = j.lv[0];
   const int nch = L0.G.nchains;
@@ -902,8 +905,22 @@ int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr
     CK(launch_chain_factor(fl, KT, st));
   }
   prof_mark(ctx, st, "factor");
-  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
-  const double* Cin = j.ident;
+  return 0;
+}
+
+// stage 2: C's down the local tree from Ctop, per-tile coefficients, heads'
+// Q_ rows, LAPACK signs (on the rank that owns the top rows: Rfin -> Rout),
+// and this rank's Y2 = -V_b^T Q_ into Y2full
+int fast_coef(ots_ctx* ctx, Job& j, const double* Ctop, bool do_sign, double* Q, long ldq, const double* Rfin,
+              double* Rout, long ldr) {
+  const JobCfg& c = j.c;
+  cudaStream_t st = c.st;
+  const int KT = j.KT;
+  const long k0 = c.k0, k = c.k;
+  FastArgs fa = fast_args(ctx, j);
+  Level& L0 = j.lv[0];
+  const int nch = L0.G.nchains;
+  const double* Cin = Ctop;
   for (int l = (int)j.lv.size() - 1; l >= 1; --l) {
     Level& L = j.lv[l];
     QformArgs qa{L.D, L.ldd, L.ncols, L.G, L.UT, Cin, 0};
@@ -919,14 +936,22 @@ int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr
     qa.grid_max = j.nsm_use;
     CK(launch_gs_coef(qa, st));
   }
-  CK(launch_sign(j.s, Q + k0 * ldq, ldq, j.lv.back().R, KT, R, (int)ldr, st));
+  if (do_sign) CK(launch_sign(j.s, Q + k0 * ldq, ldq, Rfin, KT, Rout, (int)ldr, st));
   // Y2 = -V_b^T Q_ = -(sum_t Cx_t K_t + sum_heads V_h^T Q_h)
   const int gb = j.nsm_use, gh = std::min(nch, j.nsm_use);
   CK(launch_coef_b(fa, j.fpart, gb, st));
   CK(launch_head_rows(fa, 2, nullptr, 0, nullptr, j.fpart + (size_t)gb * j.PW * 64, gh, st));
   CK(launch_reduce_strided(j.fpart, gb + gh, (int)k0, (int)k, 64, j.Y2full, j.BWa, -1.0, st));
-  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)k0, (int)k);
-  CK(launch_z2(j.s, st));
+  return 0;
+}
+
+// stage 3 (Z2 and the signs known): coefficient rows += Z2, the final pass and
+// the heads' final rows
+int fast_final(ots_ctx* ctx, Job& j, bool diag_side) {
+  cudaStream_t st = j.c.st;
+  FastArgs fa = fast_args(ctx, j);
+  Level& L0 = j.lv[0];
+  const int ghead = std::min(L0.G.nchains, 2 * ctx->nsm);
   CK(launch_coef_add_z2(fa, j.s.Z2, j.ld, st));
   prof_mark(ctx, st, "coef");
   if (diag_side) {
@@ -946,6 +971,19 @@ int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr
   }
   prof_mark(ctx, st, "final");
   return 0;
+}
+
+int fast_pipeline(ots_ctx* ctx, Job& j, double* Q, long ldq, double* R, long ldr, bool diag_side) {
+  const JobCfg& c = j.c;
+  cudaStream_t st = c.st;
+  const int KT = j.KT;
+  int rc = fast_factor(ctx, j);
+  if (rc) return rc;
+  set_identity_kernel<<<(KT * KT + 255) / 256, 256, 0, st>>>(j.ident, KT);
+  if ((rc = fast_coef(ctx, j, j.ident, true, Q, ldq, j.lv.back().R, R, ldr))) return rc;
+  copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, (int)c.k0, (int)c.k);
+  CK(launch_z2(j.s, st));
+  return fast_final(ctx, j, diag_side);
 }
 
 int two_stage_pipeline(ots_ctx* ctx, const JobCfg& c, int intra, double* Q, long ldq, double* R, long ldr,
@@ -1614,6 +1652,8 @@ int ots_dist_begin(ots_ctx* ctx, int64_t n_local, int64_t row0, int64_t k0, int6
   // three CTAs) run beside apply1 and the factor, which are planned for the
   // remaining SMs
   if (ctx->nsm > 16) c.nsm_avail = ctx->nsm - 3;
+  c.fast_try = true;     // each rank picks its route on its own rows: R, C and Y2 are exchanged either way
+  ctx->fast_taken = 0;
   return job_setup(ctx, *ctx->job, c);
 }
 
@@ -1629,7 +1669,7 @@ int ots_dist_sizes(ots_ctx* ctx, int64_t* out4) {
 
 int ots_dist_gram(ots_ctx* ctx, double* gram_out) {
   Job& j = *ctx->job;
-  int rc = phase_gram(ctx, j);
+  int rc = j.fast ? fast_gram(ctx, j) : phase_gram(ctx, j);
   if (rc) return rc;
   long cnt = (long)j.PW * j.NTOT1;
   if (gram_out) CK(cudaMemcpyAsync(gram_out, j.Gfull, cnt * 8, cudaMemcpyDeviceToDevice, j.c.st));
@@ -1703,9 +1743,18 @@ int ots_dist_factor(ots_ctx* ctx, double* r_local_out) {
   Job& j = *ctx->job;
   // apply1 (dynamic tiles) and the factor (chains planned for nsm - 3 SMs)
   // run beside the diagnostics launched by ots_dist_seed
-  int rc = phase_apply1(ctx, j);
-  if (rc) return rc;
-  if ((rc = run_factor_levels(ctx, j.lv, j.KT, j.c.st))) return rc;
+  int rc;
+  j.fast_active = false;
+  if (j.fast) {
+    rc = fast_factor(ctx, j);
+    if (rc < 0) return rc;
+    j.fast_active = rc == 0;
+    ctx->fast_taken = j.fast_active ? 1 : 0;
+  }
+  if (!j.fast_active) {
+    if ((rc = phase_apply1(ctx, j))) return rc;
+    if ((rc = run_factor_levels(ctx, j.lv, j.KT, j.c.st))) return rc;
+  }
   if (r_local_out)
     CK(cudaMemcpyAsync(r_local_out, j.lv.back().R, (size_t)j.KT * j.KT * 8, cudaMemcpyDeviceToDevice, j.c.st));
   return OTS_OK;
@@ -1760,12 +1809,19 @@ int ots_dist_qform(ots_ctx* ctx, double* y2_out, double* sign_out) {
   Job& j = *ctx->job;
   cudaStream_t st = j.c.st;
   int rc;
-  if ((rc = run_qform_levels(ctx, j.lv, j.KT, j.Cglob, st, j.nsm_use))) return rc;
-  if (j.c.row0 == 0) {
-    CK(launch_sign(j.s, j.c.Q + j.c.k0 * j.c.ldq, j.c.ldq, j.Rfinal, j.KT, j.s.D1 /*scratch R*/, j.ld, st));
-    if (sign_out) CK(cudaMemcpyAsync(sign_out, j.svec, j.c.k * 8, cudaMemcpyDeviceToDevice, st));
+  if (j.fast_active) {
+    if ((rc = fast_coef(ctx, j, j.Cglob, j.c.row0 == 0, j.c.Q, j.c.ldq, j.Rfinal, j.s.D1 /*scratch R*/, j.ld)))
+      return rc;
+    if (j.c.row0 == 0 && sign_out)
+      CK(cudaMemcpyAsync(sign_out, j.svec, j.c.k * 8, cudaMemcpyDeviceToDevice, st));
+  } else {
+    if ((rc = run_qform_levels(ctx, j.lv, j.KT, j.Cglob, st, j.nsm_use))) return rc;
+    if (j.c.row0 == 0) {
+      CK(launch_sign(j.s, j.c.Q + j.c.k0 * j.c.ldq, j.c.ldq, j.Rfinal, j.KT, j.s.D1 /*scratch R*/, j.ld, st));
+      if (sign_out) CK(cudaMemcpyAsync(sign_out, j.svec, j.c.k * 8, cudaMemcpyDeviceToDevice, st));
+    }
+    if ((rc = phase_gram2(ctx, j))) return rc;
   }
-  if ((rc = phase_gram2(ctx, j))) return rc;
   long cnt = (long)j.PW * j.BWa;
   if (y2_out) CK(cudaMemcpyAsync(y2_out, j.Y2full, cnt * 8, cudaMemcpyDeviceToDevice, st));
   return OTS_OK;
@@ -1795,7 +1851,7 @@ int ots_dist_finish(ots_ctx* ctx, const double* y2_sum, const double* sign, doub
   copy_y2_kernel<<<16, 256, 0, st>>>(j.Y2full, j.BWa, j.s.Z2, j.ld, k0, k);
   CK(launch_z2(j.s, st));
   int rc;
-  if ((rc = phase_apply2(ctx, j))) return rc;
+  if ((rc = j.fast_active ? fast_final(ctx, j, true) : phase_apply2(ctx, j))) return rc;
   if (j.c.row0 == 0) CK(launch_qtop(j.s, j.c.Q, j.c.ldq, st));
   if (R) rscale_kernel<<<8, 256, 0, st>>>(j.Rfinal, j.KT, j.svec, R, ldr, k);
   if (S) copy_s_kernel<<<8, 256, 0, st>>>(j.s.Sd, j.ld, S, lds, k0, k);
