@@ -1,5 +1,5 @@
-// Direct-Q pipeline of the headline shape (real f64, k0 <= 128, 32 < k <= 64,
-// one device): the Gram-form level-0 factor (gsweep.inc) only needs the tile
+// Direct-Q pipeline of the headline shape (real f64, 96 < k0 <= 128, 32 < k <= 64,
+// one device or one rank's row shard): the Gram-form level-0 factor (gsweep.inc) only needs the tile
 // Grams of X = A_b + V_b Z1, and its Q formation is Q_tile = X_tile K_tile
 // with a 64 x 64 coefficient per tall tile, so X never has to exist:
 //
@@ -20,6 +20,8 @@
 // Householder) are materialised in the Q buffer by small kernels.
 //
 // Reference semantics: twostage.py:90-97 (H^* A, intra QR, Q = H [0; Q_]).
+// tgram_kernel (k = 0) and final_nn_kernel<128> also serve the complex128
+// Gram-form intra QR on the interleaved real views (zpath.inc: zgs_intra).
 #include "common.cuh"
 #include "kernels.cuh"
 

@@ -497,8 +497,10 @@ int job_setup(ots_ctx* ctx, Job& j, const JobCfg& c) {
   // direct-Q pipeline: per-tall-tile Grams of [V | A] and coefficients
   j.fast = false;
   size_t f_tg = 0, f_coef = 0, f_part = 0;
-  // (a caller-supplied V^T V is not needed here: the tile pass forms V^T V per tile anyway)
-  if (c.fast_try && fast_on() && !c.exact_intra && c.ld_min == 0 &&
+  // (callers that bring their own V^T V are Krylov-type drivers whose new block A = L Q_prev lies
+  // mostly in range(V): the attempt would be rejected after a wasted tile pass -- measured +13 ms
+  // on the k0 = 128 step of configs[4] -- so they keep the materialised-X pipeline)
+  if (c.fast_try && fast_on() && !c.gram_in && !c.exact_intra && c.ld_min == 0 &&
       k0 > 96 && k0 <= 128 && KT == 64 && gsweep_on(KT, 128) && j.m >= fast_min_rows()) {
     const ChainGeom G = level0_geom(j.m, KT, gs_tile_rows(j.m, nsm_use), nsm_use);
     if (G.L >= 1) {
