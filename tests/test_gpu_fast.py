@@ -184,7 +184,9 @@ def test_complex_gram_form_falls_back():
     assert loss <= 10 * max(rl, 4 * U) and resid <= 10 * max(rr, 4 * U)
 
 
-def test_complex_weighted_rows_keep_the_exact_intra_qr():
+def test_complex_weighted_rows_gram_form_vs_oracle():
+    """B = diag(d), complex: the scaled Euclidean problem takes the Gram-form
+    intra QR too; Q, R, S per entry against the oracle's B-path."""
     n, k0, k = 560000, 16, 48
     rng = W.make_rng(29)
     d = 10.0 ** W.uniform(W.make_rng(30), 0.0, 4.0, n)
@@ -192,7 +194,10 @@ def test_complex_weighted_rows_keep_the_exact_intra_qr():
     v = np.linalg.qr(sq[:, None] * _cgauss(rng, n, k0))[0] / sq[:, None]
     a = _cgauss(rng, n, k)
     ip = P.InnerProduct.weighted(d)
-    res = P.b_two_stage_qr(v, a, P.initial_b_basis(ip, k0 + k), ip)
-    assert took_fast() == 0
+    u = P.initial_b_basis(ip, k0 + k)
+    res = P.b_two_stage_qr(v, a, u, ip)
+    assert took_fast() == 1
+    ref = O.b_two_stage(v, a, u, O.BInner(diag=d), "qr", diagnostics=False)
+    assert rel(res.q, ref["q"]) < 1e-10 and rel(res.r, ref["r"]) < 1e-10 and rel(res.s, ref["s"]) < 1e-10
     m = P.compute_metrics(v, a, res, inner=ip)
     assert m.loss_orth <= 10 * n * U and m.rel_residual <= 10 * n * U

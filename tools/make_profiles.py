@@ -112,8 +112,8 @@ if os.path.exists(G("configs.log")):
     o = [f"# Full-size BASELINE configurations (one B200, `tools/configs_report.py`, {tag})\n",
          "Device time per call (CUDA events, inputs resident; median of 3 after a warm-up, C5 one call per step), stability from the GPU "
          "metrics judge (`compute_metrics`, augmented [V, Q], real and complex), against 10 n u.  C3's inputs cancel (A partly in "
-         "range(V)): the direct-Q attempt is rejected on the device and the call takes the materialised-X pipeline.  C4 runs the complex "
-         "Gram-form intra QR (its B-inner variant keeps the exact path).  its GFLOP/s "
+         "range(V)): the direct-Q attempt is rejected on the device and the call takes the materialised-X pipeline.  C4 and its B-inner variant run the complex "
+         "Gram-form intra QR.  its GFLOP/s "
          "column counts executed work of the incremental-Gram formulation, not F_alg.\n",
          "| config | n | k0 | k | ms | GFLOP/s | loss | residual | 10 n u | kappa(T) |", "|---|---|---|---|---|---|---|---|---|---|"]
     for d in recs:
