@@ -222,10 +222,29 @@ struct NnCfg {
   static constexpr int RT = NWM * 32;
   static constexpr int NT = 256;
   static constexpr int KC = 32;
-  static constexpr int STAGE = RT * KC + KC * KT;
+  // Stage rows are stored linearly with padded pitches (the row-major A operand,
+  // 8 rows x 4 columns per fragment, wants 32 bytes mod 128 per row, the B
+  // operand, 4 rows x 8 columns, 64 bytes mod 128: two wavefronts per operand
+  // load either way) so that full chunks can be written by bulk row copies
+  // (cp.async.bulk, SASS UBLKCP) completing on an mbarrier by bytes.
+  static constexpr int PP = KC + 4, PZ = KT + 8;
+  static constexpr int STAGE = RT * PP + KC * PZ;
   static constexpr int NSTAGE = 2;                    // 2 CTAs / SM share the SM
   static constexpr int SMEM = NSTAGE * STAGE * 8;
 };
+
+__device__ __forceinline__ void nn_bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void nn_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
 
 template <int KT>
 __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
@@ -248,26 +267,54 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
   // 3-slot ring: slot (lt % 3) holds local tile lt; tile lt+2 is fetched at
   // chunk 0 of tile lt, after a barrier that retires tile lt-1's slot.
   __shared__ long s_tile[3];
+  __shared__ __align__(8) unsigned long long full_bar[C::NSTAGE];
   const bool dyn = a.tile_counter != nullptr;
   if (tid == 0) {
     s_tile[0] = blockIdx.x;
     s_tile[1] = dyn ? gridDim.x + atomicAdd(a.tile_counter, 1) : blockIdx.x + (long)gridDim.x;
+    for (int s = 0; s < C::NSTAGE; ++s) mbar_init(&full_bar[s], C::NT);
+    fence_mbar_init();
   }
   __syncthreads();
+  constexpr int PP = C::PP, PZ = C::PZ;
+  // bulk copies need 16-byte row pieces: even widths, and a full Z row (ncols = KT)
+  const bool bulk_ok = !(a.kdim & 1) && a.ncols == KT && C::RT + C::KC <= C::NT && !(a.ldz & 1) && !(a.ldp & 1) &&
+                       ((reinterpret_cast<uintptr_t>(a.Z) | reinterpret_cast<uintptr_t>(a.P)) & 15) == 0;
   auto tile_of = [&](long lt) { return s_tile[lt % 3]; };
   auto tile_r0 = [&](long lt) { return a.row_begin + tile_of(lt) * (long)C::RT; };
+  // Stage it: columns ch * 32 .. of one RT-row tile of P and the matching 32
+  // rows of Z.  Full chunks: one bulk copy per row (threads 0 .. RT-1 a P row,
+  // RT .. RT+31 a Z row), thread 0 posts the byte count; chunks cut by the last
+  // row or by kdim: 16-byte cp.async units with zero fill.
   auto issue = [&](long it) {
     const long lt = it / nchunks;
-    if (tile_of(lt) < ntiles_total) {
-      int s = (int)(it % C::NSTAGE);
-      int ch = (int)(it - lt * nchunks);
-      double* Ps = smem + s * C::STAGE;
-      double* Zs = Ps + C::RT * C::KC;
-      load_tile_async(Ps, C::KC, a.P, a.ldp, tile_r0(lt), C::RT, a.row_begin, a.row_end, ch * C::KC, C::KC,
-                      a.kdim, tid, C::NT);
-      load_tile_async(Zs, KT, a.Z, a.ldz, (long)ch * C::KC, C::KC, 0, a.kdim, 0, KT, a.ncols, tid, C::NT);
+    if (tile_of(lt) >= ntiles_total) return;
+    const int s = (int)(it % C::NSTAGE);
+    const int ch = (int)(it - lt * nchunks);
+    double* Ps = smem + s * C::STAGE;
+    double* Zs = Ps + C::RT * PP;
+    const long r0 = tile_r0(lt);
+    if (bulk_ok && r0 + C::RT <= a.row_end && (ch + 1) * C::KC <= a.kdim) {
+      if (tid < C::RT) nn_bulk_g2s(Ps + tid * PP, a.P + (r0 + tid) * a.ldp + ch * C::KC, C::KC * 8, &full_bar[s]);
+      else if (tid < C::RT + C::KC)
+        nn_bulk_g2s(Zs + (tid - C::RT) * PZ, a.Z + (long)(ch * C::KC + tid - C::RT) * a.ldz, KT * 8, &full_bar[s]);
+      if (tid == 0) nn_arrive_expect_tx(&full_bar[s], (C::RT * C::KC + C::KC * KT) * 8);
+      else mbar_arrive(&full_bar[s]);
+    } else {
+      for (int i = tid; i < C::RT * (C::KC / 2); i += C::NT) {
+        const int r = i / (C::KC / 2), u = i - r * (C::KC / 2);
+        const int c = ch * C::KC + 2 * u;
+        const bool in = r0 + r < a.row_end && c < a.kdim;
+        cp_async16(Ps + r * PP + 2 * u, in ? a.P + (r0 + r) * a.ldp + c : a.P, in ? (c + 1 < a.kdim ? 16 : 8) : 0);
+      }
+      for (int i = tid; i < C::KC * (KT / 2); i += C::NT) {
+        const int r = i / (KT / 2), u = i - r * (KT / 2);
+        const int zr = ch * C::KC + r, c = 2 * u;
+        const bool in = zr < a.kdim && c < a.ncols;
+        cp_async16(Zs + r * PZ + 2 * u, in ? a.Z + (long)zr * a.ldz + c : a.Z, in ? (c + 1 < a.ncols ? 16 : 8) : 0);
+      }
+      cp_async_mbar_arrive(&full_bar[s]);
     }
-    cp_async_commit();
   };
 
   double acc[4][NJ][2];
@@ -338,8 +385,7 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
     const int ch = (int)(it - lt * nchunks);
     if (tile_of(lt) >= ntiles_total) break;
     if (ch == 0) acc_from_b(tile_r0(lt));
-    cp_async_wait<C::NSTAGE - 2>();
-    __syncthreads();
+    __syncthreads();                                   // everyone is done with the other stage
     if (ch == 0 && tid == 0)
       s_tile[(lt + 2) % 3] = dyn ? gridDim.x + atomicAdd(a.tile_counter, 1) : tile_of(lt + 1) + gridDim.x;
     issue(it + C::NSTAGE - 1);
@@ -358,15 +404,16 @@ __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
       }
     }
     const int s = (int)(it % C::NSTAGE);
+    mbar_wait(&full_bar[s], (unsigned)((it / C::NSTAGE) & 1));
     const double* Ps = smem + s * C::STAGE;
-    const double* Zs = Ps + C::RT * C::KC;
+    const double* Zs = Ps + C::RT * PP;
 #pragma unroll
     for (int kk = 0; kk < C::KC / 4; ++kk) {
       double af[4], bf[NJ];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = Ps[swz(wm0 + 8 * i + g, 4 * kk + t, C::KC)];
+      for (int i = 0; i < 4; ++i) af[i] = Ps[(wm0 + 8 * i + g) * PP + 4 * kk + t];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) bf[j] = Zs[swz(4 * kk + t, wn0 + 8 * j + g, KT)];
+      for (int j = 0; j < NJ; ++j) bf[j] = Zs[(4 * kk + t) * PZ + wn0 + 8 * j + g];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
