@@ -448,9 +448,9 @@ int grid_for_tn(int PW, int BW, bool alias, bool sym, int nsm) {
   int mb = PW / 32;
   int nt = (alias ? (sym ? mb * (mb + 1) / 2 : mb * mb) : 0) + mb * (BW / 32);
   if (nt % 4 == 2 && nt > 4) nt += 2;   // mirrors TnCfg::NSPLIT
-  const int RT = 32;                                   // mirrors TnCfg
-  int stage = RT * (PW + BW) * 8;
-  int nst = std::min(4, std::max(2, (200 * 1024) / stage));
+  const int RT = 32;                                   // mirrors TnCfg (padded pitches, 220 KB budget)
+  int stage = RT * (PW + 8 + (BW > 0 ? BW + 8 : 0)) * 8;
+  int nst = std::min(4, std::max(2, (220 * 1024) / stage));
   int smem = nst * stage;
   int by_smem = std::max(1, (227 * 1024) / (smem + 1024));
   int by_threads = std::max(1, 2048 / (nt * 32));

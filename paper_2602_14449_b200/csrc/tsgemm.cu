@@ -17,6 +17,21 @@
 
 namespace ots {
 
+// cp.async.bulk global -> shared row copy completing on an mbarrier by bytes,
+// and the arrival that posts a stage's byte count
+__device__ __forceinline__ void nn_bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+__device__ __forceinline__ void nn_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
 // ============================================================================
 // TN: per-CTA partial inner products
 // ============================================================================
@@ -37,8 +52,12 @@ struct TnCfg {
   // ring hand-offs per DMMA of 32-row stages (measured: gram 19.5 -> 18.4 ms)
   // (for the cross product V^T Q_ it measured slower: 8.87 -> 9.15 ms)
   static constexpr int RT = (PW == 128 && BW == 64 && ALIAS) ? 64 : 32;
-  static constexpr int STAGE = RT * (PW + BW);
-  static constexpr int NSTAGE_RAW = (200 * 1024) / (STAGE * 8);
+  // Stage rows are stored linearly with padded pitches (a row advances 64
+  // bytes of bank space: the 4 rows x 8 columns of an operand fragment take
+  // the 2-wavefront minimum), the layout bulk row copies (cp.async.bulk) write.
+  static constexpr int PPW = PW + 8, PBW = BW > 0 ? BW + 8 : 0;
+  static constexpr int STAGE = RT * (PPW + PBW);
+  static constexpr int NSTAGE_RAW = (220 * 1024) / (STAGE * 8);
   static constexpr int NSTAGE = NSTAGE_RAW > 4 ? 4 : (NSTAGE_RAW < 2 ? 2 : NSTAGE_RAW);
   static constexpr int SMEM = NSTAGE * STAGE * 8;
   static constexpr int NTOT = NBV * 32 + BW;
@@ -91,7 +110,7 @@ tsgemm_tn_kernel(TnArgs a) {
   const long blo = a.row_begin > a.b_row_begin ? a.row_begin : a.b_row_begin;
 
   auto stage_p = [&](int s) { return smem + s * C::STAGE; };
-  auto stage_b = [&](int s) { return smem + s * C::STAGE + C::RT * PW; };
+  auto stage_b = [&](int s) { return smem + s * C::STAGE + C::RT * C::PPW; };
   // mbarrier ring instead of a CTA barrier per stage: every thread issues its
   // share of tile it+LA (cp.async, then cp.async.mbarrier.arrive on full[s])
   // once all warps have released that stage (empty[s], one arrival per warp);
@@ -108,16 +127,55 @@ tsgemm_tn_kernel(TnArgs a) {
     }
     fence_mbar_init();
   }
+  // Full stages: one bulk copy per row (threads 0 .. RT-1 a P row, RT .. 2RT-1 a
+  // B row), completing on the stage's mbarrier by bytes, thread 0 posts the byte
+  // count; stages cut by the row ranges, odd widths / offsets: 16-byte cp.async
+  // units with zero fill.  Columns beyond pcols / bcols are zeroed once (bulk
+  // copies never touch them).
+  constexpr bool BULK_T = C::NT >= C::RT * (BW > 0 ? 2 : 1);
+  const bool bulk_ok = BULK_T && !(a.pcols & 1) && !(a.pc0 & 1) && !(a.ldp & 1) &&
+                       (reinterpret_cast<uintptr_t>(a.P) & 15) == 0 &&
+                       (BW == 0 || (!(a.bcols & 1) && !(a.bc0 & 1) && !(a.ldb & 1) &&
+                                    (reinterpret_cast<uintptr_t>(a.B) & 15) == 0));
+  if (bulk_ok) {
+    for (int e = tid; e < C::NSTAGE * C::STAGE; e += C::NT) smem[e] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   __syncthreads();
   auto produce = [&](int j) {
     if (j >= ntiles) return;
     const int s = j % C::NSTAGE, rnd = j / C::NSTAGE;
     if (rnd >= 1) mbar_wait(&empty_bar[s], (rnd - 1) & 1);
     const long r0 = r_lo + (long)j * C::RT;
-    load_tile_async(stage_p(s), PW, a.P, a.ldp, r0, C::RT, plo, r_hi, a.pc0, PW, a.pc0 + a.pcols, tid, C::NT);
-    if (BW > 0)
-      load_tile_async(stage_b(s), BW, a.B, a.ldb, r0, C::RT, blo, r_hi, a.bc0, BW, a.bc0 + a.bcols, tid, C::NT);
-    cp_async_mbar_arrive(&full_bar[s]);
+    double* Ps = stage_p(s);
+    double* Bs = stage_b(s);
+    if (bulk_ok && r0 >= plo && r0 + C::RT <= r_hi && (BW == 0 || r0 >= blo)) {
+      if (tid < C::RT)
+        nn_bulk_g2s(Ps + tid * C::PPW, a.P + (r0 + tid) * a.ldp + a.pc0, (unsigned)a.pcols * 8u, &full_bar[s]);
+      else if (BW > 0 && tid < 2 * C::RT)
+        nn_bulk_g2s(Bs + (tid - C::RT) * C::PBW, a.B + (r0 + tid - C::RT) * a.ldb + a.bc0, (unsigned)a.bcols * 8u,
+                    &full_bar[s]);
+      if (tid == 0) nn_arrive_expect_tx(&full_bar[s], (unsigned)(C::RT * (a.pcols + (BW > 0 ? a.bcols : 0))) * 8u);
+      else mbar_arrive(&full_bar[s]);
+    } else {
+      for (int i = tid; i < C::RT * (PW / 2); i += C::NT) {
+        const int r = i / (PW / 2), u = i - r * (PW / 2);
+        const long gr = r0 + r;
+        const int c = 2 * u;
+        const bool in = gr >= plo && gr < r_hi && c < a.pcols;
+        cp_async16(Ps + r * C::PPW + c, in ? a.P + gr * a.ldp + a.pc0 + c : a.P, in ? (c + 1 < a.pcols ? 16 : 8) : 0);
+      }
+      if (BW > 0) {
+        for (int i = tid; i < C::RT * (BW / 2 > 0 ? BW / 2 : 1); i += C::NT) {
+          const int r = i / (BW / 2 > 0 ? BW / 2 : 1), u = i - r * (BW / 2 > 0 ? BW / 2 : 1);
+          const long gr = r0 + r;
+          const int c = 2 * u;
+          const bool in = gr >= blo && gr < r_hi && c < a.bcols;
+          cp_async16(Bs + r * C::PBW + c, in ? a.B + gr * a.ldb + a.bc0 + c : a.B, in ? (c + 1 < a.bcols ? 16 : 8) : 0);
+        }
+      }
+      cp_async_mbar_arrive(&full_bar[s]);
+    }
   };
   for (int j = 0; j < LA; ++j) produce(j);
 
@@ -133,7 +191,7 @@ tsgemm_tn_kernel(TnArgs a) {
     mbar_wait(&full_bar[s], (it / C::NSTAGE) & 1);
     const double* Ps = stage_p(s);
     const double* Bs = fromP ? Ps : stage_b(s);
-    const int BWs = fromP ? PW : (BW > 0 ? BW : 32);
+    const int BWs = fromP ? C::PPW : (BW > 0 ? C::PBW : 32);
     const int nb0 = fromP ? 32 * ni : 32 * ni;
     if (SYM && fromP && mi == ni && !half) {   // diagonal block: fragments i >= j only
 #pragma unroll
@@ -141,9 +199,9 @@ tsgemm_tn_kernel(TnArgs a) {
         const int r = 4 * kk + t;
         double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Ps[r * C::PPW + 32 * mi + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, nb0 + 8 * j + g, BWs)];
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[r * BWs + nb0 + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -155,9 +213,9 @@ tsgemm_tn_kernel(TnArgs a) {
         const int r = 4 * kk + t;
         double af[4], bf[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Ps[r * C::PPW + 32 * mi + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bf[j] = Bs[swz(r, nb0 + 8 * j + g, BWs)];
+        for (int j = 0; j < 4; ++j) bf[j] = Bs[r * BWs + nb0 + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -170,9 +228,9 @@ tsgemm_tn_kernel(TnArgs a) {
         const int r = 4 * kk + t;
         double af[4], bf[2];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) af[i] = Ps[swz(r, 32 * mi + 8 * i + g, PW)];
+        for (int i = 0; i < 4; ++i) af[i] = Ps[r * C::PPW + 32 * mi + 8 * i + g];
 #pragma unroll
-        for (int j = 0; j < 2; ++j) bf[j] = Bs[swz(r, nbh + 8 * j + g, BWs)];
+        for (int j = 0; j < 2; ++j) bf[j] = Bs[r * BWs + nbh + 8 * j + g];
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -232,19 +290,6 @@ struct NnCfg {
   static constexpr int NSTAGE = 2;                    // 2 CTAs / SM share the SM
   static constexpr int SMEM = NSTAGE * STAGE * 8;
 };
-
-__device__ __forceinline__ void nn_bulk_g2s(void* smem, const void* gmem, unsigned bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(smem)),
-               "l"(gmem), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
-               : "memory");
-}
-__device__ __forceinline__ void nn_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
 
 template <int KT>
 __global__ void __launch_bounds__(256, 2) tsgemm_nn_kernel(NnArgs a) {
