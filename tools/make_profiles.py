@@ -121,8 +121,8 @@ if os.path.exists(G("configs.log")):
                  f"{d['residual']:.2e} | {d['bound_10nu']:.1e} | {d.get('kappa_t', 0):.4f} |")
     c5 = [d["ms"] for d in recs if d["config"].startswith("C5")]
     if c5:
-        o.append(f"\nC5 sweep (8 steps after the first block): {sum(c5):.1f} ms.  Single shots: a step can include a re-allocation "
-                 f"of the context-owned workspace as k0 grows (up to +140 ms); `tools/krylov_c5.py` alone measures the sweep at "
+        o.append(f"\nC5 sweep (8 steps after the first block): {sum(c5):.1f} ms.  Single shots in a process holding ~150 GB of tensors: a step can include "
+                 f"allocator work (up to +140 ms); `tools/krylov_c5.py` alone measures the sweep at "
                  f"1046.5 ms (`profiles/{tag}_c5_sweep.json`).")
     open(P("configs.md"), "w").write("\n".join(o) + "\n")
 if os.path.exists(G("share2.log")):
