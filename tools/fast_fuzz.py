@@ -27,18 +27,35 @@ def shapes(ncases):
     return out
 
 
+CPLX = os.environ.get("FUZZ_COMPLEX") == "1"
+
+
+def cshapes(ncases):
+    rng = np.random.default_rng(77)
+    out = []
+    for i in range(ncases):
+        out.append((int(rng.integers(540000, 1800000)), int(rng.integers(1, 65)), int(rng.integers(33, 65)),
+                    ("qr", "mlu", "polar")[i % 3]))
+    out += [(524288 + 64, 64, 64, "qr"), (4096 * 148 + 64 + 64 + 1, 64, 64, "qr"), (1 << 21, 64, 33, "mlu")]
+    return out
+
+
 def one(ncases, path):
     import torch
     import paper_2602_14449_b200 as P
     from paper_2602_14449_b200 import _native as NT
     res_all = {}
-    for idx, (n, k0, k, ch) in enumerate(shapes(ncases)):
+    for idx, (n, k0, k, ch) in enumerate(cshapes(ncases) if CPLX else shapes(ncases)):
         g = torch.Generator(device="cuda:0")
         g.manual_seed(100 + idx)
-        v0 = torch.randn((n, k0), generator=g, dtype=torch.float64, device="cuda:0")
+
+        def gen(r, c):
+            x = torch.randn((r, c), generator=g, dtype=torch.float64, device="cuda:0")
+            return torch.complex(x, torch.randn((r, c), generator=g, dtype=torch.float64, device="cuda:0")) if CPLX else x
+        v0 = gen(n, k0)
         blocks = [v0[:, i:i + 64].contiguous() for i in range(0, k0, 64)]
         V = P.block_householder_qr(blocks).q.contiguous()
-        A = torch.randn((n, k), generator=g, dtype=torch.float64, device="cuda:0")
+        A = gen(n, k)
         r = P.two_stage_qr(V, A, choice=ch)
         fast = NT.last_fast(NT.context(0))
         m = P.compute_metrics(V, A, r, augmented=True)
@@ -56,7 +73,7 @@ if __name__ == "__main__":
     ncases = int(sys.argv[1]) if len(sys.argv) > 1 else 12
     for f in ("1", "0"):
         e = dict(os.environ)
-        e["OTS_FAST"] = f
+        e["OTS_ZGS" if CPLX else "OTS_FAST"] = f
         subprocess.run([sys.executable, __file__, "one", str(ncases), f"/tmp/fuzz{f}"], env=e, check=True)
     a, b = json.load(open("/tmp/fuzz1.json")), json.load(open("/tmp/fuzz0.json"))
     rel = lambda x, y: float((np.abs(x - y) / (np.abs(y) + 1e-4 * np.abs(y).max())).max())
